@@ -1,0 +1,407 @@
+#!/usr/bin/env python
+"""Benchmark of the fused ring allreduce (Horovod, arXiv 1802.05799) on B200.
+
+Contract (driver): ``python bench.py --gpus N --steps K --warmup W`` prints ONE
+JSON line on rank 0.  For N > 1 it is launched by torchrun, one process per
+GPU.  A "step" is one pass of the whole hot path — plan -> pack (x 1/N) ->
+ring reduce-scatter + all-gather -> unpack — over one synthetic gradient set,
+through the C ABI ``hvd_allreduce_average``.
+
+Metric (BASELINE.json): fused ring-allreduce bus GB/s of a 64 MB fp32 gradient
+buffer.  busBW = payload_bytes / t * 2(N-1)/N (nccl-tests convention; the
+per-rank ring traffic of P:L197-204).  At N = 1 the ring has no iterations
+(factor 0), so ``value`` is the algorithmic bandwidth payload_bytes / t of the
+N = 1 path (pack/scale + unpack) and ``value_kind`` says so.
+
+``--impl reference`` times the CPU oracle (``oracle/``) — the only reference
+this tier has — on the same workload, on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MIB = 1 << 20
+METRIC = "fused ring-allreduce bus GB/s (64 MB fp32) at 2/4/8 B200 vs 900 GB/s NVLink"
+NVLINK_NOMINAL_GBPS = 900.0
+NVLINK_MEASURED_GBPS = 770.0  # B200_PROFILING.md: measured peer copy per direction per GPU
+L2_BYTES = 126 * MIB
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+def _workload_counts(name):
+    import workloads
+    if name == "fp32_64MiB":
+        return [16 * MIB], "f32"           # one 64 MiB fp32 gradient = one full fusion buffer
+    model, dt = name.rsplit("_", 1) if name.endswith(("_f32", "_bf16")) else (name, "f32")
+    return [c for _, c in workloads.gradient_set(model)], dt
+
+
+def _bus_factor(n):
+    return 2.0 * (n - 1) / n if n > 1 else 0.0
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, devices):
+        self.devices = devices
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                self.out, _ = self.p.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.p.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in (getattr(self, "out", "") or "").splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8 or not f[0].isdigit() or int(f[0]) not in self.devices:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- distributed plumbing
+def _dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), \
+        int(os.environ.get("LOCAL_RANK", os.environ.get("RANK", "0")))
+
+
+def _max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _barrier(world):
+    import torch
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_1802_05799_b200 as hvd
+    rank, world, local = _dist_env()
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+    comm = hvd.init(fusion_bytes=64 * MIB, device=local)
+    counts, dt = _workload_counts(args.workload)
+    tdt = {"f32": torch.float32, "bf16": torch.bfloat16}[dt]
+    esz = 4 if dt == "f32" else 2
+    payload = sum(counts) * esz
+    # inputs larger than L2: rotate over enough gradient sets that the set a step
+    # reads was evicted by the others (>= 2 x L2 of distinct gradient bytes)
+    nsets = max(2, -(-2 * L2_BYTES // payload))
+    g = torch.Generator(device="cuda").manual_seed(180205799 + rank)
+    sets = [[torch.randn(c, generator=g, device="cuda", dtype=torch.float32).to(tdt) for c in counts]
+            for _ in range(nsets)]
+    L = hvd._lib
+    comm.set_config(L.HVD_CFG_PROFILE, 1)
+
+    def step(i):
+        comm.allreduce_average(sets[i % nsets])
+
+    for i in range(args.warmup):
+        step(i)
+    comm.kernel_stats()  # reset counters
+    _barrier(world)
+    with ClockSampler({local} if world == 1 else set(range(world))) as clk:
+        # keep the GPU busy ~1 s so the sampler sees clocks under load, then time K steps
+        t_end = time.time() + args.clock_window
+        i = 0
+        while time.time() < t_end:
+            step(i)
+            i += 1
+            if i % 64 == 0:
+                torch.cuda.synchronize()
+        comm.kernel_stats()
+        _barrier(world)
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for i in range(args.steps):
+            step(i)
+        s1.record()
+        _barrier(world)
+    ms_local = s0.elapsed_time(s1)
+    ks = comm.kernel_stats()
+    ms = _max_over_ranks(ms_local, world)
+    t = ms / 1e3 / args.steps
+    n = world
+    algbw = payload / t / 1e9
+    value = algbw * _bus_factor(n) if n > 1 else algbw
+
+    # ---- roofline of the dominant kernel (device time of each launch, CUDA events on its stream)
+    peaks = _peaks()
+    kt = {k: (v[0], v[1]) for k, v in ks.items() if v[0]}
+    dom = max(kt, key=lambda k: kt[k][1])
+    launches, dev_ms = kt[dom]
+    avg_s = dev_ms / 1e3 / launches
+    esz_of = {"f32": 4, "bf16": 2}
+    fplan = hvd.plan(counts, [dt] * len(counts))
+    if dom == "ring":
+        # NVLink bytes this rank pushes per step: sum over fusion buffers of
+        # (2L - |c_{r+1}| - |c_{r+2}|) * esz  (~ 2(N-1)/N * S)
+        step_bytes = 0
+        for bdt, Lb, _ in fplan:
+            cb = hvd.chunk_bounds(Lb, n, bdt)
+            sz = [cb[i + 1] - cb[i] for i in range(n)]
+            step_bytes += (2 * Lb - sz[(rank + 1) % n] - sz[(rank + 2) % n]) * esz_of[bdt]
+        per_launch = step_bytes * args.steps / launches
+        roof = {"kernel": "ring_allreduce_kernel", "bound": "nvlink", "unit": "GB/s",
+                "achieved": per_launch / avg_s / 1e9, "peak": NVLINK_MEASURED_GBPS,
+                "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction (no NVLink figure in "
+                               "MEASURED_PEAKS.json); nominal 900",
+                "algorithmic_bytes_per_launch": per_launch}
+        roof["frac"] = roof["achieved"] / roof["peak"]
+        roof["frac_of_nominal_900"] = roof["achieved"] / NVLINK_NOMINAL_GBPS
+    else:
+        # pack / unpack: read the members + write the buffer (or back), per step
+        step_bytes = payload + sum(Lb * esz_of[bdt] for bdt, Lb, _ in fplan)
+        per_launch = step_bytes * args.steps / launches
+        roof = {"kernel": f"{dom}_kernel", "bound": "hbm", "unit": "GB/s",
+                "achieved": per_launch / avg_s / 1e9, "peak": peaks.get("hbm_gbs", 6650.0),
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650",
+                "algorithmic_bytes_per_launch": per_launch}
+        roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = _ncu_traffic(roof["kernel"])
+    roof["share_of_step"] = dev_ms / ms_local if ms_local else None
+    kernels = {k: {"launches_per_step": v[0] / args.steps, "avg_us": v[1] / v[0] * 1e3} for k, v in kt.items()}
+    gpu_launches = int(sum(v[0] for v in kt.values()))
+
+    # ---- headline ring only: hvd_allreduce_buffer on one 64 MiB fp32 buffer (no pack/unpack)
+    ring_only = None
+    if n > 1:
+        cnt = 16 * MIB
+        for _ in range(args.warmup):
+            comm.allreduce_buffer(cnt, L.HVD_FLOAT32, "sum")
+        comm.kernel_stats()
+        _barrier(world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            comm.allreduce_buffer(cnt, L.HVD_FLOAT32, "sum")
+        e1.record()
+        _barrier(world)
+        rms = _max_over_ranks(e0.elapsed_time(e1), world) / args.steps
+        comm.kernel_stats()
+        ring_only = {"bytes": cnt * 4, "us": rms * 1e3, "busbw_GBps": cnt * 4 / (rms / 1e3) / 1e9 * _bus_factor(n)}
+
+    # ---- e2e: through the C ABI with HOST buffers (pinned H2D in, D2H of the averaged result out)
+    host_in = [torch.empty(c, dtype=tdt).pin_memory() for c in counts]
+    host_out = [torch.empty(c, dtype=tdt).pin_memory() for c in counts]
+    for h, d in zip(host_in, sets[0]):
+        h.copy_(d.cpu())
+    dev = [torch.empty(c, dtype=tdt, device="cuda") for c in counts]
+    e2e_steps = max(3, min(args.steps, 20))
+
+    def e2e_step():
+        for d, h in zip(dev, host_in):
+            d.copy_(h, non_blocking=True)
+        comm.allreduce_average(dev)
+        for h, d in zip(host_out, dev):
+            h.copy_(d, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    _barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(e2e_steps):
+        e2e_step()
+    e1.record()
+    _barrier(world)
+    ems = _max_over_ranks(e0.elapsed_time(e1), world) / e2e_steps
+    e_alg = payload / (ems / 1e3) / 1e9
+    e2e = {"value": e_alg * _bus_factor(n) if n > 1 else e_alg, "unit": "GB/s", "h2d_bytes_per_step": payload,
+           "d2h_bytes_per_step": payload, "ms_per_step": ems}
+    assert comm.poll_error() == 0, hvd._lib.strerror(comm.poll_error())
+
+    cpu = None
+    if rank == 0 and n == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args, counts, dt, n)
+
+    clocks = clk.summary()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": n, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": dt, "data": "synthetic",
+            "value_kind": "busBW = payload/t * 2(N-1)/N" if n > 1 else
+                          "algBW = payload/t (N=1: the ring has no iterations, bus factor 0)",
+            "config": {"workload": args.workload, "payload_bytes": payload, "tensors": len(counts),
+                       "fusion_bytes": 64 * MIB, "op": "average",
+                       "l2": f"inputs rotate over {nsets} gradient sets ({nsets * payload / MIB:.0f} MiB > L2)",
+                       "parallelism": f"dp{n}", "ranks": "one process per GPU, CUDA-IPC ring"},
+            "roofline": roof, "kernels": kernels, "ring_only_64MiB": ring_only, "e2e": e2e,
+            "gpu_launches": gpu_launches, "cpu_baseline": cpu, "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    comm.finalize()
+
+
+def _ncu_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------- CPU oracle (baseline / reference arm)
+def _oracle_inputs(counts, dt, n, max_elems):
+    """Seeded inputs of a bounded sample of the workload: the first tensors up to max_elems."""
+    import workloads
+    sample, tot = [], 0
+    for c in counts:
+        if tot >= max_elems:
+            break
+        take = min(c, max_elems - tot)
+        sample.append(take)
+        tot += take
+    return sample, workloads.all_ranks(sample, dt, n)
+
+
+def cpu_baseline(args, counts, dt, n, budget_s=10.0):
+    import oracle
+    esz = 4 if dt == "f32" else 2
+    sample, xs = _oracle_inputs(counts, dt, n, 16 * MIB)
+    payload = sum(sample) * esz
+    dts = [dt] * len(sample)
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        oracle.allreduce(xs, dts, "average")
+        reps += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    t = (time.perf_counter() - t0) / reps
+    alg = payload / t / 1e9
+    # C1: 1,048,576 fp32 x 4 simulated ranks, median of 5, seconds
+    x4 = _oracle_inputs([1 << 20], "f32", 4, 1 << 20)[1]
+    c1 = []
+    for _ in range(5):
+        s = time.perf_counter()
+        oracle.allreduce(x4, ["f32"], "average")
+        c1.append(time.perf_counter() - s)
+    return {"value": alg * _bus_factor(n) if n > 1 else alg, "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": f"oracle.allreduce of {len(sample)} tensor(s), {payload / MIB:.0f} MiB {dt} per rank, "
+                      f"{n} simulated rank(s), {reps} reps in {reps * t:.1f} s (numpy, single thread)",
+            "c1_seconds_median5": statistics.median(c1), "host_cpus": os.cpu_count()}
+
+
+def run_reference(args):
+    rank, world, _ = _dist_env()
+    if rank != 0:
+        return
+    import oracle
+    counts, dt = _workload_counts(args.workload)
+    n = args.gpus
+    esz = 4 if dt == "f32" else 2
+    sample, xs = _oracle_inputs(counts, dt, n, 16 * MIB)
+    payload = sum(sample) * esz
+    dts = [dt] * len(sample)
+    steps, warm = max(1, min(args.steps, 8)), max(0, min(args.warmup, 1))
+    for _ in range(warm):
+        oracle.allreduce(xs, dts, "average")
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        oracle.allreduce(xs, dts, "average")
+    t = (time.perf_counter() - t0) / steps
+    alg = payload / t / 1e9
+    value = alg * _bus_factor(n) if n > 1 else alg
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": n, "steps": steps,
+            "warmup": warm, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": dt, "data": "synthetic",
+            "config": {"workload": args.workload, "payload_bytes": payload, "simulated_ranks": n},
+            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{len(sample)} tensor(s), {payload / MIB:.0f} MiB per rank, {n} simulated "
+                                       f"rank(s); numpy single thread"},
+            "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="fp32_64MiB",
+                    help="fp32_64MiB | resnet101 | inception_v3[_bf16] | vgg16")
+    ap.add_argument("--clock-window", type=float, default=1.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,214 @@
+/*
+ * hvd.h — C ABI of the B200-native fused ring allreduce (Horovod, arXiv 1802.05799).
+ *
+ * The library implements the data-parallel hot path of the paper:
+ *   Tensor Fusion (§7): pack many gradient tensors into a
+ *   fusion buffer, fused with the averaging scale 1/N, run the ring
+ *   allreduce on the buffer, unpack the result into the tensors;
+ *   ring-allreduce (§3): N-1 reduce-scatter iterations in
+ *   which "received values are added", then N-1 all-gather iterations in which
+ *   "received values replace", each rank talking only to its ring neighbours.
+ * The API follows the paper's four user calls:
+ * init, allreduce-average of the gradients, broadcast of the initial state,
+ * plus allgather (north_star).
+ *
+ * Conventions
+ *   - Every call returns an hvd_status (0 = OK, < 0 = error); nothing throws or
+ *     aborts across the ABI.  Argument errors are reported synchronously and
+ *     leave the communicator unchanged.  Device-side errors (the spin-wait
+ *     watchdog) are asynchronous: they are latched in host-mapped memory and
+ *     returned by hvd_poll_error() and by every later call on that comm.
+ *   - Device pointers are plain CUDA device addresses on the comm's device.
+ *     Streams are cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Work is enqueued on the stream and the call returns without a host
+ *     synchronisation (stream-ordered completion, north_star); the caller's
+ *     tensors must stay valid and unmodified until that work completes.
+ *   - Ownership: the caller owns its tensors; the library owns the fusion
+ *     buffer, the reduce-scatter scratch, the signal flags and the peer
+ *     mappings ("Allocate a fusion buffer if it was not previously
+ *     allocated"), all released by hvd_finalize.
+ *   - Collective contract: every rank makes the same sequence of collective
+ *     calls with identical tensor counts, dtypes, op, threshold and root.  A
+ *     mismatch is undefined behaviour (it can hang until the watchdog fires).
+ *   - A comm is not thread-safe; use one comm per thread.
+ *
+ * Virtual ranks: hvd_init_virtual() creates a comm that simulates all N ranks
+ * on ONE device (one kernel launch spans every rank, so the ranks' CTAs are
+ * co-resident).  It runs exactly the same kernels and signal protocol as the
+ * multi-process path, with "peer" pointers that are same-device buffers.  In
+ * that mode every tensor-list argument holds the lists of all local ranks,
+ * rank-major: element [r * n + k] is tensor k of rank r.
+ */
+#ifndef HVD_B200_H
+#define HVD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HVD_ABI_VERSION 1
+
+typedef enum {
+  HVD_OK = 0,
+  HVD_ERR_INVALID = -1,        /* bad argument (null pointer, size, rank, count overflow) */
+  HVD_ERR_UNSUPPORTED = -2,    /* e.g. AVERAGE on an integer dtype      */
+  HVD_ERR_CUDA = -3,           /* a CUDA runtime call failed                              */
+  HVD_ERR_NOT_CONNECTED = -4,  /* size > 1 and hvd_connect() has not completed            */
+  HVD_ERR_TIMEOUT = -5,        /* a device spin-wait exceeded the watchdog (async)        */
+  HVD_ERR_CLOSED = -6          /* comm already finalized                                  */
+} hvd_status;
+
+typedef enum { HVD_FLOAT32 = 1, HVD_BFLOAT16 = 2, HVD_INT32 = 3, HVD_INT64 = 4 } hvd_dtype;
+typedef enum { HVD_SUM = 0, HVD_AVERAGE = 1 } hvd_op;
+
+/* A flat, contiguous tensor in device memory.  count == 0 is a legal no-op. */
+typedef struct {
+  void* data;      /* device pointer (any alignment; 16 B alignment is the fast path) */
+  uint64_t count;  /* elements */
+  int32_t dtype;   /* hvd_dtype */
+  int32_t reserved;
+} hvd_tensor;
+
+typedef struct hvd_comm hvd_comm; /* opaque */
+
+/* ---- lifecycle ("hvd.init() initializes Horovod") ------------------------ */
+
+/* Create the comm of ring rank `rank` of `size` on CUDA device `device` and
+ * allocate its fusion buffer of `fusion_bytes` (0 = default 64 MiB, P:L368-369;
+ * rounded up to 4 KiB) plus an equal-size reduce-scatter scratch and the signal
+ * flags.  For size > 1 the comm must then exchange blobs and hvd_connect().
+ * Errors: INVALID (size < 1, rank out of range, null out), CUDA. */
+int hvd_init(int rank, int size, int device, uint64_t fusion_bytes, hvd_comm** out);
+
+/* Create a comm that simulates all `size` ranks on one device (see header
+ * comment).  It is connected on return.  Errors: INVALID (size < 1 or > 8), CUDA. */
+int hvd_init_virtual(int size, int device, uint64_t fusion_bytes, hvd_comm** out);
+
+/* Bootstrap: write this rank's CUDA-IPC blob into `out` (caller-owned,
+ * *len bytes).  With out == NULL only *len (the blob size) is returned.  The
+ * caller gathers the blobs of all ranks in rank order (any transport) and
+ * passes them to hvd_connect.  Errors: INVALID (len too small). */
+int hvd_get_ipc_blob(hvd_comm* c, void* out, uint64_t* len);
+
+/* Map the ring successor's buffers from the gathered blobs
+ * (`blobs` = size * len_each bytes, rank order).  Must be called on every
+ * rank; the caller must barrier all ranks after it before the first
+ * collective.  Errors: INVALID (blob mismatch), CUDA (IPC open failed). */
+int hvd_connect(hvd_comm* c, const void* blobs, uint64_t len_each);
+
+/* Release everything.  Idempotent on a NULL comm; waits for the device.  */
+int hvd_finalize(hvd_comm* c);
+
+int hvd_rank(const hvd_comm* c);        /* ring rank (virtual comm: 0)                */
+int hvd_size(const hvd_comm* c);        /* N                                          */
+int hvd_local_ranks(const hvd_comm* c); /* ranks driven by this comm (1 or N)         */
+
+/* ---- the hot path ---------------------------------------------------------------------------- */
+
+/* In-place allreduce of the n tensors `t` (n per local rank, see header).
+ * Tensor Fusion: tensors are grouped next-fit in the given order
+ * into fusion buffers of at most min(fusion_threshold, capacity) bytes (16 B
+ * aligned members, same dtype; fusion_threshold == 0 turns fusion off; a tensor
+ * larger than the limit is split into limit-sized segments — DESIGN.md R6-R8).
+ * Per buffer: pack (with x * fl32(1/N) for AVERAGE, R1) -> ring reduce-scatter
+ * + all-gather -> unpack, all enqueued on `stream`.
+ * op: HVD_SUM (all dtypes) or HVD_AVERAGE (float dtypes only).
+ * Errors: INVALID (null/size), UNSUPPORTED (AVERAGE on integers, bad dtype),
+ * NOT_CONNECTED, TIMEOUT (latched), CUDA. */
+int hvd_allreduce(hvd_comm* c, const hvd_tensor* t, int n, int op, uint64_t fusion_threshold,
+                  void* stream);
+
+/* hvd_allreduce(c, t, n, HVD_AVERAGE, fusion_threshold, stream): the paper's
+ * "average gradients among those multiple copies". */
+int hvd_allreduce_average(hvd_comm* c, const hvd_tensor* t, int n, uint64_t fusion_threshold,
+                          void* stream);
+
+/* Raw ring on the first `count` elements of the registered fusion buffer(s),
+ * no pack/unpack (the headline 64 MiB measurement).  AVERAGE prescales in
+ * place first.  count * esz must be <= capacity.  Same errors as above. */
+int hvd_allreduce_buffer(hvd_comm* c, uint64_t count, int dtype, int op, void* stream);
+
+/* Device address of local rank `local`'s fusion buffer (capacity bytes), NULL on error. */
+void* hvd_fusion_buffer(hvd_comm* c, int local);
+uint64_t hvd_fusion_capacity(const hvd_comm* c);
+
+/* ---- broadcast and allgather (north_star) ---------------------------------------- */
+
+/* Every rank's n tensors become bitwise copies of rank `root`'s (pipelined ring
+ * forward through the fusion buffer).  Errors: INVALID (root), as above. */
+int hvd_broadcast(hvd_comm* c, const hvd_tensor* t, int n, int root, void* stream);
+
+/* out (size * in.count elements, same dtype) = concatenation of every rank's
+ * `in` in rank order (ring all-gather, R12).  `in` and `out` hold one
+ * tensor per local rank.  Errors: INVALID (out too small, dtype mismatch). */
+int hvd_allgather(hvd_comm* c, const hvd_tensor* in, const hvd_tensor* out, void* stream);
+
+/* ---- errors, statistics, tuning -------------------------------------------------------------- */
+
+/* Latched asynchronous error (HVD_OK if none).  Non-blocking. */
+int hvd_poll_error(hvd_comm* c);
+const char* hvd_strerror(int status);
+
+/* Device-side traffic counters of local rank `local` since init: bytes pushed
+ * to the successor and chunk messages sent (one per ring iteration; P:L197-198
+ * "communicates with two of its peers 2*(N-1) times").  Reads device memory
+ * (synchronises the device).  Errors: INVALID, CUDA. */
+int hvd_traffic(hvd_comm* c, int local, uint64_t* sent_bytes, uint64_t* sends);
+
+typedef enum {
+  HVD_CFG_CHANNELS = 1,      /* CTAs per rank in the ring kernel (1..64)                */
+  HVD_CFG_SLICE_BYTES = 2,   /* pipelining slice per channel (multiple of 256 B)        */
+  HVD_CFG_THREADS = 3,       /* threads per ring CTA (128..1024, multiple of 32)         */
+  HVD_CFG_TIMEOUT_MS = 4,    /* device spin-wait watchdog                               */
+  HVD_CFG_PACK_CTAS_PER_SM = 5,
+  HVD_CFG_PROFILE = 6        /* 1: record CUDA events around every kernel launch        */
+} hvd_config_key;
+/* Set a tuning knob; every rank must set identical values.  Errors: INVALID. */
+int hvd_set_config(hvd_comm* c, int key, int64_t value);
+int64_t hvd_get_config(const hvd_comm* c, int key);
+
+typedef enum { HVD_KERNEL_PACK = 0, HVD_KERNEL_RING = 1, HVD_KERNEL_UNPACK = 2, HVD_KERNEL_SCALE = 3,
+               HVD_KERNEL_KINDS = 4 } hvd_kernel_kind;
+/* Kernel launches of each kind since the last call (always counted) and, with
+ * HVD_CFG_PROFILE on, the summed device time in ms between the CUDA events
+ * recorded on the launch stream around each launch (waits for those events).
+ * launches[HVD_KERNEL_KINDS], device_ms[HVD_KERNEL_KINDS]; counters reset.
+ * Errors: INVALID, CUDA. */
+int hvd_kernel_stats(hvd_comm* c, uint64_t* launches, double* device_ms);
+
+/* ---- host-only plan inspection (no device needed) -------------------------------------------- */
+
+typedef struct {
+  int32_t tensor;    /* index into the submitted list */
+  int32_t buffer;    /* fusion buffer index */
+  uint64_t src_off;  /* element offset in the tensor */
+  uint64_t dst_off;  /* element offset in the fusion buffer */
+  uint64_t count;    /* elements */
+} hvd_plan_entry;
+
+typedef struct {
+  int32_t dtype;
+  int32_t n_entries;
+  int32_t first_entry;
+  int32_t reserved;
+  uint64_t length;   /* L, elements */
+} hvd_plan_buffer;
+
+/* Compute the Tensor Fusion plan of (counts[k], dtypes[k]) exactly as
+ * hvd_allreduce does.  On input *n_entries / *n_buffers are the capacities of
+ * the output arrays; on output the sizes used.  Errors: INVALID (capacity too
+ * small: sizes needed are returned), UNSUPPORTED (dtype). */
+int hvd_plan(const uint64_t* counts, const int32_t* dtypes, int n, uint64_t fusion_threshold,
+             uint64_t capacity, hvd_plan_entry* entries, int* n_entries, hvd_plan_buffer* buffers,
+             int* n_buffers);
+
+/* Chunk partition of a buffer of `length` elements over `size` ranks
+ * ("chunks of the data buffer"; R2): out[0..size] boundaries. */
+int hvd_chunk_bounds(uint64_t length, int size, int dtype, uint64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HVD_B200_H */

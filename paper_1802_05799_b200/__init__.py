@@ -1,0 +1,262 @@
+"""B200-native fused ring allreduce (Horovod, arXiv 1802.05799) — Python API.
+
+A thin layer over the C ABI (``include/hvd.h``, ``libhvd_b200.so``): it takes
+``data_ptr()`` / ``numel()`` / dtype from torch tensors, the current CUDA
+stream, and exchanges CUDA-IPC blobs over a ``torch.distributed`` gloo group
+at init.  Every step of the hot path (pack, ring, unpack) runs in the
+library's sm_100a kernels; there is no CPU or eager-torch fallback.
+
+The paper's user-facing calls:
+    hvd.init()                              -> ``init()``
+    hvd.DistributedOptimizer (averaging)    -> ``Comm.allreduce_average(grads)``
+    hvd.broadcast_global_variables(0)       -> ``Comm.broadcast(tensors, root=0)``
+plus ``Comm.allgather`` (north_star).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from . import _lib
+from ._lib import (HVD_AVERAGE, HVD_BFLOAT16, HVD_FLOAT32, HVD_INT32, HVD_INT64, HVD_SUM,  # noqa: F401
+                   HvdError, check, lib)
+
+DEFAULT_FUSION_BYTES = 64 * 1024 * 1024
+
+_TORCH_DTYPE_CODE = None
+
+
+def _dtype_code(t) -> int:
+    global _TORCH_DTYPE_CODE
+    if _TORCH_DTYPE_CODE is None:
+        import torch
+        _TORCH_DTYPE_CODE = {torch.float32: HVD_FLOAT32, torch.bfloat16: HVD_BFLOAT16,
+                             torch.int32: HVD_INT32, torch.int64: HVD_INT64}
+    try:
+        return _TORCH_DTYPE_CODE[t.dtype]
+    except KeyError:
+        raise HvdError(_lib.HVD_ERR_UNSUPPORTED, f"dtype {t.dtype}") from None
+
+
+def _tensor_array(tensors):
+    arr = (_lib.hvd_tensor * max(1, len(tensors)))()
+    for i, t in enumerate(tensors):
+        if not t.is_contiguous():
+            raise HvdError(_lib.HVD_ERR_INVALID, "tensors must be contiguous")
+        arr[i].data = t.data_ptr() if t.numel() else None
+        arr[i].count = t.numel()
+        arr[i].dtype = _dtype_code(t)
+    return arr
+
+
+def _stream_handle(stream):
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return C.c_void_p(s.cuda_stream)
+
+
+_OPS = {"sum": HVD_SUM, "average": HVD_AVERAGE}
+
+
+class Comm:
+    """One communicator: a real ring rank, or all N ranks simulated on one GPU."""
+
+    def __init__(self, handle: C.c_void_p, device: int):
+        self._h = handle
+        self.device = device
+
+    # ---------------------------------------------------------------- identity
+    @property
+    def rank(self) -> int:
+        return lib.hvd_rank(self._h)
+
+    @property
+    def size(self) -> int:
+        return lib.hvd_size(self._h)
+
+    @property
+    def local_ranks(self) -> int:
+        return lib.hvd_local_ranks(self._h)
+
+    # ---------------------------------------------------------------- collectives
+    def _flat(self, tensors):
+        """Accept a list (1 local rank) or a list of per-rank lists (virtual)."""
+        if self.local_ranks == 1:
+            if tensors and isinstance(tensors[0], (list, tuple)):
+                tensors = tensors[0]
+            return list(tensors), len(tensors)
+        if len(tensors) != self.local_ranks:
+            raise HvdError(_lib.HVD_ERR_INVALID, "virtual comm needs one tensor list per rank")
+        n = len(tensors[0])
+        flat = [t for per_rank in tensors for t in per_rank]
+        return flat, n
+
+    def allreduce(self, tensors, op: str = "average", fusion_threshold: int = DEFAULT_FUSION_BYTES,
+                  stream=None):
+        """In-place allreduce of the tensor list (Tensor Fusion + ring)."""
+        flat, n = self._flat(tensors)
+        arr = _tensor_array(flat)
+        check(lib.hvd_allreduce(self._h, arr, n, _OPS[op], int(fusion_threshold), _stream_handle(stream)),
+              "hvd_allreduce")
+        return tensors
+
+    def allreduce_average(self, tensors, fusion_threshold: int = DEFAULT_FUSION_BYTES, stream=None):
+        """The paper's gradient averaging."""
+        flat, n = self._flat(tensors)
+        arr = _tensor_array(flat)
+        check(lib.hvd_allreduce_average(self._h, arr, n, int(fusion_threshold), _stream_handle(stream)),
+              "hvd_allreduce_average")
+        return tensors
+
+    def allreduce_buffer(self, count: int, dtype: int = HVD_FLOAT32, op: str = "sum", stream=None):
+        """Raw ring on the registered fusion buffer (headline measurement)."""
+        check(lib.hvd_allreduce_buffer(self._h, int(count), int(dtype), _OPS[op], _stream_handle(stream)),
+              "hvd_allreduce_buffer")
+
+    def broadcast(self, tensors, root: int = 0, stream=None):
+        flat, n = self._flat(tensors)
+        arr = _tensor_array(flat)
+        check(lib.hvd_broadcast(self._h, arr, n, int(root), _stream_handle(stream)), "hvd_broadcast")
+        return tensors
+
+    def allgather(self, inputs, outputs, stream=None):
+        if self.local_ranks == 1 and not isinstance(inputs, (list, tuple)):
+            inputs, outputs = [inputs], [outputs]
+        check(lib.hvd_allgather(self._h, _tensor_array(list(inputs)), _tensor_array(list(outputs)),
+                                _stream_handle(stream)), "hvd_allgather")
+        return outputs
+
+    # ---------------------------------------------------------------- buffers, stats, knobs
+    def fusion_buffer(self, local: int = 0, dtype=None, count=None):
+        """A torch view of local rank ``local``'s fusion buffer (library-owned memory)."""
+        import torch
+        ptr = lib.hvd_fusion_buffer(self._h, int(local))
+        if not ptr:
+            raise HvdError(_lib.HVD_ERR_INVALID, "hvd_fusion_buffer")
+        cap = lib.hvd_fusion_capacity(self._h)
+        dtype = dtype or torch.float32
+        esz = torch.empty((), dtype=dtype).element_size()
+        count = cap // esz if count is None else int(count)
+        typestr = {torch.float32: "<f4", torch.bfloat16: "<u2", torch.int32: "<i4", torch.int64: "<i8",
+                   torch.uint8: "|u1"}[dtype]
+
+        class _View:
+            __cuda_array_interface__ = {"shape": (count,), "typestr": typestr, "data": (ptr, False),
+                                        "version": 3, "strides": None}
+        t = torch.as_tensor(_View(), device=f"cuda:{self.device}")
+        return t.view(torch.bfloat16) if dtype == torch.bfloat16 else t
+
+    @property
+    def fusion_capacity(self) -> int:
+        return lib.hvd_fusion_capacity(self._h)
+
+    def traffic(self, local: int = 0):
+        sent, sends = C.c_uint64(), C.c_uint64()
+        check(lib.hvd_traffic(self._h, int(local), C.byref(sent), C.byref(sends)), "hvd_traffic")
+        return sent.value, sends.value
+
+    def kernel_stats(self):
+        """{kind: (launches, device_ms)} since the last call (ms needs HVD_CFG_PROFILE=1)."""
+        n = _lib.HVD_KERNEL_KINDS
+        la, ms = (C.c_uint64 * n)(), (C.c_double * n)()
+        check(lib.hvd_kernel_stats(self._h, la, ms), "hvd_kernel_stats")
+        names = ["pack", "ring", "unpack", "scale"]
+        return {names[i]: (la[i], ms[i]) for i in range(n)}
+
+    def poll_error(self) -> int:
+        return lib.hvd_poll_error(self._h)
+
+    def set_config(self, key: int, value: int):
+        check(lib.hvd_set_config(self._h, int(key), int(value)), "hvd_set_config")
+
+    def get_config(self, key: int) -> int:
+        return lib.hvd_get_config(self._h, int(key))
+
+    def finalize(self):
+        if self._h:
+            lib.hvd_finalize(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.finalize()
+        except Exception:
+            pass
+
+
+_DT_NAME = {HVD_FLOAT32: "f32", HVD_BFLOAT16: "bf16", HVD_INT32: "i32", HVD_INT64: "i64"}
+_DT_CODE = {v: k for k, v in _DT_NAME.items()}
+
+
+def plan(counts, dtypes, fusion_threshold=DEFAULT_FUSION_BYTES, capacity=DEFAULT_FUSION_BYTES):
+    """The library's Tensor Fusion plan (host-only ``hvd_plan``).
+
+    Returns a list of (dtype, L, [(tensor, src_off, dst_off, count), ...]).
+    """
+    n = len(counts)
+    cc = (C.c_uint64 * max(1, n))(*counts)
+    dd = (C.c_int32 * max(1, n))(*[_DT_CODE[d] if isinstance(d, str) else d for d in dtypes])
+    ne, nb = C.c_int(0), C.c_int(0)
+    lib.hvd_plan(cc, dd, n, int(fusion_threshold), int(capacity), None, C.byref(ne), None, C.byref(nb))
+    ents = (_lib.hvd_plan_entry * max(1, ne.value))()
+    bufs = (_lib.hvd_plan_buffer * max(1, nb.value))()
+    check(lib.hvd_plan(cc, dd, n, int(fusion_threshold), int(capacity), ents, C.byref(ne), bufs, C.byref(nb)),
+          "hvd_plan")
+    return [(_DT_NAME[b.dtype], b.length,
+             [(e.tensor, e.src_off, e.dst_off, e.count) for e in ents[b.first_entry:b.first_entry + b.n_entries]])
+            for b in bufs[:nb.value]]
+
+
+def chunk_bounds(length, size, dtype):
+    """The ring's chunk partition of a buffer (host-only ``hvd_chunk_bounds``)."""
+    out = (C.c_uint64 * (size + 1))()
+    check(lib.hvd_chunk_bounds(int(length), int(size), _DT_CODE[dtype] if isinstance(dtype, str) else dtype, out),
+          "hvd_chunk_bounds")
+    return list(out)
+
+
+def init_virtual(size: int, device: int = 0, fusion_bytes: int = DEFAULT_FUSION_BYTES) -> Comm:
+    """All ``size`` ring ranks simulated on one GPU (same kernels, same signals)."""
+    h = C.c_void_p()
+    check(lib.hvd_init_virtual(int(size), int(device), int(fusion_bytes), C.byref(h)), "hvd_init_virtual")
+    return Comm(h, device)
+
+
+def exchange_blobs(blob: bytes, group=None):
+    """Gather every rank's IPC blob in rank order over a torch.distributed group."""
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, blob, group=group)
+    return out
+
+
+def init(fusion_bytes: int = DEFAULT_FUSION_BYTES, device: int | None = None, group=None) -> Comm:
+    """``hvd.init()`` for one process per GPU.
+
+    Reads RANK / WORLD_SIZE / LOCAL_RANK from the environment (torchrun), pins
+    the GPU to the local rank, allocates the buffers and maps the
+    ring successor through CUDA IPC; blobs travel over ``group`` (a gloo group
+    is created if torch.distributed is not initialised).
+    """
+    import torch
+    import torch.distributed as dist
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    device = local if device is None else device
+    torch.cuda.set_device(device)
+    h = C.c_void_p()
+    check(lib.hvd_init(rank, world, device, int(fusion_bytes), C.byref(h)), "hvd_init")
+    comm = Comm(h, device)
+    if world > 1:
+        if not dist.is_initialized():
+            dist.init_process_group("gloo")
+        ln = C.c_uint64(0)
+        check(lib.hvd_get_ipc_blob(h, None, C.byref(ln)))
+        buf = C.create_string_buffer(ln.value)
+        check(lib.hvd_get_ipc_blob(h, buf, C.byref(ln)), "hvd_get_ipc_blob")
+        blobs = exchange_blobs(bytes(buf.raw), group)
+        joined = b"".join(blobs)
+        check(lib.hvd_connect(h, joined, ln.value), "hvd_connect")
+        dist.barrier(group)
+    return comm

@@ -1,0 +1,112 @@
+"""ctypes binding of ``libhvd_b200.so`` (include/hvd.h).
+
+Argument marshalling only: no arithmetic of the method lives in Python.  If
+the library is missing this module raises at import — there is no fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import pathlib
+
+LIB_PATH = pathlib.Path(__file__).resolve().parent / "libhvd_b200.so"
+
+HVD_OK = 0
+HVD_ERR_INVALID = -1
+HVD_ERR_UNSUPPORTED = -2
+HVD_ERR_CUDA = -3
+HVD_ERR_NOT_CONNECTED = -4
+HVD_ERR_TIMEOUT = -5
+HVD_ERR_CLOSED = -6
+
+HVD_FLOAT32, HVD_BFLOAT16, HVD_INT32, HVD_INT64 = 1, 2, 3, 4
+HVD_SUM, HVD_AVERAGE = 0, 1
+
+HVD_CFG_CHANNELS = 1
+HVD_CFG_SLICE_BYTES = 2
+HVD_CFG_THREADS = 3
+HVD_CFG_TIMEOUT_MS = 4
+HVD_CFG_PACK_CTAS_PER_SM = 5
+HVD_CFG_PROFILE = 6
+HVD_KERNEL_PACK, HVD_KERNEL_RING, HVD_KERNEL_UNPACK, HVD_KERNEL_SCALE, HVD_KERNEL_KINDS = 0, 1, 2, 3, 4
+
+
+class hvd_tensor(C.Structure):
+    _fields_ = [("data", C.c_void_p), ("count", C.c_uint64), ("dtype", C.c_int32), ("reserved", C.c_int32)]
+
+
+class hvd_plan_entry(C.Structure):
+    _fields_ = [("tensor", C.c_int32), ("buffer", C.c_int32), ("src_off", C.c_uint64),
+                ("dst_off", C.c_uint64), ("count", C.c_uint64)]
+
+
+class hvd_plan_buffer(C.Structure):
+    _fields_ = [("dtype", C.c_int32), ("n_entries", C.c_int32), ("first_entry", C.c_int32),
+                ("reserved", C.c_int32), ("length", C.c_uint64)]
+
+
+class HvdError(RuntimeError):
+    def __init__(self, status: int, what: str = ""):
+        self.status = status
+        super().__init__(f"{what}: {strerror(status)} ({status})" if what else f"{strerror(status)} ({status})")
+
+
+def _load():
+    if not LIB_PATH.exists():
+        raise ImportError(f"{LIB_PATH} is not built; run __graft_entry__.build() "
+                          "(python -m paper_1802_05799_b200._build)")
+    lib = C.CDLL(str(LIB_PATH))
+    P = C.c_void_p
+    sig = {
+        "hvd_init": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_uint64, C.POINTER(P)]),
+        "hvd_init_virtual": (C.c_int, [C.c_int, C.c_int, C.c_uint64, C.POINTER(P)]),
+        "hvd_get_ipc_blob": (C.c_int, [P, P, C.POINTER(C.c_uint64)]),
+        "hvd_connect": (C.c_int, [P, P, C.c_uint64]),
+        "hvd_finalize": (C.c_int, [P]),
+        "hvd_rank": (C.c_int, [P]),
+        "hvd_size": (C.c_int, [P]),
+        "hvd_local_ranks": (C.c_int, [P]),
+        "hvd_allreduce": (C.c_int, [P, C.POINTER(hvd_tensor), C.c_int, C.c_int, C.c_uint64, P]),
+        "hvd_allreduce_average": (C.c_int, [P, C.POINTER(hvd_tensor), C.c_int, C.c_uint64, P]),
+        "hvd_allreduce_buffer": (C.c_int, [P, C.c_uint64, C.c_int, C.c_int, P]),
+        "hvd_fusion_buffer": (P, [P, C.c_int]),
+        "hvd_fusion_capacity": (C.c_uint64, [P]),
+        "hvd_broadcast": (C.c_int, [P, C.POINTER(hvd_tensor), C.c_int, C.c_int, P]),
+        "hvd_allgather": (C.c_int, [P, C.POINTER(hvd_tensor), C.POINTER(hvd_tensor), P]),
+        "hvd_poll_error": (C.c_int, [P]),
+        "hvd_strerror": (C.c_char_p, [C.c_int]),
+        "hvd_traffic": (C.c_int, [P, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+        "hvd_set_config": (C.c_int, [P, C.c_int, C.c_int64]),
+        "hvd_get_config": (C.c_int64, [P, C.c_int]),
+        "hvd_plan": (C.c_int, [C.POINTER(C.c_uint64), C.POINTER(C.c_int32), C.c_int, C.c_uint64, C.c_uint64,
+                               C.POINTER(hvd_plan_entry), C.POINTER(C.c_int), C.POINTER(hvd_plan_buffer),
+                               C.POINTER(C.c_int)]),
+        "hvd_chunk_bounds": (C.c_int, [C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_uint64)]),
+        "hvd_kernel_stats": (C.c_int, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_double)]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+lib = _load()
+
+# every function declared in include/hvd.h (tests check the export table against this)
+EXPORTS = sorted([
+    "hvd_init", "hvd_init_virtual", "hvd_get_ipc_blob", "hvd_connect", "hvd_finalize", "hvd_rank",
+    "hvd_size", "hvd_local_ranks", "hvd_allreduce", "hvd_allreduce_average", "hvd_allreduce_buffer",
+    "hvd_fusion_buffer", "hvd_fusion_capacity", "hvd_broadcast", "hvd_allgather", "hvd_poll_error",
+    "hvd_strerror", "hvd_traffic", "hvd_set_config", "hvd_get_config", "hvd_plan", "hvd_chunk_bounds",
+    "hvd_kernel_stats",
+])
+
+
+def strerror(status: int) -> str:
+    return lib.hvd_strerror(int(status)).decode()
+
+
+def check(status: int, what: str = "") -> int:
+    if status != HVD_OK:
+        raise HvdError(status, what)
+    return status

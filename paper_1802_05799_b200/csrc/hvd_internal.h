@@ -1,0 +1,104 @@
+// Internal types shared by the host runtime (hvd_runtime.cpp) and the
+// sm_100a kernels (hvd_kernels.cu).  Not part of the ABI (include/hvd.h is).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace hvd {
+
+constexpr int kMaxLocal = 8;        // virtual ranks per comm (one launch spans them all)
+constexpr int kMaxChannels = 64;    // ring CTAs per rank
+constexpr int kMemberAlign = 16;    // fusion-buffer member alignment, bytes (R2)
+constexpr int kChunkQuantum = 256;  // chunk-boundary quantum, bytes (R2)
+constexpr int kPackVecBytes = 16;   // pack/unpack vector (== kMemberAlign, so a vector never
+                                    // spans two members)
+
+inline int elem_size(int dtype) {
+  switch (dtype) {
+    case 1: return 4;  // HVD_FLOAT32
+    case 2: return 2;  // HVD_BFLOAT16
+    case 3: return 4;  // HVD_INT32
+    case 4: return 8;  // HVD_INT64
+    default: return 0;
+  }
+}
+
+// ---------------------------------------------------------------- ring kernel
+// One ring rank as seen by the kernel: its own buffers and its successor's.
+struct RingRank {
+  char* buf;                     // fusion buffer (capacity bytes)
+  char* scratch;                 // reduce-scatter receive scratch (capacity bytes)
+  unsigned long long* flags;     // [kMaxChannels] written by the predecessor
+  unsigned long long* stats;     // [2] sent bytes, sent chunk messages
+  char* nbuf;                    // successor's fusion buffer (peer / same-device)
+  char* nscratch;                // successor's scratch
+  unsigned long long* nflags;    // successor's flags
+  int rank;                      // ring rank
+  int pad;
+};
+
+enum RingMode : int {
+  kRingAllreduce = 0,   // N-1 reduce-scatter + N-1 all-gather iterations
+  kRingAllgather = 1,   // N-1 all-gather iterations, blocks of `q` elements per rank
+  kRingBroadcast = 2,   // pipelined forward root -> root+1 -> ...
+};
+
+struct RingParams {
+  RingRank rk[kMaxLocal];
+  unsigned long long base[kMaxChannels];  // signal counter value before this call
+  unsigned long long L;         // elements in the buffer
+  unsigned long long q;         // chunk length, elements (multiple of the quantum)
+  unsigned long long ch_el;     // elements per channel per chunk (multiple of the quantum)
+  unsigned long long slice_el;  // elements per pipelining slice (multiple of the quantum)
+  int N;                        // ring size
+  int K;                        // slices per channel per chunk
+  int mode;                     // RingMode
+  int root;                     // broadcast root
+  int* err;                     // host-mapped error word (device address)
+  unsigned long long timeout_ns;
+};
+
+// Signals each channel sends per call (host keeps the per-channel base in step).
+inline unsigned long long ring_signals(int mode, int N, int K) {
+  if (N <= 1) return 0;
+  if (mode == kRingAllreduce) return 2ull * (N - 1) * K;
+  return 1ull * (N - 1) * K;
+}
+
+// ---------------------------------------------------------------- pack / unpack
+struct PackSeg {
+  unsigned long long dst_off;   // element offset in the fusion buffer (16 B aligned)
+  unsigned long long count;     // elements
+  unsigned long long vbeg;      // first 16 B vector of the member in the buffer
+  unsigned long long pad;
+};
+
+struct PackParams {
+  const PackSeg* segs;          // [nseg]
+  char* const* src;             // [nlocal * nseg] tensor addresses (already + src_off)
+  const int* tile_seg;          // [ntiles + 1] segment of each tile's first vector (+ last)
+  char* buf[kMaxLocal];         // fusion buffer per local rank
+  unsigned long long nvec;      // 16 B vectors in the buffer
+  unsigned long long tile_vecs; // vectors per tile
+  unsigned long long ntiles;
+  int nseg;
+  int scale_on;                 // 1: multiply by `scale` (AVERAGE)
+  float scale;                  // fl32(1/N)
+  int pad;
+};
+
+// Launchers (hvd_kernels.cu).  All return a cudaError_t.
+cudaError_t launch_pack(const PackParams& p, int dtype, int nlocal, int grid, int threads,
+                        cudaStream_t s);
+cudaError_t launch_unpack(const PackParams& p, int dtype, int nlocal, int grid, int threads,
+                          cudaStream_t s);
+cudaError_t launch_scale(char* const* bufs, int nlocal, unsigned long long count, int dtype,
+                         float scale, int grid, int threads, cudaStream_t s);
+cudaError_t launch_ring(const RingParams& p, int dtype, int nch, int nlocal, int threads,
+                        cudaStream_t s);
+cudaError_t ring_max_ctas_per_sm(int dtype, int threads, int* out);
+
+}  // namespace hvd

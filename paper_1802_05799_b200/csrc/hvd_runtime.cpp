@@ -1,0 +1,650 @@
+// Host runtime behind the C ABI (include/hvd.h): communicator, buffers, CUDA-IPC
+// peer mapping, plan cache with device-resident segment tables, and the
+// stream-ordered enqueue of pack -> ring -> unpack per fusion buffer
+// (§7 steps 2-6).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <list>
+#include <vector>
+
+#include <unistd.h>
+
+#include "../../include/hvd.h"
+#include "hvd_internal.h"
+#include "hvd_plan.h"
+
+using namespace hvd;
+
+namespace {
+
+constexpr uint64_t kDefaultFusionBytes = 64ull << 20;  // P:L368-369 "Default ... 64 MB" (R9)
+constexpr uint64_t kTailBytes = 4096;                   // flags + stats after buf and scratch
+constexpr uint32_t kBlobMagic = 0x48564442u;            // "HVDB"
+constexpr int kPackThreads = 256;
+constexpr int kPackVecsPerThread = 8;
+constexpr size_t kPlanCacheSize = 8;
+
+struct Blob {
+  uint32_t magic;
+  int32_t version;
+  int32_t rank, size, device, pid;
+  uint64_t capacity;
+  uint64_t region_bytes;
+  cudaIpcMemHandle_t handle;
+};
+
+struct DevPlanBuffer {
+  int dtype;
+  uint64_t L;
+  PackParams pp;  // device pointers filled in
+};
+
+struct CachedPlan {
+  std::vector<uint64_t> key;
+  std::vector<DevPlanBuffer> bufs;
+  void* dmem = nullptr;
+  void* hmem = nullptr;
+};
+
+}  // namespace
+
+struct hvd_comm {
+  int rank = 0, size = 1, device = 0, nlocal = 1;
+  bool virt = false, connected = false, closed = false;
+  uint64_t cap = 0;
+  char* region[kMaxLocal] = {};
+  char* peer_region = nullptr;   // successor's region (IPC mapped), real mode
+  char* pred_region = nullptr;   // predecessor's region (IPC mapped), real mode
+  RingRank rk[kMaxLocal] = {};
+  unsigned long long base[kMaxChannels] = {};
+  int* err_host = nullptr;
+  int* err_dev = nullptr;
+  int sm_count = 148;
+  // tuning (hvd_set_config)
+  int channels = 32;
+  int64_t slice_bytes = 256 << 10;
+  int threads = 512;
+  int64_t timeout_ms = 30000;
+  int pack_ctas_per_sm = 8;
+  int profile = 0;
+  std::list<CachedPlan> cache;
+  // launch statistics (hvd_kernel_stats)
+  uint64_t launches[HVD_KERNEL_KINDS] = {};
+  struct Timed { int kind; cudaEvent_t a, b; };
+  std::vector<Timed> timed;
+  std::vector<cudaEvent_t> event_pool;
+};
+
+namespace {
+
+int cuda_fail(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return HVD_OK;
+  std::fprintf(stderr, "[hvd] %s: %s\n", what, cudaGetErrorString(e));
+  return HVD_ERR_CUDA;
+}
+#define CK(call)                                    \
+  do {                                              \
+    int _st = cuda_fail((call), #call);             \
+    if (_st != HVD_OK) return _st;                  \
+  } while (0)
+
+char* buf_of(char* region) { return region; }
+char* scratch_of(char* region, uint64_t cap) { return region + cap; }
+unsigned long long* flags_of(char* region, uint64_t cap) {
+  return reinterpret_cast<unsigned long long*>(region + 2 * cap);
+}
+unsigned long long* stats_of(char* region, uint64_t cap) {
+  return reinterpret_cast<unsigned long long*>(region + 2 * cap + kMaxChannels * 8);
+}
+
+int common_init(hvd_comm* c, uint64_t fusion_bytes) {
+  c->cap = ((fusion_bytes ? fusion_bytes : kDefaultFusionBytes) + 4095) / 4096 * 4096;
+  CK(cudaSetDevice(c->device));
+  CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device));
+  CK(cudaHostAlloc(reinterpret_cast<void**>(&c->err_host), sizeof(int), cudaHostAllocMapped));
+  *c->err_host = 0;
+  CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->err_dev), c->err_host, 0));
+  const uint64_t region_bytes = 2 * c->cap + kTailBytes;
+  for (int l = 0; l < c->nlocal; ++l) {
+    CK(cudaMalloc(reinterpret_cast<void**>(&c->region[l]), region_bytes));
+    CK(cudaMemset(c->region[l] + 2 * c->cap, 0, kTailBytes));
+    RingRank& r = c->rk[l];
+    r.buf = buf_of(c->region[l]);
+    r.scratch = scratch_of(c->region[l], c->cap);
+    r.flags = flags_of(c->region[l], c->cap);
+    r.stats = stats_of(c->region[l], c->cap);
+    r.rank = c->virt ? l : c->rank;
+  }
+  CK(cudaDeviceSynchronize());
+  return HVD_OK;
+}
+
+void set_successor(RingRank& r, char* succ_region, uint64_t cap) {
+  r.nbuf = buf_of(succ_region);
+  r.nscratch = scratch_of(succ_region, cap);
+  r.nflags = flags_of(succ_region, cap);
+}
+
+int check_live(hvd_comm* c) {
+  if (!c) return HVD_ERR_INVALID;
+  if (c->closed) return HVD_ERR_CLOSED;
+  if (*c->err_host != 0) return *c->err_host;
+  if (c->size > 1 && !c->connected) return HVD_ERR_NOT_CONNECTED;
+  return HVD_OK;
+}
+
+// ------------------------------------------------------------------ plan cache
+void free_plan(CachedPlan& p) {
+  if (p.dmem) cudaFree(p.dmem);
+  if (p.hmem) cudaFreeHost(p.hmem);
+  p.dmem = p.hmem = nullptr;
+}
+
+size_t align256(size_t v) { return (v + 255) / 256 * 256; }
+
+// Build (or fetch) the device-resident pack/unpack tables of the plan of the
+// tensor list `t` (n per local rank).  The key is every tensor's address,
+// count and dtype plus the threshold, so repeated calls on the same gradient
+// tensors (the training loop) reuse the uploaded tables.
+int get_plan(hvd_comm* c, const hvd_tensor* t, int n, uint64_t threshold, cudaStream_t s,
+             CachedPlan** out) {
+  std::vector<uint64_t> key;
+  key.reserve(3 + 3 * (size_t)n * c->nlocal);
+  key.push_back(threshold);
+  key.push_back((uint64_t)n);
+  key.push_back((uint64_t)c->nlocal);
+  for (int i = 0; i < n * c->nlocal; ++i) {
+    key.push_back(reinterpret_cast<uint64_t>(t[i].data));
+    key.push_back(t[i].count);
+    key.push_back((uint64_t)t[i].dtype);
+  }
+  for (auto it = c->cache.begin(); it != c->cache.end(); ++it) {
+    if (it->key == key) {
+      c->cache.splice(c->cache.begin(), c->cache, it);
+      *out = &c->cache.front();
+      return HVD_OK;
+    }
+  }
+  std::vector<uint64_t> counts(n);
+  std::vector<int32_t> dtypes(n);
+  for (int k = 0; k < n; ++k) {
+    counts[k] = t[k].count;
+    dtypes[k] = t[k].dtype;
+  }
+  std::vector<hvd_plan_entry> ents;
+  std::vector<hvd_plan_buffer> bufs;
+  int st = build_plan(counts.data(), dtypes.data(), n, threshold, c->cap, &ents, &bufs);
+  if (st != HVD_OK) return st;
+
+  // layout: per buffer [segs][src table][tile_seg]
+  struct Off { size_t segs, src, tiles; uint64_t nvec, ntiles; };
+  std::vector<Off> offs(bufs.size());
+  const uint64_t tile_vecs = (uint64_t)kPackThreads * kPackVecsPerThread;
+  size_t total = 0;
+  for (size_t b = 0; b < bufs.size(); ++b) {
+    const int esz = elem_size(bufs[b].dtype);
+    const uint64_t vel = kPackVecBytes / esz;
+    offs[b].nvec = (bufs[b].length + vel - 1) / vel;
+    offs[b].ntiles = (offs[b].nvec + tile_vecs - 1) / tile_vecs;
+    offs[b].segs = total;
+    total = align256(total + sizeof(PackSeg) * bufs[b].n_entries);
+    offs[b].src = total;
+    total = align256(total + sizeof(char*) * bufs[b].n_entries * c->nlocal);
+    offs[b].tiles = total;
+    total = align256(total + sizeof(int) * (offs[b].ntiles + 1));
+  }
+  CachedPlan p;
+  p.key = std::move(key);
+  if (total) {
+    CK(cudaMallocHost(&p.hmem, total));
+    if (cudaMalloc(&p.dmem, total) != cudaSuccess) {
+      free_plan(p);
+      return HVD_ERR_CUDA;
+    }
+  }
+  char* h = static_cast<char*>(p.hmem);
+  char* d = static_cast<char*>(p.dmem);
+  for (size_t b = 0; b < bufs.size(); ++b) {
+    const hvd_plan_buffer& pb = bufs[b];
+    const int esz = elem_size(pb.dtype);
+    const uint64_t vel = kPackVecBytes / esz;
+    PackSeg* segs = reinterpret_cast<PackSeg*>(h + offs[b].segs);
+    char** src = reinterpret_cast<char**>(h + offs[b].src);
+    int* tiles = reinterpret_cast<int*>(h + offs[b].tiles);
+    for (int j = 0; j < pb.n_entries; ++j) {
+      const hvd_plan_entry& e = ents[pb.first_entry + j];
+      segs[j].dst_off = e.dst_off;
+      segs[j].count = e.count;
+      segs[j].vbeg = e.dst_off / vel;
+      segs[j].pad = 0;
+      for (int l = 0; l < c->nlocal; ++l)
+        src[(size_t)l * pb.n_entries + j] =
+            static_cast<char*>(t[(size_t)l * n + e.tensor].data) + e.src_off * esz;
+    }
+    // tile -> member of its first vector (merge walk); last entry = last member
+    int sidx = 0;
+    for (uint64_t tile = 0; tile < offs[b].ntiles; ++tile) {
+      const uint64_t v = tile * tile_vecs;
+      while (sidx + 1 < pb.n_entries && segs[sidx + 1].vbeg <= v) ++sidx;
+      tiles[tile] = sidx;
+    }
+    tiles[offs[b].ntiles] = pb.n_entries - 1;
+    DevPlanBuffer db;
+    db.dtype = pb.dtype;
+    db.L = pb.length;
+    std::memset(&db.pp, 0, sizeof(db.pp));
+    db.pp.segs = reinterpret_cast<const PackSeg*>(d + offs[b].segs);
+    db.pp.src = reinterpret_cast<char* const*>(d + offs[b].src);
+    db.pp.tile_seg = reinterpret_cast<const int*>(d + offs[b].tiles);
+    for (int l = 0; l < c->nlocal; ++l) db.pp.buf[l] = c->rk[l].buf;
+    db.pp.nvec = offs[b].nvec;
+    db.pp.tile_vecs = tile_vecs;
+    db.pp.ntiles = offs[b].ntiles;
+    db.pp.nseg = pb.n_entries;
+    p.bufs.push_back(db);
+  }
+  if (total) {
+    if (cudaMemcpyAsync(p.dmem, p.hmem, total, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+      free_plan(p);
+      return HVD_ERR_CUDA;
+    }
+  }
+  if (c->cache.size() >= kPlanCacheSize) {
+    cudaStreamSynchronize(s);  // the evicted tables may still be in use on the stream
+    free_plan(c->cache.back());
+    c->cache.pop_back();
+  }
+  c->cache.push_front(std::move(p));
+  *out = &c->cache.front();
+  return HVD_OK;
+}
+
+// ------------------------------------------------------------------ launch accounting
+cudaEvent_t pool_event(hvd_comm* c) {
+  if (!c->event_pool.empty()) {
+    cudaEvent_t e = c->event_pool.back();
+    c->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Wraps one kernel launch: counts it and, when profiling, brackets it with events.
+template <class F>
+int launch_counted(hvd_comm* c, int kind, cudaStream_t s, F&& launch) {
+  hvd_comm::Timed t = {kind, nullptr, nullptr};
+  if (c->profile) {
+    t.a = pool_event(c);
+    t.b = pool_event(c);
+    CK(cudaEventRecord(t.a, s));
+  }
+  CK(launch());
+  c->launches[kind] += 1;
+  if (c->profile) {
+    CK(cudaEventRecord(t.b, s));
+    c->timed.push_back(t);
+  }
+  return HVD_OK;
+}
+
+// ------------------------------------------------------------------ ring enqueue
+// Split one buffer of L elements for the ring kernel and launch it.
+int enqueue_ring(hvd_comm* c, uint64_t L, int dtype, cudaStream_t s) {
+  if (c->size <= 1 || L == 0) return HVD_OK;
+  const int esz = elem_size(dtype);
+  const uint64_t g = kChunkQuantum / esz;
+  RingParams P;
+  std::memset(&P, 0, sizeof(P));
+  for (int l = 0; l < c->nlocal; ++l) P.rk[l] = c->rk[l];
+  P.N = c->size;
+  P.L = L;
+  P.q = chunk_len(L, c->size, dtype);
+  // channels: at least 32 KiB of every chunk per channel, at most the knob and
+  // what stays co-resident (the CTAs of all ranks wait on each other)
+  int max_per_sm = 1;
+  CK(ring_max_ctas_per_sm(dtype, c->threads, &max_per_sm));
+  const int resident = std::max(1, c->sm_count * max_per_sm / c->nlocal);
+  const uint64_t qbytes = P.q * esz;
+  int nch = (int)std::min<uint64_t>((uint64_t)c->channels, std::max<uint64_t>(1, qbytes / (32 << 10)));
+  nch = std::min(nch, std::min(resident, kMaxChannels));
+  P.ch_el = (P.q + (uint64_t)nch * g - 1) / ((uint64_t)nch * g) * g;
+  uint64_t slice_el = std::max<uint64_t>(g, (uint64_t)c->slice_bytes / esz / g * g);
+  P.slice_el = std::min<uint64_t>(slice_el, P.ch_el);
+  P.K = (int)((P.ch_el + P.slice_el - 1) / P.slice_el);
+  P.mode = kRingAllreduce;
+  P.err = c->err_dev;
+  P.timeout_ns = (unsigned long long)c->timeout_ms * 1000000ull;
+  for (int ch = 0; ch < kMaxChannels; ++ch) P.base[ch] = c->base[ch];
+  int st = launch_counted(c, HVD_KERNEL_RING, s, [&] { return launch_ring(P, dtype, nch, c->nlocal, c->threads, s); });
+  if (st != HVD_OK) return st;
+  const unsigned long long inc = ring_signals(kRingAllreduce, c->size, P.K);
+  for (int ch = 0; ch < nch; ++ch) c->base[ch] += inc;
+  return HVD_OK;
+}
+
+int pack_grid(hvd_comm* c) { return c->sm_count * c->pack_ctas_per_sm / c->nlocal + 1; }
+
+int do_allreduce(hvd_comm* c, const hvd_tensor* t, int n, int op, uint64_t threshold, cudaStream_t s) {
+  int st = check_live(c);
+  if (st != HVD_OK) return st;
+  if (n < 0 || (n > 0 && !t)) return HVD_ERR_INVALID;
+  if (op != HVD_SUM && op != HVD_AVERAGE) return HVD_ERR_INVALID;
+  for (int k = 0; k < n; ++k) {
+    if (elem_size(t[k].dtype) == 0) return HVD_ERR_UNSUPPORTED;
+    if (op == HVD_AVERAGE && (t[k].dtype == HVD_INT32 || t[k].dtype == HVD_INT64)) return HVD_ERR_UNSUPPORTED;
+    for (int l = 0; l < c->nlocal; ++l) {
+      const hvd_tensor& x = t[(size_t)l * n + k];
+      if (x.count != t[k].count || x.dtype != t[k].dtype) return HVD_ERR_INVALID;
+      if (x.count && !x.data) return HVD_ERR_INVALID;
+    }
+  }
+  if (n == 0) return HVD_OK;
+  CK(cudaSetDevice(c->device));
+  CachedPlan* plan = nullptr;
+  st = get_plan(c, t, n, threshold, s, &plan);
+  if (st != HVD_OK) return st;
+  const float scale = 1.0f / (float)c->size;  // s = fl32(1/N) (R1)
+  for (DevPlanBuffer& b : plan->bufs) {       // step 6: repeat per fusion buffer
+    b.pp.scale = scale;
+    b.pp.scale_on = op == HVD_AVERAGE ? 1 : 0;
+    st = launch_counted(c, HVD_KERNEL_PACK, s, [&] {                          // step 3
+      return launch_pack(b.pp, b.dtype, c->nlocal, pack_grid(c), kPackThreads, s);
+    });
+    if (st != HVD_OK) return st;
+    st = enqueue_ring(c, b.L, b.dtype, s);                                    // step 4
+    if (st != HVD_OK) return st;
+    st = launch_counted(c, HVD_KERNEL_UNPACK, s, [&] {                        // step 5
+      return launch_unpack(b.pp, b.dtype, c->nlocal, pack_grid(c), kPackThreads, s);
+    });
+    if (st != HVD_OK) return st;
+  }
+  return HVD_OK;
+}
+
+}  // namespace
+
+// ================================================================== C ABI
+extern "C" {
+
+int hvd_init(int rank, int size, int device, uint64_t fusion_bytes, hvd_comm** out) {
+  if (!out || size < 1 || rank < 0 || rank >= size || device < 0) return HVD_ERR_INVALID;
+  *out = nullptr;
+  hvd_comm* c = new hvd_comm();
+  c->rank = rank;
+  c->size = size;
+  c->device = device;
+  c->nlocal = 1;
+  c->virt = false;
+  int st = common_init(c, fusion_bytes);
+  if (st != HVD_OK) {
+    hvd_finalize(c);
+    return st;
+  }
+  if (size == 1) {
+    set_successor(c->rk[0], c->region[0], c->cap);
+    c->connected = true;
+  }
+  *out = c;
+  return HVD_OK;
+}
+
+int hvd_init_virtual(int size, int device, uint64_t fusion_bytes, hvd_comm** out) {
+  if (!out || size < 1 || size > kMaxLocal || device < 0) return HVD_ERR_INVALID;
+  *out = nullptr;
+  hvd_comm* c = new hvd_comm();
+  c->rank = 0;
+  c->size = size;
+  c->device = device;
+  c->nlocal = size;
+  c->virt = true;
+  int st = common_init(c, fusion_bytes);
+  if (st != HVD_OK) {
+    hvd_finalize(c);
+    return st;
+  }
+  for (int l = 0; l < size; ++l) set_successor(c->rk[l], c->region[(l + 1) % size], c->cap);
+  c->connected = true;
+  *out = c;
+  return HVD_OK;
+}
+
+int hvd_get_ipc_blob(hvd_comm* c, void* out, uint64_t* len) {
+  if (!c || !len) return HVD_ERR_INVALID;
+  if (c->closed) return HVD_ERR_CLOSED;
+  if (!out) {
+    *len = sizeof(Blob);
+    return HVD_OK;
+  }
+  if (*len < sizeof(Blob) || c->virt) return HVD_ERR_INVALID;
+  Blob b;
+  std::memset(&b, 0, sizeof(b));
+  b.magic = kBlobMagic;
+  b.version = HVD_ABI_VERSION;
+  b.rank = c->rank;
+  b.size = c->size;
+  b.device = c->device;
+  b.pid = (int32_t)getpid();
+  b.capacity = c->cap;
+  b.region_bytes = 2 * c->cap + kTailBytes;
+  CK(cudaSetDevice(c->device));
+  CK(cudaIpcGetMemHandle(&b.handle, c->region[0]));
+  std::memcpy(out, &b, sizeof(b));
+  *len = sizeof(Blob);
+  return HVD_OK;
+}
+
+int hvd_connect(hvd_comm* c, const void* blobs, uint64_t len_each) {
+  if (!c || !blobs || len_each < sizeof(Blob)) return HVD_ERR_INVALID;
+  if (c->closed) return HVD_ERR_CLOSED;
+  if (c->virt || c->size == 1) return HVD_OK;
+  const char* p = static_cast<const char*>(blobs);
+  for (int r = 0; r < c->size; ++r) {
+    Blob b;
+    std::memcpy(&b, p + (size_t)r * len_each, sizeof(b));
+    if (b.magic != kBlobMagic || b.version != HVD_ABI_VERSION || b.rank != r || b.size != c->size ||
+        b.capacity != c->cap)
+      return HVD_ERR_INVALID;
+  }
+  CK(cudaSetDevice(c->device));
+  const int succ = (c->rank + 1) % c->size;
+  const int pred = (c->rank + c->size - 1) % c->size;
+  Blob bs, bp;
+  std::memcpy(&bs, p + (size_t)succ * len_each, sizeof(bs));
+  std::memcpy(&bp, p + (size_t)pred * len_each, sizeof(bp));
+  void* ptr = nullptr;
+  CK(cudaIpcOpenMemHandle(&ptr, bs.handle, cudaIpcMemLazyEnablePeerAccess));
+  c->peer_region = static_cast<char*>(ptr);
+  if (pred != succ) {
+    CK(cudaIpcOpenMemHandle(&ptr, bp.handle, cudaIpcMemLazyEnablePeerAccess));
+    c->pred_region = static_cast<char*>(ptr);
+  } else {
+    c->pred_region = c->peer_region;
+  }
+  set_successor(c->rk[0], c->peer_region, c->cap);
+  c->connected = true;
+  return HVD_OK;
+}
+
+int hvd_finalize(hvd_comm* c) {
+  if (!c) return HVD_OK;
+  if (!c->closed) {
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    for (auto& p : c->cache) free_plan(p);
+    for (auto& t : c->timed) {
+      cudaEventDestroy(t.a);
+      cudaEventDestroy(t.b);
+    }
+    for (auto e : c->event_pool) cudaEventDestroy(e);
+    c->cache.clear();
+    if (c->peer_region) cudaIpcCloseMemHandle(c->peer_region);
+    if (c->pred_region && c->pred_region != c->peer_region) cudaIpcCloseMemHandle(c->pred_region);
+    for (int l = 0; l < kMaxLocal; ++l)
+      if (c->region[l]) cudaFree(c->region[l]);
+    if (c->err_host) cudaFreeHost(c->err_host);
+    c->closed = true;
+  }
+  delete c;
+  return HVD_OK;
+}
+
+int hvd_rank(const hvd_comm* c) { return c ? c->rank : -1; }
+int hvd_size(const hvd_comm* c) { return c ? c->size : -1; }
+int hvd_local_ranks(const hvd_comm* c) { return c ? c->nlocal : -1; }
+
+int hvd_allreduce(hvd_comm* c, const hvd_tensor* t, int n, int op, uint64_t fusion_threshold, void* stream) {
+  return do_allreduce(c, t, n, op, fusion_threshold, static_cast<cudaStream_t>(stream));
+}
+
+int hvd_allreduce_average(hvd_comm* c, const hvd_tensor* t, int n, uint64_t fusion_threshold, void* stream) {
+  return do_allreduce(c, t, n, HVD_AVERAGE, fusion_threshold, static_cast<cudaStream_t>(stream));
+}
+
+int hvd_allreduce_buffer(hvd_comm* c, uint64_t count, int dtype, int op, void* stream) {
+  int st = check_live(c);
+  if (st != HVD_OK) return st;
+  const int esz = elem_size(dtype);
+  if (esz == 0) return HVD_ERR_UNSUPPORTED;
+  if (op != HVD_SUM && op != HVD_AVERAGE) return HVD_ERR_INVALID;
+  if (op == HVD_AVERAGE && (dtype == HVD_INT32 || dtype == HVD_INT64)) return HVD_ERR_UNSUPPORTED;
+  if (count > c->cap / esz) return HVD_ERR_INVALID;
+  if (count == 0) return HVD_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(c->device));
+  if (op == HVD_AVERAGE) {
+    char* bufs[kMaxLocal];
+    for (int l = 0; l < c->nlocal; ++l) bufs[l] = c->rk[l].buf;
+    st = launch_counted(c, HVD_KERNEL_SCALE, s, [&] {
+      return launch_scale(bufs, c->nlocal, count, dtype, 1.0f / (float)c->size, pack_grid(c), kPackThreads, s);
+    });
+    if (st != HVD_OK) return st;
+  }
+  return enqueue_ring(c, count, dtype, s);
+}
+
+void* hvd_fusion_buffer(hvd_comm* c, int local) {
+  if (!c || c->closed || local < 0 || local >= c->nlocal) return nullptr;
+  return c->rk[local].buf;
+}
+
+uint64_t hvd_fusion_capacity(const hvd_comm* c) { return c ? c->cap : 0; }
+
+int hvd_broadcast(hvd_comm* c, const hvd_tensor* t, int n, int root, void* stream) {
+  (void)t; (void)n; (void)stream;
+  int st = check_live(c);
+  if (st != HVD_OK) return st;
+  if (root < 0 || root >= c->size) return HVD_ERR_INVALID;
+  return HVD_ERR_UNSUPPORTED;  // ring broadcast: next milestone
+}
+
+int hvd_allgather(hvd_comm* c, const hvd_tensor* in, const hvd_tensor* out, void* stream) {
+  (void)in; (void)out; (void)stream;
+  int st = check_live(c);
+  if (st != HVD_OK) return st;
+  return HVD_ERR_UNSUPPORTED;  // ring allgather: next milestone
+}
+
+int hvd_poll_error(hvd_comm* c) {
+  if (!c) return HVD_ERR_INVALID;
+  if (c->closed) return HVD_ERR_CLOSED;
+  return *c->err_host;
+}
+
+const char* hvd_strerror(int status) {
+  switch (status) {
+    case HVD_OK: return "ok";
+    case HVD_ERR_INVALID: return "invalid argument";
+    case HVD_ERR_UNSUPPORTED: return "unsupported dtype/op combination";
+    case HVD_ERR_CUDA: return "CUDA runtime error";
+    case HVD_ERR_NOT_CONNECTED: return "communicator not connected";
+    case HVD_ERR_TIMEOUT: return "device watchdog timeout (a peer did not signal)";
+    case HVD_ERR_CLOSED: return "communicator finalized";
+    default: return "unknown status";
+  }
+}
+
+int hvd_traffic(hvd_comm* c, int local, uint64_t* sent_bytes, uint64_t* sends) {
+  if (!c || local < 0 || local >= c->nlocal || !sent_bytes || !sends) return HVD_ERR_INVALID;
+  if (c->closed) return HVD_ERR_CLOSED;
+  unsigned long long v[2];
+  CK(cudaSetDevice(c->device));
+  CK(cudaMemcpy(v, c->rk[local].stats, sizeof(v), cudaMemcpyDeviceToHost));
+  *sent_bytes = v[0];
+  *sends = v[1];
+  return HVD_OK;
+}
+
+int hvd_set_config(hvd_comm* c, int key, int64_t value) {
+  if (!c) return HVD_ERR_INVALID;
+  switch (key) {
+    case HVD_CFG_CHANNELS:
+      if (value < 1 || value > kMaxChannels) return HVD_ERR_INVALID;
+      c->channels = (int)value;
+      return HVD_OK;
+    case HVD_CFG_SLICE_BYTES:
+      if (value < kChunkQuantum || value % kChunkQuantum) return HVD_ERR_INVALID;
+      c->slice_bytes = value;
+      return HVD_OK;
+    case HVD_CFG_THREADS:
+      if (value < 128 || value > 512 || value % 32) return HVD_ERR_INVALID;
+      c->threads = (int)value;
+      return HVD_OK;
+    case HVD_CFG_TIMEOUT_MS:
+      if (value < 1) return HVD_ERR_INVALID;
+      c->timeout_ms = value;
+      return HVD_OK;
+    case HVD_CFG_PACK_CTAS_PER_SM:
+      if (value < 1 || value > 8) return HVD_ERR_INVALID;
+      c->pack_ctas_per_sm = (int)value;
+      return HVD_OK;
+    case HVD_CFG_PROFILE:
+      if (value != 0 && value != 1) return HVD_ERR_INVALID;
+      c->profile = (int)value;
+      return HVD_OK;
+    default: return HVD_ERR_INVALID;
+  }
+}
+
+int64_t hvd_get_config(const hvd_comm* c, int key) {
+  if (!c) return -1;
+  switch (key) {
+    case HVD_CFG_CHANNELS: return c->channels;
+    case HVD_CFG_SLICE_BYTES: return c->slice_bytes;
+    case HVD_CFG_THREADS: return c->threads;
+    case HVD_CFG_TIMEOUT_MS: return c->timeout_ms;
+    case HVD_CFG_PACK_CTAS_PER_SM: return c->pack_ctas_per_sm;
+    case HVD_CFG_PROFILE: return c->profile;
+    default: return -1;
+  }
+}
+
+int hvd_kernel_stats(hvd_comm* c, uint64_t* launches, double* device_ms) {
+  if (!c || !launches || !device_ms) return HVD_ERR_INVALID;
+  if (c->closed) return HVD_ERR_CLOSED;
+  for (int k = 0; k < HVD_KERNEL_KINDS; ++k) {
+    launches[k] = c->launches[k];
+    device_ms[k] = 0.0;
+    c->launches[k] = 0;
+  }
+  int st = HVD_OK;
+  for (auto& t : c->timed) {
+    float ms = 0.f;
+    if (st == HVD_OK && cudaEventSynchronize(t.b) == cudaSuccess &&
+        cudaEventElapsedTime(&ms, t.a, t.b) == cudaSuccess)
+      device_ms[t.kind] += ms;
+    else
+      st = HVD_ERR_CUDA;
+    c->event_pool.push_back(t.a);
+    c->event_pool.push_back(t.b);
+  }
+  c->timed.clear();
+  return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,112 @@
+"""Real multi-process ring over NVLink: one process per GPU, CUDA-IPC peers.
+
+Runs only with >= 2 visible GPUs (``gpurun --gpus 2|4``).  Each rank runs the
+collective on its seeded inputs; the parent compares every rank's output with
+the oracle element by element and checks cross-rank bitwise agreement.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+from hvd_testutil import HVD_CODE, assert_same, from_torch, to_torch
+
+torch = pytest.importorskip("torch")
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, cases, q):
+    os.environ.update(RANK=str(rank), WORLD_SIZE=str(world), LOCAL_RANK=str(rank),
+                      MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import paper_1802_05799_b200 as hvd
+    try:
+        comm = hvd.init()
+        comm.set_config(hvd._lib.HVD_CFG_TIMEOUT_MS, 20000)
+        out = []
+        for case in cases:
+            kind, counts, dtype, op, thr = case
+            if kind == "tensors":
+                xs = [workloads.rank_tensor(c, dtype, rank, k,
+                                            "normal" if dtype in ("f32", "bf16") else "int_uniform")
+                      for k, c in enumerate(counts)]
+                ts = [to_torch(x, dtype) for x in xs]
+                comm.allreduce(ts, op=op, fusion_threshold=thr)
+                torch.cuda.synchronize()
+                out.append([from_torch(t, dtype) for t in ts])
+            else:  # raw buffer
+                L = counts[0]
+                x = workloads.rank_tensor(L, dtype, rank, 9, "normal" if dtype in ("f32", "bf16") else "int_uniform")
+                tdt = {"f32": torch.float32, "bf16": torch.bfloat16, "i32": torch.int32, "i64": torch.int64}[dtype]
+                comm.fusion_buffer(0, tdt, L).copy_(to_torch(x, dtype))
+                sent0 = comm.traffic()
+                comm.allreduce_buffer(L, HVD_CODE[dtype], op)
+                torch.cuda.synchronize()
+                sent1 = comm.traffic()
+                out.append([from_torch(comm.fusion_buffer(0, tdt, L), dtype),
+                            np.array([sent1[0] - sent0[0], sent1[1] - sent0[1]])])
+        q.put((rank, out, comm.poll_error()))
+        import torch.distributed as dist
+        dist.barrier()
+        comm.finalize()
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e), -99))
+
+
+CASES = [
+    ("tensors", [1, 3, 64, 1000, 4097, 100_003, 7, 262_149, 33], "f32", "average", 1 << 20),
+    ("tensors", [5, 1 << 20, 12345], "bf16", "average", 64 << 20),
+    ("tensors", [5, 1000, 77_777], "i64", "sum", 0),
+    ("tensors", [3, 70_001], "i32", "sum", 64 << 20),
+    ("buffer", [16 << 20], "f32", "sum", 0),
+    ("buffer", [(1 << 20) + 3], "bf16", "average", 0),
+]
+
+
+def test_multiprocess_ring_matches_oracle():
+    n = min(torch.cuda.device_count(), 4)
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, n, port, CASES, q)) for r in range(n)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(n):
+        rank, out, err = q.get(timeout=600)
+        res[rank] = (out, err)
+    for p in procs:
+        p.join(timeout=120)
+    for r in range(n):
+        assert res[r][1] == 0, res[r]
+    for ci, (kind, counts, dtype, op, thr) in enumerate(CASES):
+        if kind == "tensors":
+            kd = "normal" if dtype in ("f32", "bf16") else "int_uniform"
+            xs = [[workloads.rank_tensor(c, dtype, r, k, kd) for k, c in enumerate(counts)] for r in range(n)]
+            ref, _, _ = oracle.allreduce(xs, [dtype] * len(counts), op, threshold=thr)
+            for r in range(n):
+                for k in range(len(counts)):
+                    assert_same(res[r][0][ci][k], ref[r][k], dtype, f"case {ci} rank {r} tensor {k}")
+        else:
+            L = counts[0]
+            kd = "normal" if dtype in ("f32", "bf16") else "int_uniform"
+            xs = [workloads.rank_tensor(L, dtype, r, 9, kd) for r in range(n)]
+            ref, tr = oracle.allreduce_buffer(xs, dtype, op)
+            for r in range(n):
+                assert_same(res[r][0][ci][0], ref[r], dtype, f"buffer case {ci} rank {r}")
+                sent, sends = res[r][0][ci][1]
+                assert sent == tr[r].sent_elems * oracle.ELEM_SIZE[dtype] and sends == 2 * (n - 1)

@@ -1,0 +1,220 @@
+"""GPU parity of the fused ring allreduce with N ranks simulated on one B200.
+
+``hvd_init_virtual`` runs the SAME kernels and signal protocol as the
+multi-process path (one launch spans every rank, so the ranks' CTAs are
+co-resident); "peer" buffers are same-device allocations.  Every result is
+compared element by element with the CPU oracle on the same seeded inputs
+(bit-exact: the ring order is reproduced).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+from hvd_testutil import HVD_CODE, assert_same, from_torch, to_torch
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def hvd():
+    import paper_1802_05799_b200 as m
+    return m
+
+
+_COMMS = {}
+
+
+def comm_for(hvd, n, cap=64 << 20):
+    key = (n, cap)
+    if key not in _COMMS:
+        c = hvd.init_virtual(n, 0, cap)
+        c.set_config(hvd._lib.HVD_CFG_TIMEOUT_MS, 20000)
+        _COMMS[key] = c
+    return _COMMS[key]
+
+
+def run_allreduce(hvd, xs, dtypes, op, threshold, cap=64 << 20, misalign=False):
+    n = len(xs)
+    comm = comm_for(hvd, n, cap)
+    ts = []
+    keep = []
+    for r in range(n):
+        row = []
+        for x, dt in zip(xs[r], dtypes):
+            t = to_torch(x, dt)
+            if misalign and len(x) > 0:      # a view whose data_ptr is off the 16 B grid
+                big = torch.empty(len(x) + 1, dtype=t.dtype, device="cuda")
+                big[1:].copy_(t)
+                keep.append(big)
+                t = big[1:]
+            row.append(t)
+        ts.append(row)
+    comm.allreduce(ts, op=op, fusion_threshold=threshold)
+    torch.cuda.synchronize()
+    assert comm.poll_error() == 0
+    return [[from_torch(t, dt) for t, dt in zip(ts[r], dtypes)] for r in range(n)]
+
+
+RAGGED = [1, 3, 64, 1000, 4097, 100_003, 7, 262_149, 0, 33]
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 5, 8])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_allreduce_average_bitexact(hvd, n, dtype):
+    xs = workloads.all_ranks(RAGGED, dtype, n)
+    dts = [dtype] * len(RAGGED)
+    ref, _, plan = oracle.allreduce(xs, dts, "average", threshold=400_000)
+    assert len(plan) > 1
+    got = run_allreduce(hvd, xs, dts, "average", 400_000)
+    for r in range(n):
+        for k in range(len(RAGGED)):
+            assert_same(got[r][k], ref[r][k], dtype, f"N={n} r={r} k={k}")
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 8])
+@pytest.mark.parametrize("dtype", ["i32", "i64"])
+def test_allreduce_sum_integers_exact(hvd, n, dtype):
+    xs = workloads.all_ranks(RAGGED, dtype, n, kind="int_uniform")
+    dts = [dtype] * len(RAGGED)
+    ref, _, _ = oracle.allreduce(xs, dts, "sum")
+    got = run_allreduce(hvd, xs, dts, "sum", 64 << 20)
+    for r in range(n):
+        for k in range(len(RAGGED)):
+            assert_same(got[r][k], ref[r][k], dtype, f"N={n} r={r} k={k}")
+
+
+@pytest.mark.parametrize("n", [1, 2, 4])
+def test_fusion_off_and_misaligned_tensors(hvd, n):
+    counts = [5, 17, 1024, 3, 65_537]
+    xs = workloads.all_ranks(counts, "f32", n)
+    dts = ["f32"] * len(counts)
+    ref, _, plan = oracle.allreduce(xs, dts, "average", threshold=0)
+    assert len(plan) == len(counts)
+    got = run_allreduce(hvd, xs, dts, "average", 0, misalign=True)
+    for r in range(n):
+        for k in range(len(counts)):
+            assert_same(got[r][k], ref[r][k], "f32", f"r={r} k={k}")
+
+
+@pytest.mark.parametrize("n", [2, 3, 8])
+def test_mixed_dtype_list(hvd, n):
+    counts = [100, 200, 300, 400, 5000]
+    dts = ["f32", "bf16", "f32", "bf16", "bf16"]
+    xs = [[workloads.rank_tensor(c, d, r, k) for k, (c, d) in enumerate(zip(counts, dts))] for r in range(n)]
+    ref, _, _ = oracle.allreduce(xs, dts, "average")
+    got = run_allreduce(hvd, xs, dts, "average", 64 << 20)
+    for r in range(n):
+        for k in range(len(counts)):
+            assert_same(got[r][k], ref[r][k], dts[k], f"r={r} k={k}")
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_specials_and_rank_agreement(hvd, n):
+    counts = [5000, 77]
+    for dt in ("f32", "bf16"):
+        xs = workloads.all_ranks(counts, dt, n, kind="specials")
+        ref, _, _ = oracle.allreduce(xs, [dt, dt], "average")
+        got = run_allreduce(hvd, xs, [dt, dt], "average", 64 << 20)
+        for r in range(n):
+            for k in range(2):
+                assert_same(got[r][k], ref[r][k], dt, f"{dt} r={r} k={k}")
+                assert np.array_equal(got[r][k].view(np.uint8), got[0][k].view(np.uint8))
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 8])
+def test_raw_buffer_ring_and_traffic(hvd, n):
+    comm = comm_for(hvd, n)
+    for dtype in ("f32", "bf16", "i32", "i64"):
+        esz = oracle.ELEM_SIZE[dtype]
+        for L in (1, 64 * n - 1, 1 << 16, 3_000_017 // esz):
+            kind = "normal" if dtype in ("f32", "bf16") else "int_uniform"
+            xs = [workloads.rank_tensor(L, dtype, r, 9, kind) for r in range(n)]
+            op = "average" if dtype in ("f32", "bf16") else "sum"
+            ref, tr = oracle.allreduce_buffer(xs, dtype, op)
+            before = [comm.traffic(r) for r in range(n)]
+            tdt = {"f32": torch.float32, "bf16": torch.bfloat16, "i32": torch.int32, "i64": torch.int64}[dtype]
+            for r in range(n):
+                comm.fusion_buffer(r, tdt, L).copy_(to_torch(xs[r], dtype))
+            comm.allreduce_buffer(L, HVD_CODE[dtype], op)
+            torch.cuda.synchronize()
+            for r in range(n):
+                got = from_torch(comm.fusion_buffer(r, tdt, L), dtype)
+                assert_same(got, ref[r], dtype, f"{dtype} L={L} r={r}")
+                sent, sends = comm.traffic(r)
+                assert sent - before[r][0] == tr[r].sent_elems * esz
+                assert sends - before[r][1] == tr[r].sends == 2 * (n - 1)
+
+
+def test_back_to_back_calls_varying_sizes(hvd):
+    """Monotone signal epochs: consecutive calls of different shapes, no resets."""
+    n = 4
+    comm = comm_for(hvd, n)
+    sizes = [[10], [1 << 20, 5], [3], [70_000, 70_001, 9], [1 << 22]]
+    pend = []
+    for i, counts in enumerate(sizes):
+        xs = workloads.all_ranks(counts, "f32", n, seed=1000 + i)
+        ts = [[to_torch(x, "f32") for x in xs[r]] for r in range(n)]
+        comm.allreduce_average(ts)
+        pend.append((xs, ts))
+    torch.cuda.synchronize()
+    assert comm.poll_error() == 0
+    for xs, ts in pend:
+        ref, _, _ = oracle.allreduce(xs, ["f32"] * len(xs[0]), "average")
+        for r in range(n):
+            for k in range(len(xs[0])):
+                assert_same(from_torch(ts[r][k], "f32"), ref[r][k], "f32")
+
+
+def test_tuning_knobs_keep_bits(hvd):
+    """Channels / slice / threads change the schedule of work, never the result."""
+    n = 3
+    comm = hvd.init_virtual(n, 0, 8 << 20)
+    try:
+        counts = [1_000_003, 4096]
+        xs = workloads.all_ranks(counts, "f32", n)
+        ref, _, _ = oracle.allreduce(xs, ["f32", "f32"], "average")
+        L = hvd._lib
+        for ch, sl, th in [(1, 256, 128), (7, 4096, 256), (64, 1 << 20, 512), (16, 65536, 384)]:
+            comm.set_config(L.HVD_CFG_CHANNELS, ch)
+            comm.set_config(L.HVD_CFG_SLICE_BYTES, sl)
+            comm.set_config(L.HVD_CFG_THREADS, th)
+            ts = [[to_torch(x, "f32") for x in xs[r]] for r in range(n)]
+            comm.allreduce_average(ts)
+            torch.cuda.synchronize()
+            for r in range(n):
+                for k in range(2):
+                    assert_same(from_torch(ts[r][k], "f32"), ref[r][k], "f32", f"cfg {ch},{sl},{th}")
+    finally:
+        comm.finalize()
+
+
+def test_errors_on_device(hvd):
+    comm = comm_for(hvd, 2)
+    t = [[torch.zeros(4, dtype=torch.int32, device="cuda")] for _ in range(2)]
+    with pytest.raises(hvd.HvdError) as e:
+        comm.allreduce(t, op="average")
+    assert e.value.status == hvd._lib.HVD_ERR_UNSUPPORTED
+    bad = [[torch.zeros(4, device="cuda")], [torch.zeros(5, device="cuda")]]
+    with pytest.raises(hvd.HvdError):
+        comm.allreduce(bad, op="sum")
+    with pytest.raises(hvd.HvdError):
+        comm.allreduce_buffer(comm.fusion_capacity // 4 + 1)
+    comm.allreduce([[], []])  # n = 0 is a no-op
+    assert comm.poll_error() == 0
+
+
+@pytest.mark.parametrize("model,dtype,n", [("resnet101", "f32", 4), ("inception_v3", "bf16", 2),
+                                           ("inception_v3", "f32", 8)])
+def test_model_gradient_sets_full_size(hvd, model, dtype, n):
+    """BASELINE configs at full size: every element vs the oracle."""
+    counts = [c for _, c in workloads.gradient_set(model)]
+    xs = workloads.all_ranks(counts, dtype, n)
+    dts = [dtype] * len(counts)
+    ref, _, plan = oracle.allreduce(xs, dts, "average")
+    got = run_allreduce(hvd, xs, dts, "average", 64 << 20)
+    for r in range(n):
+        for k in range(len(counts)):
+            assert_same(got[r][k], ref[r][k], dtype, f"{model} r={r} k={k}")
