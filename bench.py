@@ -160,19 +160,23 @@ def run_ours(args):
     def step(i):
         comm.allreduce_average(sets[i % nsets])
 
+    _barrier(world)
+    w0 = time.perf_counter()
     for i in range(args.warmup):
         step(i)
-    comm.kernel_stats()  # reset counters
     _barrier(world)
+    # every rank must make the same number of collective calls: the pre-load
+    # count is derived from the warm-up time and agreed on (max over ranks)
+    per_step = (time.perf_counter() - w0) / args.warmup
+    n_load = int(_max_over_ranks(min(20000.0, args.clock_window / max(per_step, 1e-6)), world))
+    comm.kernel_stats()  # reset counters
     with ClockSampler({local} if world == 1 else set(range(world))) as clk:
-        # keep the GPU busy ~1 s so the sampler sees clocks under load, then time K steps
-        t_end = time.time() + args.clock_window
-        i = 0
-        while time.time() < t_end:
+        # keep the GPU busy ~clock_window s so the sampler sees clocks under load, then time K steps
+        for i in range(n_load):
             step(i)
-            i += 1
-            if i % 64 == 0:
+            if i % 64 == 63:
                 torch.cuda.synchronize()
+        _barrier(world)
         comm.kernel_stats()
         _barrier(world)
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
