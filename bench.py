@@ -201,7 +201,7 @@ def run_ours(args):
     avg_s = dev_ms / 1e3 / launches
     esz_of = {"f32": 4, "bf16": 2}
     fplan = hvd.plan(counts, [dt] * len(counts))
-    if dom == "ring":
+    if dom in ("ring", "fused") and n > 1:
         # NVLink bytes this rank pushes per step: sum over fusion buffers of
         # (2L - |c_{r+1}| - |c_{r+2}|) * esz  (~ 2(N-1)/N * S)
         step_bytes = 0
@@ -210,7 +210,7 @@ def run_ours(args):
             sz = [cb[i + 1] - cb[i] for i in range(n)]
             step_bytes += (2 * Lb - sz[(rank + 1) % n] - sz[(rank + 2) % n]) * esz_of[bdt]
         per_launch = step_bytes * args.steps / launches
-        roof = {"kernel": "ring_allreduce_kernel", "bound": "nvlink", "unit": "GB/s",
+        roof = {"kernel": f"{dom}_allreduce_kernel", "bound": "nvlink", "unit": "GB/s",
                 "achieved": per_launch / avg_s / 1e9, "peak": NVLINK_MEASURED_GBPS,
                 "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction (no NVLink figure in "
                                "MEASURED_PEAKS.json); nominal 900",
@@ -218,8 +218,12 @@ def run_ours(args):
         roof["frac"] = roof["achieved"] / roof["peak"]
         roof["frac_of_nominal_900"] = roof["achieved"] / NVLINK_NOMINAL_GBPS
     else:
-        # pack / unpack: read the members + write the buffer (or back), per step
-        step_bytes = payload + sum(Lb * esz_of[bdt] for bdt, Lb, _ in fplan)
+        # HBM: fused at N=1 reads the members and writes them back; pack reads the
+        # members + writes the buffer; unpack reads the buffer + writes the members
+        if dom == "fused":
+            step_bytes = 2 * payload
+        else:
+            step_bytes = payload + sum(Lb * esz_of[bdt] for bdt, Lb, _ in fplan)
         per_launch = step_bytes * args.steps / launches
         roof = {"kernel": f"{dom}_kernel", "bound": "hbm", "unit": "GB/s",
                 "achieved": per_launch / avg_s / 1e9, "peak": peaks.get("hbm_gbs", 6650.0),

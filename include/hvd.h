@@ -158,19 +158,22 @@ const char* hvd_strerror(int status);
 int hvd_traffic(hvd_comm* c, int local, uint64_t* sent_bytes, uint64_t* sends);
 
 typedef enum {
-  HVD_CFG_CHANNELS = 1,      /* CTAs per rank in the ring kernel (1..64)                */
+  HVD_CFG_CHANNELS = 1,      /* CTAs per rank in the ring kernel (1..256)               */
   HVD_CFG_SLICE_BYTES = 2,   /* pipelining slice per channel (multiple of 256 B)        */
-  HVD_CFG_THREADS = 3,       /* threads per ring CTA (128..1024, multiple of 32)         */
+  HVD_CFG_THREADS = 3,       /* data threads per ring CTA (64..384, multiple of 32; +1 signal warp) */
   HVD_CFG_TIMEOUT_MS = 4,    /* device spin-wait watchdog                               */
   HVD_CFG_PACK_CTAS_PER_SM = 5,
-  HVD_CFG_PROFILE = 6        /* 1: record CUDA events around every kernel launch        */
+  HVD_CFG_PROFILE = 6,       /* 1: record CUDA events around every kernel launch        */
+  HVD_CFG_SIGNAL_MODE = 7,   /* ring signal: 1 fence.acq_rel.sys + relaxed store, 2 st.release.sys */
+  HVD_CFG_FUSED = 8          /* 1 (default): pack + ring + unpack in one zero-copy kernel per
+                                fusion buffer; 0: three kernels (pack, ring, unpack)       */
 } hvd_config_key;
 /* Set a tuning knob; every rank must set identical values.  Errors: INVALID. */
 int hvd_set_config(hvd_comm* c, int key, int64_t value);
 int64_t hvd_get_config(const hvd_comm* c, int key);
 
 typedef enum { HVD_KERNEL_PACK = 0, HVD_KERNEL_RING = 1, HVD_KERNEL_UNPACK = 2, HVD_KERNEL_SCALE = 3,
-               HVD_KERNEL_KINDS = 4 } hvd_kernel_kind;
+               HVD_KERNEL_FUSED = 4, HVD_KERNEL_KINDS = 5 } hvd_kernel_kind;
 /* Kernel launches of each kind since the last call (always counted) and, with
  * HVD_CFG_PROFILE on, the summed device time in ms between the CUDA events
  * recorded on the launch stream around each launch (waits for those events).

@@ -27,7 +27,10 @@ HVD_CFG_THREADS = 3
 HVD_CFG_TIMEOUT_MS = 4
 HVD_CFG_PACK_CTAS_PER_SM = 5
 HVD_CFG_PROFILE = 6
-HVD_KERNEL_PACK, HVD_KERNEL_RING, HVD_KERNEL_UNPACK, HVD_KERNEL_SCALE, HVD_KERNEL_KINDS = 0, 1, 2, 3, 4
+HVD_CFG_SIGNAL_MODE = 7
+HVD_CFG_FUSED = 8
+HVD_KERNEL_PACK, HVD_KERNEL_RING, HVD_KERNEL_UNPACK, HVD_KERNEL_SCALE, HVD_KERNEL_FUSED = 0, 1, 2, 3, 4
+HVD_KERNEL_KINDS = 5
 
 
 class hvd_tensor(C.Structure):

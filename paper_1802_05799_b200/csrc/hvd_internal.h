@@ -10,7 +10,7 @@
 namespace hvd {
 
 constexpr int kMaxLocal = 8;        // virtual ranks per comm (one launch spans them all)
-constexpr int kMaxChannels = 64;    // ring CTAs per rank
+constexpr int kMaxChannels = 256;   // ring CTAs per rank
 constexpr int kMemberAlign = 16;    // fusion-buffer member alignment, bytes (R2)
 constexpr int kChunkQuantum = 256;  // chunk-boundary quantum, bytes (R2)
 constexpr int kPackVecBytes = 16;   // pack/unpack vector (== kMemberAlign, so a vector never
@@ -59,6 +59,8 @@ struct RingParams {
   int root;                     // broadcast root
   int* err;                     // host-mapped error word (device address)
   unsigned long long timeout_ns;
+  int sig_mode;                 // signal fence variant (hvd_kernels.cu send_signal)
+  int pad2;
 };
 
 // Signals each channel sends per call (host keeps the per-channel base in step).
@@ -90,7 +92,22 @@ struct PackParams {
   int pad;
 };
 
+// Fused zero-copy allreduce of one fusion buffer (pack + ring + unpack in one launch).
+constexpr int kFusedSmemSegs = 4096;  // member-offset table cached in shared memory up to this size
+struct FusedParams {
+  RingParams ring;
+  const PackSeg* segs;               // [nseg]
+  char* const* src;                  // [nlocal * nseg]
+  const unsigned long long* vbeg_global;  // [nseg] (used when nseg > kFusedSmemSegs)
+  int nseg;
+  int scale_on;
+  float scale;
+  int dtype;
+};
+
 // Launchers (hvd_kernels.cu).  All return a cudaError_t.
+cudaError_t launch_fused(const FusedParams& p, int dtype, int nch, int nlocal, int threads, cudaStream_t s);
+cudaError_t fused_max_ctas_per_sm(int dtype, int threads, int* out);
 cudaError_t launch_pack(const PackParams& p, int dtype, int nlocal, int grid, int threads,
                         cudaStream_t s);
 cudaError_t launch_unpack(const PackParams& p, int dtype, int nlocal, int grid, int threads,

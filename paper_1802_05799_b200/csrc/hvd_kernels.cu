@@ -74,9 +74,10 @@ __device__ __forceinline__ uint16_t f32_to_bf16_bits(float x) {
 struct OpF32 {
   using E = float;
   static constexpr int kEsz = 4;
-  __device__ static __forceinline__ void add_words(V32& a, const V32& b) {
+  template <int NW>
+  __device__ static __forceinline__ void add_words(uint32_t* a, const uint32_t* b) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) a.w[i] = __float_as_uint(__fadd_rn(__uint_as_float(a.w[i]), __uint_as_float(b.w[i])));
+    for (int i = 0; i < NW; ++i) a[i] = __float_as_uint(__fadd_rn(__uint_as_float(a[i]), __uint_as_float(b[i])));
   }
   __device__ static __forceinline__ E add(E a, E b) { return __fadd_rn(a, b); }
 };
@@ -84,11 +85,11 @@ struct OpF32 {
 struct OpBF16 {
   using E = uint16_t;
   static constexpr int kEsz = 2;
-  __device__ static __forceinline__ void add_words(V32& a, const V32& b) {
+  template <int NW>
+  __device__ static __forceinline__ void add_words(uint32_t* a, const uint32_t* b) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
-      a.w[i] = pack_bf16x2(__fadd_rn(bf16lo(a.w[i]), bf16lo(b.w[i])),
-                           __fadd_rn(bf16hi(a.w[i]), bf16hi(b.w[i])));
+    for (int i = 0; i < NW; ++i)
+      a[i] = pack_bf16x2(__fadd_rn(bf16lo(a[i]), bf16lo(b[i])), __fadd_rn(bf16hi(a[i]), bf16hi(b[i])));
   }
   __device__ static __forceinline__ E add(E a, E b) {
     return f32_to_bf16_bits(__fadd_rn(__uint_as_float(uint32_t(a) << 16), __uint_as_float(uint32_t(b) << 16)));
@@ -98,9 +99,10 @@ struct OpBF16 {
 struct OpI32 {
   using E = uint32_t;  // two's-complement wrap (R11)
   static constexpr int kEsz = 4;
-  __device__ static __forceinline__ void add_words(V32& a, const V32& b) {
+  template <int NW>
+  __device__ static __forceinline__ void add_words(uint32_t* a, const uint32_t* b) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) a.w[i] += b.w[i];
+    for (int i = 0; i < NW; ++i) a[i] += b[i];
   }
   __device__ static __forceinline__ E add(E a, E b) { return a + b; }
 };
@@ -108,14 +110,15 @@ struct OpI32 {
 struct OpI64 {
   using E = unsigned long long;
   static constexpr int kEsz = 8;
-  __device__ static __forceinline__ void add_words(V32& a, const V32& b) {
+  template <int NW>
+  __device__ static __forceinline__ void add_words(uint32_t* a, const uint32_t* b) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      unsigned long long x = (unsigned long long)a.w[2 * i] | ((unsigned long long)a.w[2 * i + 1] << 32);
-      unsigned long long y = (unsigned long long)b.w[2 * i] | ((unsigned long long)b.w[2 * i + 1] << 32);
+    for (int i = 0; i < NW / 2; ++i) {
+      unsigned long long x = (unsigned long long)a[2 * i] | ((unsigned long long)a[2 * i + 1] << 32);
+      unsigned long long y = (unsigned long long)b[2 * i] | ((unsigned long long)b[2 * i + 1] << 32);
       x += y;
-      a.w[2 * i] = uint32_t(x);
-      a.w[2 * i + 1] = uint32_t(x >> 32);
+      a[2 * i] = uint32_t(x);
+      a[2 * i + 1] = uint32_t(x >> 32);
     }
   }
   __device__ static __forceinline__ E add(E a, E b) { return a + b; }
@@ -128,12 +131,13 @@ struct OpI64 {
 //   kAddLocal:   buf[lo,hi) and nbuf[lo,hi) <- buf + scratch     (last add, all-gather step 0)
 enum SliceKind { kCopy = 0, kAdd = 1, kAddLocal = 2 };
 
+constexpr int kPackBatch = 8;  // == kPackVecsPerThread in the runtime (tile = 256 x 8 vectors)
 constexpr int kUnroll = 2;  // 2 x (2 x 32 B) loads in flight per thread; 4 spills (wide-register alignment)
 
 template <class Op, int KIND>
 __device__ __forceinline__ void do_slice(const char* __restrict__ a, const char* __restrict__ b,
                                          char* __restrict__ dst, char* __restrict__ dst_local,
-                                         unsigned long long lo, unsigned long long hi) {
+                                         unsigned long long lo, unsigned long long hi, unsigned tid, unsigned nthr) {
   using E = typename Op::E;
   const unsigned long long nbytes = (hi - lo) * Op::kEsz;
   const unsigned long long nvec = nbytes / 32;
@@ -141,8 +145,7 @@ __device__ __forceinline__ void do_slice(const char* __restrict__ a, const char*
   const char* pb = b + lo * Op::kEsz;
   char* pd = dst + lo * Op::kEsz;
   char* pl = dst_local + lo * Op::kEsz;
-  const unsigned nthr = blockDim.x;
-  for (unsigned long long v0 = threadIdx.x; v0 < nvec; v0 += (unsigned long long)nthr * kUnroll) {
+  for (unsigned long long v0 = tid; v0 < nvec; v0 += (unsigned long long)nthr * kUnroll) {
     V32 x[kUnroll], y[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
@@ -156,7 +159,7 @@ __device__ __forceinline__ void do_slice(const char* __restrict__ a, const char*
     for (int u = 0; u < kUnroll; ++u) {
       const unsigned long long v = v0 + (unsigned long long)u * nthr;
       if (v < nvec) {
-        if (KIND != kCopy) Op::add_words(x[u], y[u]);
+        if (KIND != kCopy) Op::template add_words<8>(x[u].w, y[u].w);
         st_v8(pd + v * 32, x[u]);
         if (KIND == kAddLocal) st_v8(pl + v * 32, x[u]);
       }
@@ -164,7 +167,7 @@ __device__ __forceinline__ void do_slice(const char* __restrict__ a, const char*
   }
   // ragged tail (only at the end of the buffer): element by element
   const unsigned long long tail0 = nvec * 32 / Op::kEsz;
-  for (unsigned long long e = tail0 + threadIdx.x; e < hi - lo; e += nthr) {
+  for (unsigned long long e = tail0 + tid; e < hi - lo; e += nthr) {
     E x = *reinterpret_cast<const volatile E*>(pa + e * Op::kEsz);
     if (KIND != kCopy) x = Op::add(x, *reinterpret_cast<const volatile E*>(pb + e * Op::kEsz));
     *reinterpret_cast<E*>(pd + e * Op::kEsz) = x;
@@ -172,38 +175,27 @@ __device__ __forceinline__ void do_slice(const char* __restrict__ a, const char*
   }
 }
 
-// Thread 0 spins (acquire, system scope) until *flag >= target; the CTA then
-// proceeds.  Returns false on watchdog timeout (error latched in host memory).
-__device__ __forceinline__ bool wait_signal(const unsigned long long* flag, unsigned long long target,
-                                            int* err, unsigned long long timeout_ns) {
-  __shared__ int s_ok;
-  if (threadIdx.x == 0) {
-    int ok = 1;
-    if (ld_acquire_sys(flag) < target) {
-      const unsigned long long t0 = globaltimer();
-      unsigned spins = 0;
-      while (ld_acquire_sys(flag) < target) {
-        if ((++spins & 1023u) == 0) {
-          if (globaltimer() - t0 > timeout_ns || *(volatile int*)err != 0) {
-            *(volatile int*)err = kHvdErrTimeout;
-            ok = 0;
-            break;
-          }
-        }
-      }
-    }
-    s_ok = ok;
-  }
-  __syncthreads();
-  return s_ok != 0;
+// Named barriers (ids 1..5; 0 is __syncthreads).
+__device__ __forceinline__ void bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
-// All threads make their stores to the successor visible system-wide, then
-// thread 0 publishes the counter (release, system scope).
-__device__ __forceinline__ void send_signal(unsigned long long* nflag, unsigned long long value) {
-  __threadfence_system();
-  __syncthreads();
-  if (threadIdx.x == 0) st_release_sys(nflag, value);
+// The data-warp leader spins (acquire, system scope) until *flag >= target.
+// Returns false on watchdog timeout (error latched in host-mapped memory).
+__device__ __forceinline__ bool spin_until(const unsigned long long* flag, unsigned long long target, int* err,
+                                           unsigned long long timeout_ns) {
+  if (ld_acquire_sys(flag) >= target) return true;
+  const unsigned long long t0 = globaltimer();
+  unsigned spins = 0;
+  while (ld_acquire_sys(flag) < target) {
+    if ((++spins & 1023u) == 0) {
+      if (globaltimer() - t0 > timeout_ns || *(volatile int*)err != 0) {
+        *(volatile int*)err = kHvdErrTimeout;
+        return false;
+      }
+    }
+  }
+  return true;
 }
 
 __device__ __forceinline__ void slice_range(const RingParams& P, int c, int ch, int k,
@@ -225,15 +217,57 @@ __device__ __forceinline__ void slice_range(const RingParams& P, int c, int ch, 
 
 __device__ __forceinline__ int mod(int a, int n) { return ((a % n) + n) % n; }
 
-// Ring allreduce of one fusion buffer.  grid = (channels, local ranks).
+// Ring allreduce of one fusion buffer.  grid = (channels, local ranks);
+// block = D data warps + 1 signal warp.
+//
 // Iteration t = 0..2N-3 (t < N-1: reduce-scatter step s = t; else all-gather
-// step s = t-N+1).  Channel `ch` of rank r owns the ch-th sub-range of every
-// chunk and sends one signal per (t, slice k) to the same channel of r+1; it
-// waits for the predecessor's signal of (t-1, k) before touching data that
-// signal covers.  After the loop it waits for the predecessor's last signal,
-// so the kernel completes only when every chunk has arrived.
+// step s = t-N+1); slice k = 0..K-1; slice sequence number i = t*K + k.
+// Channel `ch` of rank r owns the ch-th sub-range of every chunk.
+//
+// Data warps move slice i (loads at L2, 32 B stores into the successor's HBM).
+// Before slice i of iteration t >= 1 their leader waits until the
+// predecessor's counter reaches base + (t-1)K + k + 1 (its slice (t-1, k) has
+// landed here).  One barrier per slice (data warps only) then both retires
+// slice i and releases slice i+1; the leader publishes "i+1 slices done" in
+// shared memory (release, CTA scope).
+// The signal warp never blocks the data warps: it polls that shared count,
+// makes every store of the slices done so far visible system-wide with ONE
+// fence.acq_rel.sys (barrier cumulativity covers the data warps' stores) and
+// publishes base + done in the successor's counter.  A fence waits for the
+// NVLink drain of everything in flight (~us), so one fence covers a batch of
+// slices and its latency overlaps the pushes of the next ones.  After the loop
+// the leader waits for the predecessor's last counter, so the kernel completes
+// only when every chunk has arrived.
+constexpr int kBarData = 1;
+
+__device__ __forceinline__ void st_release_cta_shared(int* p, int v) {
+  asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_cta_shared(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
+  return v;
+}
+
+// Signal warp body (lane 0): publish progress `*done` to the successor's counter.
+__device__ __forceinline__ void signal_loop(const int* done, int total, unsigned long long* nflag,
+                                            unsigned long long base, int sig_mode) {
+  int published = 0;
+  while (published < total) {
+    int d;
+    while ((d = ld_acquire_cta_shared(done)) == published) __nanosleep(32);
+    if (sig_mode == 1) {
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(nflag), "l"(base + (unsigned long long)d) : "memory");
+    } else {
+      st_release_sys(nflag, base + (unsigned long long)d);
+    }
+    published = d;
+  }
+}
+
 template <class Op>
-__global__ void __launch_bounds__(512, 1) ring_allreduce_kernel(const __grid_constant__ RingParams P) {
+__global__ void __launch_bounds__(416, 1) ring_allreduce_kernel(const __grid_constant__ RingParams P) {
   const RingRank& me = P.rk[blockIdx.y];
   const int ch = blockIdx.x;
   const int N = P.N;
@@ -241,33 +275,59 @@ __global__ void __launch_bounds__(512, 1) ring_allreduce_kernel(const __grid_con
   const int K = P.K;
   const unsigned long long base = P.base[ch];
   const int T = 2 * (N - 1);
+  const int nd = blockDim.x - 32;  // data threads
+  __shared__ int s_abort, s_done;
+  if (threadIdx.x == 0) {
+    s_abort = 0;
+    s_done = 0;
+  }
+  __syncthreads();
+
+  if (threadIdx.x >= nd) {  // ---- signal warp
+    if (threadIdx.x == nd) signal_loop(&s_done, T * K, me.nflags + ch, base, P.sig_mode);
+    return;
+  }
+
+  // ---- data warps
+  const unsigned tid = threadIdx.x;
   unsigned long long sent = 0;
+  int i = 0;
   for (int t = 0; t < T; ++t) {
     const bool rs = t < N - 1;
     const int s = rs ? t : t - (N - 1);
     const int c = rs ? mod(r - s, N) : mod(r + 1 - s, N);
-    for (int k = 0; k < K; ++k) {
+    for (int k = 0; k < K; ++k, ++i) {
       unsigned long long lo, hi;
       slice_range(P, c, ch, k, lo, hi);
-      if (t > 0 && !wait_signal(me.flags + ch, base + (unsigned long long)(t - 1) * K + k + 1, P.err,
-                                P.timeout_ns))
-        return;
-      if (hi > lo) {
+      if (hi > lo && !s_abort) {
         if (rs && s == 0)
-          do_slice<Op, kCopy>(me.buf, nullptr, me.nscratch, nullptr, lo, hi);
+          do_slice<Op, kCopy>(me.buf, nullptr, me.nscratch, nullptr, lo, hi, tid, nd);
         else if (rs)
-          do_slice<Op, kAdd>(me.buf, me.scratch, me.nscratch, nullptr, lo, hi);
+          do_slice<Op, kAdd>(me.buf, me.scratch, me.nscratch, nullptr, lo, hi, tid, nd);
         else if (s == 0)
-          do_slice<Op, kAddLocal>(me.buf, me.scratch, me.nbuf, me.buf, lo, hi);
+          do_slice<Op, kAddLocal>(me.buf, me.scratch, me.nbuf, me.buf, lo, hi, tid, nd);
         else
-          do_slice<Op, kCopy>(me.buf, nullptr, me.nbuf, nullptr, lo, hi);
+          do_slice<Op, kCopy>(me.buf, nullptr, me.nbuf, nullptr, lo, hi, tid, nd);
         sent += (hi - lo) * Op::kEsz;
       }
-      send_signal(me.nflags + ch, base + (unsigned long long)t * K + k + 1);
+      // retire slice i (all data warps' stores issued), publish it to the signal
+      // warp, THEN wait for the next slice's dependency: publishing first keeps the
+      // ring free of cycles (slice i never waits on anything downstream of itself)
+      bar_sync(kBarData, nd);
+      if (tid == 0) {
+        st_release_cta_shared(&s_done, i + 1);
+        const int tn = (k + 1 < K) ? t : t + 1;
+        const int kn = (k + 1 < K) ? k + 1 : 0;
+        // next slice needs the predecessor's (tn-1, kn); after the last slice: its (T-1, K-1)
+        unsigned long long target = 0;
+        if (tn < T && tn > 0) target = base + (unsigned long long)(tn - 1) * K + kn + 1;
+        else if (tn >= T) target = base + (unsigned long long)T * K;
+        if (target && !s_abort && !spin_until(me.flags + ch, target, P.err, P.timeout_ns)) s_abort = 1;
+      }
+      if (t + (k + 1 == K) > 0) bar_sync(kBarData, nd);  // release the next slice (no wait inside step 0)
     }
   }
-  if (!wait_signal(me.flags + ch, base + (unsigned long long)T * K, P.err, P.timeout_ns)) return;
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     atomicAdd(me.stats + 0, sent);
     if (ch == 0) atomicAdd(me.stats + 1, (unsigned long long)T);
   }
@@ -328,52 +388,273 @@ __device__ __forceinline__ void scale_elem(const char* src, char* dst, float s, 
   }
 }
 
+// Each thread owns kPackBatch vectors of a tile (stride blockDim) and issues all
+// their loads before any store, so kPackBatch x 16 B per thread are in flight.
 template <int ESZ, bool PACK>
-__global__ void __launch_bounds__(512) pack_kernel(const __grid_constant__ PackParams P, int dtype) {
+__global__ void __launch_bounds__(256) pack_kernel(const __grid_constant__ PackParams P, int dtype) {
   constexpr int VEL = kPackVecBytes / ESZ;
   char* const buf = P.buf[blockIdx.y];
   char* const* src_tab = P.src + (size_t)blockIdx.y * P.nseg;
   for (unsigned long long tile = blockIdx.x; tile < P.ntiles; tile += gridDim.x) {
-    const int s_lo = P.tile_seg[tile];
     const int s_hi = P.tile_seg[tile + 1];
     const unsigned long long v0 = tile * P.tile_vecs;
     unsigned long long v1 = v0 + P.tile_vecs;
     v1 = v1 < P.nvec ? v1 : P.nvec;
-    int s = s_lo;
-    for (unsigned long long v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
-      if (s < s_hi && P.segs[s + 1].vbeg <= v) s = find_seg(P, v, s, s_hi);
-      const PackSeg sg = P.segs[s];
-      const unsigned long long e0 = v * VEL - sg.dst_off;
-      char* tens = src_tab[s] + e0 * ESZ;
-      char* bvec = buf + v * kPackVecBytes;
-      const bool full = e0 + VEL <= sg.count;
-      const bool aligned = ((reinterpret_cast<uintptr_t>(tens) & 15) == 0);
-      if (PACK) {
-        if (full && aligned) {
-          uint4 x = __ldcs(reinterpret_cast<const uint4*>(tens));
-          *reinterpret_cast<uint4*>(bvec) = Pack16<ESZ>::conv(x, P.scale, P.scale_on, dtype);
-        } else {
-          alignas(16) char tmp[kPackVecBytes];
+    int s = P.tile_seg[tile];
+    uint4 x[kPackBatch];
+    char* tens[kPackBatch];
+    unsigned long long left[kPackBatch];  // valid elements from tens on (>= VEL: full vector)
 #pragma unroll
-          for (int i = 0; i < VEL; ++i) {
-            if (e0 + i < sg.count) scale_elem<ESZ>(tens + i * ESZ, tmp + i * ESZ, P.scale, P.scale_on, dtype);
-            else for (int b = 0; b < ESZ; ++b) tmp[i * ESZ + b] = 0;  // interior padding
+    for (int u = 0; u < kPackBatch; ++u) {
+      const unsigned long long v = v0 + (unsigned long long)u * blockDim.x + threadIdx.x;
+      left[u] = 0;
+      tens[u] = nullptr;
+      if (v < v1) {
+        if (s < s_hi && P.segs[s + 1].vbeg <= v) s = find_seg(P, v, s, s_hi);
+        const unsigned long long e0 = v * VEL - P.segs[s].dst_off;
+        const unsigned long long cnt = P.segs[s].count;
+        tens[u] = src_tab[s] + e0 * ESZ;
+        left[u] = cnt - e0;
+        const bool fast = left[u] >= (unsigned long long)VEL && ((reinterpret_cast<uintptr_t>(tens[u]) & 15) == 0);
+        if (PACK) {
+          if (fast) {
+            x[u] = __ldcs(reinterpret_cast<const uint4*>(tens[u]));
+          } else {  // ragged member end or misaligned tensor: element by element, zero padding
+            alignas(16) char tmp[kPackVecBytes];
+#pragma unroll
+            for (int i = 0; i < VEL; ++i) {
+              if ((unsigned long long)i < left[u]) {
+                for (int bb = 0; bb < ESZ; ++bb) tmp[i * ESZ + bb] = tens[u][i * ESZ + bb];
+              } else {
+                for (int bb = 0; bb < ESZ; ++bb) tmp[i * ESZ + bb] = 0;  // interior padding
+              }
+            }
+            x[u] = *reinterpret_cast<const uint4*>(tmp);
           }
-          *reinterpret_cast<uint4*>(bvec) = *reinterpret_cast<const uint4*>(tmp);
-        }
-      } else {
-        const uint4 x = __ldcg(reinterpret_cast<const uint4*>(bvec));
-        if (full && aligned) {
-          __stcs(reinterpret_cast<uint4*>(tens), x);
         } else {
-          const char* xb = reinterpret_cast<const char*>(&x);
-#pragma unroll
-          for (int i = 0; i < VEL; ++i)
-            if (e0 + i < sg.count)
-              for (int b = 0; b < ESZ; ++b) tens[i * ESZ + b] = xb[i * ESZ + b];
+          x[u] = __ldcg(reinterpret_cast<const uint4*>(buf + v * kPackVecBytes));
         }
       }
     }
+#pragma unroll
+    for (int u = 0; u < kPackBatch; ++u) {
+      const unsigned long long v = v0 + (unsigned long long)u * blockDim.x + threadIdx.x;
+      if (v >= v1) continue;
+      if (PACK) {
+        *reinterpret_cast<uint4*>(buf + v * kPackVecBytes) = Pack16<ESZ>::conv(x[u], P.scale, P.scale_on, dtype);
+      } else {
+        const bool fast = left[u] >= (unsigned long long)VEL && ((reinterpret_cast<uintptr_t>(tens[u]) & 15) == 0);
+        if (fast) {
+          __stcs(reinterpret_cast<uint4*>(tens[u]), x[u]);
+        } else {
+          const char* xb = reinterpret_cast<const char*>(&x[u]);
+#pragma unroll
+          for (int i = 0; i < VEL; ++i)
+            if ((unsigned long long)i < left[u])
+              for (int bb = 0; bb < ESZ; ++bb) tens[u][i * ESZ + bb] = xb[i * ESZ + bb];
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ fused zero-copy path
+// One launch per fusion buffer does Tensor Fusion steps 3-5 and
+// the ring without materialising the packed buffer:
+//   RS step 0      nscratch <- gather(x) * s                       (pack fused in)
+//   RS step s >= 1 nscratch <- gather(x) * s + scratch
+//   AG step 0      nbuf     <- gather(x) * s + scratch ; x <- same  (unpack fused in)
+//   AG step s >= 1 nbuf     <- buf ; x <- buf
+//   final          x <- buf for the chunk received in the last AG step
+//   N = 1          x <- gather(x) * s
+// gather/scatter map a 16 B buffer vector to its member through the plan's
+// segment table (vbeg cached in shared memory).  Every element is gathered
+// exactly once before it is scattered (same CTA, program order), so the
+// in-place update of the caller's tensors is safe.  Results are bit-identical
+// to pack -> ring -> unpack: same per-element operations in the same order.
+enum FusedKind { kF_RS0 = 0, kF_RS = 1, kF_AG0 = 2, kF_AG = 3, kF_FIN = 4, kF_SOLO = 5 };
+
+struct FusedCtx {
+  const PackSeg* segs;
+  char* const* src;                 // this rank's tensor addresses [nseg]
+  const unsigned long long* vbeg;   // shared or global copy of segs[].vbeg
+  int nseg;
+  int scale_on;
+  float scale;
+  int dtype;
+};
+
+__device__ __forceinline__ int seg_of(const FusedCtx& F, unsigned long long v, int s) {
+  if (F.vbeg[s] <= v && (s + 1 == F.nseg || F.vbeg[s + 1] > v)) return s;
+  int lo = 0, hi = F.nseg - 1;
+  while (lo < hi) {  // largest s with vbeg[s] <= v
+    const int mid = (lo + hi + 1) >> 1;
+    if (F.vbeg[mid] <= v) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+template <int ESZ>
+__device__ __forceinline__ uint4 gather16(const FusedCtx& F, unsigned long long v, int& s, char*& tp,
+                                          unsigned long long& left) {
+  constexpr int VEL = 16 / ESZ;
+  s = seg_of(F, v, s);
+  const unsigned long long e0 = v * VEL - F.segs[s].dst_off;
+  const unsigned long long cnt = F.segs[s].count;
+  tp = F.src[s] + e0 * ESZ;
+  left = e0 < cnt ? cnt - e0 : 0;
+  uint4 x;
+  if (left >= (unsigned long long)VEL && ((reinterpret_cast<uintptr_t>(tp) & 15) == 0)) {
+    x = __ldcs(reinterpret_cast<const uint4*>(tp));
+  } else {  // ragged member end / misaligned tensor / tail past the last member: zero padding
+    alignas(16) char tmp[16];
+#pragma unroll
+    for (int i = 0; i < VEL; ++i)
+#pragma unroll
+      for (int b = 0; b < ESZ; ++b) tmp[i * ESZ + b] = (unsigned long long)i < left ? tp[i * ESZ + b] : 0;
+    x = *reinterpret_cast<const uint4*>(tmp);
+  }
+  return Pack16<ESZ>::conv(x, F.scale, F.scale_on, F.dtype);
+}
+
+template <int ESZ>
+__device__ __forceinline__ void scatter16(char* tp, unsigned long long left, const uint4& x) {
+  constexpr int VEL = 16 / ESZ;
+  if (left >= (unsigned long long)VEL && ((reinterpret_cast<uintptr_t>(tp) & 15) == 0)) {
+    *reinterpret_cast<uint4*>(tp) = x;
+  } else {
+    const char* xb = reinterpret_cast<const char*>(&x);
+#pragma unroll
+    for (int i = 0; i < VEL; ++i)
+      if ((unsigned long long)i < left)
+#pragma unroll
+        for (int b = 0; b < ESZ; ++b) tp[i * ESZ + b] = xb[i * ESZ + b];
+  }
+}
+
+constexpr int kFusedUnroll = 4;
+
+template <class Op, int KIND>
+__device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& me, unsigned long long lo,
+                                            unsigned long long hi, unsigned tid, unsigned nthr, int& sc) {
+  constexpr int ESZ = Op::kEsz;
+  constexpr int VEL = 16 / ESZ;
+  const unsigned long long v_lo = lo / VEL;
+  const unsigned long long v_hi = (hi + VEL - 1) / VEL;
+  for (unsigned long long v0 = v_lo + tid; v0 < v_hi; v0 += (unsigned long long)nthr * kFusedUnroll) {
+    uint4 x[kFusedUnroll], y[kFusedUnroll];
+    char* tp[kFusedUnroll];
+    unsigned long long left[kFusedUnroll];
+#pragma unroll
+    for (int u = 0; u < kFusedUnroll; ++u) {
+      const unsigned long long v = v0 + (unsigned long long)u * nthr;
+      if (v < v_hi) {
+        if (KIND == kF_RS0 || KIND == kF_RS || KIND == kF_AG0 || KIND == kF_SOLO) {
+          x[u] = gather16<ESZ>(F, v, sc, tp[u], left[u]);
+        } else {
+          x[u] = __ldcg(reinterpret_cast<const uint4*>(me.buf + v * 16));
+          int s2 = seg_of(F, v, sc);
+          sc = s2;
+          const unsigned long long e0 = v * VEL - F.segs[s2].dst_off;
+          const unsigned long long cnt = F.segs[s2].count;
+          tp[u] = F.src[s2] + e0 * ESZ;
+          left[u] = e0 < cnt ? cnt - e0 : 0;
+        }
+        if (KIND == kF_RS || KIND == kF_AG0) y[u] = __ldcg(reinterpret_cast<const uint4*>(me.scratch + v * 16));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kFusedUnroll; ++u) {
+      const unsigned long long v = v0 + (unsigned long long)u * nthr;
+      if (v < v_hi) {
+        if (KIND == kF_RS || KIND == kF_AG0)
+          Op::template add_words<4>(reinterpret_cast<uint32_t*>(&x[u]), reinterpret_cast<const uint32_t*>(&y[u]));
+        if (KIND == kF_RS0 || KIND == kF_RS) *reinterpret_cast<uint4*>(me.nscratch + v * 16) = x[u];
+        if (KIND == kF_AG0 || KIND == kF_AG) *reinterpret_cast<uint4*>(me.nbuf + v * 16) = x[u];
+        if (KIND == kF_AG0 || KIND == kF_AG || KIND == kF_FIN || KIND == kF_SOLO) scatter16<ESZ>(tp[u], left[u], x[u]);
+      }
+    }
+  }
+}
+
+template <class Op>
+__global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_constant__ FusedParams P) {
+  extern __shared__ unsigned long long s_vbeg[];
+  const RingParams& R = P.ring;
+  const RingRank& me = R.rk[blockIdx.y];
+  const int ch = blockIdx.x;
+  const int N = R.N;
+  const int r = me.rank;
+  const int K = R.K;
+  const unsigned long long base = R.base[ch];
+  const int T = N > 1 ? 2 * (N - 1) : 0;
+  const int nd = blockDim.x - 32;
+  __shared__ int s_abort, s_done;
+  const bool cache = P.nseg <= kFusedSmemSegs;
+  if (cache)
+    for (int j = threadIdx.x; j < P.nseg; j += blockDim.x) s_vbeg[j] = P.segs[j].vbeg;
+  if (threadIdx.x == 0) {
+    s_abort = 0;
+    s_done = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x >= nd) {
+    if (threadIdx.x == nd && T > 0) signal_loop(&s_done, T * K, me.nflags + ch, base, R.sig_mode);
+    return;
+  }
+  FusedCtx F;
+  F.segs = P.segs;
+  F.src = P.src + (size_t)blockIdx.y * P.nseg;
+  F.vbeg = cache ? s_vbeg : P.vbeg_global;
+  F.nseg = P.nseg;
+  F.scale_on = P.scale_on;
+  F.scale = P.scale;
+  F.dtype = P.dtype;
+  const unsigned tid = threadIdx.x;
+  int sc = 0;
+  unsigned long long sent = 0;
+  if (N == 1) {
+    for (int k = 0; k < K; ++k) {
+      unsigned long long lo, hi;
+      slice_range(R, 0, ch, k, lo, hi);
+      if (hi > lo) fused_slice<Op, kF_SOLO>(F, me, lo, hi, tid, nd, sc);
+    }
+    return;
+  }
+  int i = 0;
+  for (int t = 0; t <= T; ++t) {  // t == T: scatter the chunk received in the last AG step
+    const bool rs = t < N - 1;
+    const int s = rs ? t : t - (N - 1);
+    const int c = t == T ? mod(r + 2, N) : (rs ? mod(r - s, N) : mod(r + 1 - s, N));
+    for (int k = 0; k < K; ++k) {
+      unsigned long long lo, hi;
+      slice_range(R, c, ch, k, lo, hi);
+      if (hi > lo && !s_abort) {
+        if (t == T) fused_slice<Op, kF_FIN>(F, me, lo, hi, tid, nd, sc);
+        else if (rs && s == 0) fused_slice<Op, kF_RS0>(F, me, lo, hi, tid, nd, sc);
+        else if (rs) fused_slice<Op, kF_RS>(F, me, lo, hi, tid, nd, sc);
+        else if (s == 0) fused_slice<Op, kF_AG0>(F, me, lo, hi, tid, nd, sc);
+        else fused_slice<Op, kF_AG>(F, me, lo, hi, tid, nd, sc);
+        if (t < T) sent += (hi - lo) * Op::kEsz;
+      }
+      if (t == T && k + 1 == K) break;
+      // retire + publish slice i, then wait for the next slice's dependency (same rule
+      // as the ring kernel; the final pseudo-iteration t == T depends on (T-1, k))
+      bar_sync(kBarData, nd);
+      if (t < T) ++i;
+      if (tid == 0) {
+        if (t < T) st_release_cta_shared(&s_done, i);
+        const int tn = (k + 1 < K) ? t : t + 1;
+        const int kn = (k + 1 < K) ? k + 1 : 0;
+        const unsigned long long target = tn > 0 ? base + (unsigned long long)(tn - 1) * K + kn + 1 : 0;
+        if (target && !s_abort && !spin_until(me.flags + ch, target, R.err, R.timeout_ns)) s_abort = 1;
+      }
+      if (t + (k + 1 == K) > 0) bar_sync(kBarData, nd);
+    }
+  }
+  if (tid == 0) {
+    atomicAdd(me.stats + 0, sent);
+    if (ch == 0) atomicAdd(me.stats + 1, (unsigned long long)T);
   }
 }
 
@@ -439,7 +720,7 @@ template <class Op>
 static cudaError_t launch_ring_t(const RingParams& p, int nch, int nlocal, int threads, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nch, nlocal);
-  cfg.blockDim = dim3(threads);
+  cfg.blockDim = dim3(threads + 32);  // + signal warp
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -460,12 +741,56 @@ cudaError_t launch_ring(const RingParams& p, int dtype, int nch, int nlocal, int
   }
 }
 
+template <class Op>
+static cudaError_t launch_fused_t(const FusedParams& p, int nch, int nlocal, int threads, cudaStream_t s) {
+  const size_t smem = p.nseg <= kFusedSmemSegs ? (size_t)p.nseg * 8 : 0;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(fused_allreduce_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kFusedSmemSegs * 8);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nch, nlocal);
+  cfg.blockDim = dim3(threads + 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, fused_allreduce_kernel<Op>, p);
+}
+
+cudaError_t launch_fused(const FusedParams& p, int dtype, int nch, int nlocal, int threads, cudaStream_t s) {
+  switch (dtype) {
+    case 1: return launch_fused_t<OpF32>(p, nch, nlocal, threads, s);
+    case 2: return launch_fused_t<OpBF16>(p, nch, nlocal, threads, s);
+    case 3: return launch_fused_t<OpI32>(p, nch, nlocal, threads, s);
+    case 4: return launch_fused_t<OpI64>(p, nch, nlocal, threads, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t fused_max_ctas_per_sm(int dtype, int threads, int* out) {
+  const size_t smem = kFusedSmemSegs * 8;
+  switch (dtype) {
+    case 1: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fused_allreduce_kernel<OpF32>, threads + 32, smem);
+    case 2: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fused_allreduce_kernel<OpBF16>, threads + 32, smem);
+    case 3: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fused_allreduce_kernel<OpI32>, threads + 32, smem);
+    case 4: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fused_allreduce_kernel<OpI64>, threads + 32, smem);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 cudaError_t ring_max_ctas_per_sm(int dtype, int threads, int* out) {
   switch (dtype) {
-    case 1: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, ring_allreduce_kernel<OpF32>, threads, 0);
-    case 2: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, ring_allreduce_kernel<OpBF16>, threads, 0);
-    case 3: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, ring_allreduce_kernel<OpI32>, threads, 0);
-    case 4: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, ring_allreduce_kernel<OpI64>, threads, 0);
+    case 1: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, ring_allreduce_kernel<OpF32>, threads + 32, 0);
+    case 2: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, ring_allreduce_kernel<OpBF16>, threads + 32, 0);
+    case 3: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, ring_allreduce_kernel<OpI32>, threads + 32, 0);
+    case 4: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, ring_allreduce_kernel<OpI64>, threads + 32, 0);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -40,7 +40,8 @@ struct Blob {
 struct DevPlanBuffer {
   int dtype;
   uint64_t L;
-  PackParams pp;  // device pointers filled in
+  PackParams pp;                        // device pointers filled in
+  const unsigned long long* vbeg;       // [nseg] member start vectors (fused kernel, large plans)
 };
 
 struct CachedPlan {
@@ -67,10 +68,12 @@ struct hvd_comm {
   // tuning (hvd_set_config)
   int channels = 32;
   int64_t slice_bytes = 256 << 10;
-  int threads = 512;
+  int threads = 384;
   int64_t timeout_ms = 30000;
   int pack_ctas_per_sm = 8;
   int profile = 0;
+  int sig_mode = 1;
+  int fused = 1;
   std::list<CachedPlan> cache;
   // launch statistics (hvd_kernel_stats)
   uint64_t launches[HVD_KERNEL_KINDS] = {};
@@ -145,6 +148,7 @@ void free_plan(CachedPlan& p) {
 }
 
 size_t align256(size_t v) { return (v + 255) / 256 * 256; }
+unsigned long long e_vbeg(const hvd_plan_entry& e, uint64_t vel) { return e.dst_off / vel; }
 
 // Build (or fetch) the device-resident pack/unpack tables of the plan of the
 // tensor list `t` (n per local rank).  The key is every tensor's address,
@@ -181,7 +185,7 @@ int get_plan(hvd_comm* c, const hvd_tensor* t, int n, uint64_t threshold, cudaSt
   if (st != HVD_OK) return st;
 
   // layout: per buffer [segs][src table][tile_seg]
-  struct Off { size_t segs, src, tiles; uint64_t nvec, ntiles; };
+  struct Off { size_t segs, src, tiles, vbeg; uint64_t nvec, ntiles; };
   std::vector<Off> offs(bufs.size());
   const uint64_t tile_vecs = (uint64_t)kPackThreads * kPackVecsPerThread;
   size_t total = 0;
@@ -196,6 +200,8 @@ int get_plan(hvd_comm* c, const hvd_tensor* t, int n, uint64_t threshold, cudaSt
     total = align256(total + sizeof(char*) * bufs[b].n_entries * c->nlocal);
     offs[b].tiles = total;
     total = align256(total + sizeof(int) * (offs[b].ntiles + 1));
+    offs[b].vbeg = total;
+    total = align256(total + sizeof(unsigned long long) * bufs[b].n_entries);
   }
   CachedPlan p;
   p.key = std::move(key);
@@ -215,7 +221,9 @@ int get_plan(hvd_comm* c, const hvd_tensor* t, int n, uint64_t threshold, cudaSt
     PackSeg* segs = reinterpret_cast<PackSeg*>(h + offs[b].segs);
     char** src = reinterpret_cast<char**>(h + offs[b].src);
     int* tiles = reinterpret_cast<int*>(h + offs[b].tiles);
+    unsigned long long* vb = reinterpret_cast<unsigned long long*>(h + offs[b].vbeg);
     for (int j = 0; j < pb.n_entries; ++j) {
+      vb[j] = e_vbeg(ents[pb.first_entry + j], vel);
       const hvd_plan_entry& e = ents[pb.first_entry + j];
       segs[j].dst_off = e.dst_off;
       segs[j].count = e.count;
@@ -240,6 +248,7 @@ int get_plan(hvd_comm* c, const hvd_tensor* t, int n, uint64_t threshold, cudaSt
     db.pp.segs = reinterpret_cast<const PackSeg*>(d + offs[b].segs);
     db.pp.src = reinterpret_cast<char* const*>(d + offs[b].src);
     db.pp.tile_seg = reinterpret_cast<const int*>(d + offs[b].tiles);
+    db.vbeg = reinterpret_cast<const unsigned long long*>(d + offs[b].vbeg);
     for (int l = 0; l < c->nlocal; ++l) db.pp.buf[l] = c->rk[l].buf;
     db.pp.nvec = offs[b].nvec;
     db.pp.tile_vecs = tile_vecs;
@@ -295,36 +304,71 @@ int launch_counted(hvd_comm* c, int kind, cudaStream_t s, F&& launch) {
 
 // ------------------------------------------------------------------ ring enqueue
 // Split one buffer of L elements for the ring kernel and launch it.
-int enqueue_ring(hvd_comm* c, uint64_t L, int dtype, cudaStream_t s) {
-  if (c->size <= 1 || L == 0) return HVD_OK;
+// Split one buffer of L elements into chunks / channels / slices (R2) for the
+// ring or fused kernel.  Returns the channel count.
+int make_ring_params(hvd_comm* c, uint64_t L, int dtype, bool fused, RingParams* P, int* nch_out) {
   const int esz = elem_size(dtype);
   const uint64_t g = kChunkQuantum / esz;
-  RingParams P;
-  std::memset(&P, 0, sizeof(P));
-  for (int l = 0; l < c->nlocal; ++l) P.rk[l] = c->rk[l];
-  P.N = c->size;
-  P.L = L;
-  P.q = chunk_len(L, c->size, dtype);
+  std::memset(P, 0, sizeof(*P));
+  for (int l = 0; l < c->nlocal; ++l) P->rk[l] = c->rk[l];
+  P->N = c->size;
+  P->L = L;
+  P->q = chunk_len(L, c->size, dtype);
   // channels: at least 32 KiB of every chunk per channel, at most the knob and
   // what stays co-resident (the CTAs of all ranks wait on each other)
   int max_per_sm = 1;
-  CK(ring_max_ctas_per_sm(dtype, c->threads, &max_per_sm));
+  CK(fused ? fused_max_ctas_per_sm(dtype, c->threads, &max_per_sm) : ring_max_ctas_per_sm(dtype, c->threads, &max_per_sm));
   const int resident = std::max(1, c->sm_count * max_per_sm / c->nlocal);
-  const uint64_t qbytes = P.q * esz;
+  const uint64_t qbytes = P->q * esz;
   int nch = (int)std::min<uint64_t>((uint64_t)c->channels, std::max<uint64_t>(1, qbytes / (32 << 10)));
   nch = std::min(nch, std::min(resident, kMaxChannels));
-  P.ch_el = (P.q + (uint64_t)nch * g - 1) / ((uint64_t)nch * g) * g;
-  uint64_t slice_el = std::max<uint64_t>(g, (uint64_t)c->slice_bytes / esz / g * g);
-  P.slice_el = std::min<uint64_t>(slice_el, P.ch_el);
-  P.K = (int)((P.ch_el + P.slice_el - 1) / P.slice_el);
-  P.mode = kRingAllreduce;
-  P.err = c->err_dev;
-  P.timeout_ns = (unsigned long long)c->timeout_ms * 1000000ull;
-  for (int ch = 0; ch < kMaxChannels; ++ch) P.base[ch] = c->base[ch];
-  int st = launch_counted(c, HVD_KERNEL_RING, s, [&] { return launch_ring(P, dtype, nch, c->nlocal, c->threads, s); });
-  if (st != HVD_OK) return st;
+  P->ch_el = (P->q + (uint64_t)nch * g - 1) / ((uint64_t)nch * g) * g;
+  const uint64_t slice_el = std::max<uint64_t>(g, (uint64_t)c->slice_bytes / esz / g * g);
+  P->slice_el = std::min<uint64_t>(slice_el, P->ch_el);
+  P->K = (int)((P->ch_el + P->slice_el - 1) / P->slice_el);
+  P->mode = kRingAllreduce;
+  P->err = c->err_dev;
+  P->timeout_ns = (unsigned long long)c->timeout_ms * 1000000ull;
+  P->sig_mode = c->sig_mode;
+  for (int ch = 0; ch < kMaxChannels; ++ch) P->base[ch] = c->base[ch];
+  *nch_out = nch;
+  return HVD_OK;
+}
+
+void advance_base(hvd_comm* c, const RingParams& P, int nch) {
   const unsigned long long inc = ring_signals(kRingAllreduce, c->size, P.K);
   for (int ch = 0; ch < nch; ++ch) c->base[ch] += inc;
+}
+
+int enqueue_ring(hvd_comm* c, uint64_t L, int dtype, cudaStream_t s) {
+  if (c->size <= 1 || L == 0) return HVD_OK;
+  RingParams P;
+  int nch = 0;
+  int st = make_ring_params(c, L, dtype, false, &P, &nch);
+  if (st != HVD_OK) return st;
+  st = launch_counted(c, HVD_KERNEL_RING, s, [&] { return launch_ring(P, dtype, nch, c->nlocal, c->threads, s); });
+  if (st != HVD_OK) return st;
+  advance_base(c, P, nch);
+  return HVD_OK;
+}
+
+int enqueue_fused(hvd_comm* c, DevPlanBuffer& b, cudaStream_t s) {
+  if (b.L == 0) return HVD_OK;
+  FusedParams F;
+  std::memset(&F, 0, sizeof(F));
+  int nch = 0;
+  int st = make_ring_params(c, b.L, b.dtype, true, &F.ring, &nch);
+  if (st != HVD_OK) return st;
+  F.segs = b.pp.segs;
+  F.src = b.pp.src;
+  F.vbeg_global = b.vbeg;
+  F.nseg = b.pp.nseg;
+  F.scale_on = b.pp.scale_on;
+  F.scale = b.pp.scale;
+  F.dtype = b.dtype;
+  st = launch_counted(c, HVD_KERNEL_FUSED, s, [&] { return launch_fused(F, b.dtype, nch, c->nlocal, c->threads, s); });
+  if (st != HVD_OK) return st;
+  advance_base(c, F.ring, nch);
   return HVD_OK;
 }
 
@@ -353,6 +397,11 @@ int do_allreduce(hvd_comm* c, const hvd_tensor* t, int n, int op, uint64_t thres
   for (DevPlanBuffer& b : plan->bufs) {       // step 6: repeat per fusion buffer
     b.pp.scale = scale;
     b.pp.scale_on = op == HVD_AVERAGE ? 1 : 0;
+    if (c->fused) {                            // steps 3-5 in one zero-copy launch
+      st = enqueue_fused(c, b, s);
+      if (st != HVD_OK) return st;
+      continue;
+    }
     st = launch_counted(c, HVD_KERNEL_PACK, s, [&] {                          // step 3
       return launch_pack(b.pp, b.dtype, c->nlocal, pack_grid(c), kPackThreads, s);
     });
@@ -592,7 +641,7 @@ int hvd_set_config(hvd_comm* c, int key, int64_t value) {
       c->slice_bytes = value;
       return HVD_OK;
     case HVD_CFG_THREADS:
-      if (value < 128 || value > 512 || value % 32) return HVD_ERR_INVALID;
+      if (value < 64 || value > 384 || value % 32) return HVD_ERR_INVALID;
       c->threads = (int)value;
       return HVD_OK;
     case HVD_CFG_TIMEOUT_MS:
@@ -607,6 +656,14 @@ int hvd_set_config(hvd_comm* c, int key, int64_t value) {
       if (value != 0 && value != 1) return HVD_ERR_INVALID;
       c->profile = (int)value;
       return HVD_OK;
+    case HVD_CFG_SIGNAL_MODE:
+      if (value < 1 || value > 2) return HVD_ERR_INVALID;
+      c->sig_mode = (int)value;
+      return HVD_OK;
+    case HVD_CFG_FUSED:
+      if (value != 0 && value != 1) return HVD_ERR_INVALID;
+      c->fused = (int)value;
+      return HVD_OK;
     default: return HVD_ERR_INVALID;
   }
 }
@@ -620,6 +677,8 @@ int64_t hvd_get_config(const hvd_comm* c, int key) {
     case HVD_CFG_TIMEOUT_MS: return c->timeout_ms;
     case HVD_CFG_PACK_CTAS_PER_SM: return c->pack_ctas_per_sm;
     case HVD_CFG_PROFILE: return c->profile;
+    case HVD_CFG_SIGNAL_MODE: return c->sig_mode;
+    case HVD_CFG_FUSED: return c->fused;
     default: return -1;
   }
 }

@@ -177,7 +177,7 @@ def test_tuning_knobs_keep_bits(hvd):
         xs = workloads.all_ranks(counts, "f32", n)
         ref, _, _ = oracle.allreduce(xs, ["f32", "f32"], "average")
         L = hvd._lib
-        for ch, sl, th in [(1, 256, 128), (7, 4096, 256), (64, 1 << 20, 512), (16, 65536, 384)]:
+        for ch, sl, th in [(1, 256, 64), (7, 4096, 256), (64, 1 << 20, 384), (16, 65536, 128), (256, 512, 96)]:
             comm.set_config(L.HVD_CFG_CHANNELS, ch)
             comm.set_config(L.HVD_CFG_SLICE_BYTES, sl)
             comm.set_config(L.HVD_CFG_THREADS, th)
@@ -218,3 +218,37 @@ def test_model_gradient_sets_full_size(hvd, model, dtype, n):
     for r in range(n):
         for k in range(len(counts)):
             assert_same(got[r][k], ref[r][k], dtype, f"{model} r={r} k={k}")
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 8])
+def test_three_kernel_path_bitexact(hvd, n):
+    """HVD_CFG_FUSED=0: pack -> ring -> unpack as three launches; same bits as the fused kernel."""
+    comm = hvd.init_virtual(n, 0, 4 << 20)
+    try:
+        comm.set_config(hvd._lib.HVD_CFG_FUSED, 0)
+        counts = [3, 1000, 262_149, 5, 77_777]
+        xs = workloads.all_ranks(counts, "f32", n)
+        ref, _, plan = oracle.allreduce(xs, ["f32"] * len(counts), "average", threshold=1 << 20, capacity=4 << 20)
+        ts = [[to_torch(x, "f32") for x in xs[r]] for r in range(n)]
+        comm.allreduce(ts, op="average", fusion_threshold=1 << 20)
+        torch.cuda.synchronize()
+        st = comm.kernel_stats()
+        assert st["fused"][0] == 0 and st["pack"][0] == len(plan) and st["unpack"][0] == len(plan)
+        for r in range(n):
+            for k in range(len(counts)):
+                assert_same(from_torch(ts[r][k], "f32"), ref[r][k], "f32", f"r={r} k={k}")
+    finally:
+        comm.finalize()
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_large_plan_global_segment_table(hvd, n):
+    """> 4096 members per fusion buffer: the fused kernel reads the member table from global memory."""
+    counts = [int(c) for c in np.random.default_rng(5).integers(1, 40, size=5000)]
+    xs = workloads.all_ranks(counts, "bf16", n)
+    ref, _, plan = oracle.allreduce(xs, ["bf16"] * len(counts), "average")
+    assert len(plan) == 1 and len(plan[0].entries) > 4096
+    got = run_allreduce(hvd, xs, ["bf16"] * len(counts), "average", 64 << 20)
+    for r in range(n):
+        for k in range(0, len(counts), 7):
+            assert_same(got[r][k], ref[r][k], "bf16", f"r={r} k={k}")
