@@ -94,6 +94,12 @@ struct PackParams {
 
 // Fused zero-copy allreduce of one fusion buffer (pack + ring + unpack in one launch).
 constexpr int kFusedSmemSegs = 4096;  // member-offset table cached in shared memory up to this size
+constexpr int kPipe = 8;              // cp.async prefetch depth (rows of 16 B per data thread)
+constexpr int kMaxRingThreads = 384;  // data threads per ring / fused CTA
+inline size_t fused_smem_bytes(int nseg, int threads) {
+  const size_t vb = nseg <= kFusedSmemSegs ? (size_t)(nseg + 1) / 2 * 2 * 8 : 0;
+  return vb + 2ull * kPipe * threads * 16;
+}
 struct FusedParams {
   RingParams ring;
   const PackSeg* segs;               // [nseg]

@@ -494,92 +494,121 @@ __device__ __forceinline__ int seg_of(const FusedCtx& F, unsigned long long v, i
   return lo;
 }
 
+// Element-by-element paths (ragged member end, misaligned tensor, tail past the
+// last member) are out of line: they are rare and would otherwise inflate the
+// register allocation of the vector loop.
 template <int ESZ>
-__device__ __forceinline__ uint4 gather16(const FusedCtx& F, unsigned long long v, int& s, char*& tp,
-                                          unsigned long long& left) {
+__device__ __noinline__ uint4 gather_slow(const char* tp, unsigned long long left) {
+  constexpr int VEL = 16 / ESZ;
+  alignas(16) char tmp[16];
+#pragma unroll
+  for (int i = 0; i < VEL; ++i)
+#pragma unroll
+    for (int b = 0; b < ESZ; ++b) tmp[i * ESZ + b] = (unsigned long long)i < left ? tp[i * ESZ + b] : 0;
+  return *reinterpret_cast<const uint4*>(tmp);
+}
+
+template <int ESZ>
+__device__ __noinline__ void scatter_slow(char* tp, unsigned long long left, uint4 x) {
+  constexpr int VEL = 16 / ESZ;
+  const char* xb = reinterpret_cast<const char*>(&x);
+#pragma unroll
+  for (int i = 0; i < VEL; ++i)
+    if ((unsigned long long)i < left)
+#pragma unroll
+      for (int b = 0; b < ESZ; ++b) tp[i * ESZ + b] = xb[i * ESZ + b];
+}
+
+// Address of buffer vector v inside its member; `left` = member elements from there on.
+template <int ESZ>
+__device__ __forceinline__ char* member_ptr(const FusedCtx& F, unsigned long long v, int& s,
+                                            unsigned long long& left) {
   constexpr int VEL = 16 / ESZ;
   s = seg_of(F, v, s);
   const unsigned long long e0 = v * VEL - F.segs[s].dst_off;
   const unsigned long long cnt = F.segs[s].count;
-  tp = F.src[s] + e0 * ESZ;
   left = e0 < cnt ? cnt - e0 : 0;
-  uint4 x;
-  if (left >= (unsigned long long)VEL && ((reinterpret_cast<uintptr_t>(tp) & 15) == 0)) {
-    x = __ldcs(reinterpret_cast<const uint4*>(tp));
-  } else {  // ragged member end / misaligned tensor / tail past the last member: zero padding
-    alignas(16) char tmp[16];
-#pragma unroll
-    for (int i = 0; i < VEL; ++i)
-#pragma unroll
-      for (int b = 0; b < ESZ; ++b) tmp[i * ESZ + b] = (unsigned long long)i < left ? tp[i * ESZ + b] : 0;
-    x = *reinterpret_cast<const uint4*>(tmp);
-  }
-  return Pack16<ESZ>::conv(x, F.scale, F.scale_on, F.dtype);
+  return F.src[s] + e0 * ESZ;
 }
 
 template <int ESZ>
-__device__ __forceinline__ void scatter16(char* tp, unsigned long long left, const uint4& x) {
-  constexpr int VEL = 16 / ESZ;
-  if (left >= (unsigned long long)VEL && ((reinterpret_cast<uintptr_t>(tp) & 15) == 0)) {
-    *reinterpret_cast<uint4*>(tp) = x;
-  } else {
-    const char* xb = reinterpret_cast<const char*>(&x);
-#pragma unroll
-    for (int i = 0; i < VEL; ++i)
-      if ((unsigned long long)i < left)
-#pragma unroll
-        for (int b = 0; b < ESZ; ++b) tp[i * ESZ + b] = xb[i * ESZ + b];
-  }
+__device__ __forceinline__ bool fast16(const char* tp, unsigned long long left) {
+  return left >= (unsigned long long)(16 / ESZ) && ((reinterpret_cast<uintptr_t>(tp) & 15) == 0);
 }
 
-constexpr int kFusedUnroll = 4;
+// cp.async (LDGSTS) 16 B global -> shared, L2 only: the slice loop prefetches each
+// thread's own future vectors kPipe rows ahead into private shared-memory slots,
+// so kPipe x (1-2) x 16 B per thread are in flight without holding registers.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+               "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// One slice [lo, hi) of the fused kernel by the data threads.  Row j of the
+// slice is vector v = v_lo + j*nthr + tid.  slots0/slots1: [kPipe][nthr] uint4.
 template <class Op, int KIND>
 __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& me, unsigned long long lo,
-                                            unsigned long long hi, unsigned tid, unsigned nthr, int& sc) {
+                                            unsigned long long hi, unsigned tid, unsigned nthr, int& sc,
+                                            uint4* slots0, uint4* slots1) {
   constexpr int ESZ = Op::kEsz;
   constexpr int VEL = 16 / ESZ;
+  constexpr bool GATHER = KIND == kF_RS0 || KIND == kF_RS || KIND == kF_AG0 || KIND == kF_SOLO;
+  constexpr bool SCATTER = KIND == kF_AG0 || KIND == kF_AG || KIND == kF_FIN || KIND == kF_SOLO;
+  constexpr bool ADD = KIND == kF_RS || KIND == kF_AG0;
   const unsigned long long v_lo = lo / VEL;
   const unsigned long long v_hi = (hi + VEL - 1) / VEL;
-  for (unsigned long long v0 = v_lo + tid; v0 < v_hi; v0 += (unsigned long long)nthr * kFusedUnroll) {
-    uint4 x[kFusedUnroll], y[kFusedUnroll];
-    char* tp[kFusedUnroll];
-    unsigned long long left[kFusedUnroll];
-#pragma unroll
-    for (int u = 0; u < kFusedUnroll; ++u) {
-      const unsigned long long v = v0 + (unsigned long long)u * nthr;
-      if (v < v_hi) {
-        if (KIND == kF_RS0 || KIND == kF_RS || KIND == kF_AG0 || KIND == kF_SOLO) {
-          x[u] = gather16<ESZ>(F, v, sc, tp[u], left[u]);
-        } else {
-          x[u] = __ldcg(reinterpret_cast<const uint4*>(me.buf + v * 16));
-          int s2 = seg_of(F, v, sc);
-          sc = s2;
-          const unsigned long long e0 = v * VEL - F.segs[s2].dst_off;
-          const unsigned long long cnt = F.segs[s2].count;
-          tp[u] = F.src[s2] + e0 * ESZ;
-          left[u] = e0 < cnt ? cnt - e0 : 0;
-        }
-        if (KIND == kF_RS || KIND == kF_AG0) y[u] = __ldcg(reinterpret_cast<const uint4*>(me.scratch + v * 16));
+  if (v_hi <= v_lo + tid) return;
+  const int rows = (int)((v_hi - v_lo - tid + nthr - 1) / nthr);  // rows this thread owns
+  auto issue = [&](int j) {
+    if (j < rows) {
+      const unsigned long long v = v_lo + (unsigned long long)j * nthr + tid;
+      uint4* d0 = slots0 + (j % kPipe) * nthr + tid;
+      if (GATHER) {
+        unsigned long long left;
+        char* tp = member_ptr<ESZ>(F, v, sc, left);
+        if (fast16<ESZ>(tp, left)) cp_async16(d0, tp);
+      } else {
+        cp_async16(d0, me.buf + v * 16);
       }
+      if (ADD) cp_async16(slots1 + (j % kPipe) * nthr + tid, me.scratch + v * 16);
     }
+    cp_async_commit();  // one group per row, possibly empty: keeps wait_group counting uniform
+  };
 #pragma unroll
-    for (int u = 0; u < kFusedUnroll; ++u) {
-      const unsigned long long v = v0 + (unsigned long long)u * nthr;
-      if (v < v_hi) {
-        if (KIND == kF_RS || KIND == kF_AG0)
-          Op::template add_words<4>(reinterpret_cast<uint32_t*>(&x[u]), reinterpret_cast<const uint32_t*>(&y[u]));
-        if (KIND == kF_RS0 || KIND == kF_RS) *reinterpret_cast<uint4*>(me.nscratch + v * 16) = x[u];
-        if (KIND == kF_AG0 || KIND == kF_AG) *reinterpret_cast<uint4*>(me.nbuf + v * 16) = x[u];
-        if (KIND == kF_AG0 || KIND == kF_AG || KIND == kF_FIN || KIND == kF_SOLO) scatter16<ESZ>(tp[u], left[u], x[u]);
-      }
+  for (int j = 0; j < kPipe - 1; ++j) issue(j);
+  for (int j = 0; j < rows; ++j) {
+    issue(j + kPipe - 1);
+    cp_async_wait<kPipe - 1>();  // row j has landed in this thread's slots
+    const unsigned long long v = v_lo + (unsigned long long)j * nthr + tid;
+    unsigned long long left;
+    char* tp = member_ptr<ESZ>(F, v, sc, left);
+    uint4 x;
+    if (GATHER) {
+      x = fast16<ESZ>(tp, left) ? slots0[(j % kPipe) * nthr + tid] : gather_slow<ESZ>(tp, left);
+      x = Pack16<ESZ>::conv(x, F.scale, F.scale_on, F.dtype);
+    } else {
+      x = slots0[(j % kPipe) * nthr + tid];
+    }
+    if (ADD) {
+      const uint4 y = slots1[(j % kPipe) * nthr + tid];
+      Op::template add_words<4>(reinterpret_cast<uint32_t*>(&x), reinterpret_cast<const uint32_t*>(&y));
+    }
+    if (KIND == kF_RS0 || KIND == kF_RS) *reinterpret_cast<uint4*>(me.nscratch + v * 16) = x;
+    if (KIND == kF_AG0 || KIND == kF_AG) *reinterpret_cast<uint4*>(me.nbuf + v * 16) = x;
+    if (SCATTER) {
+      if (fast16<ESZ>(tp, left)) *reinterpret_cast<uint4*>(tp) = x;
+      else scatter_slow<ESZ>(tp, left, x);
     }
   }
+  cp_async_wait<0>();
 }
 
 template <class Op>
 __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_constant__ FusedParams P) {
-  extern __shared__ unsigned long long s_vbeg[];
+  extern __shared__ __align__(16) unsigned long long s_dyn[];
   const RingParams& R = P.ring;
   const RingRank& me = R.rk[blockIdx.y];
   const int ch = blockIdx.x;
@@ -591,6 +620,10 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
   const int nd = blockDim.x - 32;
   __shared__ int s_abort, s_done;
   const bool cache = P.nseg <= kFusedSmemSegs;
+  unsigned long long* s_vbeg = s_dyn;
+  const int ndata = blockDim.x - 32;
+  uint4* slots0 = reinterpret_cast<uint4*>(s_dyn + (cache ? (P.nseg + 1) / 2 * 2 : 0));
+  uint4* slots1 = slots0 + kPipe * ndata;
   if (cache)
     for (int j = threadIdx.x; j < P.nseg; j += blockDim.x) s_vbeg[j] = P.segs[j].vbeg;
   if (threadIdx.x == 0) {
@@ -617,7 +650,7 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
     for (int k = 0; k < K; ++k) {
       unsigned long long lo, hi;
       slice_range(R, 0, ch, k, lo, hi);
-      if (hi > lo) fused_slice<Op, kF_SOLO>(F, me, lo, hi, tid, nd, sc);
+      if (hi > lo) fused_slice<Op, kF_SOLO>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
     }
     return;
   }
@@ -630,11 +663,11 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
       unsigned long long lo, hi;
       slice_range(R, c, ch, k, lo, hi);
       if (hi > lo && !s_abort) {
-        if (t == T) fused_slice<Op, kF_FIN>(F, me, lo, hi, tid, nd, sc);
-        else if (rs && s == 0) fused_slice<Op, kF_RS0>(F, me, lo, hi, tid, nd, sc);
-        else if (rs) fused_slice<Op, kF_RS>(F, me, lo, hi, tid, nd, sc);
-        else if (s == 0) fused_slice<Op, kF_AG0>(F, me, lo, hi, tid, nd, sc);
-        else fused_slice<Op, kF_AG>(F, me, lo, hi, tid, nd, sc);
+        if (t == T) fused_slice<Op, kF_FIN>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
+        else if (rs && s == 0) fused_slice<Op, kF_RS0>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
+        else if (rs) fused_slice<Op, kF_RS>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
+        else if (s == 0) fused_slice<Op, kF_AG0>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
+        else fused_slice<Op, kF_AG>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
         if (t < T) sent += (hi - lo) * Op::kEsz;
       }
       if (t == T && k + 1 == K) break;
@@ -743,11 +776,11 @@ cudaError_t launch_ring(const RingParams& p, int dtype, int nch, int nlocal, int
 
 template <class Op>
 static cudaError_t launch_fused_t(const FusedParams& p, int nch, int nlocal, int threads, cudaStream_t s) {
-  const size_t smem = p.nseg <= kFusedSmemSegs ? (size_t)p.nseg * 8 : 0;
+  const size_t smem = fused_smem_bytes(p.nseg, threads);
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(fused_allreduce_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kFusedSmemSegs * 8);
+                                         (int)fused_smem_bytes(kFusedSmemSegs, kMaxRingThreads));
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -775,7 +808,7 @@ cudaError_t launch_fused(const FusedParams& p, int dtype, int nch, int nlocal, i
 }
 
 cudaError_t fused_max_ctas_per_sm(int dtype, int threads, int* out) {
-  const size_t smem = kFusedSmemSegs * 8;
+  const size_t smem = fused_smem_bytes(kFusedSmemSegs, threads);
   switch (dtype) {
     case 1: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fused_allreduce_kernel<OpF32>, threads + 32, smem);
     case 2: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fused_allreduce_kernel<OpBF16>, threads + 32, smem);

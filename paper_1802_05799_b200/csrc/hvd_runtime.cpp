@@ -66,8 +66,8 @@ struct hvd_comm {
   int* err_dev = nullptr;
   int sm_count = 148;
   // tuning (hvd_set_config)
-  int channels = 32;
-  int64_t slice_bytes = 256 << 10;
+  int channels = 128;
+  int64_t slice_bytes = 128 << 10;
   int threads = 384;
   int64_t timeout_ms = 30000;
   int pack_ctas_per_sm = 8;
@@ -566,6 +566,13 @@ int hvd_allreduce_buffer(hvd_comm* c, uint64_t count, int dtype, int op, void* s
   if (count == 0) return HVD_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   CK(cudaSetDevice(c->device));
+  if (c->fused) {
+    // the fusion buffer itself is the single member: the fused kernel reduces it in
+    // place (its AVERAGE prescale happens in the gather)
+    hvd_tensor t[kMaxLocal];
+    for (int l = 0; l < c->nlocal; ++l) t[l] = {c->rk[l].buf, count, dtype, 0};
+    return do_allreduce(c, t, 1, op, c->cap, s);
+  }
   if (op == HVD_AVERAGE) {
     char* bufs[kMaxLocal];
     for (int l = 0; l < c->nlocal; ++l) bufs[l] = c->rk[l].buf;

@@ -35,6 +35,8 @@ def main():
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--out", default="gpurun_out/sweep.json")
     ap.add_argument("--nccl", action="store_true")
+    ap.add_argument("--mode", default="ring", choices=["ring", "fused", "three"],
+                    help="ring: hvd_allreduce_buffer; fused/three: hvd_allreduce_average of one tensor")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
@@ -47,6 +49,15 @@ def main():
     rows = []
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ref = {}
+    grads = {mib: torch.randn((mib << 20) // esz, device="cuda").to(torch.float32 if esz == 4 else torch.bfloat16)
+             for mib in a.mib}
+    comm.set_config(L.HVD_CFG_FUSED, 1 if a.mode == "fused" else 0)
+
+    def call(mib, cnt):
+        if a.mode == "ring":
+            comm.allreduce_buffer(cnt, code, "sum")
+        else:
+            comm.allreduce_average([grads[mib]])
     for mib, ch, sl, th, sg in itertools.product(a.mib, a.channels, a.slice_kib, a.threads, a.fence_mode):
         comm.set_config(L.HVD_CFG_SIGNAL_MODE, sg)
         comm.set_config(L.HVD_CFG_CHANNELS, ch)
@@ -60,24 +71,30 @@ def main():
             fb = comm.fusion_buffer(0, torch.float32, cnt)
             res = []
             for rep in range(3):
-                fb.copy_(x)
-                comm.allreduce_buffer(cnt, code, "sum")
-                torch.cuda.synchronize()
-                res.append(fb.clone())
+                if a.mode == "ring":
+                    fb.copy_(x)
+                    comm.allreduce_buffer(cnt, code, "sum")
+                    torch.cuda.synchronize()
+                    res.append(fb.clone())
+                else:
+                    y = x.clone()
+                    comm.allreduce_average([y])
+                    torch.cuda.synchronize()
+                    res.append(y)
             if mib not in ref:
                 ref[mib] = res[0]
             ok = all(torch.equal(r.view(torch.int32), ref[mib].view(torch.int32)) for r in res)
         for _ in range(3):
-            comm.allreduce_buffer(cnt, code, "sum")
+            call(mib, cnt)
         torch.cuda.synchronize(); dist.barrier()
         ev0.record()
         for _ in range(a.iters):
-            comm.allreduce_buffer(cnt, code, "sum")
+            call(mib, cnt)
         ev1.record()
         torch.cuda.synchronize(); dist.barrier()
         us = tmax(ev0.elapsed_time(ev1) / a.iters * 1e3)
         bus = (mib << 20) / (us * 1e-6) / 1e9 * 2 * (world - 1) / world
-        rows.append({"impl": "hvd", "mib": mib, "channels": ch, "slice_kib": sl, "threads": th, "sig": sg,
+        rows.append({"impl": "hvd", "mode": a.mode, "mib": mib, "channels": ch, "slice_kib": sl, "threads": th, "sig": sg,
                      "us": us, "busbw": bus, "bitexact_vs_first": ok})
         if rank == 0:
             print(json.dumps(rows[-1]), flush=True)
