@@ -165,21 +165,42 @@ typedef enum {
   HVD_CFG_PACK_CTAS_PER_SM = 5,
   HVD_CFG_PROFILE = 6,       /* 1: record CUDA events around every kernel launch        */
   HVD_CFG_SIGNAL_MODE = 7,   /* ring signal: 1 fence.acq_rel.sys + relaxed store, 2 st.release.sys */
-  HVD_CFG_FUSED = 8          /* 1 (default): pack + ring + unpack in one zero-copy kernel per
+  HVD_CFG_FUSED = 8,         /* 1 (default): pack + ring + unpack in one zero-copy kernel per
                                 fusion buffer; 0: three kernels (pack, ring, unpack)       */
+  HVD_CFG_TIMELINE = 9,      /* > 0: record a device timeline of every fused launch with up to
+                                this many slice records per channel; 0: off (default)      */
+  HVD_CFG_WINDOW = 10,       /* fused: max slices per channel pushed but not yet fenced (0 = no
+                                limit): bounds the NVLink backlog and so the signal latency */
+  HVD_CFG_FIN_LAG = 11       /* fused: slices by which the final local scatter trails the last
+                                all-gather iteration (>= K-1: scatter after all of it)     */
 } hvd_config_key;
 /* Set a tuning knob; every rank must set identical values.  Errors: INVALID. */
 int hvd_set_config(hvd_comm* c, int key, int64_t value);
 int64_t hvd_get_config(const hvd_comm* c, int key);
 
 typedef enum { HVD_KERNEL_PACK = 0, HVD_KERNEL_RING = 1, HVD_KERNEL_UNPACK = 2, HVD_KERNEL_SCALE = 3,
-               HVD_KERNEL_FUSED = 4, HVD_KERNEL_KINDS = 5 } hvd_kernel_kind;
+               HVD_KERNEL_FUSED = 4, HVD_KERNEL_COPY = 5, HVD_KERNEL_KINDS = 6 } hvd_kernel_kind;
 /* Kernel launches of each kind since the last call (always counted) and, with
  * HVD_CFG_PROFILE on, the summed device time in ms between the CUDA events
  * recorded on the launch stream around each launch (waits for those events).
  * launches[HVD_KERNEL_KINDS], device_ms[HVD_KERNEL_KINDS]; counters reset.
  * Errors: INVALID, CUDA. */
 int hvd_kernel_stats(hvd_comm* c, uint64_t* launches, double* device_ms);
+
+/* Horovod Timeline ("view exactly what each node was doing at each time
+ * step"), recorded on the device: with HVD_CFG_TIMELINE on, the most recent fused
+ * launch of local rank `local` leaves, per channel, `slices` data records
+ * {t_begin, t_end} (ns, %globaltimer) of its slice operations in program order
+ * (iteration t = index / K: reduce-scatter t < N-1, all-gather after, the final
+ * local scatter last) followed, at word offset channels_max * words_per_channel,
+ * by `signals` records {t_publish, slices_published} of its signal warp.
+ * out == NULL returns only `info`; otherwise cap_words must be >= the buffer
+ * size (256 * words_per_channel * 2).  Synchronises the device.  Errors: INVALID. */
+typedef struct {
+  int32_t channels, slices, signals, K, T, rank, size, reserved;
+  uint64_t words_per_channel;
+} hvd_timeline_info;
+int hvd_timeline(hvd_comm* c, int local, uint64_t* out, uint64_t cap_words, hvd_timeline_info* info);
 
 /* ---- host-only plan inspection (no device needed) -------------------------------------------- */
 

@@ -160,8 +160,29 @@ class Comm:
         n = _lib.HVD_KERNEL_KINDS
         la, ms = (C.c_uint64 * n)(), (C.c_double * n)()
         check(lib.hvd_kernel_stats(self._h, la, ms), "hvd_kernel_stats")
-        names = ["pack", "ring", "unpack", "scale", "fused"]
+        names = ["pack", "ring", "unpack", "scale", "fused", "copy"]
         return {names[i]: (la[i], ms[i]) for i in range(n)}
+
+    def timeline(self, local: int = 0):
+        """Device timeline of the most recent fused launch (needs HVD_CFG_TIMELINE > 0).
+
+        Returns {"rank", "size", "K", "T", "channels", "data": [ch][slice] -> (t0, t1) ns,
+        "signals": [ch][j] -> (t, slices_published)} or None if nothing was recorded.
+        """
+        import numpy as np
+        info = _lib.hvd_timeline_info()
+        check(lib.hvd_timeline(self._h, int(local), None, 0, C.byref(info)), "hvd_timeline")
+        if info.channels == 0:
+            return None
+        words = _lib.MAX_CHANNELS * info.words_per_channel * 2
+        buf = np.zeros(words, dtype=np.uint64)
+        check(lib.hvd_timeline(self._h, int(local), buf.ctypes.data_as(C.POINTER(C.c_uint64)), words,
+                               C.byref(info)), "hvd_timeline")
+        wpc = info.words_per_channel
+        data = buf[:_lib.MAX_CHANNELS * wpc].reshape(_lib.MAX_CHANNELS, wpc // 2, 2)[:info.channels, :info.slices]
+        sig = buf[_lib.MAX_CHANNELS * wpc:].reshape(_lib.MAX_CHANNELS, wpc // 2, 2)[:info.channels, :info.signals]
+        return {"rank": info.rank, "size": info.size, "K": info.K, "T": info.T, "channels": info.channels,
+                "fin_lag": self.get_config(_lib.HVD_CFG_FIN_LAG), "data": data.copy(), "signals": sig.copy()}
 
     def poll_error(self) -> int:
         return lib.hvd_poll_error(self._h)

@@ -29,8 +29,13 @@ HVD_CFG_PACK_CTAS_PER_SM = 5
 HVD_CFG_PROFILE = 6
 HVD_CFG_SIGNAL_MODE = 7
 HVD_CFG_FUSED = 8
+HVD_CFG_TIMELINE = 9
+HVD_CFG_WINDOW = 10
+HVD_CFG_FIN_LAG = 11
+MAX_CHANNELS = 256
 HVD_KERNEL_PACK, HVD_KERNEL_RING, HVD_KERNEL_UNPACK, HVD_KERNEL_SCALE, HVD_KERNEL_FUSED = 0, 1, 2, 3, 4
-HVD_KERNEL_KINDS = 5
+HVD_KERNEL_COPY = 5
+HVD_KERNEL_KINDS = 6
 
 
 class hvd_tensor(C.Structure):
@@ -45,6 +50,12 @@ class hvd_plan_entry(C.Structure):
 class hvd_plan_buffer(C.Structure):
     _fields_ = [("dtype", C.c_int32), ("n_entries", C.c_int32), ("first_entry", C.c_int32),
                 ("reserved", C.c_int32), ("length", C.c_uint64)]
+
+
+class hvd_timeline_info(C.Structure):
+    _fields_ = [("channels", C.c_int32), ("slices", C.c_int32), ("signals", C.c_int32), ("K", C.c_int32),
+                ("T", C.c_int32), ("rank", C.c_int32), ("size", C.c_int32), ("reserved", C.c_int32),
+                ("words_per_channel", C.c_uint64)]
 
 
 class HvdError(RuntimeError):
@@ -85,6 +96,7 @@ def _load():
                                C.POINTER(C.c_int)]),
         "hvd_chunk_bounds": (C.c_int, [C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_uint64)]),
         "hvd_kernel_stats": (C.c_int, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_double)]),
+        "hvd_timeline": (C.c_int, [P, C.c_int, C.POINTER(C.c_uint64), C.c_uint64, C.POINTER(hvd_timeline_info)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -101,7 +113,7 @@ EXPORTS = sorted([
     "hvd_size", "hvd_local_ranks", "hvd_allreduce", "hvd_allreduce_average", "hvd_allreduce_buffer",
     "hvd_fusion_buffer", "hvd_fusion_capacity", "hvd_broadcast", "hvd_allgather", "hvd_poll_error",
     "hvd_strerror", "hvd_traffic", "hvd_set_config", "hvd_get_config", "hvd_plan", "hvd_chunk_bounds",
-    "hvd_kernel_stats",
+    "hvd_kernel_stats", "hvd_timeline",
 ])
 
 

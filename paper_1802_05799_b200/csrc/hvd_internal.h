@@ -36,6 +36,8 @@ struct RingRank {
   char* nbuf;                    // successor's fusion buffer (peer / same-device)
   char* nscratch;                // successor's scratch
   unsigned long long* nflags;    // successor's flags
+  unsigned long long* rflags;    // [kMaxChannels] ready flags, written by the successor (handshake)
+  unsigned long long* pready;    // predecessor's ready flags (this rank writes them)
   int rank;                      // ring rank
   int pad;
 };
@@ -59,14 +61,24 @@ struct RingParams {
   int root;                     // broadcast root
   int* err;                     // host-mapped error word (device address)
   unsigned long long timeout_ns;
-  int sig_mode;                 // signal fence variant (hvd_kernels.cu send_signal)
-  int pad2;
+  int sig_mode;                 // signal fence variant (hvd_kernels.cu signal_loop)
+  int tl_max;                   // timeline: slice records per channel (0 = timeline off)
+  unsigned long long* tl;       // timeline records of this launch (per local rank, see tl_words)
+  int window;                   // fused: max pushed-but-unfenced slices per channel (0 = no limit)
+  int fin_lag;                  // fused: final-scatter interleave lag in slices
+  unsigned long long epoch;     // copy collectives: handshake epoch of this launch
 };
+
+// Timeline buffer of one local rank (Horovod Timeline): for every
+// channel, tl_max data records {t_begin, t_end} (ns, %globaltimer) of its slice
+// operations in program order, then tl_max signal records {t_publish, count}.
+__host__ __device__ inline size_t tl_words(int tl_max) { return (size_t)kMaxChannels * tl_max * 4; }
 
 // Signals each channel sends per call (host keeps the per-channel base in step).
 inline unsigned long long ring_signals(int mode, int N, int K) {
   if (N <= 1) return 0;
   if (mode == kRingAllreduce) return 2ull * (N - 1) * K;
+  if (mode == kRingBroadcast) return (unsigned long long)K;
   return 1ull * (N - 1) * K;
 }
 
@@ -103,7 +115,8 @@ inline size_t fused_smem_bytes(int nseg, int threads) {
 struct FusedParams {
   RingParams ring;
   const PackSeg* segs;               // [nseg]
-  char* const* src;                  // [nlocal * nseg]
+  char* const* src;                  // [nlocal * nseg] gather addresses
+  char* const* dst;                  // [nlocal * nseg] scatter addresses (nullptr: same as src)
   const unsigned long long* vbeg_global;  // [nseg] (used when nseg > kFusedSmemSegs)
   int nseg;
   int scale_on;
@@ -113,6 +126,7 @@ struct FusedParams {
 
 // Launchers (hvd_kernels.cu).  All return a cudaError_t.
 cudaError_t launch_fused(const FusedParams& p, int dtype, int nch, int nlocal, int threads, cudaStream_t s);
+cudaError_t launch_copy(const FusedParams& p, int dtype, int nch, int nlocal, int threads, cudaStream_t s);
 cudaError_t fused_max_ctas_per_sm(int dtype, int threads, int* out);
 cudaError_t launch_pack(const PackParams& p, int dtype, int nlocal, int grid, int threads,
                         cudaStream_t s);

@@ -251,8 +251,9 @@ __device__ __forceinline__ int ld_acquire_cta_shared(const int* p) {
 
 // Signal warp body (lane 0): publish progress `*done` to the successor's counter.
 __device__ __forceinline__ void signal_loop(const int* done, int total, unsigned long long* nflag,
-                                            unsigned long long base, int sig_mode) {
-  int published = 0;
+                                            unsigned long long base, int sig_mode, int* pub = nullptr,
+                                            unsigned long long* tl_sig = nullptr, int tl_max = 0) {
+  int published = 0, nrec = 0;
   while (published < total) {
     int d;
     while ((d = ld_acquire_cta_shared(done)) == published) __nanosleep(32);
@@ -261,6 +262,12 @@ __device__ __forceinline__ void signal_loop(const int* done, int total, unsigned
       asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(nflag), "l"(base + (unsigned long long)d) : "memory");
     } else {
       st_release_sys(nflag, base + (unsigned long long)d);
+    }
+    if (pub) st_release_cta_shared(pub, d);
+    if (tl_sig && nrec < tl_max) {
+      tl_sig[2 * nrec] = globaltimer();
+      tl_sig[2 * nrec + 1] = (unsigned long long)d;
+      ++nrec;
     }
     published = d;
   }
@@ -472,11 +479,14 @@ __global__ void __launch_bounds__(256) pack_kernel(const __grid_constant__ PackP
 // exactly once before it is scattered (same CTA, program order), so the
 // in-place update of the caller's tensors is safe.  Results are bit-identical
 // to pack -> ring -> unpack: same per-element operations in the same order.
-enum FusedKind { kF_RS0 = 0, kF_RS = 1, kF_AG0 = 2, kF_AG = 3, kF_FIN = 4, kF_SOLO = 5 };
+enum FusedKind { kF_RS0 = 0, kF_RS = 1, kF_AG0 = 2, kF_AG = 3, kF_FIN = 4, kF_SOLO = 5,
+                 kF_G2B = 6,    // broadcast root:        nbuf <- gather(x)
+                 kF_G2BS = 7 }; // allgather own block:   nbuf <- gather(in); out <- same
 
 struct FusedCtx {
   const PackSeg* segs;
-  char* const* src;                 // this rank's tensor addresses [nseg]
+  char* const* src;                 // this rank's gather addresses [nseg]
+  char* const* dst;                 // this rank's scatter addresses [nseg] (== src for allreduce)
   const unsigned long long* vbeg;   // shared or global copy of segs[].vbeg
   int nseg;
   int scale_on;
@@ -519,16 +529,16 @@ __device__ __noinline__ void scatter_slow(char* tp, unsigned long long left, uin
       for (int b = 0; b < ESZ; ++b) tp[i * ESZ + b] = xb[i * ESZ + b];
 }
 
-// Address of buffer vector v inside its member; `left` = member elements from there on.
+// Byte offset of buffer vector v inside its member s; `left` = member elements from there on.
 template <int ESZ>
-__device__ __forceinline__ char* member_ptr(const FusedCtx& F, unsigned long long v, int& s,
-                                            unsigned long long& left) {
+__device__ __forceinline__ unsigned long long member_off(const FusedCtx& F, unsigned long long v, int& s,
+                                                         unsigned long long& left) {
   constexpr int VEL = 16 / ESZ;
   s = seg_of(F, v, s);
   const unsigned long long e0 = v * VEL - F.segs[s].dst_off;
   const unsigned long long cnt = F.segs[s].count;
   left = e0 < cnt ? cnt - e0 : 0;
-  return F.src[s] + e0 * ESZ;
+  return e0 * ESZ;
 }
 
 template <int ESZ>
@@ -555,9 +565,12 @@ __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& m
                                             uint4* slots0, uint4* slots1) {
   constexpr int ESZ = Op::kEsz;
   constexpr int VEL = 16 / ESZ;
-  constexpr bool GATHER = KIND == kF_RS0 || KIND == kF_RS || KIND == kF_AG0 || KIND == kF_SOLO;
-  constexpr bool SCATTER = KIND == kF_AG0 || KIND == kF_AG || KIND == kF_FIN || KIND == kF_SOLO;
+  constexpr bool GATHER = KIND == kF_RS0 || KIND == kF_RS || KIND == kF_AG0 || KIND == kF_SOLO ||
+                          KIND == kF_G2B || KIND == kF_G2BS;
+  constexpr bool SCATTER = KIND == kF_AG0 || KIND == kF_AG || KIND == kF_FIN || KIND == kF_SOLO || KIND == kF_G2BS;
   constexpr bool ADD = KIND == kF_RS || KIND == kF_AG0;
+  constexpr bool TO_NSCRATCH = KIND == kF_RS0 || KIND == kF_RS;
+  constexpr bool TO_NBUF = KIND == kF_AG0 || KIND == kF_AG || KIND == kF_G2B || KIND == kF_G2BS;
   const unsigned long long v_lo = lo / VEL;
   const unsigned long long v_hi = (hi + VEL - 1) / VEL;
   if (v_hi <= v_lo + tid) return;
@@ -568,7 +581,10 @@ __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& m
       uint4* d0 = slots0 + (j % kPipe) * nthr + tid;
       if (GATHER) {
         unsigned long long left;
-        char* tp = member_ptr<ESZ>(F, v, sc, left);
+        int s2 = sc;
+        const unsigned long long off = member_off<ESZ>(F, v, s2, left);
+        sc = s2;
+        const char* tp = F.src[s2] + off;
         if (fast16<ESZ>(tp, left)) cp_async16(d0, tp);
       } else {
         cp_async16(d0, me.buf + v * 16);
@@ -584,10 +600,11 @@ __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& m
     cp_async_wait<kPipe - 1>();  // row j has landed in this thread's slots
     const unsigned long long v = v_lo + (unsigned long long)j * nthr + tid;
     unsigned long long left;
-    char* tp = member_ptr<ESZ>(F, v, sc, left);
+    const unsigned long long off = member_off<ESZ>(F, v, sc, left);
     uint4 x;
     if (GATHER) {
-      x = fast16<ESZ>(tp, left) ? slots0[(j % kPipe) * nthr + tid] : gather_slow<ESZ>(tp, left);
+      const char* gp = F.src[sc] + off;
+      x = fast16<ESZ>(gp, left) ? slots0[(j % kPipe) * nthr + tid] : gather_slow<ESZ>(gp, left);
       x = Pack16<ESZ>::conv(x, F.scale, F.scale_on, F.dtype);
     } else {
       x = slots0[(j % kPipe) * nthr + tid];
@@ -596,14 +613,45 @@ __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& m
       const uint4 y = slots1[(j % kPipe) * nthr + tid];
       Op::template add_words<4>(reinterpret_cast<uint32_t*>(&x), reinterpret_cast<const uint32_t*>(&y));
     }
-    if (KIND == kF_RS0 || KIND == kF_RS) *reinterpret_cast<uint4*>(me.nscratch + v * 16) = x;
-    if (KIND == kF_AG0 || KIND == kF_AG) *reinterpret_cast<uint4*>(me.nbuf + v * 16) = x;
+    if (TO_NSCRATCH) *reinterpret_cast<uint4*>(me.nscratch + v * 16) = x;
+    if (TO_NBUF) *reinterpret_cast<uint4*>(me.nbuf + v * 16) = x;
     if (SCATTER) {
+      char* tp = F.dst[sc] + off;
       if (fast16<ESZ>(tp, left)) *reinterpret_cast<uint4*>(tp) = x;
       else scatter_slow<ESZ>(tp, left, x);
     }
   }
   cp_async_wait<0>();
+}
+
+// j-th operation of a fused launch -> (iteration t, slice k).  Iterations
+// 0..T-2 come in order; then the last all-gather iteration T-1 and the final
+// local scatter T are interleaved with a lag of `lag` slices:
+//   AG_0 .. AG_lag, then (FIN_p, AG_{p+lag+1}) for p = 0.., then the remaining FINs
+// (lag >= K-1: all AG slices first, then all FIN slices).
+__device__ __host__ __forceinline__ void fused_op(int j, int K, int T, int lag, int& t, int& k) {
+  const int head = (T - 1) * K;
+  if (j < head) {
+    t = j / K;
+    k = j - t * K;
+    return;
+  }
+  const int m = j - head;
+  const int first = lag + 1 < K ? lag + 1 : K;
+  if (m < first) {
+    t = T - 1;
+    k = m;
+    return;
+  }
+  const int q = m - first;
+  const int pairs = K - first;  // (FIN, AG) pairs
+  if (q < 2 * pairs) {
+    const int p = q >> 1;
+    if ((q & 1) == 0) { t = T; k = p; } else { t = T - 1; k = p + first; }
+  } else {
+    t = T;
+    k = pairs + (q - 2 * pairs);
+  }
 }
 
 template <class Op>
@@ -618,7 +666,7 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
   const unsigned long long base = R.base[ch];
   const int T = N > 1 ? 2 * (N - 1) : 0;
   const int nd = blockDim.x - 32;
-  __shared__ int s_abort, s_done;
+  __shared__ int s_abort, s_done, s_pub;
   const bool cache = P.nseg <= kFusedSmemSegs;
   unsigned long long* s_vbeg = s_dyn;
   const int ndata = blockDim.x - 32;
@@ -629,15 +677,22 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
   if (threadIdx.x == 0) {
     s_abort = 0;
     s_done = 0;
+    s_pub = 0;
   }
   __syncthreads();
   if (threadIdx.x >= nd) {
-    if (threadIdx.x == nd && T > 0) signal_loop(&s_done, T * K, me.nflags + ch, base, R.sig_mode);
+    if (threadIdx.x == nd && T > 0)
+      signal_loop(&s_done, T * K, me.nflags + ch, base, R.sig_mode, &s_pub,
+                  R.tl ? R.tl + tl_words(R.tl_max) * blockIdx.y + ((size_t)kMaxChannels + ch) * R.tl_max * 2 : nullptr,
+                  R.tl_max);
     return;
   }
+  unsigned long long* tl_d = R.tl ? R.tl + tl_words(R.tl_max) * blockIdx.y + (size_t)ch * R.tl_max * 2 : nullptr;
+  int nrec = 0;
   FusedCtx F;
   F.segs = P.segs;
   F.src = P.src + (size_t)blockIdx.y * P.nseg;
+  F.dst = (P.dst ? P.dst : P.src) + (size_t)blockIdx.y * P.nseg;
   F.vbeg = cache ? s_vbeg : P.vbeg_global;
   F.nseg = P.nseg;
   F.scale_on = P.scale_on;
@@ -650,44 +705,179 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
     for (int k = 0; k < K; ++k) {
       unsigned long long lo, hi;
       slice_range(R, 0, ch, k, lo, hi);
+      const unsigned long long tb = tl_d ? globaltimer() : 0;
       if (hi > lo) fused_slice<Op, kF_SOLO>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
+      if (tl_d && tid == 0 && nrec < R.tl_max) {
+        tl_d[2 * nrec] = tb;
+        tl_d[2 * nrec + 1] = globaltimer();
+        ++nrec;
+      }
     }
     return;
   }
   int i = 0;
-  for (int t = 0; t <= T; ++t) {  // t == T: scatter the chunk received in the last AG step
+  // Operation sequence: iterations t < T-1 in order, then the last all-gather step
+  // interleaved with the final local scatter one slice behind (fused_op), so the
+  // scatter of slice k overlaps the NVLink drain of slice k+1.
+  const int nops = (T + 1) * K;
+  for (int j = 0; j < nops; ++j) {
+    int t, k;
+    fused_op(j, K, T, R.fin_lag, t, k);
     const bool rs = t < N - 1;
     const int s = rs ? t : t - (N - 1);
     const int c = t == T ? mod(r + 2, N) : (rs ? mod(r - s, N) : mod(r + 1 - s, N));
-    for (int k = 0; k < K; ++k) {
-      unsigned long long lo, hi;
-      slice_range(R, c, ch, k, lo, hi);
-      if (hi > lo && !s_abort) {
-        if (t == T) fused_slice<Op, kF_FIN>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
-        else if (rs && s == 0) fused_slice<Op, kF_RS0>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
-        else if (rs) fused_slice<Op, kF_RS>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
-        else if (s == 0) fused_slice<Op, kF_AG0>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
-        else fused_slice<Op, kF_AG>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
-        if (t < T) sent += (hi - lo) * Op::kEsz;
-      }
-      if (t == T && k + 1 == K) break;
-      // retire + publish slice i, then wait for the next slice's dependency (same rule
-      // as the ring kernel; the final pseudo-iteration t == T depends on (T-1, k))
+    unsigned long long lo, hi;
+    slice_range(R, c, ch, k, lo, hi);
+    if (R.window > 0 && t < T && i > R.window) {
+      // flow control: at most `window` pushed-but-unfenced slices per channel, so the
+      // NVLink backlog (and hence fence / signal latency) stays short
+      if (tid == 0)
+        while (ld_acquire_cta_shared(&s_pub) < i - R.window) __nanosleep(64);
       bar_sync(kBarData, nd);
-      if (t < T) ++i;
-      if (tid == 0) {
-        if (t < T) st_release_cta_shared(&s_done, i);
-        const int tn = (k + 1 < K) ? t : t + 1;
-        const int kn = (k + 1 < K) ? k + 1 : 0;
-        const unsigned long long target = tn > 0 ? base + (unsigned long long)(tn - 1) * K + kn + 1 : 0;
-        if (target && !s_abort && !spin_until(me.flags + ch, target, R.err, R.timeout_ns)) s_abort = 1;
-      }
-      if (t + (k + 1 == K) > 0) bar_sync(kBarData, nd);
     }
+    const unsigned long long tb = tl_d ? globaltimer() : 0;
+    if (hi > lo && !s_abort) {
+      if (t == T) fused_slice<Op, kF_FIN>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
+      else if (rs && s == 0) fused_slice<Op, kF_RS0>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
+      else if (rs) fused_slice<Op, kF_RS>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
+      else if (s == 0) fused_slice<Op, kF_AG0>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
+      else fused_slice<Op, kF_AG>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
+      if (t < T) sent += (hi - lo) * Op::kEsz;
+    }
+    if (j + 1 == nops) {
+      if (tl_d && tid == 0 && nrec < R.tl_max) {
+        tl_d[2 * nrec] = tb;
+        tl_d[2 * nrec + 1] = globaltimer();
+      }
+      break;
+    }
+    // retire op j (publish it if it is a ring iteration), then wait for op j+1's
+    // dependency: the predecessor's (t'-1, k') — publishing first keeps the ring acyclic
+    bar_sync(kBarData, nd);
+    if (tl_d && tid == 0 && nrec < R.tl_max) {
+      tl_d[2 * nrec] = tb;
+      tl_d[2 * nrec + 1] = globaltimer();
+      ++nrec;
+    }
+    if (t < T) ++i;
+    int tn, kn;
+    fused_op(j + 1, K, T, R.fin_lag, tn, kn);
+    if (tid == 0) {
+      if (t < T) st_release_cta_shared(&s_done, i);
+      const unsigned long long target = tn > 0 ? base + (unsigned long long)(tn - 1) * K + kn + 1 : 0;
+      if (target && !s_abort && !spin_until(me.flags + ch, target, R.err, R.timeout_ns)) s_abort = 1;
+    }
+    if (tn > 0) bar_sync(kBarData, nd);
   }
   if (tid == 0) {
     atomicAdd(me.stats + 0, sent);
     if (ch == 0) atomicAdd(me.stats + 1, (unsigned long long)T);
+  }
+}
+
+// ------------------------------------------------------------------ broadcast / allgather
+// Copy collectives on the same machinery (fused_slice, counters, signal warp).
+//   broadcast: pipelined ring forward of the root's fusion buffer:
+//     root: nbuf <- gather(x); middle ranks: nbuf <- buf, x <- buf; the rank
+//     before the root: x <- buf.  One signal per slice on every rank.
+//   allgather (R12): ring all-gather of one block per rank (block b at b*q):
+//     t = 0: nbuf[r] <- in, out[r] <- in; t >= 1: nbuf[r-t] <- buf, out[r-t] <- buf;
+//     final: out[r+1] <- buf.  (N-1)K signals.
+// Unlike the allreduce, a rank's first write into its successor's fusion buffer
+// can race with the successor still reading that buffer for the previous
+// collective, so each launch starts with a handshake: every channel writes
+// "ready for epoch e" into its predecessor's ready flag, and waits for its
+// successor's before its first remote store.
+template <class Op>
+__global__ void __launch_bounds__(416, 1) copy_collective_kernel(const __grid_constant__ FusedParams P) {
+  extern __shared__ __align__(16) unsigned long long s_dyn[];
+  const RingParams& R = P.ring;
+  const RingRank& me = R.rk[blockIdx.y];
+  const int ch = blockIdx.x;
+  const int N = R.N;
+  const int r = me.rank;
+  const int K = R.K;
+  const unsigned long long base = R.base[ch];
+  const bool bcast = R.mode == kRingBroadcast;
+  const int T = N - 1;  // allgather ring iterations
+  const int nsig = bcast ? K : T * K;
+  const int nd = blockDim.x - 32;
+  __shared__ int s_abort, s_done, s_pub;
+  const bool cache = P.nseg <= kFusedSmemSegs;
+  unsigned long long* s_vbeg = s_dyn;
+  uint4* slots0 = reinterpret_cast<uint4*>(s_dyn + (cache ? (P.nseg + 1) / 2 * 2 : 0));
+  uint4* slots1 = slots0 + kPipe * nd;
+  if (cache)
+    for (int j = threadIdx.x; j < P.nseg; j += blockDim.x) s_vbeg[j] = P.segs[j].vbeg;
+  if (threadIdx.x == 0) {
+    s_abort = 0;
+    s_done = 0;
+    s_pub = 0;
+    st_release_sys(me.pready + ch, R.epoch);  // this rank's buffers are free for this launch
+  }
+  __syncthreads();
+  if (threadIdx.x >= nd) {
+    if (threadIdx.x == nd) signal_loop(&s_done, nsig, me.nflags + ch, base, R.sig_mode, &s_pub);
+    return;
+  }
+  FusedCtx F;
+  F.segs = P.segs;
+  F.src = P.src + (size_t)blockIdx.y * P.nseg;
+  F.dst = (P.dst ? P.dst : P.src) + (size_t)blockIdx.y * P.nseg;
+  F.vbeg = cache ? s_vbeg : P.vbeg_global;
+  F.nseg = P.nseg;
+  F.scale_on = 0;
+  F.scale = 1.0f;
+  F.dtype = P.dtype;
+  const unsigned tid = threadIdx.x;
+  int sc = 0;
+  unsigned long long sent = 0;
+  bool ready = false;  // successor's handshake seen
+  const int d = mod(r - R.root, N);  // broadcast: distance from the root
+  const int nops = bcast ? K : (T + 1) * K;
+  int i = 0;
+  for (int j = 0; j < nops; ++j) {
+    int t, k, c, kind;
+    if (bcast) {
+      t = 0;
+      k = j;
+      c = 0;
+      kind = d == 0 ? kF_G2B : (d == N - 1 ? kF_FIN : kF_AG);
+    } else {
+      fused_op(j, K, T, R.fin_lag, t, k);
+      c = t == T ? mod(r + 1, N) : mod(r - t, N);
+      kind = t == T ? kF_FIN : (t == 0 ? kF_G2BS : kF_AG);
+    }
+    const bool remote = kind != kF_FIN;
+    // dependency: the predecessor's slice (broadcast: same k; allgather: (t-1, k))
+    unsigned long long target = 0;
+    if (bcast && d > 0) target = base + (unsigned long long)k + 1;
+    if (!bcast && t > 0) target = base + (unsigned long long)(t - 1) * K + k + 1;
+    if (tid == 0 && !s_abort) {
+      if (target && !spin_until(me.flags + ch, target, R.err, R.timeout_ns)) s_abort = 1;
+      if (remote && !ready && !s_abort && !spin_until(me.rflags + ch, R.epoch, R.err, R.timeout_ns)) s_abort = 1;
+    }
+    if (remote) ready = true;
+    bar_sync(kBarData, nd);
+    unsigned long long lo, hi;
+    slice_range(R, c, ch, k, lo, hi);
+    if (hi > lo && !s_abort) {
+      if (kind == kF_G2B) fused_slice<Op, kF_G2B>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
+      else if (kind == kF_G2BS) fused_slice<Op, kF_G2BS>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
+      else if (kind == kF_AG) fused_slice<Op, kF_AG>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
+      else fused_slice<Op, kF_FIN>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
+      if (remote) sent += (hi - lo) * Op::kEsz;
+    }
+    bar_sync(kBarData, nd);
+    // every ring iteration (broadcast: every slice, even without data) is signalled
+    if (bcast || t < T) {
+      ++i;
+      if (tid == 0) st_release_cta_shared(&s_done, i);
+    }
+  }
+  if (tid == 0) {
+    atomicAdd(me.stats + 0, sent);
+    if (ch == 0) atomicAdd(me.stats + 1, (unsigned long long)(bcast ? (d == N - 1 ? 0 : 1) : T));
   }
 }
 
@@ -803,6 +993,39 @@ cudaError_t launch_fused(const FusedParams& p, int dtype, int nch, int nlocal, i
     case 2: return launch_fused_t<OpBF16>(p, nch, nlocal, threads, s);
     case 3: return launch_fused_t<OpI32>(p, nch, nlocal, threads, s);
     case 4: return launch_fused_t<OpI64>(p, nch, nlocal, threads, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <class Op>
+static cudaError_t launch_copy_t(const FusedParams& p, int nch, int nlocal, int threads, cudaStream_t s) {
+  const size_t smem = fused_smem_bytes(p.nseg, threads);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(copy_collective_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)fused_smem_bytes(kFusedSmemSegs, kMaxRingThreads));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nch, nlocal);
+  cfg.blockDim = dim3(threads + 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, copy_collective_kernel<Op>, p);
+}
+
+// Copy collectives only move bytes: dispatch on the element size.
+cudaError_t launch_copy(const FusedParams& p, int dtype, int nch, int nlocal, int threads, cudaStream_t s) {
+  switch (elem_size(dtype)) {
+    case 4: return launch_copy_t<OpI32>(p, nch, nlocal, threads, s);
+    case 2: return launch_copy_t<OpBF16>(p, nch, nlocal, threads, s);
+    case 8: return launch_copy_t<OpI64>(p, nch, nlocal, threads, s);
     default: return cudaErrorInvalidValue;
   }
 }

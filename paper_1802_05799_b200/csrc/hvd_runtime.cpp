@@ -22,7 +22,7 @@ using namespace hvd;
 namespace {
 
 constexpr uint64_t kDefaultFusionBytes = 64ull << 20;  // P:L368-369 "Default ... 64 MB" (R9)
-constexpr uint64_t kTailBytes = 4096;                   // flags + stats after buf and scratch
+constexpr uint64_t kTailBytes = 8192;                   // flags, stats, ready flags after buf and scratch
 constexpr uint32_t kBlobMagic = 0x48564442u;            // "HVDB"
 constexpr int kPackThreads = 256;
 constexpr int kPackVecsPerThread = 8;
@@ -42,6 +42,7 @@ struct DevPlanBuffer {
   uint64_t L;
   PackParams pp;                        // device pointers filled in
   const unsigned long long* vbeg;       // [nseg] member start vectors (fused kernel, large plans)
+  char* const* dst = nullptr;           // [nlocal * nseg] scatter addresses (nullptr: = pp.src)
 };
 
 struct CachedPlan {
@@ -67,13 +68,20 @@ struct hvd_comm {
   int sm_count = 148;
   // tuning (hvd_set_config)
   int channels = 128;
-  int64_t slice_bytes = 128 << 10;
+  int64_t slice_bytes = 64 << 10;
   int threads = 384;
   int64_t timeout_ms = 30000;
   int pack_ctas_per_sm = 8;
   int profile = 0;
   int sig_mode = 1;
   int fused = 1;
+  int window = 0;
+  int fin_lag = 1;
+  unsigned long long hs_epoch = 0;  // copy-collective handshake epochs issued
+  // timeline (HVD_CFG_TIMELINE): device records of the most recent fused launch
+  int tl_max = 0;
+  unsigned long long* tl = nullptr;
+  int tl_nch = 0, tl_K = 0, tl_T = 0, tl_slices = 0;
   std::list<CachedPlan> cache;
   // launch statistics (hvd_kernel_stats)
   uint64_t launches[HVD_KERNEL_KINDS] = {};
@@ -103,6 +111,9 @@ unsigned long long* flags_of(char* region, uint64_t cap) {
 unsigned long long* stats_of(char* region, uint64_t cap) {
   return reinterpret_cast<unsigned long long*>(region + 2 * cap + kMaxChannels * 8);
 }
+unsigned long long* rflags_of(char* region, uint64_t cap) {
+  return reinterpret_cast<unsigned long long*>(region + 2 * cap + 4096);
+}
 
 int common_init(hvd_comm* c, uint64_t fusion_bytes) {
   c->cap = ((fusion_bytes ? fusion_bytes : kDefaultFusionBytes) + 4095) / 4096 * 4096;
@@ -120,16 +131,18 @@ int common_init(hvd_comm* c, uint64_t fusion_bytes) {
     r.scratch = scratch_of(c->region[l], c->cap);
     r.flags = flags_of(c->region[l], c->cap);
     r.stats = stats_of(c->region[l], c->cap);
+    r.rflags = rflags_of(c->region[l], c->cap);
     r.rank = c->virt ? l : c->rank;
   }
   CK(cudaDeviceSynchronize());
   return HVD_OK;
 }
 
-void set_successor(RingRank& r, char* succ_region, uint64_t cap) {
+void set_neighbours(RingRank& r, char* succ_region, char* pred_region, uint64_t cap) {
   r.nbuf = buf_of(succ_region);
   r.nscratch = scratch_of(succ_region, cap);
   r.nflags = flags_of(succ_region, cap);
+  r.pready = rflags_of(pred_region, cap);
 }
 
 int check_live(hvd_comm* c) {
@@ -148,60 +161,55 @@ void free_plan(CachedPlan& p) {
 }
 
 size_t align256(size_t v) { return (v + 255) / 256 * 256; }
-unsigned long long e_vbeg(const hvd_plan_entry& e, uint64_t vel) { return e.dst_off / vel; }
 
 // Build (or fetch) the device-resident pack/unpack tables of the plan of the
 // tensor list `t` (n per local rank).  The key is every tensor's address,
 // count and dtype plus the threshold, so repeated calls on the same gradient
 // tensors (the training loop) reuse the uploaded tables.
-int get_plan(hvd_comm* c, const hvd_tensor* t, int n, uint64_t threshold, cudaStream_t s,
-             CachedPlan** out) {
-  std::vector<uint64_t> key;
-  key.reserve(3 + 3 * (size_t)n * c->nlocal);
-  key.push_back(threshold);
-  key.push_back((uint64_t)n);
-  key.push_back((uint64_t)c->nlocal);
-  for (int i = 0; i < n * c->nlocal; ++i) {
-    key.push_back(reinterpret_cast<uint64_t>(t[i].data));
-    key.push_back(t[i].count);
-    key.push_back((uint64_t)t[i].dtype);
-  }
+// Host description of one fusion buffer's member table (before upload).
+struct HostBuf {
+  int dtype = 0;
+  uint64_t L = 0;                 // elements
+  std::vector<PackSeg> segs;      // dst_off / count / vbeg per member
+  std::vector<char*> src;         // [nlocal * nseg] gather addresses
+  std::vector<char*> dst;         // [nlocal * nseg] scatter addresses; empty = same as src
+};
+
+CachedPlan* lookup_plan(hvd_comm* c, const std::vector<uint64_t>& key) {
   for (auto it = c->cache.begin(); it != c->cache.end(); ++it) {
     if (it->key == key) {
       c->cache.splice(c->cache.begin(), c->cache, it);
-      *out = &c->cache.front();
-      return HVD_OK;
+      return &c->cache.front();
     }
   }
-  std::vector<uint64_t> counts(n);
-  std::vector<int32_t> dtypes(n);
-  for (int k = 0; k < n; ++k) {
-    counts[k] = t[k].count;
-    dtypes[k] = t[k].dtype;
-  }
-  std::vector<hvd_plan_entry> ents;
-  std::vector<hvd_plan_buffer> bufs;
-  int st = build_plan(counts.data(), dtypes.data(), n, threshold, c->cap, &ents, &bufs);
-  if (st != HVD_OK) return st;
+  return nullptr;
+}
 
-  // layout: per buffer [segs][src table][tile_seg]
-  struct Off { size_t segs, src, tiles, vbeg; uint64_t nvec, ntiles; };
-  std::vector<Off> offs(bufs.size());
+// Upload the member tables of `hb` (one device allocation, one H2D copy on the
+// stream) and cache them under `key` (LRU of kPlanCacheSize plans).
+int upload_plan(hvd_comm* c, std::vector<uint64_t> key, const std::vector<HostBuf>& hb, cudaStream_t s,
+                CachedPlan** out) {
+  // layout per buffer: [segs][src][dst][tile_seg][vbeg]
+  struct Off { size_t segs, src, dst, tiles, vbeg; uint64_t nvec, ntiles; };
+  std::vector<Off> offs(hb.size());
   const uint64_t tile_vecs = (uint64_t)kPackThreads * kPackVecsPerThread;
   size_t total = 0;
-  for (size_t b = 0; b < bufs.size(); ++b) {
-    const int esz = elem_size(bufs[b].dtype);
+  for (size_t b = 0; b < hb.size(); ++b) {
+    const int esz = elem_size(hb[b].dtype);
     const uint64_t vel = kPackVecBytes / esz;
-    offs[b].nvec = (bufs[b].length + vel - 1) / vel;
+    const size_t nseg = hb[b].segs.size();
+    offs[b].nvec = (hb[b].L + vel - 1) / vel;
     offs[b].ntiles = (offs[b].nvec + tile_vecs - 1) / tile_vecs;
     offs[b].segs = total;
-    total = align256(total + sizeof(PackSeg) * bufs[b].n_entries);
+    total = align256(total + sizeof(PackSeg) * nseg);
     offs[b].src = total;
-    total = align256(total + sizeof(char*) * bufs[b].n_entries * c->nlocal);
+    total = align256(total + sizeof(char*) * nseg * c->nlocal);
+    offs[b].dst = total;
+    if (!hb[b].dst.empty()) total = align256(total + sizeof(char*) * nseg * c->nlocal);
     offs[b].tiles = total;
     total = align256(total + sizeof(int) * (offs[b].ntiles + 1));
     offs[b].vbeg = total;
-    total = align256(total + sizeof(unsigned long long) * bufs[b].n_entries);
+    total = align256(total + sizeof(unsigned long long) * nseg);
   }
   CachedPlan p;
   p.key = std::move(key);
@@ -214,46 +222,41 @@ int get_plan(hvd_comm* c, const hvd_tensor* t, int n, uint64_t threshold, cudaSt
   }
   char* h = static_cast<char*>(p.hmem);
   char* d = static_cast<char*>(p.dmem);
-  for (size_t b = 0; b < bufs.size(); ++b) {
-    const hvd_plan_buffer& pb = bufs[b];
-    const int esz = elem_size(pb.dtype);
-    const uint64_t vel = kPackVecBytes / esz;
+  for (size_t b = 0; b < hb.size(); ++b) {
+    const HostBuf& B = hb[b];
+    const int nseg = (int)B.segs.size();
     PackSeg* segs = reinterpret_cast<PackSeg*>(h + offs[b].segs);
     char** src = reinterpret_cast<char**>(h + offs[b].src);
     int* tiles = reinterpret_cast<int*>(h + offs[b].tiles);
     unsigned long long* vb = reinterpret_cast<unsigned long long*>(h + offs[b].vbeg);
-    for (int j = 0; j < pb.n_entries; ++j) {
-      vb[j] = e_vbeg(ents[pb.first_entry + j], vel);
-      const hvd_plan_entry& e = ents[pb.first_entry + j];
-      segs[j].dst_off = e.dst_off;
-      segs[j].count = e.count;
-      segs[j].vbeg = e.dst_off / vel;
-      segs[j].pad = 0;
-      for (int l = 0; l < c->nlocal; ++l)
-        src[(size_t)l * pb.n_entries + j] =
-            static_cast<char*>(t[(size_t)l * n + e.tensor].data) + e.src_off * esz;
+    for (int j = 0; j < nseg; ++j) {
+      segs[j] = B.segs[j];
+      vb[j] = B.segs[j].vbeg;
     }
+    std::memcpy(src, B.src.data(), sizeof(char*) * B.src.size());
+    if (!B.dst.empty()) std::memcpy(h + offs[b].dst, B.dst.data(), sizeof(char*) * B.dst.size());
     // tile -> member of its first vector (merge walk); last entry = last member
     int sidx = 0;
     for (uint64_t tile = 0; tile < offs[b].ntiles; ++tile) {
       const uint64_t v = tile * tile_vecs;
-      while (sidx + 1 < pb.n_entries && segs[sidx + 1].vbeg <= v) ++sidx;
+      while (sidx + 1 < nseg && segs[sidx + 1].vbeg <= v) ++sidx;
       tiles[tile] = sidx;
     }
-    tiles[offs[b].ntiles] = pb.n_entries - 1;
+    tiles[offs[b].ntiles] = nseg - 1;
     DevPlanBuffer db;
-    db.dtype = pb.dtype;
-    db.L = pb.length;
+    db.dtype = B.dtype;
+    db.L = B.L;
     std::memset(&db.pp, 0, sizeof(db.pp));
     db.pp.segs = reinterpret_cast<const PackSeg*>(d + offs[b].segs);
     db.pp.src = reinterpret_cast<char* const*>(d + offs[b].src);
+    db.dst = B.dst.empty() ? nullptr : reinterpret_cast<char* const*>(d + offs[b].dst);
     db.pp.tile_seg = reinterpret_cast<const int*>(d + offs[b].tiles);
     db.vbeg = reinterpret_cast<const unsigned long long*>(d + offs[b].vbeg);
     for (int l = 0; l < c->nlocal; ++l) db.pp.buf[l] = c->rk[l].buf;
     db.pp.nvec = offs[b].nvec;
     db.pp.tile_vecs = tile_vecs;
     db.pp.ntiles = offs[b].ntiles;
-    db.pp.nseg = pb.n_entries;
+    db.pp.nseg = nseg;
     p.bufs.push_back(db);
   }
   if (total) {
@@ -270,6 +273,53 @@ int get_plan(hvd_comm* c, const hvd_tensor* t, int n, uint64_t threshold, cudaSt
   c->cache.push_front(std::move(p));
   *out = &c->cache.front();
   return HVD_OK;
+}
+
+// Tensor Fusion plan (hvd_plan.cpp) of the tensor list `t` (n per local rank),
+// uploaded and cached by (addresses, counts, dtypes, threshold): a training loop
+// that reduces the same gradient tensors every step uploads its tables once.
+int get_plan(hvd_comm* c, const hvd_tensor* t, int n, uint64_t threshold, cudaStream_t s,
+             CachedPlan** out) {
+  std::vector<uint64_t> key;
+  key.reserve(4 + 3 * (size_t)n * c->nlocal);
+  key.push_back(0x504c414eull);  // "PLAN"
+  key.push_back(threshold);
+  key.push_back((uint64_t)n);
+  key.push_back((uint64_t)c->nlocal);
+  for (int i = 0; i < n * c->nlocal; ++i) {
+    key.push_back(reinterpret_cast<uint64_t>(t[i].data));
+    key.push_back(t[i].count);
+    key.push_back((uint64_t)t[i].dtype);
+  }
+  if ((*out = lookup_plan(c, key))) return HVD_OK;
+  std::vector<uint64_t> counts(n);
+  std::vector<int32_t> dtypes(n);
+  for (int k = 0; k < n; ++k) {
+    counts[k] = t[k].count;
+    dtypes[k] = t[k].dtype;
+  }
+  std::vector<hvd_plan_entry> ents;
+  std::vector<hvd_plan_buffer> bufs;
+  int st = build_plan(counts.data(), dtypes.data(), n, threshold, c->cap, &ents, &bufs);
+  if (st != HVD_OK) return st;
+  std::vector<HostBuf> hb(bufs.size());
+  for (size_t b = 0; b < bufs.size(); ++b) {
+    const hvd_plan_buffer& pb = bufs[b];
+    const int esz = elem_size(pb.dtype);
+    const uint64_t vel = kPackVecBytes / esz;
+    hb[b].dtype = pb.dtype;
+    hb[b].L = pb.length;
+    hb[b].segs.resize(pb.n_entries);
+    hb[b].src.resize((size_t)pb.n_entries * c->nlocal);
+    for (int j = 0; j < pb.n_entries; ++j) {
+      const hvd_plan_entry& e = ents[pb.first_entry + j];
+      hb[b].segs[j] = {e.dst_off, e.count, e.dst_off / vel, 0};
+      for (int l = 0; l < c->nlocal; ++l)
+        hb[b].src[(size_t)l * pb.n_entries + j] =
+            static_cast<char*>(t[(size_t)l * n + e.tensor].data) + e.src_off * esz;
+    }
+  }
+  return upload_plan(c, std::move(key), hb, s, out);
 }
 
 // ------------------------------------------------------------------ launch accounting
@@ -306,14 +356,15 @@ int launch_counted(hvd_comm* c, int kind, cudaStream_t s, F&& launch) {
 // Split one buffer of L elements for the ring kernel and launch it.
 // Split one buffer of L elements into chunks / channels / slices (R2) for the
 // ring or fused kernel.  Returns the channel count.
-int make_ring_params(hvd_comm* c, uint64_t L, int dtype, bool fused, RingParams* P, int* nch_out) {
+int make_ring_params(hvd_comm* c, uint64_t L, int dtype, bool fused, RingParams* P, int* nch_out,
+                     uint64_t q_override = 0) {
   const int esz = elem_size(dtype);
   const uint64_t g = kChunkQuantum / esz;
   std::memset(P, 0, sizeof(*P));
   for (int l = 0; l < c->nlocal; ++l) P->rk[l] = c->rk[l];
   P->N = c->size;
   P->L = L;
-  P->q = chunk_len(L, c->size, dtype);
+  P->q = q_override ? q_override : chunk_len(L, c->size, dtype);
   // channels: at least 32 KiB of every chunk per channel, at most the knob and
   // what stays co-resident (the CTAs of all ranks wait on each other)
   int max_per_sm = 1;
@@ -330,6 +381,10 @@ int make_ring_params(hvd_comm* c, uint64_t L, int dtype, bool fused, RingParams*
   P->err = c->err_dev;
   P->timeout_ns = (unsigned long long)c->timeout_ms * 1000000ull;
   P->sig_mode = c->sig_mode;
+  P->tl = c->tl;
+  P->window = c->window;
+  P->fin_lag = c->fin_lag;
+  P->tl_max = c->tl ? c->tl_max : 0;
   for (int ch = 0; ch < kMaxChannels; ++ch) P->base[ch] = c->base[ch];
   *nch_out = nch;
   return HVD_OK;
@@ -361,6 +416,7 @@ int enqueue_fused(hvd_comm* c, DevPlanBuffer& b, cudaStream_t s) {
   if (st != HVD_OK) return st;
   F.segs = b.pp.segs;
   F.src = b.pp.src;
+  F.dst = b.dst;
   F.vbeg_global = b.vbeg;
   F.nseg = b.pp.nseg;
   F.scale_on = b.pp.scale_on;
@@ -368,6 +424,12 @@ int enqueue_fused(hvd_comm* c, DevPlanBuffer& b, cudaStream_t s) {
   F.dtype = b.dtype;
   st = launch_counted(c, HVD_KERNEL_FUSED, s, [&] { return launch_fused(F, b.dtype, nch, c->nlocal, c->threads, s); });
   if (st != HVD_OK) return st;
+  if (c->tl) {
+    c->tl_nch = nch;
+    c->tl_K = F.ring.K;
+    c->tl_T = c->size > 1 ? 2 * (c->size - 1) : 0;
+    c->tl_slices = c->size > 1 ? (c->tl_T + 1) * F.ring.K : F.ring.K;
+  }
   advance_base(c, F.ring, nch);
   return HVD_OK;
 }
@@ -436,7 +498,7 @@ int hvd_init(int rank, int size, int device, uint64_t fusion_bytes, hvd_comm** o
     return st;
   }
   if (size == 1) {
-    set_successor(c->rk[0], c->region[0], c->cap);
+    set_neighbours(c->rk[0], c->region[0], c->region[0], c->cap);
     c->connected = true;
   }
   *out = c;
@@ -457,7 +519,8 @@ int hvd_init_virtual(int size, int device, uint64_t fusion_bytes, hvd_comm** out
     hvd_finalize(c);
     return st;
   }
-  for (int l = 0; l < size; ++l) set_successor(c->rk[l], c->region[(l + 1) % size], c->cap);
+  for (int l = 0; l < size; ++l)
+    set_neighbours(c->rk[l], c->region[(l + 1) % size], c->region[(l + size - 1) % size], c->cap);
   c->connected = true;
   *out = c;
   return HVD_OK;
@@ -515,7 +578,7 @@ int hvd_connect(hvd_comm* c, const void* blobs, uint64_t len_each) {
   } else {
     c->pred_region = c->peer_region;
   }
-  set_successor(c->rk[0], c->peer_region, c->cap);
+  set_neighbours(c->rk[0], c->peer_region, c->pred_region, c->cap);
   c->connected = true;
   return HVD_OK;
 }
@@ -537,6 +600,7 @@ int hvd_finalize(hvd_comm* c) {
     for (int l = 0; l < kMaxLocal; ++l)
       if (c->region[l]) cudaFree(c->region[l]);
     if (c->err_host) cudaFreeHost(c->err_host);
+    if (c->tl) cudaFree(c->tl);
     c->closed = true;
   }
   delete c;
@@ -592,18 +656,121 @@ void* hvd_fusion_buffer(hvd_comm* c, int local) {
 uint64_t hvd_fusion_capacity(const hvd_comm* c) { return c ? c->cap : 0; }
 
 int hvd_broadcast(hvd_comm* c, const hvd_tensor* t, int n, int root, void* stream) {
-  (void)t; (void)n; (void)stream;
   int st = check_live(c);
   if (st != HVD_OK) return st;
-  if (root < 0 || root >= c->size) return HVD_ERR_INVALID;
-  return HVD_ERR_UNSUPPORTED;  // ring broadcast: next milestone
+  if (root < 0 || root >= c->size || n < 0 || (n > 0 && !t)) return HVD_ERR_INVALID;
+  for (int k = 0; k < n; ++k) {
+    if (elem_size(t[k].dtype) == 0) return HVD_ERR_UNSUPPORTED;
+    for (int l = 0; l < c->nlocal; ++l) {
+      const hvd_tensor& x = t[(size_t)l * n + k];
+      if (x.count != t[k].count || x.dtype != t[k].dtype) return HVD_ERR_INVALID;
+      if (x.count && !x.data) return HVD_ERR_INVALID;
+    }
+  }
+  if (n == 0 || c->size == 1) return HVD_OK;  // N = 1: the root's tensors are the result
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(c->device));
+  CachedPlan* plan = nullptr;
+  st = get_plan(c, t, n, c->cap, s, &plan);  // fuse the tensors into as few buffers as possible
+  if (st != HVD_OK) return st;
+  for (DevPlanBuffer& b : plan->bufs) {
+    if (b.L == 0) continue;
+    const uint64_t g = kChunkQuantum / elem_size(b.dtype);
+    FusedParams F;
+    std::memset(&F, 0, sizeof(F));
+    int nch = 0;
+    st = make_ring_params(c, b.L, b.dtype, true, &F.ring, &nch, (b.L + g - 1) / g * g);  // one chunk
+    if (st != HVD_OK) return st;
+    F.ring.mode = kRingBroadcast;
+    F.ring.root = root;
+    F.ring.epoch = ++c->hs_epoch;
+    F.segs = b.pp.segs;
+    F.src = b.pp.src;
+    F.dst = nullptr;
+    F.vbeg_global = b.vbeg;
+    F.nseg = b.pp.nseg;
+    F.dtype = b.dtype;
+    st = launch_counted(c, HVD_KERNEL_COPY, s, [&] { return launch_copy(F, b.dtype, nch, c->nlocal, c->threads, s); });
+    if (st != HVD_OK) return st;
+    const unsigned long long inc = ring_signals(kRingBroadcast, c->size, F.ring.K);
+    for (int ch = 0; ch < nch; ++ch) c->base[ch] += inc;
+  }
+  return HVD_OK;
 }
 
 int hvd_allgather(hvd_comm* c, const hvd_tensor* in, const hvd_tensor* out, void* stream) {
-  (void)in; (void)out; (void)stream;
   int st = check_live(c);
   if (st != HVD_OK) return st;
-  return HVD_ERR_UNSUPPORTED;  // ring allgather: next milestone
+  if (!in || !out) return HVD_ERR_INVALID;
+  const int dtype = in[0].dtype;
+  const int esz = elem_size(dtype);
+  if (esz == 0) return HVD_ERR_UNSUPPORTED;
+  const uint64_t count = in[0].count;
+  const int N = c->size;
+  for (int l = 0; l < c->nlocal; ++l) {
+    if (in[l].count != count || in[l].dtype != dtype || out[l].dtype != dtype) return HVD_ERR_INVALID;
+    if (out[l].count != count * (uint64_t)N) return HVD_ERR_INVALID;
+    if (count && (!in[l].data || !out[l].data)) return HVD_ERR_INVALID;
+  }
+  if (count == 0) return HVD_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(c->device));
+  const uint64_t g = kChunkQuantum / esz;
+  const uint64_t m_max = c->cap / ((uint64_t)N * esz) / g * g;  // elements per rank per piece
+  if (m_max == 0) return HVD_ERR_INVALID;
+  const uint64_t vel = kPackVecBytes / esz;
+  for (uint64_t off = 0; off < count; off += m_max) {
+    const uint64_t m = std::min(m_max, count - off);
+    const uint64_t qpad = (m + g - 1) / g * g;  // block b of the buffer at b * qpad
+    std::vector<uint64_t> key = {0x41475448ull /* "AGTH" */, (uint64_t)c->nlocal, count, (uint64_t)dtype, off, m};
+    for (int l = 0; l < c->nlocal; ++l) {
+      key.push_back(reinterpret_cast<uint64_t>(in[l].data));
+      key.push_back(reinterpret_cast<uint64_t>(out[l].data));
+    }
+    CachedPlan* plan = lookup_plan(c, key);
+    if (!plan) {
+      std::vector<HostBuf> hb(1);
+      HostBuf& B = hb[0];
+      B.dtype = dtype;
+      B.L = (uint64_t)N * qpad;
+      B.segs.resize(N);
+      B.src.resize((size_t)N * c->nlocal);
+      B.dst.resize((size_t)N * c->nlocal);
+      for (int b = 0; b < N; ++b) {
+        B.segs[b] = {(unsigned long long)b * qpad, m, (unsigned long long)b * qpad / vel, 0};
+        for (int l = 0; l < c->nlocal; ++l) {
+          B.src[(size_t)l * N + b] = static_cast<char*>(in[l].data) + off * esz;  // gathered for b == rank only
+          B.dst[(size_t)l * N + b] = static_cast<char*>(out[l].data) + ((uint64_t)b * count + off) * esz;
+        }
+      }
+      st = upload_plan(c, std::move(key), hb, s, &plan);
+      if (st != HVD_OK) return st;
+    }
+    DevPlanBuffer& b = plan->bufs[0];
+    FusedParams F;
+    std::memset(&F, 0, sizeof(F));
+    int nch = 0;
+    st = make_ring_params(c, b.L, dtype, true, &F.ring, &nch, qpad);
+    if (st != HVD_OK) return st;
+    F.segs = b.pp.segs;
+    F.src = b.pp.src;
+    F.dst = b.dst;
+    F.vbeg_global = b.vbeg;
+    F.nseg = b.pp.nseg;
+    F.dtype = dtype;
+    if (N == 1) {  // out = in: the fused kernel's N = 1 path (gather -> scatter), no scale
+      st = launch_counted(c, HVD_KERNEL_FUSED, s, [&] { return launch_fused(F, dtype, nch, c->nlocal, c->threads, s); });
+      if (st != HVD_OK) return st;
+      continue;
+    }
+    F.ring.mode = kRingAllgather;
+    F.ring.epoch = ++c->hs_epoch;
+    st = launch_counted(c, HVD_KERNEL_COPY, s, [&] { return launch_copy(F, dtype, nch, c->nlocal, c->threads, s); });
+    if (st != HVD_OK) return st;
+    const unsigned long long inc = ring_signals(kRingAllgather, N, F.ring.K);
+    for (int ch = 0; ch < nch; ++ch) c->base[ch] += inc;
+  }
+  return HVD_OK;
 }
 
 int hvd_poll_error(hvd_comm* c) {
@@ -671,6 +838,29 @@ int hvd_set_config(hvd_comm* c, int key, int64_t value) {
       if (value != 0 && value != 1) return HVD_ERR_INVALID;
       c->fused = (int)value;
       return HVD_OK;
+    case HVD_CFG_WINDOW:
+      if (value < 0 || value > 1024) return HVD_ERR_INVALID;
+      c->window = (int)value;
+      return HVD_OK;
+    case HVD_CFG_FIN_LAG:
+      if (value < 0 || value > 1 << 20) return HVD_ERR_INVALID;
+      c->fin_lag = (int)value;
+      return HVD_OK;
+    case HVD_CFG_TIMELINE: {
+      if (value < 0 || value > 65536) return HVD_ERR_INVALID;
+      CK(cudaSetDevice(c->device));
+      CK(cudaDeviceSynchronize());
+      if (c->tl) cudaFree(c->tl);
+      c->tl = nullptr;
+      c->tl_max = (int)value;
+      c->tl_slices = 0;
+      if (value > 0) {
+        const size_t bytes = tl_words(c->tl_max) * c->nlocal * sizeof(unsigned long long);
+        CK(cudaMalloc(reinterpret_cast<void**>(&c->tl), bytes));
+        CK(cudaMemset(c->tl, 0, bytes));
+      }
+      return HVD_OK;
+    }
     default: return HVD_ERR_INVALID;
   }
 }
@@ -686,8 +876,33 @@ int64_t hvd_get_config(const hvd_comm* c, int key) {
     case HVD_CFG_PROFILE: return c->profile;
     case HVD_CFG_SIGNAL_MODE: return c->sig_mode;
     case HVD_CFG_FUSED: return c->fused;
+    case HVD_CFG_TIMELINE: return c->tl_max;
+    case HVD_CFG_WINDOW: return c->window;
+    case HVD_CFG_FIN_LAG: return c->fin_lag;
     default: return -1;
   }
+}
+
+int hvd_timeline(hvd_comm* c, int local, uint64_t* out, uint64_t cap_words, hvd_timeline_info* info) {
+  if (!c || !info || local < 0 || local >= c->nlocal) return HVD_ERR_INVALID;
+  if (c->closed) return HVD_ERR_CLOSED;
+  std::memset(info, 0, sizeof(*info));
+  if (!c->tl || c->tl_slices == 0) return HVD_OK;
+  info->channels = c->tl_nch;
+  info->slices = std::min(c->tl_slices, c->tl_max);
+  info->signals = std::min(c->tl_T * c->tl_K, c->tl_max);
+  info->K = c->tl_K;
+  info->T = c->tl_T;
+  info->rank = c->virt ? local : c->rank;
+  info->size = c->size;
+  info->words_per_channel = (uint64_t)c->tl_max * 2;
+  const size_t words = tl_words(c->tl_max);
+  if (!out) return HVD_OK;
+  if (cap_words < words) return HVD_ERR_INVALID;
+  CK(cudaSetDevice(c->device));
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(out, c->tl + words * local, words * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  return HVD_OK;
 }
 
 int hvd_kernel_stats(hvd_comm* c, uint64_t* launches, double* device_ms) {

@@ -1,0 +1,108 @@
+"""Horovod Timeline (§6) for the B200 path.
+
+The paper's Timeline is a Chrome ``about:tracing`` view of "exactly what each
+node was doing at each time step", switched on by one setting.
+Here the events come from the device: with ``HVD_CFG_TIMELINE`` on, every
+fused allreduce launch records, per rank and channel (CTA), the begin/end
+of each slice operation — reduce-scatter step s, all-gather step s, the final
+local scatter — and each signal the channel published to its ring successor
+(``hvd_timeline``).  This module turns those records into Chrome trace-event
+JSON: one process lane per rank, one thread lane per channel.
+
+Timestamps are each GPU's %globaltimer (ns); lanes of different GPUs are
+aligned on their own first event, so cross-rank skew is not meaningful below
+a few microseconds.
+"""
+from __future__ import annotations
+
+import json
+
+
+def op_of(j: int, K: int, T: int, lag: int = 1):
+    """j-th slice operation of a fused launch -> (t, k); mirrors fused_op in hvd_kernels.cu."""
+    head = (T - 1) * K
+    if j < head:
+        return j // K, j % K
+    m = j - head
+    first = min(lag + 1, K)
+    if m < first:
+        return T - 1, m
+    q = m - first
+    pairs = K - first
+    if q < 2 * pairs:
+        p = q >> 1
+        return (T, p) if q % 2 == 0 else (T - 1, p + first)
+    return T, pairs + (q - 2 * pairs)
+
+
+def _phase(idx: int, K: int, T: int, N: int, lag: int = 1) -> str:
+    t, k = (idx // K, idx % K) if N == 1 else op_of(idx, K, T, lag)
+    if N == 1:
+        return f"scale+copy k={k}"
+    if t < N - 1:
+        return f"reduce-scatter s={t} k={k}"
+    if t < T:
+        return f"all-gather s={t - (N - 1)} k={k}"
+    return f"final scatter k={k}"
+
+
+def chrome_trace(timelines, align: str = "per_rank") -> dict:
+    """Chrome trace-event dict from a list of ``Comm.timeline()`` results (one per rank)."""
+    events = []
+    for tl in timelines:
+        if tl is None:
+            continue
+        r, K, T, N = tl["rank"], tl["K"], tl["T"], tl["size"]
+        lag = tl.get("fin_lag", 1)
+        d, sg = tl["data"], tl["signals"]
+        starts = [int(x) for x in d[:, :, 0].ravel() if int(x)]
+        t0 = min(starts) if starts else 0
+        events.append({"name": "process_name", "ph": "M", "pid": r, "args": {"name": f"rank {r}"}})
+        for ch in range(d.shape[0]):
+            events.append({"name": "thread_name", "ph": "M", "pid": r, "tid": ch, "args": {"name": f"channel {ch}"}})
+            prev_end = None
+            for i in range(d.shape[1]):
+                b, e = int(d[ch, i, 0]), int(d[ch, i, 1])
+                if not b or not e:
+                    continue
+                if prev_end is not None and b > prev_end:
+                    events.append({"name": "wait (predecessor signal)", "cat": "WAIT", "ph": "X", "pid": r,
+                                   "tid": ch, "ts": (prev_end - t0) / 1e3, "dur": (b - prev_end) / 1e3})
+                events.append({"name": _phase(i, K, T, N, lag), "cat": "RING", "ph": "X", "pid": r, "tid": ch,
+                               "ts": (b - t0) / 1e3, "dur": max(e - b, 1) / 1e3})
+                prev_end = e
+            for j in range(sg.shape[1]):
+                t, n = int(sg[ch, j, 0]), int(sg[ch, j, 1])
+                if t:
+                    events.append({"name": f"signal {n}", "cat": "SIGNAL", "ph": "i", "s": "t", "pid": r,
+                                   "tid": ch, "ts": (t - t0) / 1e3})
+    return {"traceEvents": events, "displayTimeUnit": "ns"}
+
+
+def write_chrome_trace(path: str, timelines) -> None:
+    with open(path, "w") as f:
+        json.dump(chrome_trace(timelines), f)
+
+
+def summarize(tl) -> dict:
+    """Per-phase busy time, waits and the span of one rank's launch (microseconds)."""
+    d = tl["data"]
+    K, T, N = tl["K"], tl["T"], tl["size"]
+    lag = tl.get("fin_lag", 1)
+    b = d[:, :, 0].astype("int64")
+    e = d[:, :, 1].astype("int64")
+    valid = (b > 0) & (e > 0)
+    span = (e[valid].max() - b[valid].min()) / 1e3 if valid.any() else 0.0
+    busy = {}
+    for i in range(d.shape[1]):
+        name = _phase(i, K, T, N, lag).rsplit(" k=", 1)[0]
+        m = valid[:, i]
+        busy[name] = busy.get(name, 0.0) + float(((e[:, i] - b[:, i])[m]).mean() / 1e3 if m.any() else 0.0)
+    waits = []
+    for ch in range(d.shape[0]):
+        for i in range(1, d.shape[1]):
+            if valid[ch, i] and valid[ch, i - 1]:
+                waits.append((b[ch, i] - e[ch, i - 1]) / 1e3)
+    return {"span_us": span, "busy_us_per_phase": busy,
+            "mean_wait_us": float(sum(waits) / len(waits)) if waits else 0.0,
+            "max_wait_us": float(max(waits)) if waits else 0.0}

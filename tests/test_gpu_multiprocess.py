@@ -45,6 +45,19 @@ def _worker(rank, world, port, cases, q):
                 comm.allreduce(ts, op=op, fusion_threshold=thr)
                 torch.cuda.synchronize()
                 out.append([from_torch(t, dtype) for t in ts])
+            elif kind == "bcast":
+                xs = [workloads.rank_tensor(c, dtype, rank, k, "specials") for k, c in enumerate(counts)]
+                ts = [to_torch(x, dtype) for x in xs]
+                comm.broadcast(ts, root=op)
+                torch.cuda.synchronize()
+                out.append([from_torch(t, dtype) for t in ts])
+            elif kind == "allgather":
+                x = workloads.rank_tensor(counts[0], dtype, rank, 4, "normal")
+                o = torch.empty(world * counts[0], dtype=torch.float32 if dtype == "f32" else torch.bfloat16,
+                                device="cuda")
+                comm.allgather(to_torch(x, dtype), o)
+                torch.cuda.synchronize()
+                out.append([from_torch(o, dtype)])
             else:  # raw buffer
                 L = counts[0]
                 x = workloads.rank_tensor(L, dtype, rank, 9, "normal" if dtype in ("f32", "bf16") else "int_uniform")
@@ -71,6 +84,9 @@ CASES = [
     ("tensors", [3, 70_001], "i32", "sum", 64 << 20),
     ("buffer", [16 << 20], "f32", "sum", 0),
     ("buffer", [(1 << 20) + 3], "bf16", "average", 0),
+    ("bcast", [5, 1 << 20, 333], "f32", 1, 0),
+    ("allgather", [100_003], "f32", None, 0),
+    ("allgather", [8_000_001], "bf16", None, 0),
 ]
 
 
@@ -94,7 +110,18 @@ def test_multiprocess_ring_matches_oracle():
     for r in range(n):
         assert res[r][1] == 0, res[r]
     for ci, (kind, counts, dtype, op, thr) in enumerate(CASES):
-        if kind == "tensors":
+        if kind == "bcast":
+            xs = [[workloads.rank_tensor(c, dtype, r, k, "specials") for k, c in enumerate(counts)] for r in range(n)]
+            ref, _ = oracle.broadcast(xs, op)
+            for r in range(n):
+                for k in range(len(counts)):
+                    assert np.array_equal(res[r][0][ci][k].view(np.uint8), ref[r][k].view(np.uint8))
+        elif kind == "allgather":
+            xs = [workloads.rank_tensor(counts[0], dtype, r, 4, "normal") for r in range(n)]
+            ref, _ = oracle.allgather(xs)
+            for r in range(n):
+                assert_same(res[r][0][ci][0], ref[r], dtype, f"allgather case {ci} rank {r}")
+        elif kind == "tensors":
             kd = "normal" if dtype in ("f32", "bf16") else "int_uniform"
             xs = [[workloads.rank_tensor(c, dtype, r, k, kd) for k, c in enumerate(counts)] for r in range(n)]
             ref, _, _ = oracle.allreduce(xs, [dtype] * len(counts), op, threshold=thr)

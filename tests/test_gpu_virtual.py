@@ -252,3 +252,100 @@ def test_large_plan_global_segment_table(hvd, n):
     for r in range(n):
         for k in range(0, len(counts), 7):
             assert_same(got[r][k], ref[r][k], "bf16", f"r={r} k={k}")
+
+
+def test_timeline_records_every_slice(hvd):
+    """Horovod Timeline: one record per slice op, ordered, plus signals."""
+    from paper_1802_05799_b200 import timeline
+    n = 3
+    comm = hvd.init_virtual(n, 0, 8 << 20)
+    try:
+        comm.set_config(hvd._lib.HVD_CFG_TIMELINE, 256)
+        ts = [[torch.randn(1 << 20, device="cuda")] for _ in range(n)]
+        comm.allreduce_average(ts)
+        torch.cuda.synchronize()
+        for r in range(n):
+            tl = comm.timeline(r)
+            assert tl["rank"] == r and tl["size"] == n and tl["T"] == 2 * (n - 1)
+            d = tl["data"]
+            assert d.shape[1] == (tl["T"] + 1) * tl["K"]
+            b, e = d[:, :, 0].astype(np.int64), d[:, :, 1].astype(np.int64)
+            assert (b > 0).all() and (e >= b).all()
+            assert (b[:, 1:] >= e[:, :-1]).all()            # program order per channel
+            sg = tl["signals"]
+            assert sg.shape[1] >= 1 and sg[:, :, 1].max() == tl["T"] * tl["K"]
+        tr = timeline.chrome_trace([comm.timeline(r) for r in range(n)])
+        assert any(ev.get("cat") == "RING" for ev in tr["traceEvents"])
+        comm.set_config(hvd._lib.HVD_CFG_TIMELINE, 0)
+        assert comm.timeline(0) is None
+    finally:
+        comm.finalize()
+
+
+# ---------------------------------------------------------------- broadcast / allgather (P:L238-242; R12)
+@pytest.mark.parametrize("n", [2, 3, 4, 8])
+def test_broadcast_bitwise(hvd, n):
+    comm = comm_for(hvd, n)
+    counts = [7, 300, 1 << 20, 5, 65_537]
+    for dtype in ("f32", "bf16", "i64"):
+        kind = "specials" if dtype != "i64" else "int_uniform"
+        xs = [workloads.rank_tensors(counts, dtype, r, kind) for r in range(n)]
+        for root in sorted({0, n - 1, n // 2}):
+            ref, _ = oracle.broadcast(xs, root)
+            ts = [[to_torch(x, dtype) for x in xs[r]] for r in range(n)]
+            comm.broadcast(ts, root=root)
+            torch.cuda.synchronize()
+            for r in range(n):
+                for k in range(len(counts)):
+                    got = from_torch(ts[r][k], dtype)
+                    assert np.array_equal(got.view(np.uint8), ref[r][k].view(np.uint8)), (dtype, root, r, k)
+    assert comm.poll_error() == 0
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 8])
+def test_allgather_rank_order(hvd, n):
+    comm = comm_for(hvd, n, 4 << 20)
+    for dtype, count in (("f32", 1), ("f32", 100_003), ("bf16", 777), ("i64", 300_001), ("i32", 64)):
+        kind = "normal" if dtype in ("f32", "bf16") else "int_uniform"
+        xs = [workloads.rank_tensor(count, dtype, r, 4, kind) for r in range(n)]
+        ref, _ = oracle.allgather(xs)
+        ins = [to_torch(x, dtype) for x in xs]
+        outs = [torch.empty(n * count, dtype=ins[0].dtype, device="cuda") for _ in range(n)]
+        comm.allgather(ins, outs)
+        torch.cuda.synchronize()
+        for r in range(n):
+            assert_same(from_torch(outs[r], dtype), ref[r], dtype, f"{dtype} count={count} r={r}")
+    assert comm.poll_error() == 0
+
+
+def test_mixed_collective_sequence_no_sync(hvd):
+    """allreduce / broadcast / allgather back to back on one stream (buffer reuse hazards)."""
+    n = 4
+    comm = comm_for(hvd, n, 1 << 20)  # small capacity: several fusion buffers and allgather pieces
+    counts = [100_000, 3, 200_000]
+    xs = workloads.all_ranks(counts, "f32", n, seed=77)
+    ys = workloads.all_ranks(counts, "f32", n, seed=78)
+    g = [workloads.rank_tensor(150_000, "f32", r, 1, seed=79) for r in range(n)]
+    tx = [[to_torch(x, "f32") for x in xs[r]] for r in range(n)]
+    ty = [[to_torch(x, "f32") for x in ys[r]] for r in range(n)]
+    gi = [to_torch(x, "f32") for x in g]
+    go = [torch.empty(n * 150_000, device="cuda") for _ in range(n)]
+    for it in range(3):
+        comm.allreduce(tx, op="average", fusion_threshold=1 << 20)
+        comm.broadcast(ty, root=it % n)
+        comm.allgather(gi, go)
+        comm.allreduce(ty, op="sum", fusion_threshold=0)
+    torch.cuda.synchronize()
+    assert comm.poll_error() == 0
+    rx = xs
+    ry = ys
+    for it in range(3):
+        rx, _, _ = oracle.allreduce(rx, ["f32"] * 3, "average", threshold=1 << 20, capacity=1 << 20)
+        ry, _ = oracle.broadcast(ry, it % n)
+        ry, _, _ = oracle.allreduce(ry, ["f32"] * 3, "sum", threshold=0, capacity=1 << 20)
+    rg, _ = oracle.allgather(g)
+    for r in range(n):
+        for k in range(3):
+            assert_same(from_torch(tx[r][k], "f32"), rx[r][k], "f32", f"x r={r} k={k}")
+            assert_same(from_torch(ty[r][k], "f32"), ry[r][k], "f32", f"y r={r} k={k}")
+        assert_same(from_torch(go[r], "f32"), rg[r], "f32", f"g r={r}")

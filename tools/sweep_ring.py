@@ -30,7 +30,9 @@ def main():
     ap.add_argument("--slice-kib", type=int, nargs="+", default=[64, 256, 1024])
     ap.add_argument("--threads", type=int, nargs="+", default=[256, 512])
     ap.add_argument("--iters", type=int, default=20)
-    ap.add_argument("--fence-mode", type=int, nargs="+", default=[0])
+    ap.add_argument("--fence-mode", type=int, nargs="+", default=[1])
+    ap.add_argument("--window", type=int, nargs="+", default=[0])
+    ap.add_argument("--fin-lag", type=int, nargs="+", default=[1])
     ap.add_argument("--check", action="store_true", help="verify bit-exactness of every point vs a reference run")
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--out", default="gpurun_out/sweep.json")
@@ -58,8 +60,11 @@ def main():
             comm.allreduce_buffer(cnt, code, "sum")
         else:
             comm.allreduce_average([grads[mib]])
-    for mib, ch, sl, th, sg in itertools.product(a.mib, a.channels, a.slice_kib, a.threads, a.fence_mode):
+    for mib, ch, sl, th, sg, win, lag in itertools.product(a.mib, a.channels, a.slice_kib, a.threads, a.fence_mode,
+                                                           a.window, a.fin_lag):
         comm.set_config(L.HVD_CFG_SIGNAL_MODE, sg)
+        comm.set_config(L.HVD_CFG_WINDOW, win)
+        comm.set_config(L.HVD_CFG_FIN_LAG, lag)
         comm.set_config(L.HVD_CFG_CHANNELS, ch)
         comm.set_config(L.HVD_CFG_SLICE_BYTES, sl << 10)
         comm.set_config(L.HVD_CFG_THREADS, th)
@@ -94,7 +99,7 @@ def main():
         torch.cuda.synchronize(); dist.barrier()
         us = tmax(ev0.elapsed_time(ev1) / a.iters * 1e3)
         bus = (mib << 20) / (us * 1e-6) / 1e9 * 2 * (world - 1) / world
-        rows.append({"impl": "hvd", "mode": a.mode, "mib": mib, "channels": ch, "slice_kib": sl, "threads": th, "sig": sg,
+        rows.append({"impl": "hvd", "mode": a.mode, "mib": mib, "channels": ch, "slice_kib": sl, "threads": th, "sig": sg, "window": win, "fin_lag": lag,
                      "us": us, "busbw": bus, "bitexact_vs_first": ok})
         if rank == 0:
             print(json.dumps(rows[-1]), flush=True)
