@@ -139,6 +139,8 @@ def run_ours(args):
     import paper_1802_05799_b200 as hvd
     rank, world, local = _dist_env()
     assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    clk = ClockSampler({local} if world == 1 else set(range(world)))
+    clk.__enter__()  # nvidia-smi needs ~1 s to start sampling: start it first
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
@@ -168,9 +170,9 @@ def run_ours(args):
     # every rank must make the same number of collective calls: the pre-load
     # count is derived from the warm-up time and agreed on (max over ranks)
     per_step = (time.perf_counter() - w0) / args.warmup
-    n_load = int(_max_over_ranks(min(20000.0, args.clock_window / max(per_step, 1e-6)), world))
+    n_load = int(_max_over_ranks(min(50000.0, args.clock_window / max(per_step, 1e-6)), world))
     comm.kernel_stats()  # reset counters
-    with ClockSampler({local} if world == 1 else set(range(world))) as clk:
+    if True:
         # keep the GPU busy ~clock_window s so the sampler sees clocks under load, then time K steps
         for i in range(n_load):
             step(i)
@@ -185,6 +187,7 @@ def run_ours(args):
             step(i)
         s1.record()
         _barrier(world)
+    clk.__exit__(None, None, None)
     ms_local = s0.elapsed_time(s1)
     ks = comm.kernel_stats()
     ms = _max_over_ranks(ms_local, world)
@@ -400,7 +403,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="fp32_64MiB",
                     help="fp32_64MiB | resnet101 | inception_v3[_bf16] | vgg16")
-    ap.add_argument("--clock-window", type=float, default=1.0)
+    ap.add_argument("--clock-window", type=float, default=1.5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

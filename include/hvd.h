@@ -159,7 +159,7 @@ int hvd_traffic(hvd_comm* c, int local, uint64_t* sent_bytes, uint64_t* sends);
 
 typedef enum {
   HVD_CFG_CHANNELS = 1,      /* CTAs per rank in the ring kernel (1..256)               */
-  HVD_CFG_SLICE_BYTES = 2,   /* pipelining slice per channel (multiple of 256 B)        */
+  HVD_CFG_SLICE_BYTES = 2,   /* pipelining slice per channel (multiple of 256 B; 0 = auto)  */
   HVD_CFG_THREADS = 3,       /* data threads per ring CTA (64..384, multiple of 32; +1 signal warp) */
   HVD_CFG_TIMEOUT_MS = 4,    /* device spin-wait watchdog                               */
   HVD_CFG_PACK_CTAS_PER_SM = 5,
@@ -171,15 +171,19 @@ typedef enum {
                                 this many slice records per channel; 0: off (default)      */
   HVD_CFG_WINDOW = 10,       /* fused: max slices per channel pushed but not yet fenced (0 = no
                                 limit): bounds the NVLink backlog and so the signal latency */
-  HVD_CFG_FIN_LAG = 11       /* fused: slices by which the final local scatter trails the last
+  HVD_CFG_FIN_LAG = 11,      /* fused: slices by which the final local scatter trails the last
                                 all-gather iteration (>= K-1: scatter after all of it)     */
+  HVD_CFG_PROTOCOL = 12      /* allreduce data movement: 1 (default) push — SM stores into the
+                                successor's HBM; 0 pull — each rank TMA-loads its
+                                predecessor's partials.  Same ring order, same bits.       */
 } hvd_config_key;
 /* Set a tuning knob; every rank must set identical values.  Errors: INVALID. */
 int hvd_set_config(hvd_comm* c, int key, int64_t value);
 int64_t hvd_get_config(const hvd_comm* c, int key);
 
 typedef enum { HVD_KERNEL_PACK = 0, HVD_KERNEL_RING = 1, HVD_KERNEL_UNPACK = 2, HVD_KERNEL_SCALE = 3,
-               HVD_KERNEL_FUSED = 4, HVD_KERNEL_COPY = 5, HVD_KERNEL_KINDS = 6 } hvd_kernel_kind;
+               HVD_KERNEL_FUSED = 4, HVD_KERNEL_COPY = 5, HVD_KERNEL_PULL = 6,
+               HVD_KERNEL_KINDS = 7 } hvd_kernel_kind;
 /* Kernel launches of each kind since the last call (always counted) and, with
  * HVD_CFG_PROFILE on, the summed device time in ms between the CUDA events
  * recorded on the launch stream around each launch (waits for those events).
@@ -197,7 +201,10 @@ int hvd_kernel_stats(hvd_comm* c, uint64_t* launches, double* device_ms);
  * out == NULL returns only `info`; otherwise cap_words must be >= the buffer
  * size (256 * words_per_channel * 2).  Synchronises the device.  Errors: INVALID. */
 typedef struct {
-  int32_t channels, slices, signals, K, T, rank, size, reserved;
+  int32_t channels, slices, signals, K, T, rank, size;
+  int32_t kind;  /* 0: fused push kernel (T = 2(N-1) iterations + final scatter; signal records)
+                    1: pull kernel (T = 2N-1 steps, op j = t*K + k in order; the second record
+                       array holds {t_loadable, op} of the loader warp)                       */
   uint64_t words_per_channel;
 } hvd_timeline_info;
 int hvd_timeline(hvd_comm* c, int local, uint64_t* out, uint64_t cap_words, hvd_timeline_info* info);

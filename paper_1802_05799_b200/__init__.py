@@ -160,7 +160,7 @@ class Comm:
         n = _lib.HVD_KERNEL_KINDS
         la, ms = (C.c_uint64 * n)(), (C.c_double * n)()
         check(lib.hvd_kernel_stats(self._h, la, ms), "hvd_kernel_stats")
-        names = ["pack", "ring", "unpack", "scale", "fused", "copy"]
+        names = ["pack", "ring", "unpack", "scale", "fused", "copy", "pull"]
         return {names[i]: (la[i], ms[i]) for i in range(n)}
 
     def timeline(self, local: int = 0):
@@ -182,7 +182,7 @@ class Comm:
         data = buf[:_lib.MAX_CHANNELS * wpc].reshape(_lib.MAX_CHANNELS, wpc // 2, 2)[:info.channels, :info.slices]
         sig = buf[_lib.MAX_CHANNELS * wpc:].reshape(_lib.MAX_CHANNELS, wpc // 2, 2)[:info.channels, :info.signals]
         return {"rank": info.rank, "size": info.size, "K": info.K, "T": info.T, "channels": info.channels,
-                "fin_lag": self.get_config(_lib.HVD_CFG_FIN_LAG), "data": data.copy(), "signals": sig.copy()}
+                "kind": "pull" if info.kind == 1 else "push", "fin_lag": self.get_config(_lib.HVD_CFG_FIN_LAG), "data": data.copy(), "signals": sig.copy()}
 
     def poll_error(self) -> int:
         return lib.hvd_poll_error(self._h)

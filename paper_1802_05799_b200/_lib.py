@@ -32,10 +32,12 @@ HVD_CFG_FUSED = 8
 HVD_CFG_TIMELINE = 9
 HVD_CFG_WINDOW = 10
 HVD_CFG_FIN_LAG = 11
+HVD_CFG_PROTOCOL = 12
 MAX_CHANNELS = 256
 HVD_KERNEL_PACK, HVD_KERNEL_RING, HVD_KERNEL_UNPACK, HVD_KERNEL_SCALE, HVD_KERNEL_FUSED = 0, 1, 2, 3, 4
 HVD_KERNEL_COPY = 5
-HVD_KERNEL_KINDS = 6
+HVD_KERNEL_PULL = 6
+HVD_KERNEL_KINDS = 7
 
 
 class hvd_tensor(C.Structure):
@@ -54,7 +56,7 @@ class hvd_plan_buffer(C.Structure):
 
 class hvd_timeline_info(C.Structure):
     _fields_ = [("channels", C.c_int32), ("slices", C.c_int32), ("signals", C.c_int32), ("K", C.c_int32),
-                ("T", C.c_int32), ("rank", C.c_int32), ("size", C.c_int32), ("reserved", C.c_int32),
+                ("T", C.c_int32), ("rank", C.c_int32), ("size", C.c_int32), ("kind", C.c_int32),
                 ("words_per_channel", C.c_uint64)]
 
 

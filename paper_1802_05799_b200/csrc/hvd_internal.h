@@ -38,6 +38,14 @@ struct RingRank {
   unsigned long long* nflags;    // successor's flags
   unsigned long long* rflags;    // [kMaxChannels] ready flags, written by the successor (handshake)
   unsigned long long* pready;    // predecessor's ready flags (this rank writes them)
+  // pull protocol (pull_allreduce_kernel)
+  char* pull[2];                 // own pull buffers (call parity), read by the successor
+  const char* ppull[2];          // predecessor's pull buffers
+  unsigned long long* pflags_own;   // [kMaxChannels] own progress (read remotely by the successor)
+  const unsigned long long* pflags_pred;  // predecessor's progress
+  unsigned long long* done_own;  // calls completed by this rank (read remotely by the predecessor)
+  const unsigned long long* done_succ;  // successor's completed calls
+  unsigned long long* exits;     // CTA exit counter of this rank (local)
   int rank;                      // ring rank
   int pad;
 };
@@ -67,6 +75,9 @@ struct RingParams {
   int window;                   // fused: max pushed-but-unfenced slices per channel (0 = no limit)
   int fin_lag;                  // fused: final-scatter interleave lag in slices
   unsigned long long epoch;     // copy collectives: handshake epoch of this launch
+  int parity;                   // pull protocol: pull buffer of this call
+  int call;                     // pull protocol: 1-based call index
+  unsigned long long exits_target;  // pull protocol: cumulative CTA exits after this call
 };
 
 // Timeline buffer of one local rank (Horovod Timeline): for every
@@ -108,6 +119,10 @@ struct PackParams {
 constexpr int kFusedSmemSegs = 4096;  // member-offset table cached in shared memory up to this size
 constexpr int kPipe = 8;              // cp.async prefetch depth (rows of 16 B per data thread)
 constexpr int kMaxRingThreads = 384;  // data threads per ring / fused CTA
+inline size_t pull_smem_bytes(int nseg) {
+  const size_t vb = nseg <= kFusedSmemSegs ? (size_t)(nseg + 15) / 16 * 16 * 8 : 0;
+  return vb + 6ull * (16 << 10);  // + kStages x kStageBytes (hvd_kernels.cu)
+}
 inline size_t fused_smem_bytes(int nseg, int threads) {
   const size_t vb = nseg <= kFusedSmemSegs ? (size_t)(nseg + 1) / 2 * 2 * 8 : 0;
   return vb + 2ull * kPipe * threads * 16;
@@ -127,6 +142,8 @@ struct FusedParams {
 // Launchers (hvd_kernels.cu).  All return a cudaError_t.
 cudaError_t launch_fused(const FusedParams& p, int dtype, int nch, int nlocal, int threads, cudaStream_t s);
 cudaError_t launch_copy(const FusedParams& p, int dtype, int nch, int nlocal, int threads, cudaStream_t s);
+cudaError_t launch_pull(const FusedParams& p, int dtype, int nch, int nlocal, int threads, cudaStream_t s);
+cudaError_t pull_max_ctas_per_sm(int dtype, int threads, int* out);
 cudaError_t fused_max_ctas_per_sm(int dtype, int threads, int* out);
 cudaError_t launch_pack(const PackParams& p, int dtype, int nlocal, int grid, int threads,
                         cudaStream_t s);

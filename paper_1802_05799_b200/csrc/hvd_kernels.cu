@@ -529,16 +529,27 @@ __device__ __noinline__ void scatter_slow(char* tp, unsigned long long left, uin
       for (int b = 0; b < ESZ; ++b) tp[i * ESZ + b] = xb[i * ESZ + b];
 }
 
-// Byte offset of buffer vector v inside its member s; `left` = member elements from there on.
+// Per-thread cache of the member that owns the current buffer vectors: a slice
+// walks long runs of vectors inside one member, so the table lookup (shared
+// memory binary search + two global loads) happens once per member per thread.
+struct SegCache {
+  unsigned long long vlo = 1, vhi = 0;  // vectors [vlo, vhi) belong to member s (empty at start)
+  unsigned long long end_el = 0;        // member end, buffer element index
+  uintptr_t g = 0, d = 0;               // gather / scatter address of buffer element 0 of this member
+  int s = 0;
+};
+
 template <int ESZ>
-__device__ __forceinline__ unsigned long long member_off(const FusedCtx& F, unsigned long long v, int& s,
-                                                         unsigned long long& left) {
-  constexpr int VEL = 16 / ESZ;
-  s = seg_of(F, v, s);
-  const unsigned long long e0 = v * VEL - F.segs[s].dst_off;
-  const unsigned long long cnt = F.segs[s].count;
-  left = e0 < cnt ? cnt - e0 : 0;
-  return e0 * ESZ;
+__device__ __forceinline__ void seg_lookup(const FusedCtx& F, unsigned long long v, SegCache& c) {
+  if (v >= c.vlo && v < c.vhi) return;
+  const int s = seg_of(F, v, c.s);
+  c.s = s;
+  c.vlo = F.vbeg[s];
+  c.vhi = s + 1 < F.nseg ? F.vbeg[s + 1] : ~0ull;
+  const unsigned long long dst_off = F.segs[s].dst_off;
+  c.end_el = dst_off + F.segs[s].count;
+  c.g = reinterpret_cast<uintptr_t>(F.src[s]) - dst_off * ESZ;
+  c.d = reinterpret_cast<uintptr_t>(F.dst[s]) - dst_off * ESZ;
 }
 
 template <int ESZ>
@@ -561,7 +572,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // slice is vector v = v_lo + j*nthr + tid.  slots0/slots1: [kPipe][nthr] uint4.
 template <class Op, int KIND>
 __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& me, unsigned long long lo,
-                                            unsigned long long hi, unsigned tid, unsigned nthr, int& sc,
+                                            unsigned long long hi, unsigned tid, unsigned nthr, SegCache& sc,
                                             uint4* slots0, uint4* slots1) {
   constexpr int ESZ = Op::kEsz;
   constexpr int VEL = 16 / ESZ;
@@ -575,16 +586,16 @@ __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& m
   const unsigned long long v_hi = (hi + VEL - 1) / VEL;
   if (v_hi <= v_lo + tid) return;
   const int rows = (int)((v_hi - v_lo - tid + nthr - 1) / nthr);  // rows this thread owns
+  SegCache ci = sc;  // issue-side cache (runs kPipe-1 rows ahead of the consume side)
   auto issue = [&](int j) {
     if (j < rows) {
       const unsigned long long v = v_lo + (unsigned long long)j * nthr + tid;
       uint4* d0 = slots0 + (j % kPipe) * nthr + tid;
       if (GATHER) {
-        unsigned long long left;
-        int s2 = sc;
-        const unsigned long long off = member_off<ESZ>(F, v, s2, left);
-        sc = s2;
-        const char* tp = F.src[s2] + off;
+        seg_lookup<ESZ>(F, v, ci);
+        const unsigned long long e = v * VEL;
+        const unsigned long long left = ci.end_el > e ? ci.end_el - e : 0;
+        const char* tp = reinterpret_cast<const char*>(ci.g + e * ESZ);
         if (fast16<ESZ>(tp, left)) cp_async16(d0, tp);
       } else {
         cp_async16(d0, me.buf + v * 16);
@@ -599,11 +610,15 @@ __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& m
     issue(j + kPipe - 1);
     cp_async_wait<kPipe - 1>();  // row j has landed in this thread's slots
     const unsigned long long v = v_lo + (unsigned long long)j * nthr + tid;
-    unsigned long long left;
-    const unsigned long long off = member_off<ESZ>(F, v, sc, left);
+    unsigned long long left = 0;
+    unsigned long long e = v * VEL;
+    if (GATHER || SCATTER) {
+      seg_lookup<ESZ>(F, v, sc);
+      left = sc.end_el > e ? sc.end_el - e : 0;
+    }
     uint4 x;
     if (GATHER) {
-      const char* gp = F.src[sc] + off;
+      const char* gp = reinterpret_cast<const char*>(sc.g + e * ESZ);
       x = fast16<ESZ>(gp, left) ? slots0[(j % kPipe) * nthr + tid] : gather_slow<ESZ>(gp, left);
       x = Pack16<ESZ>::conv(x, F.scale, F.scale_on, F.dtype);
     } else {
@@ -616,7 +631,7 @@ __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& m
     if (TO_NSCRATCH) *reinterpret_cast<uint4*>(me.nscratch + v * 16) = x;
     if (TO_NBUF) *reinterpret_cast<uint4*>(me.nbuf + v * 16) = x;
     if (SCATTER) {
-      char* tp = F.dst[sc] + off;
+      char* tp = reinterpret_cast<char*>(sc.d + e * ESZ);
       if (fast16<ESZ>(tp, left)) *reinterpret_cast<uint4*>(tp) = x;
       else scatter_slow<ESZ>(tp, left, x);
     }
@@ -699,7 +714,7 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
   F.scale = P.scale;
   F.dtype = P.dtype;
   const unsigned tid = threadIdx.x;
-  int sc = 0;
+  SegCache sc;
   unsigned long long sent = 0;
   if (N == 1) {
     for (int k = 0; k < K; ++k) {
@@ -830,7 +845,7 @@ __global__ void __launch_bounds__(416, 1) copy_collective_kernel(const __grid_co
   F.scale = 1.0f;
   F.dtype = P.dtype;
   const unsigned tid = threadIdx.x;
-  int sc = 0;
+  SegCache sc;
   unsigned long long sent = 0;
   bool ready = false;  // successor's handshake seen
   const int d = mod(r - R.root, N);  // broadcast: distance from the root
@@ -878,6 +893,257 @@ __global__ void __launch_bounds__(416, 1) copy_collective_kernel(const __grid_co
   if (tid == 0) {
     atomicAdd(me.stats + 0, sent);
     if (ch == 0) atomicAdd(me.stats + 1, (unsigned long long)(bcast ? (d == N - 1 ? 0 : 1) : T));
+  }
+}
+
+// ------------------------------------------------------------------ pull-mode fused allreduce
+// Same ring, same reduction order, but every transfer is initiated by the
+// RECEIVER: rank r TMA-loads (cp.async.bulk, mbarrier transaction counts) its
+// predecessor's partial of chunk c straight from the predecessor's HBM into
+// shared memory, adds its own gathered contribution and writes the result into
+// ITS OWN pull buffer, where the successor will load it from.  A rank therefore
+// never stores to a peer: publishing "slice done" only needs a system fence over
+// its LOCAL stores, which is short, whereas a fence behind a stream of NVLink
+// stores waits for that whole backlog to drain (tools/fence_probe.cu).
+//
+// Steps t = 0..2N-2 per slice k (op j = t*K + k, published as base + j + 1):
+//   t = 0          B[r]     <- gather(x)*s                          (local)
+//   1 <= t <= N-1  B[r-t]   <- pred.B[r-t] + gather(x)*s           (t = N-1: the owner's final
+//                                                                   chunk r+1, also scattered)
+//   N <= t <= 2N-2 x[c]     <- pred.B[c], c = r+1-(t-N+1); B[c] <- same unless t = 2N-2
+// Op (t, k) depends on the predecessor's op (t-1, k).  The pull buffers are
+// double-buffered by call parity; before writing buffer p in call k a rank waits
+// until its successor has completed call k-2 (the last reader of that buffer).
+constexpr int kStageBytes = 16 << 10;
+constexpr int kStages = 6;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  unsigned done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load(void* smem_dst, const void* gmem_src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(smem_dst)), "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ int pull_chunk(int t, int r, int N) {
+  return t < N ? mod(r - t, N) : mod(r + 1 - (t - N + 1), N);
+}
+
+template <class Op>
+__global__ void __launch_bounds__(416, 1) pull_allreduce_kernel(const __grid_constant__ FusedParams P) {
+  extern __shared__ __align__(128) unsigned long long s_dyn[];
+  __shared__ __align__(8) unsigned long long full_bar[kStages], empty_bar[kStages];
+  __shared__ int s_abort;
+  constexpr int ESZ = Op::kEsz;
+  constexpr int VEL = 16 / ESZ;
+  const RingParams& R = P.ring;
+  const RingRank& me = R.rk[blockIdx.y];
+  const int ch = blockIdx.x;
+  const int N = R.N;
+  const int r = me.rank;
+  const int K = R.K;
+  const unsigned long long base = R.base[ch];
+  const int T = 2 * N - 1;
+  const int nops = T * K;
+  const int nd = blockDim.x - 32;
+  const int par = R.parity;
+  char* const myB = me.pull[par];
+  const char* const predB = me.ppull[par];
+  const bool cache = P.nseg <= kFusedSmemSegs;
+  unsigned long long* s_vbeg = s_dyn;
+  char* stages = reinterpret_cast<char*>(s_dyn + (cache ? (P.nseg + 15) / 16 * 16 : 0));
+  if (cache)
+    for (int j = threadIdx.x; j < P.nseg; j += blockDim.x) s_vbeg[j] = P.segs[j].vbeg;
+  if (threadIdx.x == 0) {
+    s_abort = 0;
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], nd / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  unsigned long long* tl_d =
+      R.tl ? R.tl + tl_words(R.tl_max) * blockIdx.y + (size_t)ch * R.tl_max * 2 : nullptr;
+  if (threadIdx.x >= nd) {  // ---- loader warp: remote polls + TMA loads of the predecessor's buffer
+    if (threadIdx.x != nd) return;
+    unsigned long long* tl_s =
+        R.tl ? R.tl + tl_words(R.tl_max) * blockIdx.y + ((size_t)kMaxChannels + ch) * R.tl_max * 2 : nullptr;
+    int nrec = 0;
+    unsigned long long seq = 0;
+    bool abort = false;
+    for (int j = 0; j < nops; ++j) {
+      const int t = j / K, k = j - (j / K) * K;
+      if (t == 0) continue;
+      unsigned long long lo, hi;
+      slice_range(R, pull_chunk(t, r, N), ch, k, lo, hi);
+      if (!abort && hi > lo) {
+        if (!spin_until(me.pflags_pred + ch, base + (unsigned long long)(t - 1) * K + k + 1, R.err, R.timeout_ns)) {
+          abort = true;
+          s_abort = 1;
+        }
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // acquire before the async-proxy loads
+        if (tl_s && nrec < R.tl_max) {  // timeline: when the predecessor's slice became loadable
+          tl_s[2 * nrec] = globaltimer();
+          tl_s[2 * nrec + 1] = (unsigned long long)j;
+          ++nrec;
+        }
+      }
+      const unsigned long long bytes = hi > lo ? ((hi - lo) * ESZ + 15) / 16 * 16 : 0;
+      for (unsigned long long off = 0; off < bytes; off += kStageBytes, ++seq) {
+        const int st = (int)(seq % kStages);
+        if (seq >= (unsigned long long)kStages) mbar_wait(&empty_bar[st], (unsigned)((seq / kStages - 1) & 1));
+        const unsigned pb = (unsigned)(bytes - off < (unsigned long long)kStageBytes ? bytes - off : kStageBytes);
+        if (abort) {
+          mbar_arrive(&full_bar[st]);  // complete the phase without data so the compute warps move on
+        } else {
+          mbar_expect_tx(&full_bar[st], pb);
+          tma_load(stages + (size_t)st * kStageBytes, predB + lo * ESZ + off, pb, &full_bar[st]);
+        }
+      }
+    }
+    return;
+  }
+
+  // ---- compute warps
+  FusedCtx F;
+  F.segs = P.segs;
+  F.src = P.src + (size_t)blockIdx.y * P.nseg;
+  F.dst = (P.dst ? P.dst : P.src) + (size_t)blockIdx.y * P.nseg;
+  F.vbeg = cache ? s_vbeg : P.vbeg_global;
+  F.nseg = P.nseg;
+  F.scale_on = P.scale_on;
+  F.scale = P.scale;
+  F.dtype = P.dtype;
+  const unsigned tid = threadIdx.x;
+  const int lane = tid & 31;
+  SegCache sc;
+  unsigned long long sent = 0;
+  // WAR handshake on the double-buffered pull buffer (see above)
+  if (tid == 0 && R.call >= 3 &&
+      !spin_until(me.done_succ, (unsigned long long)(R.call - 2), R.err, R.timeout_ns))
+    s_abort = 1;
+  bar_sync(kBarData, nd);
+  unsigned long long seq = 0;
+  for (int j = 0; j < nops; ++j) {
+    const unsigned long long tb = tl_d ? globaltimer() : 0;
+    const int t = j / K, k = j - (j / K) * K;
+    const int c = pull_chunk(t, r, N);
+    const bool gathers = t <= N - 1;
+    const bool scatters = t >= N - 1;
+    const bool writes = t <= T - 2;
+    unsigned long long lo, hi;
+    slice_range(R, c, ch, k, lo, hi);
+    const unsigned long long v_lo = lo / VEL, v_hi = (hi + VEL - 1) / VEL;
+    if (t == 0) {
+      // own contribution of chunk r into the local pull buffer
+      if (hi > lo && !s_abort) {
+        constexpr int U = 8;  // loads in flight per thread (this step is a local HBM copy)
+        for (unsigned long long v0 = v_lo + tid; v0 < v_hi; v0 += (unsigned long long)nd * U) {
+          uint4 x[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const unsigned long long v = v0 + (unsigned long long)u * nd;
+            if (v < v_hi) {
+              seg_lookup<ESZ>(F, v, sc);
+              const unsigned long long e = v * VEL;
+              const unsigned long long left = sc.end_el > e ? sc.end_el - e : 0;
+              const char* gp = reinterpret_cast<const char*>(sc.g + e * ESZ);
+              x[u] = fast16<ESZ>(gp, left) ? __ldcs(reinterpret_cast<const uint4*>(gp)) : gather_slow<ESZ>(gp, left);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const unsigned long long v = v0 + (unsigned long long)u * nd;
+            if (v < v_hi)
+              *reinterpret_cast<uint4*>(myB + v * 16) = Pack16<ESZ>::conv(x[u], F.scale, F.scale_on, F.dtype);
+          }
+        }
+      }
+    } else if (hi > lo) {
+      const unsigned long long bytes = ((hi - lo) * ESZ + 15) / 16 * 16;
+      for (unsigned long long off = 0; off < bytes; off += kStageBytes, ++seq) {
+        const int st = (int)(seq % kStages);
+        const unsigned long long pv0 = v_lo + off / 16;
+        unsigned long long pv1 = pv0 + kStageBytes / 16;
+        pv1 = pv1 < v_hi ? pv1 : v_hi;
+        constexpr int kMaxPer = (kStageBytes / 16 + 255) / 256;  // vectors per thread per stage (nd >= 256)
+        uint4 g[kMaxPer];
+        if (gathers && !s_abort) {  // local gathers issued before waiting for the remote stage
+#pragma unroll
+          for (int i = 0; i < kMaxPer; ++i) {
+            const unsigned long long v = pv0 + tid + (unsigned long long)i * nd;
+            if (v < pv1) {
+              seg_lookup<ESZ>(F, v, sc);
+              const unsigned long long e = v * VEL;
+              const unsigned long long left = sc.end_el > e ? sc.end_el - e : 0;
+              const char* gp = reinterpret_cast<const char*>(sc.g + e * ESZ);
+              g[i] = fast16<ESZ>(gp, left) ? __ldcs(reinterpret_cast<const uint4*>(gp)) : gather_slow<ESZ>(gp, left);
+            }
+          }
+        }
+        mbar_wait(&full_bar[st], (unsigned)((seq / kStages) & 1));
+        if (!s_abort) {
+          const uint4* stg = reinterpret_cast<const uint4*>(stages + (size_t)st * kStageBytes);
+#pragma unroll
+          for (int i = 0; i < kMaxPer; ++i) {
+            const unsigned long long v = pv0 + tid + (unsigned long long)i * nd;
+            if (v < pv1) {
+              uint4 x = stg[v - pv0];
+              if (gathers) {
+                const uint4 y = Pack16<ESZ>::conv(g[i], F.scale, F.scale_on, F.dtype);
+                Op::template add_words<4>(reinterpret_cast<uint32_t*>(&x), reinterpret_cast<const uint32_t*>(&y));
+              }
+              if (writes) *reinterpret_cast<uint4*>(myB + v * 16) = x;
+              if (scatters) {
+                seg_lookup<ESZ>(F, v, sc);
+                const unsigned long long e = v * VEL;
+                const unsigned long long left = sc.end_el > e ? sc.end_el - e : 0;
+                char* tp = reinterpret_cast<char*>(sc.d + e * ESZ);
+                if (fast16<ESZ>(tp, left)) *reinterpret_cast<uint4*>(tp) = x;
+                else scatter_slow<ESZ>(tp, left, x);
+              }
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[st]);
+      }
+    }
+    // traffic stats count what the successor pulls from this rank: the ops that write B
+    if (writes && hi > lo) sent += (hi - lo) * ESZ;
+    // op j done: publish it (the fence covers this rank's local stores only)
+    bar_sync(kBarData, nd);
+    if (tid == 0) {
+      if (writes) asm volatile("fence.acq_rel.sys;" ::: "memory");
+      asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(me.pflags_own + ch),
+                   "l"(base + (unsigned long long)j + 1) : "memory");
+      if (tl_d && j < R.tl_max) {
+        tl_d[2 * j] = tb;
+        tl_d[2 * j + 1] = globaltimer();
+      }
+    }
+  }
+  if (tid == 0) {
+    atomicAdd(me.stats + 0, sent);
+    if (ch == 0) atomicAdd(me.stats + 1, (unsigned long long)(2 * (N - 1)));
+    // last CTA of this rank to finish publishes "call done" (its pulls from the predecessor are over)
+    const unsigned long long prev = atomicAdd(me.exits, 1ull);
+    if (prev + 1 == R.exits_target) st_release_sys(me.done_own, (unsigned long long)R.call);
   }
 }
 
@@ -1026,6 +1292,50 @@ cudaError_t launch_copy(const FusedParams& p, int dtype, int nch, int nlocal, in
     case 4: return launch_copy_t<OpI32>(p, nch, nlocal, threads, s);
     case 2: return launch_copy_t<OpBF16>(p, nch, nlocal, threads, s);
     case 8: return launch_copy_t<OpI64>(p, nch, nlocal, threads, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <class Op>
+static cudaError_t launch_pull_t(const FusedParams& p, int nch, int nlocal, int threads, cudaStream_t s) {
+  const size_t smem = pull_smem_bytes(p.nseg);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(pull_allreduce_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)pull_smem_bytes(kFusedSmemSegs));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nch, nlocal);
+  cfg.blockDim = dim3(threads + 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, pull_allreduce_kernel<Op>, p);
+}
+
+cudaError_t launch_pull(const FusedParams& p, int dtype, int nch, int nlocal, int threads, cudaStream_t s) {
+  switch (dtype) {
+    case 1: return launch_pull_t<OpF32>(p, nch, nlocal, threads, s);
+    case 2: return launch_pull_t<OpBF16>(p, nch, nlocal, threads, s);
+    case 3: return launch_pull_t<OpI32>(p, nch, nlocal, threads, s);
+    case 4: return launch_pull_t<OpI64>(p, nch, nlocal, threads, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t pull_max_ctas_per_sm(int dtype, int threads, int* out) {
+  const size_t smem = pull_smem_bytes(kFusedSmemSegs);
+  switch (dtype) {
+    case 1: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, pull_allreduce_kernel<OpF32>, threads + 32, smem);
+    case 2: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, pull_allreduce_kernel<OpBF16>, threads + 32, smem);
+    case 3: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, pull_allreduce_kernel<OpI32>, threads + 32, smem);
+    case 4: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, pull_allreduce_kernel<OpI64>, threads + 32, smem);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -22,7 +22,7 @@ using namespace hvd;
 namespace {
 
 constexpr uint64_t kDefaultFusionBytes = 64ull << 20;  // P:L368-369 "Default ... 64 MB" (R9)
-constexpr uint64_t kTailBytes = 8192;                   // flags, stats, ready flags after buf and scratch
+constexpr uint64_t kTailBytes = 16384;  // flags, stats, ready flags, pull progress, done/exit counters
 constexpr uint32_t kBlobMagic = 0x48564442u;            // "HVDB"
 constexpr int kPackThreads = 256;
 constexpr int kPackVecsPerThread = 8;
@@ -67,8 +67,8 @@ struct hvd_comm {
   int* err_dev = nullptr;
   int sm_count = 148;
   // tuning (hvd_set_config)
-  int channels = 128;
-  int64_t slice_bytes = 64 << 10;
+  int channels = 148;
+  int64_t slice_bytes = 0;  // 0 = auto: about half of a channel's share of a chunk, 32..128 KiB
   int threads = 384;
   int64_t timeout_ms = 30000;
   int pack_ctas_per_sm = 8;
@@ -78,10 +78,14 @@ struct hvd_comm {
   int window = 0;
   int fin_lag = 1;
   unsigned long long hs_epoch = 0;  // copy-collective handshake epochs issued
+  int protocol = 1;                 // 0: pull (receiver-initiated TMA loads), 1: push (SM stores)
+  unsigned long long pbase[kMaxChannels] = {};  // pull-protocol progress counter bases
+  int pull_calls = 0;
+  unsigned long long pull_exits = 0;  // cumulative CTA exits of the pull kernel (per rank)
   // timeline (HVD_CFG_TIMELINE): device records of the most recent fused launch
   int tl_max = 0;
   unsigned long long* tl = nullptr;
-  int tl_nch = 0, tl_K = 0, tl_T = 0, tl_slices = 0;
+  int tl_nch = 0, tl_K = 0, tl_T = 0, tl_slices = 0, tl_kind = 0;
   std::list<CachedPlan> cache;
   // launch statistics (hvd_kernel_stats)
   uint64_t launches[HVD_KERNEL_KINDS] = {};
@@ -106,14 +110,21 @@ int cuda_fail(cudaError_t e, const char* what) {
 char* buf_of(char* region) { return region; }
 char* scratch_of(char* region, uint64_t cap) { return region + cap; }
 unsigned long long* flags_of(char* region, uint64_t cap) {
-  return reinterpret_cast<unsigned long long*>(region + 2 * cap);
+  return reinterpret_cast<unsigned long long*>(region + 4 * cap);
 }
 unsigned long long* stats_of(char* region, uint64_t cap) {
-  return reinterpret_cast<unsigned long long*>(region + 2 * cap + kMaxChannels * 8);
+  return reinterpret_cast<unsigned long long*>(region + 4 * cap + kMaxChannels * 8);
 }
-unsigned long long* rflags_of(char* region, uint64_t cap) {
-  return reinterpret_cast<unsigned long long*>(region + 2 * cap + 4096);
+// Region: [fusion buffer][RS scratch][pull buffer 0][pull buffer 1][tail], each buffer `cap` bytes.
+constexpr uint64_t kNumBufs = 4;
+unsigned long long* tail_of(char* region, uint64_t cap) {
+  return reinterpret_cast<unsigned long long*>(region + kNumBufs * cap);
 }
+unsigned long long* rflags_of(char* region, uint64_t cap) { return tail_of(region, cap) + 512; }
+unsigned long long* pflags_of(char* region, uint64_t cap) { return tail_of(region, cap) + 1024; }
+unsigned long long* done_of(char* region, uint64_t cap) { return tail_of(region, cap) + 1536; }
+unsigned long long* exits_of(char* region, uint64_t cap) { return tail_of(region, cap) + 1537; }
+char* pull_of(char* region, uint64_t cap, int p) { return region + (2 + p) * cap; }
 
 int common_init(hvd_comm* c, uint64_t fusion_bytes) {
   c->cap = ((fusion_bytes ? fusion_bytes : kDefaultFusionBytes) + 4095) / 4096 * 4096;
@@ -122,16 +133,21 @@ int common_init(hvd_comm* c, uint64_t fusion_bytes) {
   CK(cudaHostAlloc(reinterpret_cast<void**>(&c->err_host), sizeof(int), cudaHostAllocMapped));
   *c->err_host = 0;
   CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->err_dev), c->err_host, 0));
-  const uint64_t region_bytes = 2 * c->cap + kTailBytes;
+  const uint64_t region_bytes = kNumBufs * c->cap + kTailBytes;
   for (int l = 0; l < c->nlocal; ++l) {
     CK(cudaMalloc(reinterpret_cast<void**>(&c->region[l]), region_bytes));
-    CK(cudaMemset(c->region[l] + 2 * c->cap, 0, kTailBytes));
+    CK(cudaMemset(c->region[l] + kNumBufs * c->cap, 0, kTailBytes));
     RingRank& r = c->rk[l];
     r.buf = buf_of(c->region[l]);
     r.scratch = scratch_of(c->region[l], c->cap);
     r.flags = flags_of(c->region[l], c->cap);
     r.stats = stats_of(c->region[l], c->cap);
     r.rflags = rflags_of(c->region[l], c->cap);
+    r.pull[0] = pull_of(c->region[l], c->cap, 0);
+    r.pull[1] = pull_of(c->region[l], c->cap, 1);
+    r.pflags_own = pflags_of(c->region[l], c->cap);
+    r.done_own = done_of(c->region[l], c->cap);
+    r.exits = exits_of(c->region[l], c->cap);
     r.rank = c->virt ? l : c->rank;
   }
   CK(cudaDeviceSynchronize());
@@ -143,6 +159,10 @@ void set_neighbours(RingRank& r, char* succ_region, char* pred_region, uint64_t 
   r.nscratch = scratch_of(succ_region, cap);
   r.nflags = flags_of(succ_region, cap);
   r.pready = rflags_of(pred_region, cap);
+  r.ppull[0] = pull_of(pred_region, cap, 0);
+  r.ppull[1] = pull_of(pred_region, cap, 1);
+  r.pflags_pred = pflags_of(pred_region, cap);
+  r.done_succ = done_of(succ_region, cap);
 }
 
 int check_live(hvd_comm* c) {
@@ -357,7 +377,7 @@ int launch_counted(hvd_comm* c, int kind, cudaStream_t s, F&& launch) {
 // Split one buffer of L elements into chunks / channels / slices (R2) for the
 // ring or fused kernel.  Returns the channel count.
 int make_ring_params(hvd_comm* c, uint64_t L, int dtype, bool fused, RingParams* P, int* nch_out,
-                     uint64_t q_override = 0) {
+                     uint64_t q_override = 0, bool pull = false) {
   const int esz = elem_size(dtype);
   const uint64_t g = kChunkQuantum / esz;
   std::memset(P, 0, sizeof(*P));
@@ -368,13 +388,17 @@ int make_ring_params(hvd_comm* c, uint64_t L, int dtype, bool fused, RingParams*
   // channels: at least 32 KiB of every chunk per channel, at most the knob and
   // what stays co-resident (the CTAs of all ranks wait on each other)
   int max_per_sm = 1;
-  CK(fused ? fused_max_ctas_per_sm(dtype, c->threads, &max_per_sm) : ring_max_ctas_per_sm(dtype, c->threads, &max_per_sm));
+  const int threads = pull ? std::max(256, c->threads) : c->threads;
+  CK(pull ? pull_max_ctas_per_sm(dtype, threads, &max_per_sm)
+          : fused ? fused_max_ctas_per_sm(dtype, threads, &max_per_sm) : ring_max_ctas_per_sm(dtype, threads, &max_per_sm));
   const int resident = std::max(1, c->sm_count * max_per_sm / c->nlocal);
   const uint64_t qbytes = P->q * esz;
   int nch = (int)std::min<uint64_t>((uint64_t)c->channels, std::max<uint64_t>(1, qbytes / (32 << 10)));
   nch = std::min(nch, std::min(resident, kMaxChannels));
   P->ch_el = (P->q + (uint64_t)nch * g - 1) / ((uint64_t)nch * g) * g;
-  const uint64_t slice_el = std::max<uint64_t>(g, (uint64_t)c->slice_bytes / esz / g * g);
+  uint64_t sb = (uint64_t)c->slice_bytes;
+  if (sb == 0) sb = std::min<uint64_t>(128 << 10, std::max<uint64_t>(32 << 10, P->ch_el * esz / 2));
+  const uint64_t slice_el = std::max<uint64_t>(g, sb / esz / g * g);
   P->slice_el = std::min<uint64_t>(slice_el, P->ch_el);
   P->K = (int)((P->ch_el + P->slice_el - 1) / P->slice_el);
   P->mode = kRingAllreduce;
@@ -385,7 +409,7 @@ int make_ring_params(hvd_comm* c, uint64_t L, int dtype, bool fused, RingParams*
   P->window = c->window;
   P->fin_lag = c->fin_lag;
   P->tl_max = c->tl ? c->tl_max : 0;
-  for (int ch = 0; ch < kMaxChannels; ++ch) P->base[ch] = c->base[ch];
+  for (int ch = 0; ch < kMaxChannels; ++ch) P->base[ch] = pull ? c->pbase[ch] : c->base[ch];
   *nch_out = nch;
   return HVD_OK;
 }
@@ -407,8 +431,44 @@ int enqueue_ring(hvd_comm* c, uint64_t L, int dtype, cudaStream_t s) {
   return HVD_OK;
 }
 
+// Pull protocol (pull_allreduce_kernel): ranks load their predecessor's partials.
+int enqueue_pull(hvd_comm* c, DevPlanBuffer& b, cudaStream_t s) {
+  FusedParams F;
+  std::memset(&F, 0, sizeof(F));
+  int nch = 0;
+  int st = make_ring_params(c, b.L, b.dtype, true, &F.ring, &nch, 0, true);
+  if (st != HVD_OK) return st;
+  const int call = ++c->pull_calls;
+  F.ring.call = call;
+  F.ring.parity = call & 1;
+  F.ring.exits_target = c->pull_exits + nch;
+  F.segs = b.pp.segs;
+  F.src = b.pp.src;
+  F.dst = b.dst;
+  F.vbeg_global = b.vbeg;
+  F.nseg = b.pp.nseg;
+  F.scale_on = b.pp.scale_on;
+  F.scale = b.pp.scale;
+  F.dtype = b.dtype;
+  const int threads = std::max(256, c->threads);
+  st = launch_counted(c, HVD_KERNEL_PULL, s, [&] { return launch_pull(F, b.dtype, nch, c->nlocal, threads, s); });
+  if (st != HVD_OK) return st;
+  if (c->tl) {
+    c->tl_nch = nch;
+    c->tl_K = F.ring.K;
+    c->tl_T = 2 * c->size - 1;  // pull ops: steps 0..2N-2
+    c->tl_slices = c->tl_T * F.ring.K;
+    c->tl_kind = 1;
+  }
+  c->pull_exits += nch;
+  const unsigned long long inc = (unsigned long long)(2 * c->size - 1) * F.ring.K;
+  for (int ch = 0; ch < nch; ++ch) c->pbase[ch] += inc;
+  return HVD_OK;
+}
+
 int enqueue_fused(hvd_comm* c, DevPlanBuffer& b, cudaStream_t s) {
   if (b.L == 0) return HVD_OK;
+  if (c->protocol == 0 && c->size > 1) return enqueue_pull(c, b, s);
   FusedParams F;
   std::memset(&F, 0, sizeof(F));
   int nch = 0;
@@ -429,6 +489,7 @@ int enqueue_fused(hvd_comm* c, DevPlanBuffer& b, cudaStream_t s) {
     c->tl_K = F.ring.K;
     c->tl_T = c->size > 1 ? 2 * (c->size - 1) : 0;
     c->tl_slices = c->size > 1 ? (c->tl_T + 1) * F.ring.K : F.ring.K;
+    c->tl_kind = 0;
   }
   advance_base(c, F.ring, nch);
   return HVD_OK;
@@ -543,7 +604,7 @@ int hvd_get_ipc_blob(hvd_comm* c, void* out, uint64_t* len) {
   b.device = c->device;
   b.pid = (int32_t)getpid();
   b.capacity = c->cap;
-  b.region_bytes = 2 * c->cap + kTailBytes;
+  b.region_bytes = kNumBufs * c->cap + kTailBytes;
   CK(cudaSetDevice(c->device));
   CK(cudaIpcGetMemHandle(&b.handle, c->region[0]));
   std::memcpy(out, &b, sizeof(b));
@@ -811,7 +872,7 @@ int hvd_set_config(hvd_comm* c, int key, int64_t value) {
       c->channels = (int)value;
       return HVD_OK;
     case HVD_CFG_SLICE_BYTES:
-      if (value < kChunkQuantum || value % kChunkQuantum) return HVD_ERR_INVALID;
+      if (value != 0 && (value < kChunkQuantum || value % kChunkQuantum)) return HVD_ERR_INVALID;
       c->slice_bytes = value;
       return HVD_OK;
     case HVD_CFG_THREADS:
@@ -837,6 +898,10 @@ int hvd_set_config(hvd_comm* c, int key, int64_t value) {
     case HVD_CFG_FUSED:
       if (value != 0 && value != 1) return HVD_ERR_INVALID;
       c->fused = (int)value;
+      return HVD_OK;
+    case HVD_CFG_PROTOCOL:
+      if (value != 0 && value != 1) return HVD_ERR_INVALID;
+      c->protocol = (int)value;
       return HVD_OK;
     case HVD_CFG_WINDOW:
       if (value < 0 || value > 1024) return HVD_ERR_INVALID;
@@ -878,6 +943,7 @@ int64_t hvd_get_config(const hvd_comm* c, int key) {
     case HVD_CFG_FUSED: return c->fused;
     case HVD_CFG_TIMELINE: return c->tl_max;
     case HVD_CFG_WINDOW: return c->window;
+    case HVD_CFG_PROTOCOL: return c->protocol;
     case HVD_CFG_FIN_LAG: return c->fin_lag;
     default: return -1;
   }
@@ -891,6 +957,7 @@ int hvd_timeline(hvd_comm* c, int local, uint64_t* out, uint64_t cap_words, hvd_
   info->channels = c->tl_nch;
   info->slices = std::min(c->tl_slices, c->tl_max);
   info->signals = std::min(c->tl_T * c->tl_K, c->tl_max);
+  info->kind = c->tl_kind;  // 0: push/fused kernel records, 1: pull kernel records
   info->K = c->tl_K;
   info->T = c->tl_T;
   info->rank = c->virt ? local : c->rank;

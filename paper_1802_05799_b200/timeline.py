@@ -35,7 +35,14 @@ def op_of(j: int, K: int, T: int, lag: int = 1):
     return T, pairs + (q - 2 * pairs)
 
 
-def _phase(idx: int, K: int, T: int, N: int, lag: int = 1) -> str:
+def _phase(idx: int, K: int, T: int, N: int, lag: int = 1, kind: str = "push") -> str:
+    if kind == "pull":
+        t, k = idx // K, idx % K
+        if t == 0:
+            return f"stage own chunk k={k}"
+        if t < N:
+            return f"reduce-scatter s={t} k={k}"
+        return f"all-gather s={t - N + 1} k={k}"
     t, k = (idx // K, idx % K) if N == 1 else op_of(idx, K, T, lag)
     if N == 1:
         return f"scale+copy k={k}"
@@ -54,6 +61,7 @@ def chrome_trace(timelines, align: str = "per_rank") -> dict:
             continue
         r, K, T, N = tl["rank"], tl["K"], tl["T"], tl["size"]
         lag = tl.get("fin_lag", 1)
+        kind = tl.get("kind", "push")
         d, sg = tl["data"], tl["signals"]
         starts = [int(x) for x in d[:, :, 0].ravel() if int(x)]
         t0 = min(starts) if starts else 0
@@ -68,13 +76,14 @@ def chrome_trace(timelines, align: str = "per_rank") -> dict:
                 if prev_end is not None and b > prev_end:
                     events.append({"name": "wait (predecessor signal)", "cat": "WAIT", "ph": "X", "pid": r,
                                    "tid": ch, "ts": (prev_end - t0) / 1e3, "dur": (b - prev_end) / 1e3})
-                events.append({"name": _phase(i, K, T, N, lag), "cat": "RING", "ph": "X", "pid": r, "tid": ch,
+                events.append({"name": _phase(i, K, T, N, lag, kind), "cat": "RING", "ph": "X", "pid": r, "tid": ch,
                                "ts": (b - t0) / 1e3, "dur": max(e - b, 1) / 1e3})
                 prev_end = e
             for j in range(sg.shape[1]):
                 t, n = int(sg[ch, j, 0]), int(sg[ch, j, 1])
                 if t:
-                    events.append({"name": f"signal {n}", "cat": "SIGNAL", "ph": "i", "s": "t", "pid": r,
+                    nm = f"loadable op {n}" if kind == "pull" else f"signal {n}"
+                    events.append({"name": nm, "cat": "SIGNAL", "ph": "i", "s": "t", "pid": r,
                                    "tid": ch, "ts": (t - t0) / 1e3})
     return {"traceEvents": events, "displayTimeUnit": "ns"}
 
@@ -89,13 +98,14 @@ def summarize(tl) -> dict:
     d = tl["data"]
     K, T, N = tl["K"], tl["T"], tl["size"]
     lag = tl.get("fin_lag", 1)
+    kind = tl.get("kind", "push")
     b = d[:, :, 0].astype("int64")
     e = d[:, :, 1].astype("int64")
     valid = (b > 0) & (e > 0)
     span = (e[valid].max() - b[valid].min()) / 1e3 if valid.any() else 0.0
     busy = {}
     for i in range(d.shape[1]):
-        name = _phase(i, K, T, N, lag).rsplit(" k=", 1)[0]
+        name = _phase(i, K, T, N, lag, kind).rsplit(" k=", 1)[0]
         m = valid[:, i]
         busy[name] = busy.get(name, 0.0) + float(((e[:, i] - b[:, i])[m]).mean() / 1e3 if m.any() else 0.0)
     waits = []

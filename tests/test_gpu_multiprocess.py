@@ -25,7 +25,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, cases, q):
+def _worker(rank, world, port, cases, q, protocol):
     os.environ.update(RANK=str(rank), WORLD_SIZE=str(world), LOCAL_RANK=str(rank),
                       MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import sys
@@ -34,6 +34,7 @@ def _worker(rank, world, port, cases, q):
     try:
         comm = hvd.init()
         comm.set_config(hvd._lib.HVD_CFG_TIMEOUT_MS, 20000)
+        comm.set_config(hvd._lib.HVD_CFG_PROTOCOL, protocol)
         out = []
         for case in cases:
             kind, counts, dtype, op, thr = case
@@ -90,7 +91,8 @@ CASES = [
 ]
 
 
-def test_multiprocess_ring_matches_oracle():
+@pytest.mark.parametrize("protocol", [1, 0])
+def test_multiprocess_ring_matches_oracle(protocol):
     n = min(torch.cuda.device_count(), 4)
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
@@ -98,7 +100,7 @@ def test_multiprocess_ring_matches_oracle():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, n, port, CASES, q)) for r in range(n)]
+    procs = [ctx.Process(target=_worker, args=(r, n, port, CASES, q, protocol)) for r in range(n)]
     for p in procs:
         p.start()
     res = {}

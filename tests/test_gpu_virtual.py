@@ -261,6 +261,7 @@ def test_timeline_records_every_slice(hvd):
     comm = hvd.init_virtual(n, 0, 8 << 20)
     try:
         comm.set_config(hvd._lib.HVD_CFG_TIMELINE, 256)
+        comm.set_config(hvd._lib.HVD_CFG_PROTOCOL, 1)  # push kernel records
         ts = [[torch.randn(1 << 20, device="cuda")] for _ in range(n)]
         comm.allreduce_average(ts)
         torch.cuda.synchronize()
@@ -276,6 +277,14 @@ def test_timeline_records_every_slice(hvd):
             assert sg.shape[1] >= 1 and sg[:, :, 1].max() == tl["T"] * tl["K"]
         tr = timeline.chrome_trace([comm.timeline(r) for r in range(n)])
         assert any(ev.get("cat") == "RING" for ev in tr["traceEvents"])
+        comm.set_config(hvd._lib.HVD_CFG_PROTOCOL, 0)  # pull kernel records
+        comm.allreduce_average(ts)
+        torch.cuda.synchronize()
+        tl = comm.timeline(1)
+        assert tl["kind"] == "pull" and tl["T"] == 2 * n - 1 and tl["data"].shape[1] == tl["T"] * tl["K"]
+        b, e = tl["data"][:, :, 0].astype(np.int64), tl["data"][:, :, 1].astype(np.int64)
+        assert (b > 0).all() and (e >= b).all() and (b[:, 1:] >= e[:, :-1]).all()
+        assert timeline.chrome_trace([tl])["traceEvents"]
         comm.set_config(hvd._lib.HVD_CFG_TIMELINE, 0)
         assert comm.timeline(0) is None
     finally:
@@ -349,3 +358,28 @@ def test_mixed_collective_sequence_no_sync(hvd):
             assert_same(from_torch(tx[r][k], "f32"), rx[r][k], "f32", f"x r={r} k={k}")
             assert_same(from_torch(ty[r][k], "f32"), ry[r][k], "f32", f"y r={r} k={k}")
         assert_same(from_torch(go[r], "f32"), rg[r], "f32", f"g r={r}")
+
+
+@pytest.mark.parametrize("protocol", [0, 1])
+@pytest.mark.parametrize("n", [2, 3, 5, 8])
+def test_both_protocols_bitexact(hvd, n, protocol):
+    """Pull (receiver TMA-loads) and push (sender stores) move the same partials: same bits."""
+    comm = hvd.init_virtual(n, 0, 2 << 20)
+    try:
+        comm.set_config(hvd._lib.HVD_CFG_PROTOCOL, protocol)
+        counts = [3, 1000, 262_149, 5, 77_777, 400_000]
+        for it, dtype in enumerate(["f32", "bf16", "f32"]):
+            xs = workloads.all_ranks(counts, dtype, n, seed=500 + it)
+            ref, _, plan = oracle.allreduce(xs, [dtype] * len(counts), "average", threshold=1 << 20,
+                                            capacity=2 << 20)
+            ts = [[to_torch(x, dtype) for x in xs[r]] for r in range(n)]
+            comm.allreduce(ts, op="average", fusion_threshold=1 << 20)
+            torch.cuda.synchronize()
+            assert comm.poll_error() == 0
+            st = comm.kernel_stats()
+            assert st["pull" if protocol == 0 else "fused"][0] == len(plan)
+            for r in range(n):
+                for k in range(len(counts)):
+                    assert_same(from_torch(ts[r][k], dtype), ref[r][k], dtype, f"it={it} r={r} k={k}")
+    finally:
+        comm.finalize()

@@ -80,6 +80,42 @@ __global__ void tma_push(char* __restrict__ dst, size_t bytes, int chunk, int de
   }
 }
 
+// TMA bulk pull: one thread per CTA streams its share of the PEER buffer into a
+// ring of `depth` shared-memory stages (mbarrier transaction counts, no fences).
+__global__ void tma_pull(const char* __restrict__ src, size_t bytes, int chunk, int depth) {
+  extern __shared__ __align__(128) char smem[];
+  __shared__ __align__(8) unsigned long long bars[16];
+  if (threadIdx.x != 0) return;
+  const size_t per = (bytes / gridDim.x) / chunk * chunk;
+  const char* base = src + blockIdx.x * per;
+  for (int i = 0; i < depth; ++i) {
+    uint32_t b = (uint32_t)__cvta_generic_to_shared(&bars[i]);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  const size_t n = per / chunk;
+  uint32_t phase[16] = {0};
+  for (size_t i = 0; i < n + depth; ++i) {
+    if (i >= (size_t)depth) {  // retire the load issued depth iterations ago
+      const int st = (i - depth) % depth;
+      uint32_t b = (uint32_t)__cvta_generic_to_shared(&bars[st]);
+      uint32_t done = 0;
+      while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done) : "r"(b), "r"(phase[st]) : "memory");
+      phase[st] ^= 1;
+    }
+    if (i < n) {
+      const int st = i % depth;
+      uint32_t b = (uint32_t)__cvta_generic_to_shared(&bars[st]);
+      uint32_t d = (uint32_t)__cvta_generic_to_shared(smem + (size_t)st * chunk);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(chunk) : "memory");
+      asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(d), "l"(base + i * chunk), "r"(chunk), "r"(b) : "memory");
+    }
+  }
+}
+
 struct Res { double uni, bi; };
 
 template <class F>
@@ -137,6 +173,7 @@ int main(int argc, char** argv) {
     CK(cudaMemset(srcs[g], 1, bytes));
     CK(cudaStreamCreateWithFlags(&st[g], cudaStreamNonBlocking));
     CK(cudaFuncSetAttribute(tma_push, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10));
+    CK(cudaFuncSetAttribute(tma_pull, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10));
   }
   printf("{\"bytes\": %zu, \"results\": [\n", bytes);
   bool first = true;
@@ -146,8 +183,22 @@ int main(int argc, char** argv) {
     first = false;
     fflush(stdout);
   };
+  const bool pull_only = argc > 2 && !strcmp(argv[2], "pull");
   int grids[] = {16, 32, 64, 132, 148, 296};
   for (int gi = 0; gi < 6; ++gi) {
+    int grid = grids[gi];
+    for (int chunk : {16 << 10, 32 << 10, 64 << 10}) {
+      for (int depth : {2, 3, 4, 6}) {
+        if ((size_t)chunk * depth > (200u << 10)) continue;
+        char nm[64];
+        snprintf(nm, sizeof nm, "tma_pull_%dK_d%d", chunk >> 10, depth);
+        out(nm, grid, 32, measure([&](int g, cudaStream_t s, char*, char*) {
+              tma_pull<<<grid, 32, (size_t)chunk * depth, s>>>(srcs[1 - g], bytes, chunk, depth); }, bytes, iters, bufs,
+              srcs, st));
+      }
+    }
+  }
+  for (int gi = 0; gi < 6 && !pull_only; ++gi) {
     int grid = grids[gi];
     for (int thr : {256, 512, 1024}) {
       out("push_v8", grid, thr, measure([&](int, cudaStream_t s, char* d, char* src) {
