@@ -120,6 +120,17 @@ int hvd_local_ranks(const hvd_comm* c); /* ranks driven by this comm (1 or N)   
 int hvd_allreduce(hvd_comm* c, const hvd_tensor* t, int n, int op, uint64_t fusion_threshold,
                   void* stream);
 
+/* hvd_allreduce with a wire dtype (R14): the fusion buffer
+ * and every ring step use `wire_dtype` instead of the tensors' dtype.  All n
+ * tensors must share one float dtype; wire_dtype is HVD_FLOAT32 or HVD_BFLOAT16
+ * (0 or the tensors' dtype = plain hvd_allreduce).  fp32 tensors over a bf16
+ * wire: pack rounds fl32(x*s) to bf16 RNE (half the NVLink bytes), unpack
+ * widens exactly; bf16 tensors over an fp32 wire: fp32 partials, one final
+ * RNE rounding.  Fusion limits count wire bytes.  Needs HVD_CFG_FUSED=1.
+ * Errors: as hvd_allreduce; UNSUPPORTED for mixed or integer tensor dtypes. */
+int hvd_allreduce_ex(hvd_comm* c, const hvd_tensor* t, int n, int op, uint64_t fusion_threshold,
+                     int wire_dtype, void* stream);
+
 /* hvd_allreduce(c, t, n, HVD_AVERAGE, fusion_threshold, stream): the paper's
  * "average gradients among those multiple copies". */
 int hvd_allreduce_average(hvd_comm* c, const hvd_tensor* t, int n, uint64_t fusion_threshold,

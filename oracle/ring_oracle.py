@@ -28,7 +28,7 @@ runs the paper's algorithm step by step, in the paper's order:
     in all-gather step s it sends chunk (r+1-s) mod N.
 
 Readings of silent/ambiguous passages are listed in DESIGN.md §Readings
-(R1..R12); the ones this file implements are cited inline.
+(R1..R14); the ones this file implements are cited inline.
 
 Value representation: see ``workloads`` (bf16 = uint16 bit patterns).
 Parity pins for every function live in ``tests/test_oracle_pins.py``.
@@ -95,6 +95,25 @@ def scale_w(x: np.ndarray, s: np.float32, dtype: str) -> np.ndarray:
         if dtype == "bf16":
             return f32_to_bf16_rne(bf16_to_f32(x) * s)
     raise ValueError("AVERAGE is undefined for integer dtypes (R11)")
+
+
+def to_wire(x: np.ndarray, dtype: str, wire: str, s) -> np.ndarray:
+    """Pack with a wire dtype: fl32(f32(x) * s), then cast to ``wire``.
+
+    ``s`` is None for SUM.  f32 -> bf16 wire rounds RNE; bf16 -> f32 wire widens exactly.
+    """
+    with np.errstate(all="ignore"):
+        f = bf16_to_f32(x) if dtype == "bf16" else np.asarray(x, dtype=np.float32)
+        if s is not None:
+            f = (f * s).astype(np.float32)
+        return f32_to_bf16_rne(f) if wire == "bf16" else f.astype(np.float32)
+
+
+def from_wire(b: np.ndarray, wire: str, dtype: str) -> np.ndarray:
+    """Unpack with a wire dtype: bf16 wire -> f32 widens exactly; f32 wire -> bf16 rounds RNE."""
+    if wire == dtype:
+        return b
+    return bf16_to_f32(b) if wire == "bf16" else f32_to_bf16_rne(b)
 
 
 def inv_n(nranks: int) -> np.float32:
@@ -265,15 +284,39 @@ def ring_allreduce(bufs, dtype: str, traffic=None):
 # --------------------------------------------------------------------------
 def allreduce(xs_by_rank, dtypes, op: str = "average",
               threshold: int = DEFAULT_FUSION_BYTES,
-              capacity: int = DEFAULT_FUSION_BYTES):
+              capacity: int = DEFAULT_FUSION_BYTES, wire=None):
     """Tensor Fusion steps 1-6 around the ring, for every simulated rank.
 
     ``xs_by_rank[r][k]`` is tensor k on rank r (numpy, ``workloads`` format),
     ``dtypes[k]`` its dtype.  ``op`` is "sum" or "average".
+    ``wire`` (R14): the fusion buffer / ring dtype when it differs from the
+    tensors' (all tensors must then share one float dtype); None = same.
     Returns (outs_by_rank, traffic_per_rank, plan).
     """
     n = len(xs_by_rank)
     counts = [len(x) for x in xs_by_rank[0]]
+    if wire is not None and any(d != wire for d in dtypes):
+        if len(set(dtypes)) != 1 or dtypes[0] not in FLOAT_TYPES or wire not in FLOAT_TYPES:
+            raise ValueError("a wire dtype needs one float tensor dtype (R14)")
+        tdt = dtypes[0]
+        plan = fusion_plan([(c, wire) for c in counts], threshold, capacity)
+        outs = [[x.copy() for x in xs] for xs in xs_by_rank]
+        traffic = [Traffic() for _ in range(n)]
+        scale = inv_n(n) if op == "average" else None
+        for fb in plan:
+            bufs = []
+            for r in range(n):
+                buf = np.zeros(fb.length, dtype=NP_TYPE[wire])
+                for e in fb.entries:
+                    x = xs_by_rank[r][e.tensor][e.src_off:e.src_off + e.count]
+                    buf[e.dst_off:e.dst_off + e.count] = to_wire(x, tdt, wire, scale)
+                bufs.append(buf)
+            ring_allreduce(bufs, wire, traffic)
+            for r in range(n):
+                for e in fb.entries:
+                    outs[r][e.tensor][e.src_off:e.src_off + e.count] = from_wire(
+                        bufs[r][e.dst_off:e.dst_off + e.count], wire, tdt)
+        return outs, traffic, plan
     plan = fusion_plan(list(zip(counts, dtypes)), threshold, capacity)
     outs = [[x.copy() for x in xs] for xs in xs_by_rank]
     traffic = [Traffic() for _ in range(n)]

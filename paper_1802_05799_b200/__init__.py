@@ -92,12 +92,21 @@ class Comm:
         return flat, n
 
     def allreduce(self, tensors, op: str = "average", fusion_threshold: int = DEFAULT_FUSION_BYTES,
-                  stream=None):
-        """In-place allreduce of the tensor list (Tensor Fusion + ring)."""
+                  stream=None, wire=None):
+        """In-place allreduce of the tensor list (Tensor Fusion + ring).
+
+        ``wire`` ("f32" / "bf16" / a torch dtype): the ring dtype when it should
+        differ from the tensors' (``hvd_allreduce_ex``, R14).
+        """
         flat, n = self._flat(tensors)
         arr = _tensor_array(flat)
-        check(lib.hvd_allreduce(self._h, arr, n, _OPS[op], int(fusion_threshold), _stream_handle(stream)),
-              "hvd_allreduce")
+        if wire is None:
+            check(lib.hvd_allreduce(self._h, arr, n, _OPS[op], int(fusion_threshold), _stream_handle(stream)),
+                  "hvd_allreduce")
+        else:
+            code = _DT_CODE[wire] if isinstance(wire, str) else _dtype_code(__import__("torch").empty((), dtype=wire))
+            check(lib.hvd_allreduce_ex(self._h, arr, n, _OPS[op], int(fusion_threshold), code,
+                                       _stream_handle(stream)), "hvd_allreduce_ex")
         return tensors
 
     def allreduce_average(self, tensors, fusion_threshold: int = DEFAULT_FUSION_BYTES, stream=None):

@@ -125,7 +125,7 @@ inline size_t pull_smem_bytes(int nseg) {
 }
 inline size_t fused_smem_bytes(int nseg, int threads) {
   const size_t vb = nseg <= kFusedSmemSegs ? (size_t)(nseg + 1) / 2 * 2 * 8 : 0;
-  return vb + 2ull * kPipe * threads * 16;
+  return vb + 3ull * kPipe * threads * 16;  // slots0: 32 B per row (wire conversion), slots1: 16 B
 }
 struct FusedParams {
   RingParams ring;
@@ -136,7 +136,9 @@ struct FusedParams {
   int nseg;
   int scale_on;
   float scale;
-  int dtype;
+  int dtype;                         // wire dtype (fusion buffer / ring)
+  int tdtype;                        // tensor dtype (0: same as dtype)
+  int pad3;
 };
 
 // Launchers (hvd_kernels.cu).  All return a cudaError_t.

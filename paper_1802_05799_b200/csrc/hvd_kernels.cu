@@ -568,14 +568,122 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// Tensor <-> wire conversion of one 16 B wire vector (R14).  W = wire element
+// size, T = tensor element size; TB = tensor bytes per wire vector.  Same
+// dtype: plain 16 B (plus the AVERAGE prescale).  fp32 tensor / bf16 wire:
+// 32 B of tensor, fl32(x*s) rounded RNE.  bf16 tensor / fp32 wire: 8 B of
+// tensor, widened exactly, then fl32(x*s).
+struct Raw32 { uint4 a, b; };
+
+template <int W, int T> struct WireCvt;
+
+template <int E> struct WireCvt<E, E> {
+  static constexpr int VEL = 16 / E;
+  __device__ static __forceinline__ bool fast(const char* p, unsigned long long left) { return fast16<E>(p, left); }
+  __device__ static __forceinline__ void issue(Raw32* slot, const char* p) { cp_async16(&slot->a, p); }
+  __device__ static __forceinline__ uint4 take(const Raw32& r, float s, int on, int dtype) {
+    return Pack16<E>::conv(r.a, s, on, dtype);
+  }
+  __device__ static __forceinline__ uint4 slow(const char* p, unsigned long long left, float s, int on, int dtype) {
+    return Pack16<E>::conv(gather_slow<E>(p, left), s, on, dtype);
+  }
+  __device__ static __forceinline__ void put(char* p, unsigned long long left, const uint4& x) {
+    if (fast16<E>(p, left)) *reinterpret_cast<uint4*>(p) = x;
+    else scatter_slow<E>(p, left, x);
+  }
+};
+
+template <> struct WireCvt<2, 4> {  // fp32 tensor, bf16 wire
+  static constexpr int VEL = 8;
+  __device__ static __forceinline__ bool fast(const char* p, unsigned long long left) {
+    return left >= 8 && ((reinterpret_cast<uintptr_t>(p) & 15) == 0);
+  }
+  __device__ static __forceinline__ void issue(Raw32* slot, const char* p) {
+    cp_async16(&slot->a, p);
+    cp_async16(&slot->b, p + 16);
+  }
+  __device__ static __forceinline__ uint4 pack8(const float (&f)[8], float s, int on) {
+    float g[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) g[i] = on ? __fmul_rn(f[i], s) : f[i];
+    return make_uint4(pack_bf16x2(g[0], g[1]), pack_bf16x2(g[2], g[3]), pack_bf16x2(g[4], g[5]),
+                      pack_bf16x2(g[6], g[7]));
+  }
+  __device__ static __forceinline__ uint4 take(const Raw32& r, float s, int on, int) {
+    const float f[8] = {__uint_as_float(r.a.x), __uint_as_float(r.a.y), __uint_as_float(r.a.z), __uint_as_float(r.a.w),
+                        __uint_as_float(r.b.x), __uint_as_float(r.b.y), __uint_as_float(r.b.z), __uint_as_float(r.b.w)};
+    return pack8(f, s, on);
+  }
+  __device__ static __noinline__ uint4 slow(const char* p, unsigned long long left, float s, int on, int) {
+    float f[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f[i] = (unsigned long long)i < left ? reinterpret_cast<const float*>(p)[i] : 0.f;
+    return pack8(f, s, on);
+  }
+  __device__ static __forceinline__ void put(char* p, unsigned long long left, const uint4& x) {
+    const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+    float f[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      f[2 * i] = bf16lo(w[i]);
+      f[2 * i + 1] = bf16hi(w[i]);
+    }
+    if (fast(p, left)) {
+      reinterpret_cast<float4*>(p)[0] = make_float4(f[0], f[1], f[2], f[3]);
+      reinterpret_cast<float4*>(p)[1] = make_float4(f[4], f[5], f[6], f[7]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if ((unsigned long long)i < left) reinterpret_cast<float*>(p)[i] = f[i];
+    }
+  }
+};
+
+template <> struct WireCvt<4, 2> {  // bf16 tensor, fp32 wire
+  static constexpr int VEL = 4;
+  __device__ static __forceinline__ bool fast(const char* p, unsigned long long left) {
+    return left >= 4 && ((reinterpret_cast<uintptr_t>(p) & 7) == 0);
+  }
+  __device__ static __forceinline__ void issue(Raw32* slot, const char* p) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(&slot->a)),
+                 "l"(p) : "memory");
+  }
+  __device__ static __forceinline__ uint4 widen4(uint32_t lo2, uint32_t hi2, float s, int on) {
+    float f[4] = {bf16lo(lo2), bf16hi(lo2), bf16lo(hi2), bf16hi(hi2)};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) f[i] = on ? __fmul_rn(f[i], s) : f[i];
+    return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]), __float_as_uint(f[3]));
+  }
+  __device__ static __forceinline__ uint4 take(const Raw32& r, float s, int on, int) { return widen4(r.a.x, r.a.y, s, on); }
+  __device__ static __noinline__ uint4 slow(const char* p, unsigned long long left, float s, int on, int) {
+    uint16_t h[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = (unsigned long long)i < left ? reinterpret_cast<const uint16_t*>(p)[i] : 0;
+    return widen4(uint32_t(h[0]) | (uint32_t(h[1]) << 16), uint32_t(h[2]) | (uint32_t(h[3]) << 16), s, on);
+  }
+  __device__ static __forceinline__ void put(char* p, unsigned long long left, const uint4& x) {
+    const uint32_t a = pack_bf16x2(__uint_as_float(x.x), __uint_as_float(x.y));
+    const uint32_t b = pack_bf16x2(__uint_as_float(x.z), __uint_as_float(x.w));
+    if (fast(p, left)) {
+      *reinterpret_cast<uint2*>(p) = make_uint2(a, b);
+    } else {
+      const uint16_t h[4] = {uint16_t(a), uint16_t(a >> 16), uint16_t(b), uint16_t(b >> 16)};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if ((unsigned long long)i < left) reinterpret_cast<uint16_t*>(p)[i] = h[i];
+    }
+  }
+};
+
 // One slice [lo, hi) of the fused kernel by the data threads.  Row j of the
 // slice is vector v = v_lo + j*nthr + tid.  slots0/slots1: [kPipe][nthr] uint4.
-template <class Op, int KIND>
+template <class Op, int KIND, int TESZ = Op::kEsz>
 __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& me, unsigned long long lo,
                                             unsigned long long hi, unsigned tid, unsigned nthr, SegCache& sc,
-                                            uint4* slots0, uint4* slots1) {
-  constexpr int ESZ = Op::kEsz;
+                                            Raw32* slots0, uint4* slots1) {
+  constexpr int ESZ = Op::kEsz;  // wire element size
   constexpr int VEL = 16 / ESZ;
+  using Cvt = WireCvt<ESZ, TESZ>;
   constexpr bool GATHER = KIND == kF_RS0 || KIND == kF_RS || KIND == kF_AG0 || KIND == kF_SOLO ||
                           KIND == kF_G2B || KIND == kF_G2BS;
   constexpr bool SCATTER = KIND == kF_AG0 || KIND == kF_AG || KIND == kF_FIN || KIND == kF_SOLO || KIND == kF_G2BS;
@@ -590,15 +698,15 @@ __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& m
   auto issue = [&](int j) {
     if (j < rows) {
       const unsigned long long v = v_lo + (unsigned long long)j * nthr + tid;
-      uint4* d0 = slots0 + (j % kPipe) * nthr + tid;
+      Raw32* d0 = slots0 + (j % kPipe) * nthr + tid;
       if (GATHER) {
-        seg_lookup<ESZ>(F, v, ci);
+        seg_lookup<TESZ>(F, v, ci);
         const unsigned long long e = v * VEL;
         const unsigned long long left = ci.end_el > e ? ci.end_el - e : 0;
-        const char* tp = reinterpret_cast<const char*>(ci.g + e * ESZ);
-        if (fast16<ESZ>(tp, left)) cp_async16(d0, tp);
+        const char* tp = reinterpret_cast<const char*>(ci.g + e * TESZ);
+        if (Cvt::fast(tp, left)) Cvt::issue(d0, tp);
       } else {
-        cp_async16(d0, me.buf + v * 16);
+        cp_async16(&d0->a, me.buf + v * 16);
       }
       if (ADD) cp_async16(slots1 + (j % kPipe) * nthr + tid, me.scratch + v * 16);
     }
@@ -613,16 +721,16 @@ __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& m
     unsigned long long left = 0;
     unsigned long long e = v * VEL;
     if (GATHER || SCATTER) {
-      seg_lookup<ESZ>(F, v, sc);
+      seg_lookup<TESZ>(F, v, sc);
       left = sc.end_el > e ? sc.end_el - e : 0;
     }
     uint4 x;
     if (GATHER) {
-      const char* gp = reinterpret_cast<const char*>(sc.g + e * ESZ);
-      x = fast16<ESZ>(gp, left) ? slots0[(j % kPipe) * nthr + tid] : gather_slow<ESZ>(gp, left);
-      x = Pack16<ESZ>::conv(x, F.scale, F.scale_on, F.dtype);
+      const char* gp = reinterpret_cast<const char*>(sc.g + e * TESZ);
+      x = Cvt::fast(gp, left) ? Cvt::take(slots0[(j % kPipe) * nthr + tid], F.scale, F.scale_on, F.dtype)
+                              : Cvt::slow(gp, left, F.scale, F.scale_on, F.dtype);
     } else {
-      x = slots0[(j % kPipe) * nthr + tid];
+      x = slots0[(j % kPipe) * nthr + tid].a;
     }
     if (ADD) {
       const uint4 y = slots1[(j % kPipe) * nthr + tid];
@@ -630,11 +738,7 @@ __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& m
     }
     if (TO_NSCRATCH) *reinterpret_cast<uint4*>(me.nscratch + v * 16) = x;
     if (TO_NBUF) *reinterpret_cast<uint4*>(me.nbuf + v * 16) = x;
-    if (SCATTER) {
-      char* tp = reinterpret_cast<char*>(sc.d + e * ESZ);
-      if (fast16<ESZ>(tp, left)) *reinterpret_cast<uint4*>(tp) = x;
-      else scatter_slow<ESZ>(tp, left, x);
-    }
+    if (SCATTER) Cvt::put(reinterpret_cast<char*>(sc.d + e * TESZ), left, x);
   }
   cp_async_wait<0>();
 }
@@ -669,7 +773,7 @@ __device__ __host__ __forceinline__ void fused_op(int j, int K, int T, int lag, 
   }
 }
 
-template <class Op>
+template <class Op, int TESZ>
 __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_constant__ FusedParams P) {
   extern __shared__ __align__(16) unsigned long long s_dyn[];
   const RingParams& R = P.ring;
@@ -685,8 +789,8 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
   const bool cache = P.nseg <= kFusedSmemSegs;
   unsigned long long* s_vbeg = s_dyn;
   const int ndata = blockDim.x - 32;
-  uint4* slots0 = reinterpret_cast<uint4*>(s_dyn + (cache ? (P.nseg + 1) / 2 * 2 : 0));
-  uint4* slots1 = slots0 + kPipe * ndata;
+  Raw32* slots0 = reinterpret_cast<Raw32*>(s_dyn + (cache ? (P.nseg + 1) / 2 * 2 : 0));
+  uint4* slots1 = reinterpret_cast<uint4*>(slots0 + kPipe * ndata);
   if (cache)
     for (int j = threadIdx.x; j < P.nseg; j += blockDim.x) s_vbeg[j] = P.segs[j].vbeg;
   if (threadIdx.x == 0) {
@@ -721,7 +825,7 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
       unsigned long long lo, hi;
       slice_range(R, 0, ch, k, lo, hi);
       const unsigned long long tb = tl_d ? globaltimer() : 0;
-      if (hi > lo) fused_slice<Op, kF_SOLO>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
+      if (hi > lo) fused_slice<Op, kF_SOLO, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
       if (tl_d && tid == 0 && nrec < R.tl_max) {
         tl_d[2 * nrec] = tb;
         tl_d[2 * nrec + 1] = globaltimer();
@@ -752,11 +856,11 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
     }
     const unsigned long long tb = tl_d ? globaltimer() : 0;
     if (hi > lo && !s_abort) {
-      if (t == T) fused_slice<Op, kF_FIN>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
-      else if (rs && s == 0) fused_slice<Op, kF_RS0>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
-      else if (rs) fused_slice<Op, kF_RS>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
-      else if (s == 0) fused_slice<Op, kF_AG0>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
-      else fused_slice<Op, kF_AG>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
+      if (t == T) fused_slice<Op, kF_FIN, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
+      else if (rs && s == 0) fused_slice<Op, kF_RS0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
+      else if (rs) fused_slice<Op, kF_RS, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
+      else if (s == 0) fused_slice<Op, kF_AG0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
+      else fused_slice<Op, kF_AG, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
       if (t < T) sent += (hi - lo) * Op::kEsz;
     }
     if (j + 1 == nops) {
@@ -820,8 +924,8 @@ __global__ void __launch_bounds__(416, 1) copy_collective_kernel(const __grid_co
   __shared__ int s_abort, s_done, s_pub;
   const bool cache = P.nseg <= kFusedSmemSegs;
   unsigned long long* s_vbeg = s_dyn;
-  uint4* slots0 = reinterpret_cast<uint4*>(s_dyn + (cache ? (P.nseg + 1) / 2 * 2 : 0));
-  uint4* slots1 = slots0 + kPipe * nd;
+  Raw32* slots0 = reinterpret_cast<Raw32*>(s_dyn + (cache ? (P.nseg + 1) / 2 * 2 : 0));
+  uint4* slots1 = reinterpret_cast<uint4*>(slots0 + kPipe * nd);
   if (cache)
     for (int j = threadIdx.x; j < P.nseg; j += blockDim.x) s_vbeg[j] = P.segs[j].vbeg;
   if (threadIdx.x == 0) {
@@ -1230,12 +1334,12 @@ cudaError_t launch_ring(const RingParams& p, int dtype, int nch, int nlocal, int
   }
 }
 
-template <class Op>
+template <class Op, int TESZ>
 static cudaError_t launch_fused_t(const FusedParams& p, int nch, int nlocal, int threads, cudaStream_t s) {
   const size_t smem = fused_smem_bytes(p.nseg, threads);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(fused_allreduce_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(fused_allreduce_kernel<Op, TESZ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)fused_smem_bytes(kFusedSmemSegs, kMaxRingThreads));
     if (e != cudaSuccess) return e;
     attr_set = true;
@@ -1250,17 +1354,24 @@ static cudaError_t launch_fused_t(const FusedParams& p, int nch, int nlocal, int
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, fused_allreduce_kernel<Op>, p);
+  return cudaLaunchKernelEx(&cfg, fused_allreduce_kernel<Op, TESZ>, p);
 }
 
+// dtype = wire (fusion buffer / ring) dtype; p.tdtype = tensor dtype (R14)
 cudaError_t launch_fused(const FusedParams& p, int dtype, int nch, int nlocal, int threads, cudaStream_t s) {
-  switch (dtype) {
-    case 1: return launch_fused_t<OpF32>(p, nch, nlocal, threads, s);
-    case 2: return launch_fused_t<OpBF16>(p, nch, nlocal, threads, s);
-    case 3: return launch_fused_t<OpI32>(p, nch, nlocal, threads, s);
-    case 4: return launch_fused_t<OpI64>(p, nch, nlocal, threads, s);
-    default: return cudaErrorInvalidValue;
+  const int td = p.tdtype ? p.tdtype : dtype;
+  if (td == dtype) {
+    switch (dtype) {
+      case 1: return launch_fused_t<OpF32, 4>(p, nch, nlocal, threads, s);
+      case 2: return launch_fused_t<OpBF16, 2>(p, nch, nlocal, threads, s);
+      case 3: return launch_fused_t<OpI32, 4>(p, nch, nlocal, threads, s);
+      case 4: return launch_fused_t<OpI64, 8>(p, nch, nlocal, threads, s);
+      default: return cudaErrorInvalidValue;
+    }
   }
+  if (dtype == 2 && td == 1) return launch_fused_t<OpBF16, 4>(p, nch, nlocal, threads, s);
+  if (dtype == 1 && td == 2) return launch_fused_t<OpF32, 2>(p, nch, nlocal, threads, s);
+  return cudaErrorInvalidValue;
 }
 
 template <class Op>
@@ -1343,10 +1454,10 @@ cudaError_t pull_max_ctas_per_sm(int dtype, int threads, int* out) {
 cudaError_t fused_max_ctas_per_sm(int dtype, int threads, int* out) {
   const size_t smem = fused_smem_bytes(kFusedSmemSegs, threads);
   switch (dtype) {
-    case 1: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fused_allreduce_kernel<OpF32>, threads + 32, smem);
-    case 2: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fused_allreduce_kernel<OpBF16>, threads + 32, smem);
-    case 3: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fused_allreduce_kernel<OpI32>, threads + 32, smem);
-    case 4: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fused_allreduce_kernel<OpI64>, threads + 32, smem);
+    case 1: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fused_allreduce_kernel<OpF32, 4>, threads + 32, smem);
+    case 2: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fused_allreduce_kernel<OpBF16, 2>, threads + 32, smem);
+    case 3: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fused_allreduce_kernel<OpI32, 4>, threads + 32, smem);
+    case 4: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fused_allreduce_kernel<OpI64, 8>, threads + 32, smem);
     default: return cudaErrorInvalidValue;
   }
 }

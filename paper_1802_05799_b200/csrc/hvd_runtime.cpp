@@ -38,7 +38,8 @@ struct Blob {
 };
 
 struct DevPlanBuffer {
-  int dtype;
+  int dtype;                            // buffer (wire) dtype
+  int tdtype = 0;                       // tensor dtype
   uint64_t L;
   PackParams pp;                        // device pointers filled in
   const unsigned long long* vbeg;       // [nseg] member start vectors (fused kernel, large plans)
@@ -188,7 +189,8 @@ size_t align256(size_t v) { return (v + 255) / 256 * 256; }
 // tensors (the training loop) reuse the uploaded tables.
 // Host description of one fusion buffer's member table (before upload).
 struct HostBuf {
-  int dtype = 0;
+  int dtype = 0;                  // buffer (wire) dtype
+  int tdtype = 0;                 // tensor dtype (0: same)
   uint64_t L = 0;                 // elements
   std::vector<PackSeg> segs;      // dst_off / count / vbeg per member
   std::vector<char*> src;         // [nlocal * nseg] gather addresses
@@ -265,6 +267,7 @@ int upload_plan(hvd_comm* c, std::vector<uint64_t> key, const std::vector<HostBu
     tiles[offs[b].ntiles] = nseg - 1;
     DevPlanBuffer db;
     db.dtype = B.dtype;
+    db.tdtype = B.tdtype ? B.tdtype : B.dtype;
     db.L = B.L;
     std::memset(&db.pp, 0, sizeof(db.pp));
     db.pp.segs = reinterpret_cast<const PackSeg*>(d + offs[b].segs);
@@ -299,10 +302,11 @@ int upload_plan(hvd_comm* c, std::vector<uint64_t> key, const std::vector<HostBu
 // uploaded and cached by (addresses, counts, dtypes, threshold): a training loop
 // that reduces the same gradient tensors every step uploads its tables once.
 int get_plan(hvd_comm* c, const hvd_tensor* t, int n, uint64_t threshold, cudaStream_t s,
-             CachedPlan** out) {
+             CachedPlan** out, int wire = 0) {
   std::vector<uint64_t> key;
-  key.reserve(4 + 3 * (size_t)n * c->nlocal);
+  key.reserve(5 + 3 * (size_t)n * c->nlocal);
   key.push_back(0x504c414eull);  // "PLAN"
+  key.push_back((uint64_t)wire);
   key.push_back(threshold);
   key.push_back((uint64_t)n);
   key.push_back((uint64_t)c->nlocal);
@@ -316,7 +320,7 @@ int get_plan(hvd_comm* c, const hvd_tensor* t, int n, uint64_t threshold, cudaSt
   std::vector<int32_t> dtypes(n);
   for (int k = 0; k < n; ++k) {
     counts[k] = t[k].count;
-    dtypes[k] = t[k].dtype;
+    dtypes[k] = wire ? wire : t[k].dtype;  // with a wire dtype the buffers hold wire elements (R14)
   }
   std::vector<hvd_plan_entry> ents;
   std::vector<hvd_plan_buffer> bufs;
@@ -325,9 +329,11 @@ int get_plan(hvd_comm* c, const hvd_tensor* t, int n, uint64_t threshold, cudaSt
   std::vector<HostBuf> hb(bufs.size());
   for (size_t b = 0; b < bufs.size(); ++b) {
     const hvd_plan_buffer& pb = bufs[b];
-    const int esz = elem_size(pb.dtype);
+    const int esz = elem_size(pb.dtype);                                  // wire element size
+    const int tesz = elem_size(t[ents[pb.first_entry].tensor].dtype);     // tensor element size
     const uint64_t vel = kPackVecBytes / esz;
     hb[b].dtype = pb.dtype;
+    hb[b].tdtype = t[ents[pb.first_entry].tensor].dtype;
     hb[b].L = pb.length;
     hb[b].segs.resize(pb.n_entries);
     hb[b].src.resize((size_t)pb.n_entries * c->nlocal);
@@ -336,7 +342,7 @@ int get_plan(hvd_comm* c, const hvd_tensor* t, int n, uint64_t threshold, cudaSt
       hb[b].segs[j] = {e.dst_off, e.count, e.dst_off / vel, 0};
       for (int l = 0; l < c->nlocal; ++l)
         hb[b].src[(size_t)l * pb.n_entries + j] =
-            static_cast<char*>(t[(size_t)l * n + e.tensor].data) + e.src_off * esz;
+            static_cast<char*>(t[(size_t)l * n + e.tensor].data) + e.src_off * tesz;
     }
   }
   return upload_plan(c, std::move(key), hb, s, out);
@@ -468,7 +474,7 @@ int enqueue_pull(hvd_comm* c, DevPlanBuffer& b, cudaStream_t s) {
 
 int enqueue_fused(hvd_comm* c, DevPlanBuffer& b, cudaStream_t s) {
   if (b.L == 0) return HVD_OK;
-  if (c->protocol == 0 && c->size > 1) return enqueue_pull(c, b, s);
+  if (c->protocol == 0 && c->size > 1 && b.tdtype == b.dtype) return enqueue_pull(c, b, s);
   FusedParams F;
   std::memset(&F, 0, sizeof(F));
   int nch = 0;
@@ -482,6 +488,7 @@ int enqueue_fused(hvd_comm* c, DevPlanBuffer& b, cudaStream_t s) {
   F.scale_on = b.pp.scale_on;
   F.scale = b.pp.scale;
   F.dtype = b.dtype;
+  F.tdtype = b.tdtype;
   st = launch_counted(c, HVD_KERNEL_FUSED, s, [&] { return launch_fused(F, b.dtype, nch, c->nlocal, c->threads, s); });
   if (st != HVD_OK) return st;
   if (c->tl) {
@@ -497,11 +504,25 @@ int enqueue_fused(hvd_comm* c, DevPlanBuffer& b, cudaStream_t s) {
 
 int pack_grid(hvd_comm* c) { return c->sm_count * c->pack_ctas_per_sm / c->nlocal + 1; }
 
-int do_allreduce(hvd_comm* c, const hvd_tensor* t, int n, int op, uint64_t threshold, cudaStream_t s) {
+int do_allreduce(hvd_comm* c, const hvd_tensor* t, int n, int op, uint64_t threshold, cudaStream_t s,
+                 int wire = 0) {
   int st = check_live(c);
   if (st != HVD_OK) return st;
   if (n < 0 || (n > 0 && !t)) return HVD_ERR_INVALID;
   if (op != HVD_SUM && op != HVD_AVERAGE) return HVD_ERR_INVALID;
+  if (wire) {  // R14: one float tensor dtype, a different float wire dtype, fused kernel only
+    if (wire != HVD_FLOAT32 && wire != HVD_BFLOAT16) return HVD_ERR_UNSUPPORTED;
+    bool same = true;
+    for (int k = 0; k < n; ++k) same = same && t[k].dtype == wire;
+    if (same) {
+      wire = 0;
+    } else {
+      for (int k = 0; k < n; ++k)
+        if (t[k].dtype != t[0].dtype || (t[k].dtype != HVD_FLOAT32 && t[k].dtype != HVD_BFLOAT16))
+          return HVD_ERR_UNSUPPORTED;
+      if (!c->fused) return HVD_ERR_UNSUPPORTED;
+    }
+  }
   for (int k = 0; k < n; ++k) {
     if (elem_size(t[k].dtype) == 0) return HVD_ERR_UNSUPPORTED;
     if (op == HVD_AVERAGE && (t[k].dtype == HVD_INT32 || t[k].dtype == HVD_INT64)) return HVD_ERR_UNSUPPORTED;
@@ -514,7 +535,7 @@ int do_allreduce(hvd_comm* c, const hvd_tensor* t, int n, int op, uint64_t thres
   if (n == 0) return HVD_OK;
   CK(cudaSetDevice(c->device));
   CachedPlan* plan = nullptr;
-  st = get_plan(c, t, n, threshold, s, &plan);
+  st = get_plan(c, t, n, threshold, s, &plan, wire);
   if (st != HVD_OK) return st;
   const float scale = 1.0f / (float)c->size;  // s = fl32(1/N) (R1)
   for (DevPlanBuffer& b : plan->bufs) {       // step 6: repeat per fusion buffer
@@ -674,6 +695,11 @@ int hvd_local_ranks(const hvd_comm* c) { return c ? c->nlocal : -1; }
 
 int hvd_allreduce(hvd_comm* c, const hvd_tensor* t, int n, int op, uint64_t fusion_threshold, void* stream) {
   return do_allreduce(c, t, n, op, fusion_threshold, static_cast<cudaStream_t>(stream));
+}
+
+int hvd_allreduce_ex(hvd_comm* c, const hvd_tensor* t, int n, int op, uint64_t fusion_threshold, int wire_dtype,
+                     void* stream) {
+  return do_allreduce(c, t, n, op, fusion_threshold, static_cast<cudaStream_t>(stream), wire_dtype);
 }
 
 int hvd_allreduce_average(hvd_comm* c, const hvd_tensor* t, int n, uint64_t fusion_threshold, void* stream) {

@@ -383,3 +383,34 @@ def test_both_protocols_bitexact(hvd, n, protocol):
                     assert_same(from_torch(ts[r][k], dtype), ref[r][k], dtype, f"it={it} r={r} k={k}")
     finally:
         comm.finalize()
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("tdt,wire", [("f32", "bf16"), ("bf16", "f32")])
+def test_wire_dtype_variants_bitexact(hvd, n, tdt, wire):
+    """hvd_allreduce_ex (R14): fp32 grads over a bf16 wire, bf16 grads over fp32 partials."""
+    counts = [1, 7, 1000, 4097, 100_003, 262_149, 33]
+    xs = workloads.all_ranks(counts, tdt, n)
+    ref, _, plan = oracle.allreduce(xs, [tdt] * len(counts), "average", threshold=400_000, wire=wire)
+    comm = comm_for(hvd, n)
+    ts = []
+    keep = []
+    for r in range(n):
+        row = []
+        for k, x in enumerate(xs[r]):
+            t = to_torch(x, tdt)
+            if k % 2 and len(x):  # misaligned views as well
+                big = torch.empty(len(x) + 1, dtype=t.dtype, device="cuda")
+                big[1:].copy_(t)
+                keep.append(big)
+                t = big[1:]
+            row.append(t)
+        ts.append(row)
+    comm.kernel_stats()
+    comm.allreduce(ts, op="average", fusion_threshold=400_000, wire=wire)
+    torch.cuda.synchronize()
+    assert comm.poll_error() == 0
+    assert comm.kernel_stats()["fused"][0] == len(plan)
+    for r in range(n):
+        for k in range(len(counts)):
+            assert_same(from_torch(ts[r][k], tdt), ref[r][k], tdt, f"N={n} r={r} k={k}")

@@ -476,3 +476,61 @@ def test_allgather_is_rank_order_concatenation(n):
         assert np.array_equal(o, ref)
     for t in tr:
         assert t.sent_elems == (n - 1) * 37 and t.recv_elems == (n - 1) * 37
+
+
+# ---------------------------------------------------------------- wire-dtype variants
+def test_bf16_wire_for_f32_n2_textbook():
+    """N=2, fp32 grads, bf16 wire: y = f32( rne( f32(rne(x0/2)) + f32(rne(x1/2)) ) ), chunk-independent."""
+    xs = [[workloads.rank_tensor(30_001, "f32", r, 0)] for r in range(2)]
+    outs, _, _ = oracle.allreduce(xs, ["f32"], "average", wire="bf16")
+    h = [(x[0] * np.float32(0.5)).astype(ml_dtypes.bfloat16).astype(np.float32) for x in xs]
+    ref = (h[0] + h[1]).astype(ml_dtypes.bfloat16).astype(np.float32)
+    for r in range(2):
+        assert np.array_equal(outs[r][0].view(np.uint32), ref.view(np.uint32))
+
+
+def test_f32_wire_for_bf16_rotated_fold():
+    """bf16 grads, fp32 wire: chunk c = rne( fold_fp32(f32(x_j) * s) ), one final rounding."""
+    n, L = 4, 70_001
+    xs = [[workloads.rank_tensor(L, "bf16", r, 2)] for r in range(n)]
+    outs, _, plan = oracle.allreduce(xs, ["bf16"], "average", wire="f32")
+    s = np.float32(1.0) / np.float32(n)
+    w = [(x[0].view(ml_dtypes.bfloat16).astype(np.float32) * s).astype(np.float32) for x in xs]
+    b = oracle.chunk_bounds(L, n, "f32")
+    ref = np.empty(L, dtype=np.float32)
+    for c in range(n):
+        sl = slice(b[c], b[c + 1])
+        acc = w[c][sl].copy()
+        for j in range(1, n):
+            acc = (acc + w[(c + j) % n][sl]).astype(np.float32)
+        ref[sl] = acc
+    ref16 = ref.astype(ml_dtypes.bfloat16).view(np.uint16)
+    for r in range(n):
+        assert np.array_equal(outs[r][0], ref16)
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_wire_variant_accuracy(n):
+    """bf16 grads with fp32 partials meet north_star's 1e-2 elementwise (R5 note); bf16 wire for
+    fp32 grads stays within the bf16 gamma bound."""
+    L = 100_000
+    xs = [[workloads.rank_tensor(L, "bf16", r, 1)] for r in range(n)]
+    outs, _, _ = oracle.allreduce(xs, ["bf16"], "average", wire="f32")
+    X = np.stack([_f64(x[0], "bf16") for x in xs])
+    m, a = X.sum(0) / n, np.abs(X).sum(0) / n
+    assert np.all(np.abs(_f64(outs[0][0], "bf16") - m) <= 1e-2 * a + 1e-300)
+    xf = [[workloads.rank_tensor(L, "f32", r, 1)] for r in range(n)]
+    outs, _, _ = oracle.allreduce(xf, ["f32"], "average", wire="bf16")
+    X = np.stack([x[0].astype(np.float64) for x in xf])
+    m, a = X.sum(0) / n, np.abs(X).sum(0) / n
+    k = n + 1
+    u = 2.0 ** -8
+    assert np.all(np.abs(outs[0][0].astype(np.float64) - m) <= k * u / (1 - k * u) * a + 1e-300)
+
+
+def test_wire_plan_uses_wire_bytes():
+    """64 MiB of bf16 wire holds 32 Mi fp32 gradient elements: fusion limits count wire bytes."""
+    p = oracle.fusion_plan([(24 << 20, "bf16")])
+    assert len(p) == 1
+    p32 = oracle.fusion_plan([(24 << 20, "f32")])
+    assert len(p32) == 2
