@@ -26,7 +26,7 @@ constexpr uint64_t kTailBytes = 16384;  // flags, stats, ready flags, pull progr
 constexpr uint32_t kBlobMagic = 0x48564442u;            // "HVDB"
 constexpr int kPackThreads = 256;
 constexpr int kPackVecsPerThread = 8;
-constexpr size_t kPlanCacheSize = 8;
+constexpr size_t kPlanCacheSize = 32;
 
 struct Blob {
   uint32_t magic;
@@ -83,6 +83,7 @@ struct hvd_comm {
   unsigned long long pbase[kMaxChannels] = {};  // pull-protocol progress counter bases
   int pull_calls = 0;
   unsigned long long pull_exits = 0;  // cumulative CTA exits of the pull kernel (per rank)
+  std::vector<std::pair<int, int>> occ_cache;  // (kernel/dtype/threads key, CTAs per SM)
   // timeline (HVD_CFG_TIMELINE): device records of the most recent fused launch
   int tl_max = 0;
   unsigned long long* tl = nullptr;
@@ -393,10 +394,18 @@ int make_ring_params(hvd_comm* c, uint64_t L, int dtype, bool fused, RingParams*
   P->q = q_override ? q_override : chunk_len(L, c->size, dtype);
   // channels: at least 32 KiB of every chunk per channel, at most the knob and
   // what stays co-resident (the CTAs of all ranks wait on each other)
-  int max_per_sm = 1;
   const int threads = pull ? std::max(256, c->threads) : c->threads;
-  CK(pull ? pull_max_ctas_per_sm(dtype, threads, &max_per_sm)
-          : fused ? fused_max_ctas_per_sm(dtype, threads, &max_per_sm) : ring_max_ctas_per_sm(dtype, threads, &max_per_sm));
+  // occupancy of (kernel, dtype, threads), cached: a driver query per launch costs microseconds
+  const int okey = (pull ? 2 : fused ? 1 : 0) * 100000 + dtype * 10000 + threads;
+  int max_per_sm = 0;
+  for (auto& kv : c->occ_cache)
+    if (kv.first == okey) max_per_sm = kv.second;
+  if (max_per_sm == 0) {
+    CK(pull ? pull_max_ctas_per_sm(dtype, threads, &max_per_sm)
+            : fused ? fused_max_ctas_per_sm(dtype, threads, &max_per_sm) : ring_max_ctas_per_sm(dtype, threads, &max_per_sm));
+    max_per_sm = std::max(1, max_per_sm);
+    c->occ_cache.push_back({okey, max_per_sm});
+  }
   const int resident = std::max(1, c->sm_count * max_per_sm / c->nlocal);
   const uint64_t qbytes = P->q * esz;
   int nch = (int)std::min<uint64_t>((uint64_t)c->channels, std::max<uint64_t>(1, qbytes / (32 << 10)));

@@ -22,6 +22,8 @@ def main():
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--slice-kib", type=int, default=0)
     ap.add_argument("--time", action="store_true")
+    ap.add_argument("--model", default="")
+    ap.add_argument("--dtype", default="f32")
     a = ap.parse_args()
     L = hvd._lib
     comm = hvd.init_virtual(a.n, 0, a.mib << 20)
@@ -33,8 +35,13 @@ def main():
     if a.slice_kib:
         comm.set_config(L.HVD_CFG_SLICE_BYTES, a.slice_kib << 10)
     comm.set_config(L.HVD_CFG_PROFILE, 1)
-    cnt = (a.mib << 20) // 4
-    ts = [[torch.randn(cnt, device="cuda")] for _ in range(a.n)]
+    tdt = torch.float32 if a.dtype == "f32" else torch.bfloat16
+    if a.model:
+        import workloads
+        counts = [c for _, c in workloads.gradient_set(a.model)]
+    else:
+        counts = [(a.mib << 20) // 4]
+    ts = [[torch.randn(c, device="cuda").to(tdt) for c in counts] for _ in range(a.n)]
     for _ in range(a.iters):
         comm.allreduce_average(ts)
     torch.cuda.synchronize()

@@ -32,7 +32,8 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--fence-mode", type=int, nargs="+", default=[1])
     ap.add_argument("--window", type=int, nargs="+", default=[0])
-    ap.add_argument("--protocol", type=int, default=0, help="0 pull, 1 push")
+    ap.add_argument("--protocol", type=int, default=1, help="0 pull, 1 push")
+    ap.add_argument("--fused", type=int, default=-1, help="ring mode: 1 fused kernel on the buffer, 0 ring kernel")
     ap.add_argument("--fin-lag", type=int, nargs="+", default=[1])
     ap.add_argument("--check", action="store_true", help="verify bit-exactness of every point vs a reference run")
     ap.add_argument("--dtype", default="f32")
@@ -54,7 +55,7 @@ def main():
     ref = {}
     grads = {mib: torch.randn((mib << 20) // esz, device="cuda").to(torch.float32 if esz == 4 else torch.bfloat16)
              for mib in a.mib}
-    comm.set_config(L.HVD_CFG_FUSED, 1 if a.mode == "fused" else 0)
+    comm.set_config(L.HVD_CFG_FUSED, (1 if a.mode == "fused" else 0) if a.fused < 0 else a.fused)
     comm.set_config(L.HVD_CFG_PROTOCOL, a.protocol)
 
     def call(mib, cnt):
@@ -101,7 +102,7 @@ def main():
         torch.cuda.synchronize(); dist.barrier()
         us = tmax(ev0.elapsed_time(ev1) / a.iters * 1e3)
         bus = (mib << 20) / (us * 1e-6) / 1e9 * 2 * (world - 1) / world
-        rows.append({"impl": "hvd", "mode": a.mode, "protocol": a.protocol, "mib": mib, "channels": ch, "slice_kib": sl, "threads": th, "sig": sg, "window": win, "fin_lag": lag,
+        rows.append({"impl": "hvd", "mode": a.mode, "fused": comm.get_config(L.HVD_CFG_FUSED), "protocol": a.protocol, "mib": mib, "channels": ch, "slice_kib": sl, "threads": th, "sig": sg, "window": win, "fin_lag": lag,
                      "us": us, "busbw": bus, "bitexact_vs_first": ok})
         if rank == 0:
             print(json.dumps(rows[-1]), flush=True)
