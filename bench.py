@@ -60,7 +60,7 @@ def _bus_factor(n):
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
@@ -85,25 +85,33 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self.p.kill()
 
-    def summary(self):
+    def summary(self, t0=None, t1=None):
+        """Median SM clock and active throttle reasons over samples taken in [t0, t1] (epoch s)."""
+        import datetime
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in (getattr(self, "out", "") or "").splitlines():
             f = [x.strip() for x in line.split(",")]
-            if len(f) < 8 or not f[0].isdigit() or int(f[0]) not in self.devices:
+            if len(f) < 9 or not f[1].isdigit() or int(f[1]) not in self.devices:
                 continue
             try:
-                sm.append(float(f[1]))
-                mx.append(float(f[2]))
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                ts = None
+            if t0 is not None and ts is not None and not (t0 - 0.15 <= ts <= t1 + 0.15):
+                continue
+            try:
+                sm.append(float(f[2]))
+                mx.append(float(f[3]))
             except ValueError:
                 continue
-            for nm, v in zip(names, f[4:8]):
+            for nm, v in zip(names, f[5:9]):
                 if v.lower() == "active":
                     reasons.add(nm)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "window": "pre-load + timed region"}
 
 
 # ---------------------------------------------------------------- distributed plumbing
@@ -158,9 +166,12 @@ def run_ours(args):
             for _ in range(nsets)]
     L = hvd._lib
     comm.set_config(L.HVD_CFG_PROFILE, 1)
+    # the gradient tensors of a training loop persist across steps: register them once
+    # (zero-copy both ways: the all-gather writes final values into the successor's tensors)
+    handles = [comm.register(st) for st in sets] if args.registered else [comm.prepare(st) for st in sets]
 
     def step(i):
-        comm.allreduce_average(sets[i % nsets])
+        comm.allreduce_average(handles[i % nsets])
 
     _barrier(world)
     w0 = time.perf_counter()
@@ -172,6 +183,7 @@ def run_ours(args):
     per_step = (time.perf_counter() - w0) / args.warmup
     n_load = int(_max_over_ranks(min(50000.0, args.clock_window / max(per_step, 1e-6)), world))
     comm.kernel_stats()  # reset counters
+    t_load0 = time.time()
     if True:
         # keep the GPU busy ~clock_window s so the sampler sees clocks under load, then time K steps
         for i in range(n_load):
@@ -187,6 +199,7 @@ def run_ours(args):
             step(i)
         s1.record()
         _barrier(world)
+    t_load1 = time.time()
     clk.__exit__(None, None, None)
     ms_local = s0.elapsed_time(s1)
     ks = comm.kernel_stats()
@@ -290,7 +303,7 @@ def run_ours(args):
     if rank == 0 and n == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args, counts, dt, n)
 
-    clocks = clk.summary()
+    clocks = clk.summary(t_load0, t_load1)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": n, "steps": args.steps,
@@ -299,6 +312,7 @@ def run_ours(args):
             "value_kind": "busBW = payload/t * 2(N-1)/N" if n > 1 else
                           "algBW = payload/t (N=1: the ring has no iterations, bus factor 0)",
             "config": {"workload": args.workload, "payload_bytes": payload, "tensors": len(counts),
+                       "tensors_registered": bool(args.registered),
                        "fusion_bytes": 64 * MIB, "op": "average",
                        "l2": f"inputs rotate over {nsets} gradient sets ({nsets * payload / MIB:.0f} MiB > L2)",
                        "parallelism": f"dp{n}", "ranks": "one process per GPU, CUDA-IPC ring"},
@@ -405,6 +419,7 @@ def main():
                     help="fp32_64MiB | resnet101 | inception_v3[_bf16] | vgg16")
     ap.add_argument("--clock-window", type=float, default=1.5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--registered", type=int, default=1, help="1: registered gradient tensors (zero-copy)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -131,6 +131,25 @@ int hvd_allreduce(hvd_comm* c, const hvd_tensor* t, int n, int op, uint64_t fusi
 int hvd_allreduce_ex(hvd_comm* c, const hvd_tensor* t, int n, int op, uint64_t fusion_threshold,
                      int wire_dtype, void* stream);
 
+/* ---- registered tensors: zero-copy both ways (SURVEY §8f-1 "the last AG step writes
+ * straight into outputs") ----------------------------------------------------------------
+ * A training loop reduces the same gradient tensors every step.  Registering them
+ * once maps every rank's tensors into its predecessor (CUDA IPC), so the all-gather
+ * iterations write the final values directly into the successor's tensors: no
+ * fusion-buffer forward and no final unpack.  Same ring order, same bits.
+ * Collective: every rank registers the same list shape.  Bootstrap like hvd_init:
+ * hvd_register_blob (blob == NULL -> *len only) -> gather the blobs of all ranks
+ * (rank order) -> hvd_register (virtual comms: blobs may be NULL).  The tensors
+ * must stay allocated until hvd_deregister / hvd_finalize.
+ * Errors: INVALID (shape mismatch across ranks, bad id), CUDA (IPC).             */
+int hvd_register_blob(hvd_comm* c, const hvd_tensor* t, int n, void* blob, uint64_t* len);
+int hvd_register(hvd_comm* c, const hvd_tensor* t, int n, const void* blobs, uint64_t len_each,
+                 int* reg_id);
+/* In-place allreduce of registered tensor list `reg_id` (op, fusion as hvd_allreduce). */
+int hvd_allreduce_registered(hvd_comm* c, int reg_id, int op, uint64_t fusion_threshold,
+                             void* stream);
+int hvd_deregister(hvd_comm* c, int reg_id);
+
 /* hvd_allreduce(c, t, n, HVD_AVERAGE, fusion_threshold, stream): the paper's
  * "average gradients among those multiple copies". */
 int hvd_allreduce_average(hvd_comm* c, const hvd_tensor* t, int n, uint64_t fusion_threshold,

@@ -72,6 +72,15 @@ class Prepared:
         self.n = n
 
 
+class Registered:
+    """A tensor list registered with ``Comm.register`` (zero-copy both ways)."""
+
+    def __init__(self, comm, tensors, reg_id):
+        self.comm = comm
+        self.tensors = tensors
+        self.reg_id = reg_id
+
+
 class Comm:
     """One communicator: a real ring rank, or all N ranks simulated on one GPU."""
 
@@ -105,6 +114,26 @@ class Comm:
         flat = [t for per_rank in tensors for t in per_rank]
         return flat, n
 
+    def register(self, tensors, group=None) -> Registered:
+        """Register a tensor list once (collective): later allreduces write the final values
+        straight into the successor's tensors (``hvd_register``)."""
+        flat, n = self._flat(tensors)
+        arr = _tensor_array(flat)
+        rid = C.c_int(-1)
+        if self.local_ranks == 1 and self.size > 1:
+            ln = C.c_uint64(0)
+            check(lib.hvd_register_blob(self._h, arr, n, None, C.byref(ln)), "hvd_register_blob")
+            buf = C.create_string_buffer(ln.value)
+            check(lib.hvd_register_blob(self._h, arr, n, buf, C.byref(ln)), "hvd_register_blob")
+            blobs = b"".join(exchange_blobs(bytes(buf.raw), group))
+            check(lib.hvd_register(self._h, arr, n, blobs, ln.value, C.byref(rid)), "hvd_register")
+        else:
+            check(lib.hvd_register(self._h, arr, n, None, 0, C.byref(rid)), "hvd_register")
+        return Registered(self, tensors, rid.value)
+
+    def deregister(self, reg: Registered):
+        check(lib.hvd_deregister(self._h, reg.reg_id), "hvd_deregister")
+
     def prepare(self, tensors) -> Prepared:
         """Marshal a tensor list once for repeated collectives on the same tensors."""
         return Prepared(self, tensors)
@@ -123,6 +152,12 @@ class Comm:
         ``wire`` ("f32" / "bf16" / a torch dtype): the ring dtype when it should
         differ from the tensors' (``hvd_allreduce_ex``, R14).
         """
+        if isinstance(tensors, Registered):
+            if wire is not None:
+                raise HvdError(_lib.HVD_ERR_UNSUPPORTED, "wire dtype with registered tensors")
+            check(lib.hvd_allreduce_registered(self._h, tensors.reg_id, _OPS[op], int(fusion_threshold),
+                                               _stream_handle(stream)), "hvd_allreduce_registered")
+            return tensors.tensors
         arr, n = self._marshal(tensors)
         if wire is None:
             check(lib.hvd_allreduce(self._h, arr, n, _OPS[op], int(fusion_threshold), _stream_handle(stream)),
@@ -135,6 +170,8 @@ class Comm:
 
     def allreduce_average(self, tensors, fusion_threshold: int = DEFAULT_FUSION_BYTES, stream=None):
         """The paper's gradient averaging."""
+        if isinstance(tensors, Registered):
+            return self.allreduce(tensors, "average", fusion_threshold, stream)
         arr, n = self._marshal(tensors)
         check(lib.hvd_allreduce_average(self._h, arr, n, int(fusion_threshold), _stream_handle(stream)),
               "hvd_allreduce_average")

@@ -84,6 +84,10 @@ def _load():
         "hvd_allreduce": (C.c_int, [P, C.POINTER(hvd_tensor), C.c_int, C.c_int, C.c_uint64, P]),
         "hvd_allreduce_average": (C.c_int, [P, C.POINTER(hvd_tensor), C.c_int, C.c_uint64, P]),
         "hvd_allreduce_ex": (C.c_int, [P, C.POINTER(hvd_tensor), C.c_int, C.c_int, C.c_uint64, C.c_int, P]),
+        "hvd_register_blob": (C.c_int, [P, C.POINTER(hvd_tensor), C.c_int, P, C.POINTER(C.c_uint64)]),
+        "hvd_register": (C.c_int, [P, C.POINTER(hvd_tensor), C.c_int, P, C.c_uint64, C.POINTER(C.c_int)]),
+        "hvd_allreduce_registered": (C.c_int, [P, C.c_int, C.c_int, C.c_uint64, P]),
+        "hvd_deregister": (C.c_int, [P, C.c_int]),
         "hvd_allreduce_buffer": (C.c_int, [P, C.c_uint64, C.c_int, C.c_int, P]),
         "hvd_fusion_buffer": (P, [P, C.c_int]),
         "hvd_fusion_capacity": (C.c_uint64, [P]),
@@ -116,7 +120,8 @@ EXPORTS = sorted([
     "hvd_size", "hvd_local_ranks", "hvd_allreduce", "hvd_allreduce_average", "hvd_allreduce_buffer",
     "hvd_fusion_buffer", "hvd_fusion_capacity", "hvd_broadcast", "hvd_allgather", "hvd_poll_error",
     "hvd_strerror", "hvd_traffic", "hvd_set_config", "hvd_get_config", "hvd_plan", "hvd_chunk_bounds",
-    "hvd_kernel_stats", "hvd_timeline", "hvd_allreduce_ex",
+    "hvd_kernel_stats", "hvd_timeline", "hvd_allreduce_ex", "hvd_register_blob", "hvd_register",
+    "hvd_allreduce_registered", "hvd_deregister",
 ])
 
 

@@ -138,7 +138,8 @@ struct FusedParams {
   float scale;
   int dtype;                         // wire dtype (fusion buffer / ring)
   int tdtype;                        // tensor dtype (0: same as dtype)
-  int pad3;
+  int registered;                    // 1: all-gather writes into the successor's tensors (rdst)
+  char* const* rdst;                 // [nlocal * nseg] successor's tensor addresses (registered)
 };
 
 // Launchers (hvd_kernels.cu).  All return a cudaError_t.

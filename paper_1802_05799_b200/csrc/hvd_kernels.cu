@@ -480,6 +480,8 @@ __global__ void __launch_bounds__(256) pack_kernel(const __grid_constant__ PackP
 // in-place update of the caller's tensors is safe.  Results are bit-identical
 // to pack -> ring -> unpack: same per-element operations in the same order.
 enum FusedKind { kF_RS0 = 0, kF_RS = 1, kF_AG0 = 2, kF_AG = 3, kF_FIN = 4, kF_SOLO = 5,
+                 kF_RAG0 = 8,   // registered all-gather step 0: final -> own tensors + successor's tensors
+                 kF_RAG = 9,    // registered all-gather step s >= 1: own tensors -> successor's tensors
                  kF_G2B = 6,    // broadcast root:        nbuf <- gather(x)
                  kF_G2BS = 7 }; // allgather own block:   nbuf <- gather(in); out <- same
 
@@ -487,6 +489,7 @@ struct FusedCtx {
   const PackSeg* segs;
   char* const* src;                 // this rank's gather addresses [nseg]
   char* const* dst;                 // this rank's scatter addresses [nseg] (== src for allreduce)
+  char* const* rdst;                // registered mode: the successor's tensor addresses [nseg]
   const unsigned long long* vbeg;   // shared or global copy of segs[].vbeg
   int nseg;
   int scale_on;
@@ -536,6 +539,7 @@ struct SegCache {
   unsigned long long vlo = 1, vhi = 0;  // vectors [vlo, vhi) belong to member s (empty at start)
   unsigned long long end_el = 0;        // member end, buffer element index
   uintptr_t g = 0, d = 0;               // gather / scatter address of buffer element 0 of this member
+  uintptr_t rd = 0;                     // registered mode: successor's address of buffer element 0
   int s = 0;
 };
 
@@ -550,6 +554,7 @@ __device__ __forceinline__ void seg_lookup(const FusedCtx& F, unsigned long long
   c.end_el = dst_off + F.segs[s].count;
   c.g = reinterpret_cast<uintptr_t>(F.src[s]) - dst_off * ESZ;
   c.d = reinterpret_cast<uintptr_t>(F.dst[s]) - dst_off * ESZ;
+  if (F.rdst) c.rd = reinterpret_cast<uintptr_t>(F.rdst[s]) - dst_off * ESZ;
 }
 
 template <int ESZ>
@@ -685,9 +690,12 @@ __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& m
   constexpr int VEL = 16 / ESZ;
   using Cvt = WireCvt<ESZ, TESZ>;
   constexpr bool GATHER = KIND == kF_RS0 || KIND == kF_RS || KIND == kF_AG0 || KIND == kF_SOLO ||
-                          KIND == kF_G2B || KIND == kF_G2BS;
-  constexpr bool SCATTER = KIND == kF_AG0 || KIND == kF_AG || KIND == kF_FIN || KIND == kF_SOLO || KIND == kF_G2BS;
-  constexpr bool ADD = KIND == kF_RS || KIND == kF_AG0;
+                          KIND == kF_G2B || KIND == kF_G2BS || KIND == kF_RAG0 || KIND == kF_RAG;
+  constexpr bool SCALE = KIND != kF_RAG;  // the registered forward reads final values: no prescale
+  constexpr bool SCATTER = KIND == kF_AG0 || KIND == kF_AG || KIND == kF_FIN || KIND == kF_SOLO || KIND == kF_G2BS ||
+                           KIND == kF_RAG0;
+  constexpr bool RSCATTER = KIND == kF_RAG0 || KIND == kF_RAG;  // into the successor's tensors
+  constexpr bool ADD = KIND == kF_RS || KIND == kF_AG0 || KIND == kF_RAG0;
   constexpr bool TO_NSCRATCH = KIND == kF_RS0 || KIND == kF_RS;
   constexpr bool TO_NBUF = KIND == kF_AG0 || KIND == kF_AG || KIND == kF_G2B || KIND == kF_G2BS;
   const unsigned long long v_lo = lo / VEL;
@@ -727,8 +735,9 @@ __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& m
     uint4 x;
     if (GATHER) {
       const char* gp = reinterpret_cast<const char*>(sc.g + e * TESZ);
-      x = Cvt::fast(gp, left) ? Cvt::take(slots0[(j % kPipe) * nthr + tid], F.scale, F.scale_on, F.dtype)
-                              : Cvt::slow(gp, left, F.scale, F.scale_on, F.dtype);
+      const int on = SCALE ? F.scale_on : 0;
+      x = Cvt::fast(gp, left) ? Cvt::take(slots0[(j % kPipe) * nthr + tid], F.scale, on, F.dtype)
+                              : Cvt::slow(gp, left, F.scale, on, F.dtype);
     } else {
       x = slots0[(j % kPipe) * nthr + tid].a;
     }
@@ -739,6 +748,7 @@ __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& m
     if (TO_NSCRATCH) *reinterpret_cast<uint4*>(me.nscratch + v * 16) = x;
     if (TO_NBUF) *reinterpret_cast<uint4*>(me.nbuf + v * 16) = x;
     if (SCATTER) Cvt::put(reinterpret_cast<char*>(sc.d + e * TESZ), left, x);
+    if (RSCATTER) Cvt::put(reinterpret_cast<char*>(sc.rd + e * TESZ), left, x);
   }
   cp_async_wait<0>();
 }
@@ -812,6 +822,7 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
   F.segs = P.segs;
   F.src = P.src + (size_t)blockIdx.y * P.nseg;
   F.dst = (P.dst ? P.dst : P.src) + (size_t)blockIdx.y * P.nseg;
+  F.rdst = P.registered ? P.rdst + (size_t)blockIdx.y * P.nseg : nullptr;
   F.vbeg = cache ? s_vbeg : P.vbeg_global;
   F.nseg = P.nseg;
   F.scale_on = P.scale_on;
@@ -835,6 +846,51 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
     return;
   }
   int i = 0;
+  if (P.registered) {
+    // Registered tensors (zero-copy both ways): the all-gather steps write the final
+    // values straight into the successor's tensors, so there is no fusion-buffer
+    // forward and no final local scatter.  Ops (t, k) in order, t = 0..T-1.
+    for (int j = 0; j < T * K; ++j) {
+      const int t = j / K, k = j - (j / K) * K;
+      const bool rs = t < N - 1;
+      const int s = rs ? t : t - (N - 1);
+      const int c = rs ? mod(r - s, N) : mod(r + 1 - s, N);
+      unsigned long long lo, hi;
+      slice_range(R, c, ch, k, lo, hi);
+      const unsigned long long tb = tl_d ? globaltimer() : 0;
+      if (hi > lo && !s_abort) {
+        if (rs && s == 0) fused_slice<Op, kF_RS0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
+        else if (rs) fused_slice<Op, kF_RS, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
+        else if (s == 0) fused_slice<Op, kF_RAG0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
+        else fused_slice<Op, kF_RAG, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
+        sent += (hi - lo) * Op::kEsz;
+      }
+      bar_sync(kBarData, nd);
+      if (tl_d && tid == 0 && nrec < R.tl_max) {
+        tl_d[2 * nrec] = tb;
+        tl_d[2 * nrec + 1] = globaltimer();
+        ++nrec;
+      }
+      ++i;
+      // next op's dependency; after the last op: the predecessor's last all-gather slice,
+      // which lands in this rank's tensors (completion on the stream = all data arrived)
+      const int tn = (k + 1 < K) ? t : t + 1;
+      const int kn = (k + 1 < K) ? k + 1 : 0;
+      if (tid == 0) {
+        st_release_cta_shared(&s_done, i);
+        unsigned long long target = 0;
+        if (tn < T && tn > 0) target = base + (unsigned long long)(tn - 1) * K + kn + 1;
+        else if (tn >= T) target = base + (unsigned long long)T * K;
+        if (target && !s_abort && !spin_until(me.flags + ch, target, R.err, R.timeout_ns)) s_abort = 1;
+      }
+      if (tn > 0) bar_sync(kBarData, nd);
+    }
+    if (tid == 0) {
+      atomicAdd(me.stats + 0, sent);
+      if (ch == 0) atomicAdd(me.stats + 1, (unsigned long long)T);
+    }
+    return;
+  }
   // Operation sequence: iterations t < T-1 in order, then the last all-gather step
   // interleaved with the final local scatter one slice behind (fused_op), so the
   // scatter of slice k overlaps the NVLink drain of slice k+1.
@@ -943,6 +999,7 @@ __global__ void __launch_bounds__(416, 1) copy_collective_kernel(const __grid_co
   F.segs = P.segs;
   F.src = P.src + (size_t)blockIdx.y * P.nseg;
   F.dst = (P.dst ? P.dst : P.src) + (size_t)blockIdx.y * P.nseg;
+  F.rdst = nullptr;
   F.vbeg = cache ? s_vbeg : P.vbeg_global;
   F.nseg = P.nseg;
   F.scale_on = 0;
@@ -1128,6 +1185,7 @@ __global__ void __launch_bounds__(416, 1) pull_allreduce_kernel(const __grid_con
   F.segs = P.segs;
   F.src = P.src + (size_t)blockIdx.y * P.nseg;
   F.dst = (P.dst ? P.dst : P.src) + (size_t)blockIdx.y * P.nseg;
+  F.rdst = nullptr;
   F.vbeg = cache ? s_vbeg : P.vbeg_global;
   F.nseg = P.nseg;
   F.scale_on = P.scale_on;

@@ -2,9 +2,12 @@
 // peer mapping, plan cache with device-resident segment tables, and the
 // stream-ordered enqueue of pack -> ring -> unpack per fusion buffer
 // (§7 steps 2-6).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
+#include <string>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -44,6 +47,17 @@ struct DevPlanBuffer {
   PackParams pp;                        // device pointers filled in
   const unsigned long long* vbeg;       // [nseg] member start vectors (fused kernel, large plans)
   char* const* dst = nullptr;           // [nlocal * nseg] scatter addresses (nullptr: = pp.src)
+  char* const* rdst = nullptr;          // [nlocal * nseg] registered: successor's addresses
+};
+
+// A registered tensor list (hvd_register): this rank's tensors plus the successor's
+// same-index tensors mapped into this process (CUDA IPC), so the all-gather steps
+// can write final values straight into the successor's tensors.
+struct Registration {
+  int n = 0;
+  std::vector<hvd_tensor> own;     // [nlocal * n]
+  std::vector<char*> succ;         // [nlocal * n] successor's tensor addresses
+  bool live = false;
 };
 
 struct CachedPlan {
@@ -68,7 +82,7 @@ struct hvd_comm {
   int* err_dev = nullptr;
   int sm_count = 148;
   // tuning (hvd_set_config)
-  int channels = 148;
+  int channels = 128;
   int64_t slice_bytes = 0;  // 0 = auto: about half of a channel's share of a chunk, 32..128 KiB
   int threads = 384;
   int64_t timeout_ms = 30000;
@@ -84,6 +98,8 @@ struct hvd_comm {
   int pull_calls = 0;
   unsigned long long pull_exits = 0;  // cumulative CTA exits of the pull kernel (per rank)
   std::vector<std::pair<int, int>> occ_cache;  // (kernel/dtype/threads key, CTAs per SM)
+  std::vector<Registration> regs;               // hvd_register
+  std::map<std::string, char*> ipc_maps;        // opened peer allocations (by handle bytes)
   // timeline (HVD_CFG_TIMELINE): device records of the most recent fused launch
   int tl_max = 0;
   unsigned long long* tl = nullptr;
@@ -192,6 +208,7 @@ size_t align256(size_t v) { return (v + 255) / 256 * 256; }
 struct HostBuf {
   int dtype = 0;                  // buffer (wire) dtype
   int tdtype = 0;                 // tensor dtype (0: same)
+  std::vector<char*> rdst;        // [nlocal * nseg] registered: successor's addresses
   uint64_t L = 0;                 // elements
   std::vector<PackSeg> segs;      // dst_off / count / vbeg per member
   std::vector<char*> src;         // [nlocal * nseg] gather addresses
@@ -213,7 +230,7 @@ CachedPlan* lookup_plan(hvd_comm* c, const std::vector<uint64_t>& key) {
 int upload_plan(hvd_comm* c, std::vector<uint64_t> key, const std::vector<HostBuf>& hb, cudaStream_t s,
                 CachedPlan** out) {
   // layout per buffer: [segs][src][dst][tile_seg][vbeg]
-  struct Off { size_t segs, src, dst, tiles, vbeg; uint64_t nvec, ntiles; };
+  struct Off { size_t segs, src, dst, rdst, tiles, vbeg; uint64_t nvec, ntiles; };
   std::vector<Off> offs(hb.size());
   const uint64_t tile_vecs = (uint64_t)kPackThreads * kPackVecsPerThread;
   size_t total = 0;
@@ -229,6 +246,8 @@ int upload_plan(hvd_comm* c, std::vector<uint64_t> key, const std::vector<HostBu
     total = align256(total + sizeof(char*) * nseg * c->nlocal);
     offs[b].dst = total;
     if (!hb[b].dst.empty()) total = align256(total + sizeof(char*) * nseg * c->nlocal);
+    offs[b].rdst = total;
+    if (!hb[b].rdst.empty()) total = align256(total + sizeof(char*) * nseg * c->nlocal);
     offs[b].tiles = total;
     total = align256(total + sizeof(int) * (offs[b].ntiles + 1));
     offs[b].vbeg = total;
@@ -258,6 +277,7 @@ int upload_plan(hvd_comm* c, std::vector<uint64_t> key, const std::vector<HostBu
     }
     std::memcpy(src, B.src.data(), sizeof(char*) * B.src.size());
     if (!B.dst.empty()) std::memcpy(h + offs[b].dst, B.dst.data(), sizeof(char*) * B.dst.size());
+    if (!B.rdst.empty()) std::memcpy(h + offs[b].rdst, B.rdst.data(), sizeof(char*) * B.rdst.size());
     // tile -> member of its first vector (merge walk); last entry = last member
     int sidx = 0;
     for (uint64_t tile = 0; tile < offs[b].ntiles; ++tile) {
@@ -274,6 +294,7 @@ int upload_plan(hvd_comm* c, std::vector<uint64_t> key, const std::vector<HostBu
     db.pp.segs = reinterpret_cast<const PackSeg*>(d + offs[b].segs);
     db.pp.src = reinterpret_cast<char* const*>(d + offs[b].src);
     db.dst = B.dst.empty() ? nullptr : reinterpret_cast<char* const*>(d + offs[b].dst);
+    db.rdst = B.rdst.empty() ? nullptr : reinterpret_cast<char* const*>(d + offs[b].rdst);
     db.pp.tile_seg = reinterpret_cast<const int*>(d + offs[b].tiles);
     db.vbeg = reinterpret_cast<const unsigned long long*>(d + offs[b].vbeg);
     for (int l = 0; l < c->nlocal; ++l) db.pp.buf[l] = c->rk[l].buf;
@@ -303,11 +324,12 @@ int upload_plan(hvd_comm* c, std::vector<uint64_t> key, const std::vector<HostBu
 // uploaded and cached by (addresses, counts, dtypes, threshold): a training loop
 // that reduces the same gradient tensors every step uploads its tables once.
 int get_plan(hvd_comm* c, const hvd_tensor* t, int n, uint64_t threshold, cudaStream_t s,
-             CachedPlan** out, int wire = 0) {
+             CachedPlan** out, int wire = 0, const Registration* reg = nullptr) {
   std::vector<uint64_t> key;
-  key.reserve(5 + 3 * (size_t)n * c->nlocal);
+  key.reserve(6 + 3 * (size_t)n * c->nlocal);
   key.push_back(0x504c414eull);  // "PLAN"
   key.push_back((uint64_t)wire);
+  key.push_back(reinterpret_cast<uint64_t>(reg));
   key.push_back(threshold);
   key.push_back((uint64_t)n);
   key.push_back((uint64_t)c->nlocal);
@@ -344,6 +366,11 @@ int get_plan(hvd_comm* c, const hvd_tensor* t, int n, uint64_t threshold, cudaSt
       for (int l = 0; l < c->nlocal; ++l)
         hb[b].src[(size_t)l * pb.n_entries + j] =
             static_cast<char*>(t[(size_t)l * n + e.tensor].data) + e.src_off * tesz;
+      if (reg) {
+        hb[b].rdst.resize((size_t)pb.n_entries * c->nlocal);
+        for (int l = 0; l < c->nlocal; ++l)
+          hb[b].rdst[(size_t)l * pb.n_entries + j] = reg->succ[(size_t)l * n + e.tensor] + e.src_off * tesz;
+      }
     }
   }
   return upload_plan(c, std::move(key), hb, s, out);
@@ -483,7 +510,7 @@ int enqueue_pull(hvd_comm* c, DevPlanBuffer& b, cudaStream_t s) {
 
 int enqueue_fused(hvd_comm* c, DevPlanBuffer& b, cudaStream_t s) {
   if (b.L == 0) return HVD_OK;
-  if (c->protocol == 0 && c->size > 1 && b.tdtype == b.dtype) return enqueue_pull(c, b, s);
+  if (c->protocol == 0 && c->size > 1 && b.tdtype == b.dtype && !b.rdst) return enqueue_pull(c, b, s);
   FusedParams F;
   std::memset(&F, 0, sizeof(F));
   int nch = 0;
@@ -498,6 +525,8 @@ int enqueue_fused(hvd_comm* c, DevPlanBuffer& b, cudaStream_t s) {
   F.scale = b.pp.scale;
   F.dtype = b.dtype;
   F.tdtype = b.tdtype;
+  F.registered = b.rdst != nullptr && c->size > 1;
+  F.rdst = b.rdst;
   st = launch_counted(c, HVD_KERNEL_FUSED, s, [&] { return launch_fused(F, b.dtype, nch, c->nlocal, c->threads, s); });
   if (st != HVD_OK) return st;
   if (c->tl) {
@@ -514,7 +543,7 @@ int enqueue_fused(hvd_comm* c, DevPlanBuffer& b, cudaStream_t s) {
 int pack_grid(hvd_comm* c) { return c->sm_count * c->pack_ctas_per_sm / c->nlocal + 1; }
 
 int do_allreduce(hvd_comm* c, const hvd_tensor* t, int n, int op, uint64_t threshold, cudaStream_t s,
-                 int wire = 0) {
+                 int wire = 0, const Registration* reg = nullptr) {
   int st = check_live(c);
   if (st != HVD_OK) return st;
   if (n < 0 || (n > 0 && !t)) return HVD_ERR_INVALID;
@@ -544,7 +573,8 @@ int do_allreduce(hvd_comm* c, const hvd_tensor* t, int n, int op, uint64_t thres
   if (n == 0) return HVD_OK;
   CK(cudaSetDevice(c->device));
   CachedPlan* plan = nullptr;
-  st = get_plan(c, t, n, threshold, s, &plan, wire);
+  if (reg && !c->fused) return HVD_ERR_UNSUPPORTED;
+  st = get_plan(c, t, n, threshold, s, &plan, wire, reg);
   if (st != HVD_OK) return st;
   const float scale = 1.0f / (float)c->size;  // s = fl32(1/N) (R1)
   for (DevPlanBuffer& b : plan->bufs) {       // step 6: repeat per fusion buffer
@@ -686,6 +716,7 @@ int hvd_finalize(hvd_comm* c) {
     }
     for (auto e : c->event_pool) cudaEventDestroy(e);
     c->cache.clear();
+    for (auto& kv : c->ipc_maps) cudaIpcCloseMemHandle(kv.second);
     if (c->peer_region) cudaIpcCloseMemHandle(c->peer_region);
     if (c->pred_region && c->pred_region != c->peer_region) cudaIpcCloseMemHandle(c->pred_region);
     for (int l = 0; l < kMaxLocal; ++l)
@@ -709,6 +740,137 @@ int hvd_allreduce(hvd_comm* c, const hvd_tensor* t, int n, int op, uint64_t fusi
 int hvd_allreduce_ex(hvd_comm* c, const hvd_tensor* t, int n, int op, uint64_t fusion_threshold, int wire_dtype,
                      void* stream) {
   return do_allreduce(c, t, n, op, fusion_threshold, static_cast<cudaStream_t>(stream), wire_dtype);
+}
+
+// ---- registered tensors -------------------------------------------------------------------
+namespace {
+// cuMemGetAddressRange through the runtime's driver entry point: no link-time
+// dependency on libcuda (the library must load on CPU-only hosts).
+typedef CUresult (*MemGetAddressRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+MemGetAddressRangeFn mem_get_address_range() {
+  static MemGetAddressRangeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuMemGetAddressRange", &p, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<MemGetAddressRangeFn>(p);
+  }
+  return fn;
+}
+
+struct RegEntry {
+  cudaIpcMemHandle_t handle;
+  uint64_t offset;  // tensor address - allocation base
+  uint64_t count;
+  int32_t dtype;
+  int32_t pad;
+};
+constexpr uint32_t kRegMagic = 0x48565247u;  // "HVRG"
+}  // namespace
+
+int hvd_register_blob(hvd_comm* c, const hvd_tensor* t, int n, void* blob, uint64_t* len) {
+  if (!c || !len || n < 0 || (n > 0 && !t)) return HVD_ERR_INVALID;
+  if (c->closed) return HVD_ERR_CLOSED;
+  const uint64_t need = 8 + (uint64_t)n * sizeof(RegEntry);
+  if (!blob) {
+    *len = need;
+    return HVD_OK;
+  }
+  if (*len < need) return HVD_ERR_INVALID;
+  char* p = static_cast<char*>(blob);
+  const uint32_t magic = kRegMagic;
+  const int32_t nn = n;
+  std::memcpy(p, &magic, 4);
+  std::memcpy(p + 4, &nn, 4);
+  CK(cudaSetDevice(c->device));
+  for (int k = 0; k < n; ++k) {
+    RegEntry e;
+    std::memset(&e, 0, sizeof(e));
+    e.count = t[k].count;
+    e.dtype = t[k].dtype;
+    if (!c->virt && c->size > 1 && t[k].count) {
+      CUdeviceptr base = 0;
+      size_t size = 0;
+      MemGetAddressRangeFn range = mem_get_address_range();
+      if (!range || range(&base, &size, reinterpret_cast<CUdeviceptr>(t[k].data)) != CUDA_SUCCESS)
+        return HVD_ERR_CUDA;
+      CK(cudaIpcGetMemHandle(&e.handle, reinterpret_cast<void*>(base)));
+      e.offset = reinterpret_cast<uint64_t>(t[k].data) - (uint64_t)base;
+    }
+    std::memcpy(p + 8 + (size_t)k * sizeof(RegEntry), &e, sizeof(e));
+  }
+  *len = need;
+  return HVD_OK;
+}
+
+int hvd_register(hvd_comm* c, const hvd_tensor* t, int n, const void* blobs, uint64_t len_each, int* reg_id) {
+  int st = check_live(c);
+  if (st != HVD_OK) return st;
+  if (!reg_id || n < 0 || (n > 0 && !t)) return HVD_ERR_INVALID;
+  for (int k = 0; k < n; ++k) {
+    if (elem_size(t[k].dtype) == 0) return HVD_ERR_UNSUPPORTED;
+    for (int l = 0; l < c->nlocal; ++l) {
+      const hvd_tensor& x = t[(size_t)l * n + k];
+      if (x.count != t[k].count || x.dtype != t[k].dtype || (x.count && !x.data)) return HVD_ERR_INVALID;
+    }
+  }
+  Registration R;
+  R.n = n;
+  R.own.assign(t, t + (size_t)n * c->nlocal);
+  R.succ.resize((size_t)n * c->nlocal);
+  if (c->virt || c->size == 1) {
+    for (int l = 0; l < c->nlocal; ++l)
+      for (int k = 0; k < n; ++k)
+        R.succ[(size_t)l * n + k] = static_cast<char*>(t[(size_t)((l + 1) % c->nlocal) * n + k].data);
+  } else {
+    if (!blobs || len_each < 8 + (uint64_t)n * sizeof(RegEntry)) return HVD_ERR_INVALID;
+    const char* p = static_cast<const char*>(blobs) + (size_t)((c->rank + 1) % c->size) * len_each;
+    uint32_t magic;
+    int32_t nn;
+    std::memcpy(&magic, p, 4);
+    std::memcpy(&nn, p + 4, 4);
+    if (magic != kRegMagic || nn != n) return HVD_ERR_INVALID;
+    CK(cudaSetDevice(c->device));
+    for (int k = 0; k < n; ++k) {
+      RegEntry e;
+      std::memcpy(&e, p + 8 + (size_t)k * sizeof(RegEntry), sizeof(e));
+      if (e.count != t[k].count || e.dtype != t[k].dtype) return HVD_ERR_INVALID;
+      if (!e.count) {
+        R.succ[k] = nullptr;
+        continue;
+      }
+      const std::string hk(reinterpret_cast<const char*>(&e.handle), sizeof(e.handle));
+      auto it = c->ipc_maps.find(hk);
+      char* base = nullptr;
+      if (it != c->ipc_maps.end()) {
+        base = it->second;
+      } else {
+        void* ptr = nullptr;
+        CK(cudaIpcOpenMemHandle(&ptr, e.handle, cudaIpcMemLazyEnablePeerAccess));
+        base = static_cast<char*>(ptr);
+        c->ipc_maps[hk] = base;
+      }
+      R.succ[k] = base + e.offset;
+    }
+  }
+  R.live = true;
+  c->regs.push_back(std::move(R));
+  *reg_id = (int)c->regs.size() - 1;
+  return HVD_OK;
+}
+
+int hvd_allreduce_registered(hvd_comm* c, int reg_id, int op, uint64_t fusion_threshold, void* stream) {
+  if (!c || reg_id < 0 || reg_id >= (int)c->regs.size() || !c->regs[reg_id].live) return HVD_ERR_INVALID;
+  const Registration& R = c->regs[reg_id];
+  return do_allreduce(c, R.own.data(), R.n, op, fusion_threshold, static_cast<cudaStream_t>(stream), 0,
+                      c->size > 1 ? &R : nullptr);
+}
+
+int hvd_deregister(hvd_comm* c, int reg_id) {
+  if (!c || reg_id < 0 || reg_id >= (int)c->regs.size()) return HVD_ERR_INVALID;
+  c->regs[reg_id].live = false;  // mapped peer allocations stay open until hvd_finalize
+  return HVD_OK;
 }
 
 int hvd_allreduce_average(hvd_comm* c, const hvd_tensor* t, int n, uint64_t fusion_threshold, void* stream) {

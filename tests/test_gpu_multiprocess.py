@@ -46,6 +46,17 @@ def _worker(rank, world, port, cases, q, protocol):
                 comm.allreduce(ts, op=op, fusion_threshold=thr)
                 torch.cuda.synchronize()
                 out.append([from_torch(t, dtype) for t in ts])
+            elif kind == "registered":
+                res_its = []
+                ts = [torch.empty(c, device="cuda") for c in counts]
+                reg = comm.register(ts)
+                for it in range(2):
+                    for k, c in enumerate(counts):
+                        ts[k].copy_(to_torch(workloads.rank_tensor(c, "f32", rank, k, seed=700 + it), "f32"))
+                    comm.allreduce_average(reg, fusion_threshold=thr)
+                    torch.cuda.synchronize()
+                    res_its.append([from_torch(t, "f32") for t in ts])
+                out.append(res_its)
             elif kind == "bcast":
                 xs = [workloads.rank_tensor(c, dtype, rank, k, "specials") for k, c in enumerate(counts)]
                 ts = [to_torch(x, dtype) for x in xs]
@@ -86,6 +97,7 @@ CASES = [
     ("buffer", [16 << 20], "f32", "sum", 0),
     ("buffer", [(1 << 20) + 3], "bf16", "average", 0),
     ("bcast", [5, 1 << 20, 333], "f32", 1, 0),
+    ("registered", [17, 3_000_001, 64, 500_000], "f32", "average", 8 << 20),
     ("allgather", [100_003], "f32", None, 0),
     ("allgather", [8_000_001], "bf16", None, 0),
 ]
@@ -112,7 +124,15 @@ def test_multiprocess_ring_matches_oracle(protocol):
     for r in range(n):
         assert res[r][1] == 0, res[r]
     for ci, (kind, counts, dtype, op, thr) in enumerate(CASES):
-        if kind == "bcast":
+        if kind == "registered":
+            for it in range(2):
+                xs = [[workloads.rank_tensor(c, "f32", r, k, seed=700 + it) for k, c in enumerate(counts)]
+                      for r in range(n)]
+                ref, _, _ = oracle.allreduce(xs, ["f32"] * len(counts), "average", threshold=thr)
+                for r in range(n):
+                    for k in range(len(counts)):
+                        assert_same(res[r][0][ci][it][k], ref[r][k], "f32", f"registered it={it} r={r} k={k}")
+        elif kind == "bcast":
             xs = [[workloads.rank_tensor(c, dtype, r, k, "specials") for k, c in enumerate(counts)] for r in range(n)]
             ref, _ = oracle.broadcast(xs, op)
             for r in range(n):

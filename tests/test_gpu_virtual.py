@@ -414,3 +414,32 @@ def test_wire_dtype_variants_bitexact(hvd, n, tdt, wire):
     for r in range(n):
         for k in range(len(counts)):
             assert_same(from_torch(ts[r][k], tdt), ref[r][k], tdt, f"N={n} r={r} k={k}")
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 8])
+def test_registered_zero_copy_bitexact(hvd, n):
+    """hvd_register: all-gather writes straight into the successor's tensors; same bits."""
+    comm = hvd.init_virtual(n, 0, 1 << 20)  # small buffer: several fusion buffers
+    try:
+        counts = [3, 1000, 262_149, 5, 77_777, 400_001]
+        ts = [[torch.empty(c, device="cuda") for c in counts] for _ in range(n)]
+        keep = []
+        ts[0][1] = torch.empty(1001, device="cuda")[1:]  # a misaligned view on one rank
+        keep.append(ts[0][1])
+        reg = comm.register(ts)
+        for it in range(3):
+            xs = workloads.all_ranks(counts, "f32", n, seed=900 + it)
+            for r in range(n):
+                for k in range(len(counts)):
+                    ts[r][k].copy_(to_torch(xs[r][k], "f32"))
+            ref, _, plan = oracle.allreduce(xs, ["f32"] * len(counts), "average", threshold=1 << 19,
+                                            capacity=1 << 20)
+            comm.allreduce_average(reg, fusion_threshold=1 << 19)
+            torch.cuda.synchronize()
+            assert comm.poll_error() == 0
+            for r in range(n):
+                for k in range(len(counts)):
+                    assert_same(from_torch(ts[r][k], "f32"), ref[r][k], "f32", f"it={it} r={r} k={k}")
+        comm.deregister(reg)
+    finally:
+        comm.finalize()

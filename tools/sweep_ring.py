@@ -39,7 +39,7 @@ def main():
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--out", default="gpurun_out/sweep.json")
     ap.add_argument("--nccl", action="store_true")
-    ap.add_argument("--mode", default="ring", choices=["ring", "fused", "three"],
+    ap.add_argument("--mode", default="ring", choices=["ring", "fused", "three", "registered"],
                     help="ring: hvd_allreduce_buffer; fused/three: hvd_allreduce_average of one tensor")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -55,12 +55,16 @@ def main():
     ref = {}
     grads = {mib: torch.randn((mib << 20) // esz, device="cuda").to(torch.float32 if esz == 4 else torch.bfloat16)
              for mib in a.mib}
-    comm.set_config(L.HVD_CFG_FUSED, (1 if a.mode == "fused" else 0) if a.fused < 0 else a.fused)
+    comm.set_config(L.HVD_CFG_FUSED, (1 if a.mode in ("fused", "registered") else 0) if a.fused < 0 else a.fused)
     comm.set_config(L.HVD_CFG_PROTOCOL, a.protocol)
+
+    regs = {mib: comm.register([grads[mib]]) for mib in a.mib} if a.mode == "registered" else {}
 
     def call(mib, cnt):
         if a.mode == "ring":
             comm.allreduce_buffer(cnt, code, "sum")
+        elif a.mode == "registered":
+            comm.allreduce_average(regs[mib])
         else:
             comm.allreduce_average([grads[mib]])
     for mib, ch, sl, th, sg, win, lag in itertools.product(a.mib, a.channels, a.slice_kib, a.threads, a.fence_mode,
