@@ -203,6 +203,8 @@ typedef enum {
                                 limit): bounds the NVLink backlog and so the signal latency */
   HVD_CFG_FIN_LAG = 11,      /* fused: slices by which the final local scatter trails the last
                                 all-gather iteration (>= K-1: scatter after all of it)     */
+  HVD_CFG_MULTI_BUFFERS = 13, /* fusion buffers per fused launch (1..48, default 48): the
+                                buffers of one call pipeline inside one persistent launch  */
   HVD_CFG_PROTOCOL = 12      /* allreduce data movement: 1 (default) push — SM stores into the
                                 successor's HBM; 0 pull — each rank TMA-loads its
                                 predecessor's partials.  Same ring order, same bits.       */

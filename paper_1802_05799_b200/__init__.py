@@ -250,7 +250,7 @@ class Comm:
         data = buf[:_lib.MAX_CHANNELS * wpc].reshape(_lib.MAX_CHANNELS, wpc // 2, 2)[:info.channels, :info.slices]
         sig = buf[_lib.MAX_CHANNELS * wpc:].reshape(_lib.MAX_CHANNELS, wpc // 2, 2)[:info.channels, :info.signals]
         return {"rank": info.rank, "size": info.size, "K": info.K, "T": info.T, "channels": info.channels,
-                "kind": "pull" if info.kind == 1 else "push", "fin_lag": self.get_config(_lib.HVD_CFG_FIN_LAG), "data": data.copy(), "signals": sig.copy()}
+                "kind": {1: "pull", 2: "registered"}.get(info.kind, "push"), "fin_lag": self.get_config(_lib.HVD_CFG_FIN_LAG), "data": data.copy(), "signals": sig.copy()}
 
     def poll_error(self) -> int:
         return lib.hvd_poll_error(self._h)

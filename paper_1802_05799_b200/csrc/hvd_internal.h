@@ -115,6 +115,20 @@ struct PackParams {
   int pad;
 };
 
+// One fusion buffer of a multi-buffer fused launch (geometry + member tables).
+struct BufDesc {
+  const PackSeg* segs;               // [nseg]
+  char* const* src;                  // [nlocal * nseg] gather addresses
+  char* const* dst;                  // [nlocal * nseg] scatter addresses
+  char* const* rdst;                 // [nlocal * nseg] registered: successor's addresses
+  const unsigned long long* vbeg;    // [nseg] member start vectors
+  unsigned long long L, q, ch_el, slice_el;
+  int nseg, K;
+  int owner;                         // -1: every channel takes a share; else the one channel
+  int pad;                           //  that runs this (small) buffer alone
+};
+constexpr int kMaxMultiBufs = 96;    // fusion buffers per fused launch (kernel parameter space)
+
 // Fused zero-copy allreduce of one fusion buffer (pack + ring + unpack in one launch).
 constexpr int kFusedSmemSegs = 4096;  // member-offset table cached in shared memory up to this size
 constexpr int kPipe = 8;              // cp.async prefetch depth (rows of 16 B per data thread)
@@ -140,6 +154,11 @@ struct FusedParams {
   int tdtype;                        // tensor dtype (0: same as dtype)
   int registered;                    // 1: all-gather writes into the successor's tensors (rdst)
   char* const* rdst;                 // [nlocal * nseg] successor's tensor addresses (registered)
+  // multi-buffer fused kernel
+  int nbuf;
+  int cache_segs;                    // member-offset cache entries in shared memory
+  unsigned long long region_el;      // channel-private region of scratch / buffer, elements
+  BufDesc bufs[kMaxMultiBufs];
 };
 
 // Launchers (hvd_kernels.cu).  All return a cudaError_t.

@@ -685,7 +685,9 @@ template <> struct WireCvt<4, 2> {  // bf16 tensor, fp32 wire
 template <class Op, int KIND, int TESZ = Op::kEsz>
 __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& me, unsigned long long lo,
                                             unsigned long long hi, unsigned tid, unsigned nthr, SegCache& sc,
-                                            Raw32* slots0, uint4* slots1) {
+                                            Raw32* slots0, uint4* slots1, long long pv = 0) {
+  // pv: shift from a buffer vector index to its slot in the channel-private layout of
+  // the scratch / fusion-buffer regions (0: buffer order)
   constexpr int ESZ = Op::kEsz;  // wire element size
   constexpr int VEL = 16 / ESZ;
   using Cvt = WireCvt<ESZ, TESZ>;
@@ -714,9 +716,9 @@ __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& m
         const char* tp = reinterpret_cast<const char*>(ci.g + e * TESZ);
         if (Cvt::fast(tp, left)) Cvt::issue(d0, tp);
       } else {
-        cp_async16(&d0->a, me.buf + v * 16);
+        cp_async16(&d0->a, me.buf + (v + pv) * 16);
       }
-      if (ADD) cp_async16(slots1 + (j % kPipe) * nthr + tid, me.scratch + v * 16);
+      if (ADD) cp_async16(slots1 + (j % kPipe) * nthr + tid, me.scratch + (v + pv) * 16);
     }
     cp_async_commit();  // one group per row, possibly empty: keeps wait_group counting uniform
   };
@@ -745,8 +747,8 @@ __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& m
       const uint4 y = slots1[(j % kPipe) * nthr + tid];
       Op::template add_words<4>(reinterpret_cast<uint32_t*>(&x), reinterpret_cast<const uint32_t*>(&y));
     }
-    if (TO_NSCRATCH) *reinterpret_cast<uint4*>(me.nscratch + v * 16) = x;
-    if (TO_NBUF) *reinterpret_cast<uint4*>(me.nbuf + v * 16) = x;
+    if (TO_NSCRATCH) *reinterpret_cast<uint4*>(me.nscratch + (v + pv) * 16) = x;
+    if (TO_NBUF) *reinterpret_cast<uint4*>(me.nbuf + (v + pv) * 16) = x;
     if (SCATTER) Cvt::put(reinterpret_cast<char*>(sc.d + e * TESZ), left, x);
     if (RSCATTER) Cvt::put(reinterpret_cast<char*>(sc.rd + e * TESZ), left, x);
   }
@@ -783,170 +785,183 @@ __device__ __host__ __forceinline__ void fused_op(int j, int K, int T, int lag, 
   }
 }
 
+// Geometry of one slice of buffer D: chunk c, channel ch, slice k -> [lo, hi).
+__device__ __forceinline__ void slice_range_d(const BufDesc& D, int c, int ch, int k, unsigned long long& lo,
+                                              unsigned long long& hi) {
+  const unsigned long long L = D.L;
+  unsigned long long c_lo = (unsigned long long)c * D.q;
+  c_lo = c_lo < L ? c_lo : L;
+  unsigned long long c_hi = c_lo + D.q;
+  c_hi = c_hi < L ? c_hi : L;
+  unsigned long long h_lo = c_lo + (unsigned long long)ch * D.ch_el;
+  h_lo = h_lo < c_hi ? h_lo : c_hi;
+  unsigned long long h_hi = h_lo + D.ch_el;
+  h_hi = h_hi < c_hi ? h_hi : c_hi;
+  lo = h_lo + (unsigned long long)k * D.slice_el;
+  lo = lo < h_hi ? lo : h_hi;
+  hi = lo + D.slice_el;
+  hi = hi < h_hi ? hi : h_hi;
+}
+
+// Every fusion buffer of a call (up to kMaxMultiBufs) in ONE persistent launch:
+// each channel walks the buffers in order with no grid-wide barrier between
+// them, so buffer b+1's first pushes overlap buffer b's tail.  That is safe
+// because the scratch and fusion-buffer regions are laid out channel-private
+// (slot of element e of chunk c in channel ch = ch*region + c*ch_el + offset):
+// only channel ch of the successor ever reads what channel ch writes, and a
+// channel finishes buffer b (all of its own reads) before it starts b+1.  Signal
+// counters continue across buffers (base of buffer b = base + sum of T*K).
+//   N == 1: gather(x)*s -> scatter per slice (the in-place scale).
+//   registered: the all-gather writes final values into the successor's tensors.
 template <class Op, int TESZ>
 __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_constant__ FusedParams P) {
   extern __shared__ __align__(16) unsigned long long s_dyn[];
+  constexpr int VEL = 16 / Op::kEsz;
   const RingParams& R = P.ring;
   const RingRank& me = R.rk[blockIdx.y];
   const int ch = blockIdx.x;
   const int N = R.N;
   const int r = me.rank;
-  const int K = R.K;
-  const unsigned long long base = R.base[ch];
+  const unsigned long long base0 = R.base[ch];
   const int T = N > 1 ? 2 * (N - 1) : 0;
   const int nd = blockDim.x - 32;
   __shared__ int s_abort, s_done, s_pub;
-  const bool cache = P.nseg <= kFusedSmemSegs;
   unsigned long long* s_vbeg = s_dyn;
-  const int ndata = blockDim.x - 32;
-  Raw32* slots0 = reinterpret_cast<Raw32*>(s_dyn + (cache ? (P.nseg + 1) / 2 * 2 : 0));
-  uint4* slots1 = reinterpret_cast<uint4*>(slots0 + kPipe * ndata);
-  if (cache)
-    for (int j = threadIdx.x; j < P.nseg; j += blockDim.x) s_vbeg[j] = P.segs[j].vbeg;
+  Raw32* slots0 = reinterpret_cast<Raw32*>(s_dyn + P.cache_segs);
+  uint4* slots1 = reinterpret_cast<uint4*>(slots0 + kPipe * nd);
   if (threadIdx.x == 0) {
     s_abort = 0;
     s_done = 0;
     s_pub = 0;
   }
   __syncthreads();
-  if (threadIdx.x >= nd) {
-    if (threadIdx.x == nd && T > 0)
-      signal_loop(&s_done, T * K, me.nflags + ch, base, R.sig_mode, &s_pub,
+  if (threadIdx.x >= nd) {  // ---- signal warp
+    int total = 0;
+    for (int b = 0; b < P.nbuf; ++b)
+      if (P.bufs[b].owner < 0 || P.bufs[b].owner == ch) total += T * P.bufs[b].K;
+    if (threadIdx.x == nd && total > 0)
+      signal_loop(&s_done, total, me.nflags + ch, base0, R.sig_mode, &s_pub,
                   R.tl ? R.tl + tl_words(R.tl_max) * blockIdx.y + ((size_t)kMaxChannels + ch) * R.tl_max * 2 : nullptr,
                   R.tl_max);
     return;
   }
   unsigned long long* tl_d = R.tl ? R.tl + tl_words(R.tl_max) * blockIdx.y + (size_t)ch * R.tl_max * 2 : nullptr;
   int nrec = 0;
-  FusedCtx F;
-  F.segs = P.segs;
-  F.src = P.src + (size_t)blockIdx.y * P.nseg;
-  F.dst = (P.dst ? P.dst : P.src) + (size_t)blockIdx.y * P.nseg;
-  F.rdst = P.registered ? P.rdst + (size_t)blockIdx.y * P.nseg : nullptr;
-  F.vbeg = cache ? s_vbeg : P.vbeg_global;
-  F.nseg = P.nseg;
-  F.scale_on = P.scale_on;
-  F.scale = P.scale;
-  F.dtype = P.dtype;
   const unsigned tid = threadIdx.x;
-  SegCache sc;
   unsigned long long sent = 0;
-  if (N == 1) {
-    for (int k = 0; k < K; ++k) {
-      unsigned long long lo, hi;
-      slice_range(R, 0, ch, k, lo, hi);
-      const unsigned long long tb = tl_d ? globaltimer() : 0;
-      if (hi > lo) fused_slice<Op, kF_SOLO, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
-      if (tl_d && tid == 0 && nrec < R.tl_max) {
-        tl_d[2 * nrec] = tb;
-        tl_d[2 * nrec + 1] = globaltimer();
-        ++nrec;
+  int i = 0;                         // ring ops published so far (all buffers)
+  unsigned long long bbase = base0;  // counter base of the current buffer
+  bool first = true;
+  for (int b = 0; b < P.nbuf; ++b) {
+    const BufDesc& D = P.bufs[b];
+    if (D.owner >= 0 && D.owner != ch) continue;  // a small buffer run by another channel
+    const int cg = D.owner >= 0 ? 0 : ch;         // this channel's index in the buffer's geometry
+    const int K = D.K;
+    const bool cache = D.nseg <= P.cache_segs;
+    if (!first) bar_sync(kBarData, nd);  // every data warp is done with the previous member table
+    first = false;
+    if (cache)
+      for (int j = tid; j < D.nseg; j += nd) s_vbeg[j] = D.vbeg[j];
+    bar_sync(kBarData, nd);
+    FusedCtx F;
+    F.segs = D.segs;
+    F.src = D.src + (size_t)blockIdx.y * D.nseg;
+    F.dst = D.dst + (size_t)blockIdx.y * D.nseg;
+    F.rdst = P.registered ? D.rdst + (size_t)blockIdx.y * D.nseg : nullptr;
+    F.vbeg = cache ? s_vbeg : D.vbeg;
+    F.nseg = D.nseg;
+    F.scale_on = P.scale_on;
+    F.scale = P.scale;
+    F.dtype = P.dtype;
+    SegCache sc;
+    if (N == 1) {
+      for (int k = 0; k < K; ++k) {
+        unsigned long long lo, hi;
+        slice_range_d(D, 0, cg, k, lo, hi);
+        const unsigned long long tb = tl_d ? globaltimer() : 0;
+        if (hi > lo) fused_slice<Op, kF_SOLO, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
+        if (tl_d && tid == 0 && nrec < R.tl_max) {
+          tl_d[2 * nrec] = tb;
+          tl_d[2 * nrec + 1] = globaltimer();
+          ++nrec;
+        }
       }
+      continue;
     }
-    return;
-  }
-  int i = 0;
-  if (P.registered) {
-    // Registered tensors (zero-copy both ways): the all-gather steps write the final
-    // values straight into the successor's tensors, so there is no fusion-buffer
-    // forward and no final local scatter.  Ops (t, k) in order, t = 0..T-1.
-    for (int j = 0; j < T * K; ++j) {
-      const int t = j / K, k = j - (j / K) * K;
+    const int nops = P.registered ? T * K : (T + 1) * K;
+    for (int j = 0; j < nops; ++j) {
+      int t, k;
+      if (P.registered) {
+        t = j / K;
+        k = j - t * K;
+      } else {
+        fused_op(j, K, T, R.fin_lag, t, k);
+      }
       const bool rs = t < N - 1;
       const int s = rs ? t : t - (N - 1);
-      const int c = rs ? mod(r - s, N) : mod(r + 1 - s, N);
+      const int c = t == T ? mod(r + 2, N) : (rs ? mod(r - s, N) : mod(r + 1 - s, N));
       unsigned long long lo, hi;
-      slice_range(R, c, ch, k, lo, hi);
+      slice_range_d(D, c, cg, k, lo, hi);
+      // channel-private slot of this slice's first element, as a vector shift
+      const long long pv =
+          (long long)(((unsigned long long)ch * P.region_el + (unsigned long long)c * D.ch_el +
+                       (lo - (unsigned long long)c * D.q - (unsigned long long)cg * D.ch_el)) / VEL) -
+          (long long)(lo / VEL);
+      if (R.window > 0 && t < T && i > R.window) {
+        if (tid == 0)
+          while (ld_acquire_cta_shared(&s_pub) < i - R.window) __nanosleep(64);
+        bar_sync(kBarData, nd);
+      }
       const unsigned long long tb = tl_d ? globaltimer() : 0;
       if (hi > lo && !s_abort) {
-        if (rs && s == 0) fused_slice<Op, kF_RS0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
-        else if (rs) fused_slice<Op, kF_RS, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
-        else if (s == 0) fused_slice<Op, kF_RAG0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
-        else fused_slice<Op, kF_RAG, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
-        sent += (hi - lo) * Op::kEsz;
+        if (P.registered) {
+          if (rs && s == 0) fused_slice<Op, kF_RS0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv);
+          else if (rs) fused_slice<Op, kF_RS, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv);
+          else if (s == 0) fused_slice<Op, kF_RAG0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv);
+          else fused_slice<Op, kF_RAG, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv);
+        } else {
+          if (t == T) fused_slice<Op, kF_FIN, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv);
+          else if (rs && s == 0) fused_slice<Op, kF_RS0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv);
+          else if (rs) fused_slice<Op, kF_RS, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv);
+          else if (s == 0) fused_slice<Op, kF_AG0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv);
+          else fused_slice<Op, kF_AG, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv);
+        }
+        if (t < T) sent += (hi - lo) * Op::kEsz;
       }
+      // retire op j (publish it if it is a ring iteration), then wait for op j+1's
+      // dependency — the predecessor's (t'-1, k') of the same buffer; publishing first
+      // keeps the ring acyclic.  The next buffer's first op (t = 0) has none.
       bar_sync(kBarData, nd);
       if (tl_d && tid == 0 && nrec < R.tl_max) {
         tl_d[2 * nrec] = tb;
         tl_d[2 * nrec + 1] = globaltimer();
         ++nrec;
       }
-      ++i;
-      // next op's dependency; after the last op: the predecessor's last all-gather slice,
-      // which lands in this rank's tensors (completion on the stream = all data arrived)
-      const int tn = (k + 1 < K) ? t : t + 1;
-      const int kn = (k + 1 < K) ? k + 1 : 0;
+      if (t < T) ++i;
+      int tn = 0, kn = 0;
+      if (j + 1 < nops) {
+        if (P.registered) {
+          tn = (j + 1) / K;
+          kn = (j + 1) - tn * K;
+        } else {
+          fused_op(j + 1, K, T, R.fin_lag, tn, kn);
+        }
+      }
       if (tid == 0) {
-        st_release_cta_shared(&s_done, i);
-        unsigned long long target = 0;
-        if (tn < T && tn > 0) target = base + (unsigned long long)(tn - 1) * K + kn + 1;
-        else if (tn >= T) target = base + (unsigned long long)T * K;
+        if (t < T) st_release_cta_shared(&s_done, i);
+        const unsigned long long target = tn > 0 ? bbase + (unsigned long long)(tn - 1) * K + kn + 1 : 0;
         if (target && !s_abort && !spin_until(me.flags + ch, target, R.err, R.timeout_ns)) s_abort = 1;
       }
       if (tn > 0) bar_sync(kBarData, nd);
     }
-    if (tid == 0) {
-      atomicAdd(me.stats + 0, sent);
-      if (ch == 0) atomicAdd(me.stats + 1, (unsigned long long)T);
-    }
-    return;
-  }
-  // Operation sequence: iterations t < T-1 in order, then the last all-gather step
-  // interleaved with the final local scatter one slice behind (fused_op), so the
-  // scatter of slice k overlaps the NVLink drain of slice k+1.
-  const int nops = (T + 1) * K;
-  for (int j = 0; j < nops; ++j) {
-    int t, k;
-    fused_op(j, K, T, R.fin_lag, t, k);
-    const bool rs = t < N - 1;
-    const int s = rs ? t : t - (N - 1);
-    const int c = t == T ? mod(r + 2, N) : (rs ? mod(r - s, N) : mod(r + 1 - s, N));
-    unsigned long long lo, hi;
-    slice_range(R, c, ch, k, lo, hi);
-    if (R.window > 0 && t < T && i > R.window) {
-      // flow control: at most `window` pushed-but-unfenced slices per channel, so the
-      // NVLink backlog (and hence fence / signal latency) stays short
-      if (tid == 0)
-        while (ld_acquire_cta_shared(&s_pub) < i - R.window) __nanosleep(64);
-      bar_sync(kBarData, nd);
-    }
-    const unsigned long long tb = tl_d ? globaltimer() : 0;
-    if (hi > lo && !s_abort) {
-      if (t == T) fused_slice<Op, kF_FIN, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
-      else if (rs && s == 0) fused_slice<Op, kF_RS0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
-      else if (rs) fused_slice<Op, kF_RS, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
-      else if (s == 0) fused_slice<Op, kF_AG0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
-      else fused_slice<Op, kF_AG, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
-      if (t < T) sent += (hi - lo) * Op::kEsz;
-    }
-    if (j + 1 == nops) {
-      if (tl_d && tid == 0 && nrec < R.tl_max) {
-        tl_d[2 * nrec] = tb;
-        tl_d[2 * nrec + 1] = globaltimer();
-      }
-      break;
-    }
-    // retire op j (publish it if it is a ring iteration), then wait for op j+1's
-    // dependency: the predecessor's (t'-1, k') — publishing first keeps the ring acyclic
-    bar_sync(kBarData, nd);
-    if (tl_d && tid == 0 && nrec < R.tl_max) {
-      tl_d[2 * nrec] = tb;
-      tl_d[2 * nrec + 1] = globaltimer();
-      ++nrec;
-    }
-    if (t < T) ++i;
-    int tn, kn;
-    fused_op(j + 1, K, T, R.fin_lag, tn, kn);
-    if (tid == 0) {
-      if (t < T) st_release_cta_shared(&s_done, i);
-      const unsigned long long target = tn > 0 ? base + (unsigned long long)(tn - 1) * K + kn + 1 : 0;
-      if (target && !s_abort && !spin_until(me.flags + ch, target, R.err, R.timeout_ns)) s_abort = 1;
-    }
-    if (tn > 0) bar_sync(kBarData, nd);
+    bbase += (unsigned long long)T * K;
   }
   if (tid == 0) {
+    // registered: the predecessor's last all-gather slices land in this rank's tensors;
+    // completion on the stream means they have arrived
+    if (P.registered && N > 1 && !s_abort) spin_until(me.flags + ch, bbase, R.err, R.timeout_ns);
     atomicAdd(me.stats + 0, sent);
-    if (ch == 0) atomicAdd(me.stats + 1, (unsigned long long)T);
+    if (ch == 0) atomicAdd(me.stats + 1, (unsigned long long)T * P.nbuf);  // messages per buffer
   }
 }
 
@@ -1394,7 +1409,7 @@ cudaError_t launch_ring(const RingParams& p, int dtype, int nch, int nlocal, int
 
 template <class Op, int TESZ>
 static cudaError_t launch_fused_t(const FusedParams& p, int nch, int nlocal, int threads, cudaStream_t s) {
-  const size_t smem = fused_smem_bytes(p.nseg, threads);
+  const size_t smem = (size_t)p.cache_segs * 8 + fused_smem_bytes(kFusedSmemSegs + 1, threads);
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(fused_allreduce_kernel<Op, TESZ>, cudaFuncAttributeMaxDynamicSharedMemorySize,

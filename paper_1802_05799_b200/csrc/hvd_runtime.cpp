@@ -72,7 +72,8 @@ struct CachedPlan {
 struct hvd_comm {
   int rank = 0, size = 1, device = 0, nlocal = 1;
   bool virt = false, connected = false, closed = false;
-  uint64_t cap = 0;
+  uint64_t cap = 0;    // fusion capacity (plans, limits)
+  uint64_t bufsz = 0;  // bytes of each region buffer (cap + slack)
   char* region[kMaxLocal] = {};
   char* peer_region = nullptr;   // successor's region (IPC mapped), real mode
   char* pred_region = nullptr;   // predecessor's region (IPC mapped), real mode
@@ -90,6 +91,7 @@ struct hvd_comm {
   int profile = 0;
   int sig_mode = 1;
   int fused = 1;
+  int multi_bufs = kMaxMultiBufs;  // fusion buffers per fused launch
   int window = 0;
   int fin_lag = 1;
   unsigned long long hs_epoch = 0;  // copy-collective handshake epochs issued
@@ -99,6 +101,7 @@ struct hvd_comm {
   unsigned long long pull_exits = 0;  // cumulative CTA exits of the pull kernel (per rank)
   std::vector<std::pair<int, int>> occ_cache;  // (kernel/dtype/threads key, CTAs per SM)
   std::vector<Registration> regs;               // hvd_register
+  Registration bufreg;                          // hvd_allreduce_buffer: the fusion buffer itself
   std::map<std::string, char*> ipc_maps;        // opened peer allocations (by handle bytes)
   // timeline (HVD_CFG_TIMELINE): device records of the most recent fused launch
   int tl_max = 0;
@@ -125,6 +128,10 @@ int cuda_fail(cudaError_t e, const char* what) {
     if (_st != HVD_OK) return _st;                  \
   } while (0)
 
+// Region: [fusion buffer][RS scratch][pull buffer 0][pull buffer 1][tail]; each
+// buffer is `bufsz` = capacity + slack bytes (the slack absorbs the quantum rounding
+// of the channel-private layout).  `cap` arguments below are bufsz.
+constexpr uint64_t kRegionSlack = 2ull << 20;
 char* buf_of(char* region) { return region; }
 char* scratch_of(char* region, uint64_t cap) { return region + cap; }
 unsigned long long* flags_of(char* region, uint64_t cap) {
@@ -133,7 +140,6 @@ unsigned long long* flags_of(char* region, uint64_t cap) {
 unsigned long long* stats_of(char* region, uint64_t cap) {
   return reinterpret_cast<unsigned long long*>(region + 4 * cap + kMaxChannels * 8);
 }
-// Region: [fusion buffer][RS scratch][pull buffer 0][pull buffer 1][tail], each buffer `cap` bytes.
 constexpr uint64_t kNumBufs = 4;
 unsigned long long* tail_of(char* region, uint64_t cap) {
   return reinterpret_cast<unsigned long long*>(region + kNumBufs * cap);
@@ -146,26 +152,28 @@ char* pull_of(char* region, uint64_t cap, int p) { return region + (2 + p) * cap
 
 int common_init(hvd_comm* c, uint64_t fusion_bytes) {
   c->cap = ((fusion_bytes ? fusion_bytes : kDefaultFusionBytes) + 4095) / 4096 * 4096;
+  c->bufsz = c->cap + kRegionSlack;
   CK(cudaSetDevice(c->device));
   CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device));
   CK(cudaHostAlloc(reinterpret_cast<void**>(&c->err_host), sizeof(int), cudaHostAllocMapped));
   *c->err_host = 0;
   CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->err_dev), c->err_host, 0));
-  const uint64_t region_bytes = kNumBufs * c->cap + kTailBytes;
+  const uint64_t region_bytes = kNumBufs * c->bufsz + kTailBytes;
   for (int l = 0; l < c->nlocal; ++l) {
     CK(cudaMalloc(reinterpret_cast<void**>(&c->region[l]), region_bytes));
-    CK(cudaMemset(c->region[l] + kNumBufs * c->cap, 0, kTailBytes));
+    CK(cudaMemset(c->region[l] + kNumBufs * c->bufsz, 0, kTailBytes));
     RingRank& r = c->rk[l];
+    const uint64_t bz = c->bufsz;
     r.buf = buf_of(c->region[l]);
-    r.scratch = scratch_of(c->region[l], c->cap);
-    r.flags = flags_of(c->region[l], c->cap);
-    r.stats = stats_of(c->region[l], c->cap);
-    r.rflags = rflags_of(c->region[l], c->cap);
-    r.pull[0] = pull_of(c->region[l], c->cap, 0);
-    r.pull[1] = pull_of(c->region[l], c->cap, 1);
-    r.pflags_own = pflags_of(c->region[l], c->cap);
-    r.done_own = done_of(c->region[l], c->cap);
-    r.exits = exits_of(c->region[l], c->cap);
+    r.scratch = scratch_of(c->region[l], bz);
+    r.flags = flags_of(c->region[l], bz);
+    r.stats = stats_of(c->region[l], bz);
+    r.rflags = rflags_of(c->region[l], bz);
+    r.pull[0] = pull_of(c->region[l], bz, 0);
+    r.pull[1] = pull_of(c->region[l], bz, 1);
+    r.pflags_own = pflags_of(c->region[l], bz);
+    r.done_own = done_of(c->region[l], bz);
+    r.exits = exits_of(c->region[l], bz);
     r.rank = c->virt ? l : c->rank;
   }
   CK(cudaDeviceSynchronize());
@@ -508,36 +516,104 @@ int enqueue_pull(hvd_comm* c, DevPlanBuffer& b, cudaStream_t s) {
   return HVD_OK;
 }
 
-int enqueue_fused(hvd_comm* c, DevPlanBuffer& b, cudaStream_t s) {
-  if (b.L == 0) return HVD_OK;
-  if (c->protocol == 0 && c->size > 1 && b.tdtype == b.dtype && !b.rdst) return enqueue_pull(c, b, s);
+// One fused launch for consecutive fusion buffers of one dtype (<= kMaxMultiBufs).
+int enqueue_fused_multi(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStream_t s) {
+  const int dtype = bs[0]->dtype;
+  const int esz = elem_size(dtype);
+  const uint64_t g = kChunkQuantum / esz;
+  const int N = c->size;
   FusedParams F;
   std::memset(&F, 0, sizeof(F));
+  // channels: sized by the largest buffer, like a single-buffer launch
+  uint64_t maxL = 0;
+  for (int i = 0; i < nb; ++i) maxL = std::max<uint64_t>(maxL, bs[i]->L);
   int nch = 0;
-  int st = make_ring_params(c, b.L, b.dtype, true, &F.ring, &nch);
+  int st = make_ring_params(c, maxL, dtype, true, &F.ring, &nch);
   if (st != HVD_OK) return st;
-  F.segs = b.pp.segs;
-  F.src = b.pp.src;
-  F.dst = b.dst;
-  F.vbeg_global = b.vbeg;
-  F.nseg = b.pp.nseg;
-  F.scale_on = b.pp.scale_on;
-  F.scale = b.pp.scale;
-  F.dtype = b.dtype;
-  F.tdtype = b.tdtype;
-  F.registered = b.rdst != nullptr && c->size > 1;
-  F.rdst = b.rdst;
-  st = launch_counted(c, HVD_KERNEL_FUSED, s, [&] { return launch_fused(F, b.dtype, nch, c->nlocal, c->threads, s); });
+  F.region_el = c->bufsz / esz / nch / g * g;
+  F.scale_on = bs[0]->pp.scale_on;
+  F.scale = bs[0]->pp.scale;
+  F.dtype = dtype;
+  F.tdtype = bs[0]->tdtype;
+  F.registered = bs[0]->rdst != nullptr && N > 1;
+  F.nbuf = nb;
+  int maxseg = 0;
+  std::vector<unsigned long long> signals(nch, 0);
+  int next_owner = 0;
+  for (int i = 0; i < nb; ++i) {
+    const DevPlanBuffer& b = *bs[i];
+    BufDesc& D = F.bufs[i];
+    D.segs = b.pp.segs;
+    D.src = b.pp.src;
+    D.dst = b.dst ? b.dst : b.pp.src;
+    D.rdst = b.rdst;
+    D.vbeg = b.vbeg;
+    D.nseg = b.pp.nseg;
+    D.L = b.L;
+    D.q = chunk_len(b.L, N, dtype);
+    // A buffer too small to give every channel 32 KiB per chunk runs whole on one
+    // channel (round robin), so many small buffers of one call proceed in parallel.
+    const bool small = nb > 1 && nch > 1 && D.q * esz < (uint64_t)nch * (32 << 10) &&
+                       (uint64_t)N * ((D.q + g - 1) / g * g) <= F.region_el;  // fits one channel's region
+    D.owner = small ? (next_owner++ % nch) : -1;
+    const int geo_ch = small ? 1 : nch;
+    D.ch_el = (D.q + (uint64_t)geo_ch * g - 1) / ((uint64_t)geo_ch * g) * g;
+    uint64_t sb = (uint64_t)c->slice_bytes;
+    if (sb == 0) sb = std::min<uint64_t>(128 << 10, std::max<uint64_t>(32 << 10, D.ch_el * esz / 2));
+    D.slice_el = std::min<uint64_t>(std::max<uint64_t>(g, sb / esz / g * g), std::max<uint64_t>(D.ch_el, g));
+    D.K = (int)((D.ch_el + D.slice_el - 1) / D.slice_el);
+    if (D.K < 1) D.K = 1;
+    if ((uint64_t)N * D.ch_el > F.region_el) return HVD_ERR_INVALID;  // region slack exhausted
+    maxseg = std::max(maxseg, D.nseg);
+    const unsigned long long inc = (unsigned long long)(N > 1 ? 2 * (N - 1) : 0) * D.K;
+    if (small) signals[D.owner] += inc;
+    else for (int ch = 0; ch < nch; ++ch) signals[ch] += inc;
+  }
+  F.cache_segs = maxseg <= kFusedSmemSegs ? (maxseg + 1) / 2 * 2 : 0;
+  const int tdt = F.tdtype;
+  st = launch_counted(c, HVD_KERNEL_FUSED, s, [&] { return launch_fused(F, dtype, nch, c->nlocal, c->threads, s); });
+  (void)tdt;
   if (st != HVD_OK) return st;
   if (c->tl) {
     c->tl_nch = nch;
-    c->tl_K = F.ring.K;
-    c->tl_T = c->size > 1 ? 2 * (c->size - 1) : 0;
-    c->tl_slices = c->size > 1 ? (c->tl_T + 1) * F.ring.K : F.ring.K;
-    c->tl_kind = 0;
+    c->tl_K = F.bufs[0].K;
+    c->tl_T = N > 1 ? 2 * (N - 1) : 0;
+    int ops = 0;
+    for (int i = 0; i < nb; ++i)
+      ops += N > 1 ? (F.registered ? c->tl_T : c->tl_T + 1) * F.bufs[i].K : F.bufs[i].K;
+    c->tl_slices = ops;
+    c->tl_kind = F.registered ? 2 : 0;
   }
-  advance_base(c, F.ring, nch);
+  for (int ch = 0; ch < nch; ++ch) c->base[ch] += signals[ch];
   return HVD_OK;
+}
+
+// The fused path for a whole plan: pull protocol per buffer, else multi-buffer launches.
+int enqueue_fused_plan(hvd_comm* c, CachedPlan* plan, cudaStream_t s) {
+  std::vector<DevPlanBuffer*> group;
+  auto flush = [&]() -> int {
+    int st = HVD_OK;
+    if (!group.empty()) st = enqueue_fused_multi(c, group.data(), (int)group.size(), s);
+    group.clear();
+    return st;
+  };
+  for (DevPlanBuffer& b : plan->bufs) {
+    if (b.L == 0) continue;
+    if (c->protocol == 0 && c->size > 1 && b.tdtype == b.dtype && !b.rdst) {
+      int st = flush();
+      if (st != HVD_OK) return st;
+      st = enqueue_pull(c, b, s);
+      if (st != HVD_OK) return st;
+      continue;
+    }
+    if (!group.empty() && (group[0]->dtype != b.dtype || group[0]->tdtype != b.tdtype ||
+                           (int)group.size() >= std::min(c->multi_bufs, kMaxMultiBufs))) {
+      int st = flush();
+      if (st != HVD_OK) return st;
+    }
+    group.push_back(&b);
+  }
+  return flush();
 }
 
 int pack_grid(hvd_comm* c) { return c->sm_count * c->pack_ctas_per_sm / c->nlocal + 1; }
@@ -577,14 +653,12 @@ int do_allreduce(hvd_comm* c, const hvd_tensor* t, int n, int op, uint64_t thres
   st = get_plan(c, t, n, threshold, s, &plan, wire, reg);
   if (st != HVD_OK) return st;
   const float scale = 1.0f / (float)c->size;  // s = fl32(1/N) (R1)
-  for (DevPlanBuffer& b : plan->bufs) {       // step 6: repeat per fusion buffer
+  for (DevPlanBuffer& b : plan->bufs) {
     b.pp.scale = scale;
     b.pp.scale_on = op == HVD_AVERAGE ? 1 : 0;
-    if (c->fused) {                            // steps 3-5 in one zero-copy launch
-      st = enqueue_fused(c, b, s);
-      if (st != HVD_OK) return st;
-      continue;
-    }
+  }
+  if (c->fused) return enqueue_fused_plan(c, plan, s);  // steps 3-6, zero-copy, few launches
+  for (DevPlanBuffer& b : plan->bufs) {       // step 6: repeat per fusion buffer
     st = launch_counted(c, HVD_KERNEL_PACK, s, [&] {                          // step 3
       return launch_pack(b.pp, b.dtype, c->nlocal, pack_grid(c), kPackThreads, s);
     });
@@ -619,7 +693,7 @@ int hvd_init(int rank, int size, int device, uint64_t fusion_bytes, hvd_comm** o
     return st;
   }
   if (size == 1) {
-    set_neighbours(c->rk[0], c->region[0], c->region[0], c->cap);
+    set_neighbours(c->rk[0], c->region[0], c->region[0], c->bufsz);
     c->connected = true;
   }
   *out = c;
@@ -641,7 +715,7 @@ int hvd_init_virtual(int size, int device, uint64_t fusion_bytes, hvd_comm** out
     return st;
   }
   for (int l = 0; l < size; ++l)
-    set_neighbours(c->rk[l], c->region[(l + 1) % size], c->region[(l + size - 1) % size], c->cap);
+    set_neighbours(c->rk[l], c->region[(l + 1) % size], c->region[(l + size - 1) % size], c->bufsz);
   c->connected = true;
   *out = c;
   return HVD_OK;
@@ -664,7 +738,7 @@ int hvd_get_ipc_blob(hvd_comm* c, void* out, uint64_t* len) {
   b.device = c->device;
   b.pid = (int32_t)getpid();
   b.capacity = c->cap;
-  b.region_bytes = kNumBufs * c->cap + kTailBytes;
+  b.region_bytes = kNumBufs * c->bufsz + kTailBytes;
   CK(cudaSetDevice(c->device));
   CK(cudaIpcGetMemHandle(&b.handle, c->region[0]));
   std::memcpy(out, &b, sizeof(b));
@@ -699,7 +773,7 @@ int hvd_connect(hvd_comm* c, const void* blobs, uint64_t len_each) {
   } else {
     c->pred_region = c->peer_region;
   }
-  set_neighbours(c->rk[0], c->peer_region, c->pred_region, c->cap);
+  set_neighbours(c->rk[0], c->peer_region, c->pred_region, c->bufsz);
   c->connected = true;
   return HVD_OK;
 }
@@ -889,11 +963,18 @@ int hvd_allreduce_buffer(hvd_comm* c, uint64_t count, int dtype, int op, void* s
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   CK(cudaSetDevice(c->device));
   if (c->fused) {
-    // the fusion buffer itself is the single member: the fused kernel reduces it in
-    // place (its AVERAGE prescale happens in the gather)
-    hvd_tensor t[kMaxLocal];
-    for (int l = 0; l < c->nlocal; ++l) t[l] = {c->rk[l].buf, count, dtype, 0};
-    return do_allreduce(c, t, 1, op, c->cap, s);
+    // the fusion buffer itself is the single member, reduced in place by the fused
+    // kernel as a registered tensor (the successor's buffer is already mapped), so the
+    // kernel's channel-private use of the buffer region never touches it
+    c->bufreg.n = 1;
+    c->bufreg.own.resize(c->nlocal);
+    c->bufreg.succ.resize(c->nlocal);
+    for (int l = 0; l < c->nlocal; ++l) {
+      c->bufreg.own[l] = {c->rk[l].buf, count, dtype, 0};
+      c->bufreg.succ[l] = c->rk[l].nbuf;
+    }
+    c->bufreg.live = true;
+    return do_allreduce(c, c->bufreg.own.data(), 1, op, c->cap, s, 0, c->size > 1 ? &c->bufreg : nullptr);
   }
   if (op == HVD_AVERAGE) {
     char* bufs[kMaxLocal];
@@ -1017,7 +1098,10 @@ int hvd_allgather(hvd_comm* c, const hvd_tensor* in, const hvd_tensor* out, void
     F.nseg = b.pp.nseg;
     F.dtype = dtype;
     if (N == 1) {  // out = in: the fused kernel's N = 1 path (gather -> scatter), no scale
-      st = launch_counted(c, HVD_KERNEL_FUSED, s, [&] { return launch_fused(F, dtype, nch, c->nlocal, c->threads, s); });
+      b.pp.scale_on = 0;
+      b.pp.scale = 1.0f;
+      DevPlanBuffer* one = &b;
+      st = enqueue_fused_multi(c, &one, 1, s);
       if (st != HVD_OK) return st;
       continue;
     }
@@ -1096,6 +1180,10 @@ int hvd_set_config(hvd_comm* c, int key, int64_t value) {
       if (value != 0 && value != 1) return HVD_ERR_INVALID;
       c->fused = (int)value;
       return HVD_OK;
+    case HVD_CFG_MULTI_BUFFERS:
+      if (value < 1 || value > kMaxMultiBufs) return HVD_ERR_INVALID;
+      c->multi_bufs = (int)value;
+      return HVD_OK;
     case HVD_CFG_PROTOCOL:
       if (value != 0 && value != 1) return HVD_ERR_INVALID;
       c->protocol = (int)value;
@@ -1141,6 +1229,7 @@ int64_t hvd_get_config(const hvd_comm* c, int key) {
     case HVD_CFG_TIMELINE: return c->tl_max;
     case HVD_CFG_WINDOW: return c->window;
     case HVD_CFG_PROTOCOL: return c->protocol;
+    case HVD_CFG_MULTI_BUFFERS: return c->multi_bufs;
     case HVD_CFG_FIN_LAG: return c->fin_lag;
     default: return -1;
   }

@@ -36,6 +36,9 @@ def op_of(j: int, K: int, T: int, lag: int = 1):
 
 
 def _phase(idx: int, K: int, T: int, N: int, lag: int = 1, kind: str = "push") -> str:
+    if kind == "registered":
+        t, k = idx // K, idx % K
+        return f"reduce-scatter s={t} k={k}" if t < N - 1 else f"all-gather s={t - N + 1} k={k}"
     if kind == "pull":
         t, k = idx // K, idx % K
         if t == 0:

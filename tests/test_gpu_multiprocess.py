@@ -159,3 +159,54 @@ def test_multiprocess_ring_matches_oracle(protocol):
                 assert_same(res[r][0][ci][0], ref[r], dtype, f"buffer case {ci} rank {r}")
                 sent, sends = res[r][0][ci][1]
                 assert sent == tr[r].sent_elems * oracle.ELEM_SIZE[dtype] and sends == 2 * (n - 1)
+
+
+def _timeout_worker(rank, world, port, q):
+    os.environ.update(RANK=str(rank), WORLD_SIZE=str(world), LOCAL_RANK=str(rank),
+                      MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import sys
+    import time
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import paper_1802_05799_b200 as hvd
+    import torch.distributed as dist
+    try:
+        comm = hvd.init()
+        comm.set_config(hvd._lib.HVD_CFG_TIMEOUT_MS, 1500)
+        x = torch.ones(1 << 20, device="cuda")
+        dist.barrier()
+        status = None
+        if rank == 0:  # rank 1 never joins: rank 0's kernel must give up, not hang
+            t0 = time.time()
+            comm.allreduce_average([x])
+            torch.cuda.synchronize()
+            status = (comm.poll_error(), time.time() - t0)
+            try:
+                comm.allreduce_average([x])
+                status = status + ("no error",)
+            except hvd.HvdError as e:
+                status = status + (e.status,)
+        q.put((rank, status))
+        dist.barrier()
+        comm.finalize()
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e)))
+
+
+def test_watchdog_turns_a_missing_peer_into_an_error():
+    """A rank that never joins the collective: the device spin-wait gives up after the
+    watchdog, latches HVD_ERR_TIMEOUT and every later call returns it (no GPU hang)."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_timeout_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=120)
+    err, elapsed, again = res[0]
+    assert err == -5 and again == -5, res  # HVD_ERR_TIMEOUT
+    assert 1.0 < elapsed < 60.0

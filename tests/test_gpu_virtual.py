@@ -377,7 +377,8 @@ def test_both_protocols_bitexact(hvd, n, protocol):
             torch.cuda.synchronize()
             assert comm.poll_error() == 0
             st = comm.kernel_stats()
-            assert st["pull" if protocol == 0 else "fused"][0] == len(plan)
+            # pull: one launch per fusion buffer; push: every buffer of the call in one launch
+            assert st["pull" if protocol == 0 else "fused"][0] == (len(plan) if protocol == 0 else 1)
             for r in range(n):
                 for k in range(len(counts)):
                     assert_same(from_torch(ts[r][k], dtype), ref[r][k], dtype, f"it={it} r={r} k={k}")
@@ -410,7 +411,7 @@ def test_wire_dtype_variants_bitexact(hvd, n, tdt, wire):
     comm.allreduce(ts, op="average", fusion_threshold=400_000, wire=wire)
     torch.cuda.synchronize()
     assert comm.poll_error() == 0
-    assert comm.kernel_stats()["fused"][0] == len(plan)
+    assert comm.kernel_stats()["fused"][0] == 1  # all fusion buffers of the call in one launch
     for r in range(n):
         for k in range(len(counts)):
             assert_same(from_torch(ts[r][k], tdt), ref[r][k], tdt, f"N={n} r={r} k={k}")
@@ -443,3 +444,23 @@ def test_registered_zero_copy_bitexact(hvd, n):
         comm.deregister(reg)
     finally:
         comm.finalize()
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_many_small_buffers_one_launch(hvd, n):
+    """Fusion off over 200 small tensors: up to 96 buffers per launch, small buffers each run
+    whole on one channel (round robin) so they proceed in parallel; bit-exact."""
+    comm = comm_for(hvd, n)
+    counts = [int(c) for c in np.random.default_rng(8).integers(1, 3000, size=200)]
+    xs = workloads.all_ranks(counts, "f32", n, seed=31)
+    ref, _, plan = oracle.allreduce(xs, ["f32"] * len(counts), "average", threshold=0)
+    assert len(plan) == 200
+    ts = [[to_torch(x, "f32") for x in xs[r]] for r in range(n)]
+    comm.kernel_stats()
+    comm.allreduce(ts, op="average", fusion_threshold=0)
+    torch.cuda.synchronize()
+    assert comm.poll_error() == 0
+    assert comm.kernel_stats()["fused"][0] == 3
+    for r in range(n):
+        for k in range(len(counts)):
+            assert_same(from_torch(ts[r][k], "f32"), ref[r][k], "f32", f"r={r} k={k}")
