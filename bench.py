@@ -160,7 +160,7 @@ def run_ours(args):
     payload = sum(counts) * esz
     # inputs larger than L2: rotate over enough gradient sets that the set a step
     # reads was evicted by the others (>= 2 x L2 of distinct gradient bytes)
-    nsets = max(2, -(-2 * L2_BYTES // payload))
+    nsets = args.sets if args.sets else max(2, -(-2 * L2_BYTES // payload))
     g = torch.Generator(device="cuda").manual_seed(180205799 + rank)
     sets = [[torch.randn(c, generator=g, device="cuda", dtype=torch.float32).to(tdt) for c in counts]
             for _ in range(nsets)]
@@ -420,6 +420,7 @@ def main():
     ap.add_argument("--clock-window", type=float, default=1.5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--registered", type=int, default=1, help="1: registered gradient tensors (zero-copy)")
+    ap.add_argument("--sets", type=int, default=0, help="input sets to rotate (0: enough to exceed 2 x L2)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -46,6 +46,8 @@ struct RingRank {
   unsigned long long* done_own;  // calls completed by this rank (read remotely by the predecessor)
   const unsigned long long* done_succ;  // successor's completed calls
   unsigned long long* exits;     // CTA exit counter of this rank (local)
+  unsigned long long* ll;        // LL region (small-buffer protocol), written by the predecessor
+  unsigned long long* nll;       // successor's LL region
   int rank;                      // ring rank
   int pad;
 };
@@ -165,6 +167,9 @@ struct FusedParams {
 cudaError_t launch_fused(const FusedParams& p, int dtype, int nch, int nlocal, int threads, cudaStream_t s);
 cudaError_t launch_copy(const FusedParams& p, int dtype, int nch, int nlocal, int threads, cudaStream_t s);
 cudaError_t launch_pull(const FusedParams& p, int dtype, int nch, int nlocal, int threads, cudaStream_t s);
+cudaError_t launch_ll(const FusedParams& p, int dtype, int nch, int nlocal, cudaStream_t s);
+constexpr unsigned long long kLLMaxBytes = 1ull << 20;  // largest payload for the LL protocol
+constexpr unsigned long long kLLRegionBytes = 9ull << 20;  // 2 parities x (2N-2) steps x chunk, 2x wire
 cudaError_t pull_max_ctas_per_sm(int dtype, int threads, int* out);
 cudaError_t fused_max_ctas_per_sm(int dtype, int threads, int* out);
 cudaError_t launch_pack(const PackParams& p, int dtype, int nlocal, int grid, int threads,

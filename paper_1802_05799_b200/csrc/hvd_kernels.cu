@@ -1324,6 +1324,122 @@ __global__ void __launch_bounds__(416, 1) pull_allreduce_kernel(const __grid_con
   }
 }
 
+// ------------------------------------------------------------------ LL (low-latency) small-buffer ring
+// For small buffers the ring is latency-bound: each of the 2(N-1) steps of the
+// store+fence+counter protocol costs a system fence, a counter hop and a
+// barrier.  Here every 4 B of wire data travels in one 8 B word together with
+// the call's epoch as a flag ({epoch, data}, aligned 8 B stores are single-copy
+// atomic), so a receiver polls the data itself: no fences, no counters, no
+// barriers — each thread only waits for the words it consumes.  Same ring, same
+// chunks, same reduction order as the fused kernel (bit-identical); the wire
+// carries 2x the bytes, which does not matter at these sizes.
+// LL region of a rank: [parity 2][step 2N-2][chunk slot q] words, written by the
+// predecessor.  Parity = epoch & 1: a sender reuses a parity two launches later,
+// when (stream order + the all-gather chain) its successor has finished with it.
+__device__ __forceinline__ void ll_store(unsigned long long* p, uint4 x, unsigned flag) {
+  const unsigned long long f = (unsigned long long)flag << 32;
+  asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1,%2};" ::"l"(p), "l"(f | x.x), "l"(f | x.y) : "memory");
+  asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1,%2};" ::"l"(p + 2), "l"(f | x.z), "l"(f | x.w) : "memory");
+}
+
+// Wait until the 4 words of one data vector carry `flag`; false on watchdog timeout.
+__device__ __forceinline__ bool ll_load(const unsigned long long* p, unsigned flag, uint4& x, int* err,
+                                        unsigned long long timeout_ns) {
+  unsigned long long a, b, c, d;
+  unsigned long long t0 = 0;
+  unsigned spins = 0;
+  for (;;) {
+    asm volatile("ld.relaxed.sys.global.v2.u64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.sys.global.v2.u64 {%0,%1}, [%2];" : "=l"(c), "=l"(d) : "l"(p + 2) : "memory");
+    if ((unsigned)(a >> 32) == flag && (unsigned)(b >> 32) == flag && (unsigned)(c >> 32) == flag &&
+        (unsigned)(d >> 32) == flag)
+      break;
+    if ((++spins & 255u) == 0) {
+      const unsigned long long now = globaltimer();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > timeout_ns || *(volatile int*)err != 0) {
+        *(volatile int*)err = kHvdErrTimeout;
+        return false;
+      }
+    }
+  }
+  x = make_uint4((uint32_t)a, (uint32_t)b, (uint32_t)c, (uint32_t)d);
+  return true;
+}
+
+template <class Op>
+__global__ void __launch_bounds__(256) ll_allreduce_kernel(const __grid_constant__ FusedParams P) {
+  constexpr int ESZ = Op::kEsz;
+  constexpr int VEL = 16 / ESZ;
+  const RingParams& R = P.ring;
+  const RingRank& me = R.rk[blockIdx.y];
+  const int ch = blockIdx.x;
+  const int N = R.N;
+  const int r = me.rank;
+  const int T = 2 * (N - 1);
+  const BufDesc& D = P.bufs[0];
+  const unsigned flag = (unsigned)R.epoch;
+  const int par = (int)(R.epoch & 1);
+  const unsigned long long slot_words = D.q / VEL * 4;  // words per chunk slot
+  unsigned long long* const in_ll = me.ll + (unsigned long long)par * T * slot_words;
+  unsigned long long* const out_ll = me.nll + (unsigned long long)par * T * slot_words;
+  FusedCtx F;
+  F.segs = D.segs;
+  F.src = D.src + (size_t)blockIdx.y * D.nseg;
+  F.dst = D.dst + (size_t)blockIdx.y * D.nseg;
+  F.rdst = nullptr;
+  F.vbeg = D.vbeg;
+  F.nseg = D.nseg;
+  F.scale_on = P.scale_on;
+  F.scale = P.scale;
+  F.dtype = P.dtype;
+  using Cvt = WireCvt<ESZ, ESZ>;
+  SegCache sc;
+  bool ok = true;
+  unsigned long long sent = 0;
+  for (int t = 0; t <= T && ok; ++t) {  // t == T: the chunk received in the last step
+    const bool rs = t < N - 1;
+    const int s = rs ? t : t - (N - 1);
+    const int c = t == T ? mod(r + 2, N) : (rs ? mod(r - s, N) : mod(r + 1 - s, N));
+    unsigned long long lo, hi;
+    slice_range_d(D, c, ch, 0, lo, hi);  // one slice per channel (K = 1)
+    if (hi <= lo) continue;
+    const unsigned long long c0 = (unsigned long long)c * D.q;  // chunk start: slot position base
+    const unsigned long long v_lo = lo / VEL, v_hi = (hi + VEL - 1) / VEL;
+    for (unsigned long long v = v_lo + threadIdx.x; v < v_hi; v += blockDim.x) {
+      const unsigned long long e = v * VEL;
+      const unsigned long long slot = (v - c0 / VEL) * 4;  // word offset inside the chunk slot
+      unsigned long long left = 0;
+      seg_lookup<ESZ>(F, v, sc);
+      left = sc.end_el > e ? sc.end_el - e : 0;
+      uint4 g = make_uint4(0, 0, 0, 0);
+      if (t <= N - 1) {  // own contribution, loaded before polling the predecessor's words
+        const char* gp = reinterpret_cast<const char*>(sc.g + e * ESZ);
+        g = Cvt::fast(gp, left) ? Pack16<ESZ>::conv(__ldcs(reinterpret_cast<const uint4*>(gp)), F.scale, F.scale_on,
+                                                    F.dtype)
+                                : Cvt::slow(gp, left, F.scale, F.scale_on, F.dtype);
+      }
+      uint4 x = g;
+      if (t > 0) {
+        uint4 in;
+        if (!ll_load(in_ll + (unsigned long long)(t - 1) * slot_words + slot, flag, in, R.err, R.timeout_ns)) {
+          ok = false;
+          break;
+        }
+        x = in;
+        if (t <= N - 1) Op::template add_words<4>(reinterpret_cast<uint32_t*>(&x), reinterpret_cast<const uint32_t*>(&g));
+      }
+      if (t < T) ll_store(out_ll + (unsigned long long)t * slot_words + slot, x, flag);
+      if (t >= N - 1) Cvt::put(reinterpret_cast<char*>(sc.d + e * ESZ), left, x);
+    }
+    if (t < T) sent += (hi - lo) * ESZ;
+  }
+  if (threadIdx.x == 0) {
+    atomicAdd(me.stats + 0, sent);
+    if (ch == 0) atomicAdd(me.stats + 1, (unsigned long long)T);
+  }
+}
+
 struct BufList { char* b[kMaxLocal]; };
 
 template <int ESZ>
@@ -1520,6 +1636,29 @@ cudaError_t pull_max_ctas_per_sm(int dtype, int threads, int* out) {
     case 2: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, pull_allreduce_kernel<OpBF16>, threads + 32, smem);
     case 3: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, pull_allreduce_kernel<OpI32>, threads + 32, smem);
     case 4: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, pull_allreduce_kernel<OpI64>, threads + 32, smem);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <class Op>
+static cudaError_t launch_ll_t(const FusedParams& p, int nch, int nlocal, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nch, nlocal);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // CTAs of all ranks wait on each other's words
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, ll_allreduce_kernel<Op>, p);
+}
+
+cudaError_t launch_ll(const FusedParams& p, int dtype, int nch, int nlocal, cudaStream_t s) {
+  switch (dtype) {
+    case 1: return launch_ll_t<OpF32>(p, nch, nlocal, s);
+    case 2: return launch_ll_t<OpBF16>(p, nch, nlocal, s);
+    case 3: return launch_ll_t<OpI32>(p, nch, nlocal, s);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -95,6 +95,8 @@ struct hvd_comm {
   int window = 0;
   int fin_lag = 1;
   unsigned long long hs_epoch = 0;  // copy-collective handshake epochs issued
+  unsigned long long ll_epoch = 0;  // LL launches issued (flag value = epoch)
+  int64_t ll_max = (int64_t)kLLMaxBytes;  // HVD_CFG_LL_MAX_BYTES
   int protocol = 1;                 // 0: pull (receiver-initiated TMA loads), 1: push (SM stores)
   unsigned long long pbase[kMaxChannels] = {};  // pull-protocol progress counter bases
   int pull_calls = 0;
@@ -149,6 +151,9 @@ unsigned long long* pflags_of(char* region, uint64_t cap) { return tail_of(regio
 unsigned long long* done_of(char* region, uint64_t cap) { return tail_of(region, cap) + 1536; }
 unsigned long long* exits_of(char* region, uint64_t cap) { return tail_of(region, cap) + 1537; }
 char* pull_of(char* region, uint64_t cap, int p) { return region + (2 + p) * cap; }
+unsigned long long* ll_of(char* region, uint64_t cap) {
+  return reinterpret_cast<unsigned long long*>(region + kNumBufs * cap + kTailBytes);
+}
 
 int common_init(hvd_comm* c, uint64_t fusion_bytes) {
   c->cap = ((fusion_bytes ? fusion_bytes : kDefaultFusionBytes) + 4095) / 4096 * 4096;
@@ -158,10 +163,10 @@ int common_init(hvd_comm* c, uint64_t fusion_bytes) {
   CK(cudaHostAlloc(reinterpret_cast<void**>(&c->err_host), sizeof(int), cudaHostAllocMapped));
   *c->err_host = 0;
   CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->err_dev), c->err_host, 0));
-  const uint64_t region_bytes = kNumBufs * c->bufsz + kTailBytes;
+  const uint64_t region_bytes = kNumBufs * c->bufsz + kTailBytes + kLLRegionBytes;
   for (int l = 0; l < c->nlocal; ++l) {
     CK(cudaMalloc(reinterpret_cast<void**>(&c->region[l]), region_bytes));
-    CK(cudaMemset(c->region[l] + kNumBufs * c->bufsz, 0, kTailBytes));
+    CK(cudaMemset(c->region[l] + kNumBufs * c->bufsz, 0, kTailBytes + kLLRegionBytes));
     RingRank& r = c->rk[l];
     const uint64_t bz = c->bufsz;
     r.buf = buf_of(c->region[l]);
@@ -174,6 +179,7 @@ int common_init(hvd_comm* c, uint64_t fusion_bytes) {
     r.pflags_own = pflags_of(c->region[l], bz);
     r.done_own = done_of(c->region[l], bz);
     r.exits = exits_of(c->region[l], bz);
+    r.ll = ll_of(c->region[l], bz);
     r.rank = c->virt ? l : c->rank;
   }
   CK(cudaDeviceSynchronize());
@@ -189,6 +195,7 @@ void set_neighbours(RingRank& r, char* succ_region, char* pred_region, uint64_t 
   r.ppull[1] = pull_of(pred_region, cap, 1);
   r.pflags_pred = pflags_of(pred_region, cap);
   r.done_succ = done_of(succ_region, cap);
+  r.nll = ll_of(succ_region, cap);
 }
 
 int check_live(hvd_comm* c) {
@@ -588,8 +595,48 @@ int enqueue_fused_multi(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStrea
   return HVD_OK;
 }
 
+// LL protocol for one small buffer (ll_allreduce_kernel).
+int enqueue_ll(hvd_comm* c, DevPlanBuffer& b, cudaStream_t s) {
+  const int dtype = b.dtype;
+  const int esz = elem_size(dtype);
+  const uint64_t g = kChunkQuantum / esz;
+  const int N = c->size;
+  FusedParams F;
+  std::memset(&F, 0, sizeof(F));
+  int nch = 0;
+  int st = make_ring_params(c, b.L, dtype, true, &F.ring, &nch);
+  if (st != HVD_OK) return st;
+  BufDesc& D = F.bufs[0];
+  D.q = chunk_len(b.L, N, dtype);
+  nch = (int)std::min<uint64_t>(32, std::max<uint64_t>(1, D.q * esz / (16 << 10)));
+  D.segs = b.pp.segs;
+  D.src = b.pp.src;
+  D.dst = b.dst ? b.dst : b.pp.src;
+  D.vbeg = b.vbeg;
+  D.nseg = b.pp.nseg;
+  D.L = b.L;
+  D.ch_el = (D.q + (uint64_t)nch * g - 1) / ((uint64_t)nch * g) * g;
+  D.slice_el = std::max<uint64_t>(D.ch_el, g);
+  D.K = 1;
+  D.owner = -1;
+  if ((uint64_t)2 * 2 * (N - 1) * D.q * esz > kLLRegionBytes) return HVD_ERR_INVALID;
+  F.nbuf = 1;
+  F.scale_on = b.pp.scale_on;
+  F.scale = b.pp.scale;
+  F.dtype = dtype;
+  F.tdtype = dtype;
+  F.ring.epoch = ++c->ll_epoch;
+  return launch_counted(c, HVD_KERNEL_LL, s, [&] { return launch_ll(F, dtype, nch, c->nlocal, s); });
+}
+
 // The fused path for a whole plan: pull protocol per buffer, else multi-buffer launches.
 int enqueue_fused_plan(hvd_comm* c, CachedPlan* plan, cudaStream_t s) {
+  if (plan->bufs.size() == 1 && c->size > 1 && c->protocol == 1) {  // one small buffer: LL protocol
+    DevPlanBuffer& b = plan->bufs[0];
+    const int esz = elem_size(b.dtype);
+    if (b.L > 0 && b.tdtype == b.dtype && b.dtype != HVD_INT64 && (int64_t)(b.L * esz) <= c->ll_max)
+      return enqueue_ll(c, b, s);
+  }
   std::vector<DevPlanBuffer*> group;
   auto flush = [&]() -> int {
     int st = HVD_OK;
@@ -738,7 +785,7 @@ int hvd_get_ipc_blob(hvd_comm* c, void* out, uint64_t* len) {
   b.device = c->device;
   b.pid = (int32_t)getpid();
   b.capacity = c->cap;
-  b.region_bytes = kNumBufs * c->bufsz + kTailBytes;
+  b.region_bytes = kNumBufs * c->bufsz + kTailBytes + kLLRegionBytes;
   CK(cudaSetDevice(c->device));
   CK(cudaIpcGetMemHandle(&b.handle, c->region[0]));
   std::memcpy(out, &b, sizeof(b));
@@ -1180,6 +1227,10 @@ int hvd_set_config(hvd_comm* c, int key, int64_t value) {
       if (value != 0 && value != 1) return HVD_ERR_INVALID;
       c->fused = (int)value;
       return HVD_OK;
+    case HVD_CFG_LL_MAX_BYTES:
+      if (value < 0 || value > (int64_t)kLLMaxBytes) return HVD_ERR_INVALID;
+      c->ll_max = value;
+      return HVD_OK;
     case HVD_CFG_MULTI_BUFFERS:
       if (value < 1 || value > kMaxMultiBufs) return HVD_ERR_INVALID;
       c->multi_bufs = (int)value;
@@ -1230,6 +1281,7 @@ int64_t hvd_get_config(const hvd_comm* c, int key) {
     case HVD_CFG_WINDOW: return c->window;
     case HVD_CFG_PROTOCOL: return c->protocol;
     case HVD_CFG_MULTI_BUFFERS: return c->multi_bufs;
+    case HVD_CFG_LL_MAX_BYTES: return c->ll_max;
     case HVD_CFG_FIN_LAG: return c->fin_lag;
     default: return -1;
   }

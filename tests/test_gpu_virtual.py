@@ -464,3 +464,37 @@ def test_many_small_buffers_one_launch(hvd, n):
     for r in range(n):
         for k in range(len(counts)):
             assert_same(from_torch(ts[r][k], "f32"), ref[r][k], "f32", f"r={r} k={k}")
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 5, 8])
+def test_ll_protocol_small_buffers_bitexact(hvd, n):
+    """One small fusion buffer (<= 1 MiB) takes the LL protocol ({epoch, data} words): same bits,
+    epochs/parities reused across back-to-back calls of varying size."""
+    comm = comm_for(hvd, n)
+    cases = [([1], "f32"), ([3, 5], "bf16"), ([64 * n + 7], "f32"), ([70_001, 13], "i32"),
+             ([100_000, 3, 999], "f32"), ([262_144], "f32"), ([255_000], "bf16")]
+    pend = []
+    comm.kernel_stats()
+    for it, (counts, dt) in enumerate(cases):
+        kind = "normal" if dt in ("f32", "bf16") else "int_uniform"
+        op = "average" if dt in ("f32", "bf16") else "sum"
+        xs = workloads.all_ranks(counts, dt, n, kind=kind, seed=300 + it)
+        ts = [[to_torch(x, dt) for x in xs[r]] for r in range(n)]
+        if it == 4:  # a misaligned tensor on one rank
+            big = torch.empty(counts[0] + 1, device="cuda")
+            big[1:].copy_(ts[0][0])
+            ts[0][0] = big[1:]
+            pend.append(big)
+        comm.allreduce(ts, op=op)
+        pend.append((xs, ts, dt, op, counts))
+    torch.cuda.synchronize()
+    assert comm.poll_error() == 0
+    assert comm.kernel_stats()["ll"][0] == len(cases)
+    for item in pend:
+        if not isinstance(item, tuple):
+            continue
+        xs, ts, dt, op, counts = item
+        ref, _, _ = oracle.allreduce(xs, [dt] * len(counts), op)
+        for r in range(n):
+            for k in range(len(counts)):
+                assert_same(from_torch(ts[r][k], dt), ref[r][k], dt, f"{dt} {counts} r={r} k={k}")
