@@ -154,6 +154,9 @@ def run_ours(args):
         import torch.distributed as dist
         dist.init_process_group("gloo")
     comm = hvd.init(fusion_bytes=64 * MIB, device=local)
+    for kv in args.config:
+        k, v = kv.split("=")
+        comm.set_config(getattr(hvd._lib, "HVD_CFG_" + k), int(v))
     counts, dt = _workload_counts(args.workload)
     tdt = {"f32": torch.float32, "bf16": torch.bfloat16}[dt]
     esz = 4 if dt == "f32" else 2
@@ -236,7 +239,7 @@ def run_ours(args):
     else:
         # HBM: fused at N=1 reads the members and writes them back; pack reads the
         # members + writes the buffer; unpack reads the buffer + writes the members
-        if dom == "fused":
+        if dom in ("fused", "solo"):
             step_bytes = 2 * payload
         else:
             step_bytes = payload + sum(Lb * esz_of[bdt] for bdt, Lb, _ in fplan)
@@ -314,8 +317,11 @@ def run_ours(args):
             "config": {"workload": args.workload, "payload_bytes": payload, "tensors": len(counts),
                        "tensors_registered": bool(args.registered),
                        "fusion_bytes": 64 * MIB, "op": "average",
-                       "l2": f"inputs rotate over {nsets} gradient sets ({nsets * payload / MIB:.0f} MiB > L2)",
-                       "parallelism": f"dp{n}", "ranks": "one process per GPU, CUDA-IPC ring"},
+                       "l2": f"inputs rotate over {nsets} gradient sets ({nsets * payload / MIB:.0f} MiB "
+                             + ("> 2 x L2: every step reads cold inputs)" if nsets * payload > 2 * L2_BYTES
+                                else "<= 2 x L2: WARM inputs, not a contract measurement)"),
+                       "parallelism": f"dp{n}", "ranks": "one process per GPU, CUDA-IPC ring",
+                       **({"knobs": args.config} if args.config else {})},
             "roofline": roof, "kernels": kernels, "ring_only_64MiB": ring_only, "e2e": e2e,
             "gpu_launches": gpu_launches, "cpu_baseline": cpu, "clocks": clocks,
         }
@@ -421,6 +427,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--registered", type=int, default=1, help="1: registered gradient tensors (zero-copy)")
     ap.add_argument("--sets", type=int, default=0, help="input sets to rotate (0: enough to exceed 2 x L2)")
+    ap.add_argument("--config", action="append", default=[], metavar="KEY=VALUE",
+                    help="hvd_set_config before timing, e.g. SOLO_PREFETCH=4 (repeatable)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -203,9 +203,12 @@ typedef enum {
                                 limit): bounds the NVLink backlog and so the signal latency */
   HVD_CFG_FIN_LAG = 11,      /* fused: slices by which the final local scatter trails the last
                                 all-gather iteration (>= K-1: scatter after all of it)     */
+  HVD_CFG_SOLO_PREFETCH = 15, /* N = 1 (solo stream kernel): L2 bulk-prefetch distance in grid
+                                strides (0..16, default 2; 0 = off)                        */
   HVD_CFG_LL_MAX_BYTES = 14, /* a call that is one fusion buffer of at most this many bytes
-                                (default and max 1 MiB; 0 = never) uses the LL protocol:
-                                {epoch, data} words, no fences or counters (fp32/bf16/i32) */
+                                (default 4 MiB at N = 2, 8 MiB at N > 2; max 8 MiB; 0 = never)
+                                uses the LL protocol: {epoch, data} words, no fences or
+                                counters (fp32/bf16/i32) */
   HVD_CFG_MULTI_BUFFERS = 13, /* fusion buffers per fused launch (1..96, default 96): the
                                 buffers of one call pipeline inside one persistent launch  */
   HVD_CFG_PROTOCOL = 12      /* allreduce data movement: 1 (default) push — SM stores into the
@@ -218,7 +221,7 @@ int64_t hvd_get_config(const hvd_comm* c, int key);
 
 typedef enum { HVD_KERNEL_PACK = 0, HVD_KERNEL_RING = 1, HVD_KERNEL_UNPACK = 2, HVD_KERNEL_SCALE = 3,
                HVD_KERNEL_FUSED = 4, HVD_KERNEL_COPY = 5, HVD_KERNEL_PULL = 6, HVD_KERNEL_LL = 7,
-               HVD_KERNEL_KINDS = 8 } hvd_kernel_kind;
+               HVD_KERNEL_SOLO = 8, HVD_KERNEL_KINDS = 9 } hvd_kernel_kind;
 /* Kernel launches of each kind since the last call (always counted) and, with
  * HVD_CFG_PROFILE on, the summed device time in ms between the CUDA events
  * recorded on the launch stream around each launch (waits for those events).

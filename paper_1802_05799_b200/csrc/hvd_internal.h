@@ -31,10 +31,12 @@ inline int elem_size(int dtype) {
 struct RingRank {
   char* buf;                     // fusion buffer (capacity bytes)
   char* scratch;                 // reduce-scatter receive scratch (capacity bytes)
+  char* scratch1;                // second receive half: a channel alternates halves per buffer
   unsigned long long* flags;     // [kMaxChannels] written by the predecessor
   unsigned long long* stats;     // [2] sent bytes, sent chunk messages
   char* nbuf;                    // successor's fusion buffer (peer / same-device)
   char* nscratch;                // successor's scratch
+  char* nscratch1;               // successor's second half
   unsigned long long* nflags;    // successor's flags
   unsigned long long* rflags;    // [kMaxChannels] ready flags, written by the successor (handshake)
   unsigned long long* pready;    // predecessor's ready flags (this rank writes them)
@@ -76,7 +78,7 @@ struct RingParams {
   unsigned long long* tl;       // timeline records of this launch (per local rank, see tl_words)
   int window;                   // fused: max pushed-but-unfenced slices per channel (0 = no limit)
   int fin_lag;                  // fused: final-scatter interleave lag in slices
-  unsigned long long epoch;     // copy collectives: handshake epoch of this launch
+  unsigned long long epoch;     // ring/fused/copy: handshake epoch of this launch (LL: flag)
   int parity;                   // pull protocol: pull buffer of this call
   int call;                     // pull protocol: 1-based call index
   unsigned long long exits_target;  // pull protocol: cumulative CTA exits after this call
@@ -168,9 +170,14 @@ cudaError_t launch_fused(const FusedParams& p, int dtype, int nch, int nlocal, i
 cudaError_t launch_copy(const FusedParams& p, int dtype, int nch, int nlocal, int threads, cudaStream_t s);
 cudaError_t launch_pull(const FusedParams& p, int dtype, int nch, int nlocal, int threads, cudaStream_t s);
 cudaError_t launch_ll(const FusedParams& p, int dtype, int nch, int nlocal, cudaStream_t s);
-constexpr unsigned long long kLLMaxBytes = 1ull << 20;  // largest payload for the LL protocol
-constexpr unsigned long long kLLRegionBytes = 9ull << 20;  // 2 parities x (2N-2) steps x chunk, 2x wire
+constexpr unsigned long long kLLMaxBytes = 4ull << 20;    // default LL payload limit at N = 2 (N > 2: kLLLimitBytes)
+constexpr unsigned long long kLLLimitBytes = 8ull << 20;  // largest HVD_CFG_LL_MAX_BYTES accepted
+// 2 parities x (2N-2) steps x chunk slot of 2 q esz bytes (8 B word per 4 B of data)
+// = 8 (N-1) q esz < 8 L + 8 (N-1) N 256 for L <= kLLLimitBytes.
+constexpr unsigned long long kLLRegionBytes = 8 * kLLLimitBytes + (64ull << 10);
 cudaError_t pull_max_ctas_per_sm(int dtype, int threads, int* out);
+cudaError_t ll_max_ctas_per_sm(int* out);
+cudaError_t launch_solo(const FusedParams& p, int dtype, int nlocal, int sm_count, int pf, cudaStream_t s);
 cudaError_t fused_max_ctas_per_sm(int dtype, int threads, int* out);
 cudaError_t launch_pack(const PackParams& p, int dtype, int nlocal, int grid, int threads,
                         cudaStream_t s);

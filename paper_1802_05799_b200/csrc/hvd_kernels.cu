@@ -50,6 +50,9 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -291,12 +294,17 @@ __global__ void __launch_bounds__(416, 1) ring_allreduce_kernel(const __grid_con
   __syncthreads();
 
   if (threadIdx.x >= nd) {  // ---- signal warp
-    if (threadIdx.x == nd) signal_loop(&s_done, T * K, me.nflags + ch, base, P.sig_mode);
+    if (threadIdx.x == nd) {
+      st_relaxed_sys(me.pready + ch, P.epoch);  // handshake: previous launch done with the regions
+      signal_loop(&s_done, T * K, me.nflags + ch, base, P.sig_mode);
+    }
     return;
   }
 
   // ---- data warps
   const unsigned tid = threadIdx.x;
+  if (tid == 0 && !spin_until(me.rflags + ch, P.epoch, P.err, P.timeout_ns)) s_abort = 1;
+  bar_sync(kBarData, nd);  // no push before the successor's handshake
   unsigned long long sent = 0;
   int i = 0;
   for (int t = 0; t < T; ++t) {
@@ -491,6 +499,8 @@ struct FusedCtx {
   char* const* dst;                 // this rank's scatter addresses [nseg] (== src for allreduce)
   char* const* rdst;                // registered mode: the successor's tensor addresses [nseg]
   const unsigned long long* vbeg;   // shared or global copy of segs[].vbeg
+  const char* scr;                  // fused ring: this buffer's receive half (own scratch)
+  char* nscr;                       //   and the successor's half it pushes into
   int nseg;
   int scale_on;
   float scale;
@@ -586,6 +596,7 @@ template <int E> struct WireCvt<E, E> {
   static constexpr int VEL = 16 / E;
   __device__ static __forceinline__ bool fast(const char* p, unsigned long long left) { return fast16<E>(p, left); }
   __device__ static __forceinline__ void issue(Raw32* slot, const char* p) { cp_async16(&slot->a, p); }
+  __device__ static __forceinline__ void load(Raw32& r, const char* p) { r.a = __ldcs(reinterpret_cast<const uint4*>(p)); }
   __device__ static __forceinline__ uint4 take(const Raw32& r, float s, int on, int dtype) {
     return Pack16<E>::conv(r.a, s, on, dtype);
   }
@@ -606,6 +617,10 @@ template <> struct WireCvt<2, 4> {  // fp32 tensor, bf16 wire
   __device__ static __forceinline__ void issue(Raw32* slot, const char* p) {
     cp_async16(&slot->a, p);
     cp_async16(&slot->b, p + 16);
+  }
+  __device__ static __forceinline__ void load(Raw32& r, const char* p) {
+    r.a = __ldcs(reinterpret_cast<const uint4*>(p));
+    r.b = __ldcs(reinterpret_cast<const uint4*>(p + 16));
   }
   __device__ static __forceinline__ uint4 pack8(const float (&f)[8], float s, int on) {
     float g[8];
@@ -652,6 +667,11 @@ template <> struct WireCvt<4, 2> {  // bf16 tensor, fp32 wire
   __device__ static __forceinline__ void issue(Raw32* slot, const char* p) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(&slot->a)),
                  "l"(p) : "memory");
+  }
+  __device__ static __forceinline__ void load(Raw32& r, const char* p) {
+    const uint2 h = __ldcs(reinterpret_cast<const uint2*>(p));
+    r.a.x = h.x;
+    r.a.y = h.y;
   }
   __device__ static __forceinline__ uint4 widen4(uint32_t lo2, uint32_t hi2, float s, int on) {
     float f[4] = {bf16lo(lo2), bf16hi(lo2), bf16lo(hi2), bf16hi(hi2)};
@@ -718,7 +738,7 @@ __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& m
       } else {
         cp_async16(&d0->a, me.buf + (v + pv) * 16);
       }
-      if (ADD) cp_async16(slots1 + (j % kPipe) * nthr + tid, me.scratch + (v + pv) * 16);
+      if (ADD) cp_async16(slots1 + (j % kPipe) * nthr + tid, F.scr + (v + pv) * 16);
     }
     cp_async_commit();  // one group per row, possibly empty: keeps wait_group counting uniform
   };
@@ -747,7 +767,7 @@ __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& m
       const uint4 y = slots1[(j % kPipe) * nthr + tid];
       Op::template add_words<4>(reinterpret_cast<uint32_t*>(&x), reinterpret_cast<const uint32_t*>(&y));
     }
-    if (TO_NSCRATCH) *reinterpret_cast<uint4*>(me.nscratch + (v + pv) * 16) = x;
+    if (TO_NSCRATCH) *reinterpret_cast<uint4*>(F.nscr + (v + pv) * 16) = x;
     if (TO_NBUF) *reinterpret_cast<uint4*>(me.nbuf + (v + pv) * 16) = x;
     if (SCATTER) Cvt::put(reinterpret_cast<char*>(sc.d + e * TESZ), left, x);
     if (RSCATTER) Cvt::put(reinterpret_cast<char*>(sc.rd + e * TESZ), left, x);
@@ -811,8 +831,9 @@ __device__ __forceinline__ void slice_range_d(const BufDesc& D, int c, int ch, i
 // only channel ch of the successor ever reads what channel ch writes, and a
 // channel finishes buffer b (all of its own reads) before it starts b+1.  Signal
 // counters continue across buffers (base of buffer b = base + sum of T*K).
-//   N == 1: gather(x)*s -> scatter per slice (the in-place scale).
 //   registered: the all-gather writes final values into the successor's tensors.
+// A launch begins with a handshake (ready flag per channel and epoch) so that no
+// push lands in a receive region the successor's previous launch still reads.
 template <class Op, int TESZ>
 __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_constant__ FusedParams P) {
   extern __shared__ __align__(16) unsigned long long s_dyn[];
@@ -835,7 +856,11 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
     s_pub = 0;
   }
   __syncthreads();
+  if (N == 1) return;  // N = 1 runs solo_kernel
   if (threadIdx.x >= nd) {  // ---- signal warp
+    // handshake: this launch started, so this rank's previous launch has finished with
+    // its receive regions — the predecessor may push (relaxed: the kernel boundary orders it)
+    if (threadIdx.x == nd) st_relaxed_sys(me.pready + ch, R.epoch);
     int total = 0;
     for (int b = 0; b < P.nbuf; ++b)
       if (P.bufs[b].owner < 0 || P.bufs[b].owner == ch) total += T * P.bufs[b].K;
@@ -852,6 +877,7 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
   int i = 0;                         // ring ops published so far (all buffers)
   unsigned long long bbase = base0;  // counter base of the current buffer
   bool first = true;
+  int bpar = 0;  // receive half of this channel's next buffer
   for (int b = 0; b < P.nbuf; ++b) {
     const BufDesc& D = P.bufs[b];
     if (D.owner >= 0 && D.owner != ch) continue;  // a small buffer run by another channel
@@ -859,6 +885,8 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
     const int K = D.K;
     const bool cache = D.nseg <= P.cache_segs;
     if (!first) bar_sync(kBarData, nd);  // every data warp is done with the previous member table
+    // before the first push of the launch: the successor's handshake for this epoch
+    if (first && tid == 0 && !spin_until(me.rflags + ch, R.epoch, R.err, R.timeout_ns)) s_abort = 1;
     first = false;
     if (cache)
       for (int j = tid; j < D.nseg; j += nd) s_vbeg[j] = D.vbeg[j];
@@ -873,21 +901,14 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
     F.scale_on = P.scale_on;
     F.scale = P.scale;
     F.dtype = P.dtype;
+    // Receive halves alternate buffer by buffer on a channel: the predecessor may start
+    // buffer b+1 (its reduce-scatter pushes) while this rank still reads buffer b's last
+    // partials — registered mode has no final scatter to hold it back — but it cannot
+    // start b+2 before this rank's reduce-scatter of b+1, i.e. after b is done here.
+    F.scr = bpar ? me.scratch1 : me.scratch;
+    F.nscr = bpar ? me.nscratch1 : me.nscratch;
+    bpar ^= 1;
     SegCache sc;
-    if (N == 1) {
-      for (int k = 0; k < K; ++k) {
-        unsigned long long lo, hi;
-        slice_range_d(D, 0, cg, k, lo, hi);
-        const unsigned long long tb = tl_d ? globaltimer() : 0;
-        if (hi > lo) fused_slice<Op, kF_SOLO, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1);
-        if (tl_d && tid == 0 && nrec < R.tl_max) {
-          tl_d[2 * nrec] = tb;
-          tl_d[2 * nrec + 1] = globaltimer();
-          ++nrec;
-        }
-      }
-      continue;
-    }
     const int nops = P.registered ? T * K : (T + 1) * K;
     for (int j = 0; j < nops; ++j) {
       int t, k;
@@ -1523,6 +1544,134 @@ cudaError_t launch_ring(const RingParams& p, int dtype, int nch, int nlocal, int
   }
 }
 
+// N == 1: the whole allreduce is gather x (1/N) -> scatter of every member
+// (plus the wire round trip, R14).  A plain HBM stream: no ring, no signals,
+// so none of the fused kernel's machinery — a grid of sm_count x resident
+// CTAs walking tiles of kSoloThreads x U wire vectors.  A tile that lies inside
+// one member with aligned addresses (the common case) issues its U independent
+// 16 B loads from one base pointer; one thread per CTA bulk-prefetches into L2
+// the tile this CTA will reach `pf` grid strides later (cp.async.bulk.prefetch),
+// so the loads mostly hit L2 and in-flight HBM bytes do not cost registers.
+constexpr int kSoloThreads = 256;
+
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+template <class Op, int TESZ>
+__global__ void __launch_bounds__(kSoloThreads) solo_kernel(const __grid_constant__ FusedParams P, int pf) {
+  constexpr int ESZ = Op::kEsz;
+  constexpr int VEL = 16 / ESZ;
+  constexpr int U = TESZ > ESZ ? 4 : 8;  // wider tensor vectors (fp32 tensor, bf16 wire): 32 B each
+  constexpr unsigned long long TILE = (unsigned long long)kSoloThreads * U;
+  using Cvt = WireCvt<ESZ, TESZ>;
+  const unsigned tid = threadIdx.x;
+  for (int b = 0; b < P.nbuf; ++b) {
+    const BufDesc& D = P.bufs[b];
+    FusedCtx F;
+    F.segs = D.segs;
+    F.src = D.src + (size_t)blockIdx.y * D.nseg;
+    F.dst = D.dst + (size_t)blockIdx.y * D.nseg;
+    F.rdst = nullptr;
+    F.vbeg = D.vbeg;
+    F.nseg = D.nseg;
+    F.scale_on = P.scale_on;
+    F.scale = P.scale;
+    F.dtype = P.dtype;
+    SegCache sc, pc;
+    const unsigned long long nvec = (D.L + VEL - 1) / VEL;
+    const unsigned long long gstride = (unsigned long long)gridDim.x * TILE;
+    if (tid == 0 && pf > 0)  // prime: the tiles of the first pf strides
+      for (int k = 1; k < pf; ++k) {
+        const unsigned long long pb = (unsigned long long)blockIdx.x * TILE + k * gstride;
+        if (pb >= nvec) break;
+        seg_lookup<TESZ>(F, pb, pc);
+        const unsigned long long e = pb * VEL;
+        const unsigned long long end = pc.end_el < (pb + TILE) * VEL ? pc.end_el : (pb + TILE) * VEL;
+        const uintptr_t a = (pc.g + e * TESZ) & ~(uintptr_t)15;
+        const uintptr_t z = (pc.g + end * TESZ) & ~(uintptr_t)15;
+        if (z > a) prefetch_l2(reinterpret_cast<const void*>(a), (unsigned)(z - a));
+      }
+    for (unsigned long long base = (unsigned long long)blockIdx.x * TILE; base < nvec; base += gstride) {
+      if (tid == 0 && pf > 0) {
+        const unsigned long long pb = base + (unsigned long long)pf * gstride;
+        if (pb < nvec) {
+          seg_lookup<TESZ>(F, pb, pc);  // the first member piece of that tile (a hint: best effort)
+          const unsigned long long e = pb * VEL;
+          const unsigned long long end = pc.end_el < (pb + TILE) * VEL ? pc.end_el : (pb + TILE) * VEL;
+          const uintptr_t a = (pc.g + e * TESZ) & ~(uintptr_t)15;
+          const uintptr_t z = (pc.g + end * TESZ) & ~(uintptr_t)15;
+          if (z > a) prefetch_l2(reinterpret_cast<const void*>(a), (unsigned)(z - a));
+        }
+      }
+      seg_lookup<TESZ>(F, base, sc);
+      const unsigned long long e0 = base * VEL;
+      const char* g0 = reinterpret_cast<const char*>(sc.g + e0 * TESZ);
+      char* d0 = reinterpret_cast<char*>(sc.d + e0 * TESZ);
+      if ((base + TILE) * VEL <= sc.end_el && base + TILE <= sc.vhi &&
+          ((reinterpret_cast<uintptr_t>(g0) | reinterpret_cast<uintptr_t>(d0)) & 15) == 0) {
+        // whole tile inside one member, aligned: U loads off one pointer, then U stores
+        constexpr unsigned long long VB = (unsigned long long)VEL * TESZ;  // tensor bytes per wire vector
+        const char* gp = g0 + tid * VB;
+        char* dp = d0 + tid * VB;
+        Raw32 raw[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) Cvt::load(raw[u], gp + (unsigned long long)u * kSoloThreads * VB);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          Cvt::put(dp + (unsigned long long)u * kSoloThreads * VB, VEL,
+                   Cvt::take(raw[u], F.scale, F.scale_on, F.dtype));
+        continue;
+      }
+      for (int u = 0; u < U; ++u) {  // member boundary, ragged end or misaligned tensor
+        const unsigned long long v = base + (unsigned long long)u * kSoloThreads + tid;
+        if (v >= nvec) break;
+        seg_lookup<TESZ>(F, v, sc);
+        const unsigned long long e = v * VEL;
+        const unsigned long long left = sc.end_el > e ? sc.end_el - e : 0;
+        if (left == 0) continue;  // padding after a member
+        const char* gp = reinterpret_cast<const char*>(sc.g + e * TESZ);
+        uint4 x;
+        if (Cvt::fast(gp, left)) {
+          Raw32 raw;
+          Cvt::load(raw, gp);
+          x = Cvt::take(raw, F.scale, F.scale_on, F.dtype);
+        } else {
+          x = Cvt::slow(gp, left, F.scale, F.scale_on, F.dtype);
+        }
+        Cvt::put(reinterpret_cast<char*>(sc.d + e * TESZ), left, x);
+      }
+    }
+  }
+}
+
+template <class Op, int TESZ>
+static cudaError_t launch_solo_t(const FusedParams& p, int nlocal, int sm_count, int pf, cudaStream_t s) {
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solo_kernel<Op, TESZ>, kSoloThreads, 0);
+  if (e != cudaSuccess) return e;
+  per_sm = per_sm < 1 ? 1 : per_sm;
+  const int grid = (sm_count * per_sm + nlocal - 1) / nlocal;
+  solo_kernel<Op, TESZ><<<dim3(grid, nlocal), kSoloThreads, 0, s>>>(p, pf);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_solo(const FusedParams& p, int dtype, int nlocal, int sm_count, int pf, cudaStream_t s) {
+  const int td = p.tdtype ? p.tdtype : dtype;
+  if (td == dtype) {
+    switch (dtype) {
+      case 1: return launch_solo_t<OpF32, 4>(p, nlocal, sm_count, pf, s);
+      case 2: return launch_solo_t<OpBF16, 2>(p, nlocal, sm_count, pf, s);
+      case 3: return launch_solo_t<OpI32, 4>(p, nlocal, sm_count, pf, s);
+      case 4: return launch_solo_t<OpI64, 8>(p, nlocal, sm_count, pf, s);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  if (dtype == 2 && td == 1) return launch_solo_t<OpBF16, 4>(p, nlocal, sm_count, pf, s);
+  if (dtype == 1 && td == 2) return launch_solo_t<OpF32, 2>(p, nlocal, sm_count, pf, s);
+  return cudaErrorInvalidValue;
+}
+
 template <class Op, int TESZ>
 static cudaError_t launch_fused_t(const FusedParams& p, int nch, int nlocal, int threads, cudaStream_t s) {
   const size_t smem = (size_t)p.cache_segs * 8 + fused_smem_bytes(kFusedSmemSegs + 1, threads);
@@ -1661,6 +1810,16 @@ cudaError_t launch_ll(const FusedParams& p, int dtype, int nch, int nlocal, cuda
     case 3: return launch_ll_t<OpI32>(p, nch, nlocal, s);
     default: return cudaErrorInvalidValue;
   }
+}
+
+// Co-resident LL CTAs per SM, the minimum over the dtype instantiations.
+cudaError_t ll_max_ctas_per_sm(int* out) {
+  int a = 0, b = 0, c = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, ll_allreduce_kernel<OpF32>, 256, 0);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ll_allreduce_kernel<OpBF16>, 256, 0);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, ll_allreduce_kernel<OpI32>, 256, 0);
+  *out = a < b ? (a < c ? a : c) : (b < c ? b : c);
+  return e;
 }
 
 cudaError_t fused_max_ctas_per_sm(int dtype, int threads, int* out) {

@@ -97,6 +97,8 @@ struct hvd_comm {
   unsigned long long hs_epoch = 0;  // copy-collective handshake epochs issued
   unsigned long long ll_epoch = 0;  // LL launches issued (flag value = epoch)
   int64_t ll_max = (int64_t)kLLMaxBytes;  // HVD_CFG_LL_MAX_BYTES
+  int ll_ctas = 1;                         // co-resident LL CTAs per local rank
+  int solo_pf = 2;                         // HVD_CFG_SOLO_PREFETCH
   int protocol = 1;                 // 0: pull (receiver-initiated TMA loads), 1: push (SM stores)
   unsigned long long pbase[kMaxChannels] = {};  // pull-protocol progress counter bases
   int pull_calls = 0;
@@ -134,15 +136,18 @@ int cuda_fail(cudaError_t e, const char* what) {
 // buffer is `bufsz` = capacity + slack bytes (the slack absorbs the quantum rounding
 // of the channel-private layout).  `cap` arguments below are bufsz.
 constexpr uint64_t kRegionSlack = 2ull << 20;
+// [buf][scratch][pull0][pull1][scratch1][tail][LL]: scratch1 is the second
+// reduce-scatter receive half (a channel alternates halves buffer by buffer).
+constexpr uint64_t kNumBufs = 5;
 char* buf_of(char* region) { return region; }
 char* scratch_of(char* region, uint64_t cap) { return region + cap; }
+char* scratch1_of(char* region, uint64_t cap) { return region + 4 * cap; }
 unsigned long long* flags_of(char* region, uint64_t cap) {
-  return reinterpret_cast<unsigned long long*>(region + 4 * cap);
+  return reinterpret_cast<unsigned long long*>(region + kNumBufs * cap);
 }
 unsigned long long* stats_of(char* region, uint64_t cap) {
-  return reinterpret_cast<unsigned long long*>(region + 4 * cap + kMaxChannels * 8);
+  return reinterpret_cast<unsigned long long*>(region + kNumBufs * cap + kMaxChannels * 8);
 }
-constexpr uint64_t kNumBufs = 4;
 unsigned long long* tail_of(char* region, uint64_t cap) {
   return reinterpret_cast<unsigned long long*>(region + kNumBufs * cap);
 }
@@ -171,6 +176,7 @@ int common_init(hvd_comm* c, uint64_t fusion_bytes) {
     const uint64_t bz = c->bufsz;
     r.buf = buf_of(c->region[l]);
     r.scratch = scratch_of(c->region[l], bz);
+    r.scratch1 = scratch1_of(c->region[l], bz);
     r.flags = flags_of(c->region[l], bz);
     r.stats = stats_of(c->region[l], bz);
     r.rflags = rflags_of(c->region[l], bz);
@@ -182,6 +188,11 @@ int common_init(hvd_comm* c, uint64_t fusion_bytes) {
     r.ll = ll_of(c->region[l], bz);
     r.rank = c->virt ? l : c->rank;
   }
+  int ll_per_sm = 0;
+  CK(ll_max_ctas_per_sm(&ll_per_sm));
+  c->ll_ctas = std::max(1, std::min(ll_per_sm, 4) * c->sm_count / c->nlocal);
+  // LL beats the fenced push up to ~4 MiB at N = 2 and ~8 MiB at N = 4 (profiles/r01_c5_*)
+  c->ll_max = (int64_t)(c->size <= 2 ? kLLMaxBytes : kLLLimitBytes);
   CK(cudaDeviceSynchronize());
   return HVD_OK;
 }
@@ -189,6 +200,7 @@ int common_init(hvd_comm* c, uint64_t fusion_bytes) {
 void set_neighbours(RingRank& r, char* succ_region, char* pred_region, uint64_t cap) {
   r.nbuf = buf_of(succ_region);
   r.nscratch = scratch_of(succ_region, cap);
+  r.nscratch1 = scratch1_of(succ_region, cap);
   r.nflags = flags_of(succ_region, cap);
   r.pready = rflags_of(pred_region, cap);
   r.ppull[0] = pull_of(pred_region, cap, 0);
@@ -482,6 +494,7 @@ int enqueue_ring(hvd_comm* c, uint64_t L, int dtype, cudaStream_t s) {
   int nch = 0;
   int st = make_ring_params(c, L, dtype, false, &P, &nch);
   if (st != HVD_OK) return st;
+  P.epoch = ++c->hs_epoch;
   st = launch_counted(c, HVD_KERNEL_RING, s, [&] { return launch_ring(P, dtype, nch, c->nlocal, c->threads, s); });
   if (st != HVD_OK) return st;
   advance_base(c, P, nch);
@@ -577,7 +590,12 @@ int enqueue_fused_multi(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStrea
     else for (int ch = 0; ch < nch; ++ch) signals[ch] += inc;
   }
   F.cache_segs = maxseg <= kFusedSmemSegs ? (maxseg + 1) / 2 * 2 : 0;
+  if (N == 1) {  // no ring: the in-place gather x (1/N) -> scatter stream (solo_kernel)
+    if (c->tl) c->tl_slices = 0;  // the solo kernel records no timeline
+    return launch_counted(c, HVD_KERNEL_SOLO, s, [&] { return launch_solo(F, dtype, c->nlocal, c->sm_count, c->solo_pf, s); });
+  }
   const int tdt = F.tdtype;
+  F.ring.epoch = ++c->hs_epoch;
   st = launch_counted(c, HVD_KERNEL_FUSED, s, [&] { return launch_fused(F, dtype, nch, c->nlocal, c->threads, s); });
   (void)tdt;
   if (st != HVD_OK) return st;
@@ -608,7 +626,9 @@ int enqueue_ll(hvd_comm* c, DevPlanBuffer& b, cudaStream_t s) {
   if (st != HVD_OK) return st;
   BufDesc& D = F.bufs[0];
   D.q = chunk_len(b.L, N, dtype);
-  nch = (int)std::min<uint64_t>(32, std::max<uint64_t>(1, D.q * esz / (16 << 10)));
+  // one 16 B vector per thread per step where possible (each vector costs a full
+  // NVLink round of polling), at most ll_ctas co-resident CTAs per rank
+  nch = (int)std::min<uint64_t>((uint64_t)c->ll_ctas, std::max<uint64_t>(1, (D.q * esz + 4095) / 4096));
   D.segs = b.pp.segs;
   D.src = b.pp.src;
   D.dst = b.dst ? b.dst : b.pp.src;
@@ -619,13 +639,14 @@ int enqueue_ll(hvd_comm* c, DevPlanBuffer& b, cudaStream_t s) {
   D.slice_el = std::max<uint64_t>(D.ch_el, g);
   D.K = 1;
   D.owner = -1;
-  if ((uint64_t)2 * 2 * (N - 1) * D.q * esz > kLLRegionBytes) return HVD_ERR_INVALID;
+  if ((uint64_t)8 * (N - 1) * D.q * esz > kLLRegionBytes) return HVD_ERR_INVALID;  // 2 par x T x 2 q esz
   F.nbuf = 1;
   F.scale_on = b.pp.scale_on;
   F.scale = b.pp.scale;
   F.dtype = dtype;
   F.tdtype = dtype;
   F.ring.epoch = ++c->ll_epoch;
+  if (c->tl) c->tl_slices = 0;  // the LL kernel records no timeline
   return launch_counted(c, HVD_KERNEL_LL, s, [&] { return launch_ll(F, dtype, nch, c->nlocal, s); });
 }
 
@@ -1228,8 +1249,12 @@ int hvd_set_config(hvd_comm* c, int key, int64_t value) {
       c->fused = (int)value;
       return HVD_OK;
     case HVD_CFG_LL_MAX_BYTES:
-      if (value < 0 || value > (int64_t)kLLMaxBytes) return HVD_ERR_INVALID;
+      if (value < 0 || value > (int64_t)kLLLimitBytes) return HVD_ERR_INVALID;
       c->ll_max = value;
+      return HVD_OK;
+    case HVD_CFG_SOLO_PREFETCH:
+      if (value < 0 || value > 16) return HVD_ERR_INVALID;
+      c->solo_pf = (int)value;
       return HVD_OK;
     case HVD_CFG_MULTI_BUFFERS:
       if (value < 1 || value > kMaxMultiBufs) return HVD_ERR_INVALID;
@@ -1282,6 +1307,7 @@ int64_t hvd_get_config(const hvd_comm* c, int key) {
     case HVD_CFG_PROTOCOL: return c->protocol;
     case HVD_CFG_MULTI_BUFFERS: return c->multi_bufs;
     case HVD_CFG_LL_MAX_BYTES: return c->ll_max;
+    case HVD_CFG_SOLO_PREFETCH: return c->solo_pf;
     case HVD_CFG_FIN_LAG: return c->fin_lag;
     default: return -1;
   }

@@ -94,6 +94,7 @@ CASES = [
     ("tensors", [5, 1 << 20, 12345], "bf16", "average", 64 << 20),
     ("tensors", [5, 1000, 77_777], "i64", "sum", 0),
     ("tensors", [3, 70_001], "i32", "sum", 64 << 20),
+    ("tensors", [3_000_000, 9], "f32", "average", 64 << 20),  # one buffer above the LL limit: fused push
     ("buffer", [16 << 20], "f32", "sum", 0),
     ("buffer", [(1 << 20) + 3], "bf16", "average", 0),
     ("bcast", [5, 1 << 20, 333], "f32", 1, 0),

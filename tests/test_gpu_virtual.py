@@ -177,6 +177,7 @@ def test_tuning_knobs_keep_bits(hvd):
         xs = workloads.all_ranks(counts, "f32", n)
         ref, _, _ = oracle.allreduce(xs, ["f32", "f32"], "average")
         L = hvd._lib
+        comm.set_config(L.HVD_CFG_LL_MAX_BYTES, 0)  # one small buffer: keep it on the fused kernel
         for ch, sl, th in [(1, 256, 64), (7, 4096, 256), (64, 1 << 20, 384), (16, 65536, 128), (256, 512, 96)]:
             comm.set_config(L.HVD_CFG_CHANNELS, ch)
             comm.set_config(L.HVD_CFG_SLICE_BYTES, sl)
@@ -262,6 +263,7 @@ def test_timeline_records_every_slice(hvd):
     try:
         comm.set_config(hvd._lib.HVD_CFG_TIMELINE, 256)
         comm.set_config(hvd._lib.HVD_CFG_PROTOCOL, 1)  # push kernel records
+        comm.set_config(hvd._lib.HVD_CFG_LL_MAX_BYTES, 0)  # the LL kernel records no timeline
         ts = [[torch.randn(1 << 20, device="cuda")] for _ in range(n)]
         comm.allreduce_average(ts)
         torch.cuda.synchronize()
@@ -411,7 +413,8 @@ def test_wire_dtype_variants_bitexact(hvd, n, tdt, wire):
     comm.allreduce(ts, op="average", fusion_threshold=400_000, wire=wire)
     torch.cuda.synchronize()
     assert comm.poll_error() == 0
-    assert comm.kernel_stats()["fused"][0] == 1  # all fusion buffers of the call in one launch
+    # all fusion buffers of the call in one launch (N = 1: the solo stream kernel)
+    assert comm.kernel_stats()["fused" if n > 1 else "solo"][0] == 1
     for r in range(n):
         for k in range(len(counts)):
             assert_same(from_torch(ts[r][k], tdt), ref[r][k], tdt, f"N={n} r={r} k={k}")
@@ -472,7 +475,10 @@ def test_ll_protocol_small_buffers_bitexact(hvd, n):
     epochs/parities reused across back-to-back calls of varying size."""
     comm = comm_for(hvd, n)
     cases = [([1], "f32"), ([3, 5], "bf16"), ([64 * n + 7], "f32"), ([70_001, 13], "i32"),
-             ([100_000, 3, 999], "f32"), ([262_144], "f32"), ([255_000], "bf16")]
+             ([100_000, 3, 999], "f32"), ([262_144], "f32"), ([255_000], "bf16"),
+             ([1_500_001, 17], "f32"), ([2_097_152], "f32"), ([3_000_000], "bf16")]  # LL_MAX raised to 8 MiB
+    ll_default = comm.get_config(hvd._lib.HVD_CFG_LL_MAX_BYTES)
+    comm.set_config(hvd._lib.HVD_CFG_LL_MAX_BYTES, 8 << 20)
     pend = []
     comm.kernel_stats()
     for it, (counts, dt) in enumerate(cases):
@@ -490,6 +496,7 @@ def test_ll_protocol_small_buffers_bitexact(hvd, n):
     torch.cuda.synchronize()
     assert comm.poll_error() == 0
     assert comm.kernel_stats()["ll"][0] == len(cases)
+    comm.set_config(hvd._lib.HVD_CFG_LL_MAX_BYTES, ll_default)
     for item in pend:
         if not isinstance(item, tuple):
             continue
@@ -498,3 +505,29 @@ def test_ll_protocol_small_buffers_bitexact(hvd, n):
         for r in range(n):
             for k in range(len(counts)):
                 assert_same(from_torch(ts[r][k], dt), ref[r][k], dt, f"{dt} {counts} r={r} k={k}")
+
+
+@pytest.mark.parametrize("pf", [0, 2, 7])
+def test_solo_stream_n1(hvd, pf):
+    """N = 1: the solo stream kernel (gather x 1/N -> scatter, no ring) over whole-tile, member
+    boundary, ragged and misaligned cases, at several L2 prefetch distances; same bits."""
+    comm = hvd.init_virtual(1, 0, 64 << 20)
+    try:
+        comm.set_config(hvd._lib.HVD_CFG_SOLO_PREFETCH, pf)
+        counts = [1, 8191, 2048 * 8, 5_000_011, 3, 2048 * 8 * 37 + 5, 262_144]
+        for dt in ("f32", "bf16"):
+            xs = workloads.all_ranks(counts, dt, 1, seed=77)
+            ref, _, plan = oracle.allreduce(xs, [dt] * len(counts), "average")
+            ts = [[to_torch(x, dt) for x in xs[0]]]
+            big = torch.empty(counts[1] + 1, dtype=ts[0][1].dtype, device="cuda")
+            big[1:].copy_(ts[0][1])
+            ts[0][1] = big[1:]  # misaligned member
+            comm.kernel_stats()
+            comm.allreduce(ts, op="average")
+            torch.cuda.synchronize()
+            assert comm.poll_error() == 0
+            assert comm.kernel_stats()["solo"][0] == len(plan) == 1
+            for k in range(len(counts)):
+                assert_same(from_torch(ts[0][k], dt), ref[0][k], dt, f"{dt} k={k}")
+    finally:
+        comm.finalize()

@@ -65,11 +65,16 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--only", default="C2,C3,C4,C5")
     ap.add_argument("--sweep-max-log2", type=int, default=30)
+    ap.add_argument("--sweep-min-log2", type=int, default=10)
+    ap.add_argument("--ll-max", type=int, default=-1, help="HVD_CFG_LL_MAX_BYTES (-1: library default)")
+    ap.add_argument("--no-nccl", action="store_true")
     a = ap.parse_args()
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
     dist.init_process_group("gloo")
     n = dist.get_world_size()
     comm = hvd.init(fusion_bytes=64 * MIB)
+    if a.ll_max >= 0:
+        comm.set_config(hvd._lib.HVD_CFG_LL_MAX_BYTES, a.ll_max)
     ng = dist.new_group(backend="nccl") if n > 1 else None
     res = {"n_gpus": n, "rows": []}
     only = set(a.only.split(","))
@@ -123,15 +128,16 @@ def main():
         for dt in ("f32", "bf16"):
             tdt = torch.float32 if dt == "f32" else torch.bfloat16
             esz = 4 if dt == "f32" else 2
-            for lg in range(10, a.sweep_max_log2 + 1):
+            for lg in range(a.sweep_min_log2, a.sweep_max_log2 + 1):
                 size = 1 << lg
                 cnt = size // esz
                 sets = sets_for([cnt], tdt, size)
                 preps = [comm.prepare(st) for st in sets]
                 iters = a.iters if size <= 256 * MIB else max(3, a.iters // 4)
                 us = timed(lambda i: comm.allreduce_average(preps[i % len(preps)]), iters, nsets=len(preps))
-                row = {"config": "C5", "dtype": dt, "bytes": size, "us": us, "busbw_GBps": bus(size, us, n)}
-                if n > 1:
+                row = {"config": "C5", "dtype": dt, "bytes": size, "us": us, "busbw_GBps": bus(size, us, n),
+                       "ll_max": comm.get_config(hvd._lib.HVD_CFG_LL_MAX_BYTES)}
+                if n > 1 and not a.no_nccl:
                     x = sets[0][0]
                     row["nccl_us"] = timed(lambda i: dist.all_reduce(x, group=ng), iters)
                     row["nccl_busbw_GBps"] = bus(size, row["nccl_us"], n)
