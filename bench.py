@@ -428,7 +428,7 @@ def main():
     ap.add_argument("--registered", type=int, default=1, help="1: registered gradient tensors (zero-copy)")
     ap.add_argument("--sets", type=int, default=0, help="input sets to rotate (0: enough to exceed 2 x L2)")
     ap.add_argument("--config", action="append", default=[], metavar="KEY=VALUE",
-                    help="hvd_set_config before timing, e.g. SOLO_PREFETCH=4 (repeatable)")
+                    help="hvd_set_config before timing, e.g. CHANNELS=64 (repeatable)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

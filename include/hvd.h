@@ -203,8 +203,6 @@ typedef enum {
                                 limit): bounds the NVLink backlog and so the signal latency */
   HVD_CFG_FIN_LAG = 11,      /* fused: slices by which the final local scatter trails the last
                                 all-gather iteration (>= K-1: scatter after all of it)     */
-  HVD_CFG_SOLO_PREFETCH = 15, /* N = 1 (solo stream kernel): L2 bulk-prefetch distance in grid
-                                strides (0..16, default 2; 0 = off)                        */
   HVD_CFG_LL_MAX_BYTES = 14, /* a call that is one fusion buffer of at most this many bytes
                                 (default 4 MiB at N = 2, 8 MiB at N > 2; max 8 MiB; 0 = never)
                                 uses the LL protocol: {epoch, data} words, no fences or

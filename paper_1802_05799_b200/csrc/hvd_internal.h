@@ -177,7 +177,7 @@ constexpr unsigned long long kLLLimitBytes = 8ull << 20;  // largest HVD_CFG_LL_
 constexpr unsigned long long kLLRegionBytes = 8 * kLLLimitBytes + (64ull << 10);
 cudaError_t pull_max_ctas_per_sm(int dtype, int threads, int* out);
 cudaError_t ll_max_ctas_per_sm(int* out);
-cudaError_t launch_solo(const FusedParams& p, int dtype, int nlocal, int sm_count, int pf, cudaStream_t s);
+cudaError_t launch_solo(const FusedParams& p, int dtype, int nlocal, cudaStream_t s);
 cudaError_t fused_max_ctas_per_sm(int dtype, int threads, int* out);
 cudaError_t launch_pack(const PackParams& p, int dtype, int nlocal, int grid, int threads,
                         cudaStream_t s);

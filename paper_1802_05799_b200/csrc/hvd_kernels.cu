@@ -1546,129 +1546,109 @@ cudaError_t launch_ring(const RingParams& p, int dtype, int nch, int nlocal, int
 
 // N == 1: the whole allreduce is gather x (1/N) -> scatter of every member
 // (plus the wire round trip, R14).  A plain HBM stream: no ring, no signals,
-// so none of the fused kernel's machinery — a grid of sm_count x resident
-// CTAs walking tiles of kSoloThreads x U wire vectors.  A tile that lies inside
-// one member with aligned addresses (the common case) issues its U independent
-// 16 B loads from one base pointer; one thread per CTA bulk-prefetches into L2
-// the tile this CTA will reach `pf` grid strides later (cp.async.bulk.prefetch),
-// so the loads mostly hit L2 and in-flight HBM bytes do not cost registers.
-constexpr int kSoloThreads = 256;
-
-__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
+// so none of the fused kernel's machinery.  One CTA per tile of kSoloThreads x U
+// wire vectors over all buffers of the call (the block scheduler balances the
+// tail; a persistent grid-stride walk left the SMs idle 28 % of the kernel in
+// ncu).  A tile inside one member with aligned addresses (the common case)
+// issues its U independent 16 B loads off one pointer, then its U stores.
+constexpr int kSoloThreads = 128;
 
 template <class Op, int TESZ>
-__global__ void __launch_bounds__(kSoloThreads) solo_kernel(const __grid_constant__ FusedParams P, int pf) {
+__global__ void __launch_bounds__(kSoloThreads) solo_kernel(const __grid_constant__ FusedParams P) {
   constexpr int ESZ = Op::kEsz;
   constexpr int VEL = 16 / ESZ;
-  constexpr int U = TESZ > ESZ ? 4 : 8;  // wider tensor vectors (fp32 tensor, bf16 wire): 32 B each
+  constexpr int U = TESZ > ESZ ? 2 : 4;  // wider tensor vectors (fp32 tensor, bf16 wire): 32 B each
   constexpr unsigned long long TILE = (unsigned long long)kSoloThreads * U;
   using Cvt = WireCvt<ESZ, TESZ>;
   const unsigned tid = threadIdx.x;
-  for (int b = 0; b < P.nbuf; ++b) {
-    const BufDesc& D = P.bufs[b];
-    FusedCtx F;
-    F.segs = D.segs;
-    F.src = D.src + (size_t)blockIdx.y * D.nseg;
-    F.dst = D.dst + (size_t)blockIdx.y * D.nseg;
-    F.rdst = nullptr;
-    F.vbeg = D.vbeg;
-    F.nseg = D.nseg;
-    F.scale_on = P.scale_on;
-    F.scale = P.scale;
-    F.dtype = P.dtype;
-    SegCache sc, pc;
-    const unsigned long long nvec = (D.L + VEL - 1) / VEL;
-    const unsigned long long gstride = (unsigned long long)gridDim.x * TILE;
-    if (tid == 0 && pf > 0)  // prime: the tiles of the first pf strides
-      for (int k = 1; k < pf; ++k) {
-        const unsigned long long pb = (unsigned long long)blockIdx.x * TILE + k * gstride;
-        if (pb >= nvec) break;
-        seg_lookup<TESZ>(F, pb, pc);
-        const unsigned long long e = pb * VEL;
-        const unsigned long long end = pc.end_el < (pb + TILE) * VEL ? pc.end_el : (pb + TILE) * VEL;
-        const uintptr_t a = (pc.g + e * TESZ) & ~(uintptr_t)15;
-        const uintptr_t z = (pc.g + end * TESZ) & ~(uintptr_t)15;
-        if (z > a) prefetch_l2(reinterpret_cast<const void*>(a), (unsigned)(z - a));
-      }
-    for (unsigned long long base = (unsigned long long)blockIdx.x * TILE; base < nvec; base += gstride) {
-      if (tid == 0 && pf > 0) {
-        const unsigned long long pb = base + (unsigned long long)pf * gstride;
-        if (pb < nvec) {
-          seg_lookup<TESZ>(F, pb, pc);  // the first member piece of that tile (a hint: best effort)
-          const unsigned long long e = pb * VEL;
-          const unsigned long long end = pc.end_el < (pb + TILE) * VEL ? pc.end_el : (pb + TILE) * VEL;
-          const uintptr_t a = (pc.g + e * TESZ) & ~(uintptr_t)15;
-          const uintptr_t z = (pc.g + end * TESZ) & ~(uintptr_t)15;
-          if (z > a) prefetch_l2(reinterpret_cast<const void*>(a), (unsigned)(z - a));
-        }
-      }
-      seg_lookup<TESZ>(F, base, sc);
-      const unsigned long long e0 = base * VEL;
-      const char* g0 = reinterpret_cast<const char*>(sc.g + e0 * TESZ);
-      char* d0 = reinterpret_cast<char*>(sc.d + e0 * TESZ);
-      if ((base + TILE) * VEL <= sc.end_el && base + TILE <= sc.vhi &&
-          ((reinterpret_cast<uintptr_t>(g0) | reinterpret_cast<uintptr_t>(d0)) & 15) == 0) {
-        // whole tile inside one member, aligned: U loads off one pointer, then U stores
-        constexpr unsigned long long VB = (unsigned long long)VEL * TESZ;  // tensor bytes per wire vector
-        const char* gp = g0 + tid * VB;
-        char* dp = d0 + tid * VB;
-        Raw32 raw[U];
+  unsigned long long t = blockIdx.x;  // -> (buffer b, tile t of b)
+  int b = 0;
+  for (; b < P.nbuf; ++b) {
+    const unsigned long long nt = ((P.bufs[b].L + VEL - 1) / VEL + TILE - 1) / TILE;
+    if (t < nt) break;
+    t -= nt;
+  }
+  if (b == P.nbuf) return;
+  const BufDesc& D = P.bufs[b];
+  FusedCtx F;
+  F.segs = D.segs;
+  F.src = D.src + (size_t)blockIdx.y * D.nseg;
+  F.dst = D.dst + (size_t)blockIdx.y * D.nseg;
+  F.rdst = nullptr;
+  F.vbeg = D.vbeg;
+  F.nseg = D.nseg;
+  F.scale_on = P.scale_on;
+  F.scale = P.scale;
+  F.dtype = P.dtype;
+  SegCache sc;
+  const unsigned long long nvec = (D.L + VEL - 1) / VEL;
+  const unsigned long long base = t * TILE;
+  const unsigned long long t_end = base + TILE < nvec ? base + TILE : nvec;
+  seg_lookup<TESZ>(F, base, sc);
+  const unsigned long long e0 = base * VEL;
+  const char* g0 = reinterpret_cast<const char*>(sc.g + e0 * TESZ);
+  char* d0 = reinterpret_cast<char*>(sc.d + e0 * TESZ);
+  if (t_end * VEL <= sc.end_el && t_end <= sc.vhi &&
+      ((reinterpret_cast<uintptr_t>(g0) | reinterpret_cast<uintptr_t>(d0)) & 15) == 0) {
+    constexpr unsigned long long VB = (unsigned long long)VEL * TESZ;  // tensor bytes per wire vector
+    const char* gp = g0 + tid * VB;
+    char* dp = d0 + tid * VB;
+    const unsigned long long nv = t_end - base;
+    Raw32 raw[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) Cvt::load(raw[u], gp + (unsigned long long)u * kSoloThreads * VB);
+    for (int u = 0; u < U; ++u)
+      if ((unsigned long long)u * kSoloThreads + tid < nv) Cvt::load(raw[u], gp + (unsigned long long)u * kSoloThreads * VB);
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-          Cvt::put(dp + (unsigned long long)u * kSoloThreads * VB, VEL,
-                   Cvt::take(raw[u], F.scale, F.scale_on, F.dtype));
-        continue;
-      }
-      for (int u = 0; u < U; ++u) {  // member boundary, ragged end or misaligned tensor
-        const unsigned long long v = base + (unsigned long long)u * kSoloThreads + tid;
-        if (v >= nvec) break;
-        seg_lookup<TESZ>(F, v, sc);
-        const unsigned long long e = v * VEL;
-        const unsigned long long left = sc.end_el > e ? sc.end_el - e : 0;
-        if (left == 0) continue;  // padding after a member
-        const char* gp = reinterpret_cast<const char*>(sc.g + e * TESZ);
-        uint4 x;
-        if (Cvt::fast(gp, left)) {
-          Raw32 raw;
-          Cvt::load(raw, gp);
-          x = Cvt::take(raw, F.scale, F.scale_on, F.dtype);
-        } else {
-          x = Cvt::slow(gp, left, F.scale, F.scale_on, F.dtype);
-        }
-        Cvt::put(reinterpret_cast<char*>(sc.d + e * TESZ), left, x);
-      }
+    for (int u = 0; u < U; ++u)
+      if ((unsigned long long)u * kSoloThreads + tid < nv)
+        Cvt::put(dp + (unsigned long long)u * kSoloThreads * VB, VEL, Cvt::take(raw[u], F.scale, F.scale_on, F.dtype));
+    return;
+  }
+  for (int u = 0; u < U; ++u) {  // member boundary, ragged end or misaligned tensor
+    const unsigned long long v = base + (unsigned long long)u * kSoloThreads + tid;
+    if (v >= t_end) break;
+    seg_lookup<TESZ>(F, v, sc);
+    const unsigned long long e = v * VEL;
+    const unsigned long long left = sc.end_el > e ? sc.end_el - e : 0;
+    if (left == 0) continue;  // padding after a member
+    const char* gp = reinterpret_cast<const char*>(sc.g + e * TESZ);
+    uint4 x;
+    if (Cvt::fast(gp, left)) {
+      Raw32 raw;
+      Cvt::load(raw, gp);
+      x = Cvt::take(raw, F.scale, F.scale_on, F.dtype);
+    } else {
+      x = Cvt::slow(gp, left, F.scale, F.scale_on, F.dtype);
     }
+    Cvt::put(reinterpret_cast<char*>(sc.d + e * TESZ), left, x);
   }
 }
 
 template <class Op, int TESZ>
-static cudaError_t launch_solo_t(const FusedParams& p, int nlocal, int sm_count, int pf, cudaStream_t s) {
-  int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solo_kernel<Op, TESZ>, kSoloThreads, 0);
-  if (e != cudaSuccess) return e;
-  per_sm = per_sm < 1 ? 1 : per_sm;
-  const int grid = (sm_count * per_sm + nlocal - 1) / nlocal;
-  solo_kernel<Op, TESZ><<<dim3(grid, nlocal), kSoloThreads, 0, s>>>(p, pf);
+static cudaError_t launch_solo_t(const FusedParams& p, int nlocal, cudaStream_t s) {
+  constexpr int VEL = 16 / Op::kEsz;
+  constexpr unsigned long long TILE = (unsigned long long)kSoloThreads * (TESZ > Op::kEsz ? 2 : 4);
+  unsigned long long tiles = 0;
+  for (int b = 0; b < p.nbuf; ++b) tiles += ((p.bufs[b].L + VEL - 1) / VEL + TILE - 1) / TILE;
+  if (tiles == 0) return cudaSuccess;
+  if (tiles > 0x7fffffffull) return cudaErrorInvalidValue;
+  solo_kernel<Op, TESZ><<<dim3((unsigned)tiles, nlocal), kSoloThreads, 0, s>>>(p);
   return cudaGetLastError();
 }
 
-cudaError_t launch_solo(const FusedParams& p, int dtype, int nlocal, int sm_count, int pf, cudaStream_t s) {
+cudaError_t launch_solo(const FusedParams& p, int dtype, int nlocal, cudaStream_t s) {
   const int td = p.tdtype ? p.tdtype : dtype;
   if (td == dtype) {
     switch (dtype) {
-      case 1: return launch_solo_t<OpF32, 4>(p, nlocal, sm_count, pf, s);
-      case 2: return launch_solo_t<OpBF16, 2>(p, nlocal, sm_count, pf, s);
-      case 3: return launch_solo_t<OpI32, 4>(p, nlocal, sm_count, pf, s);
-      case 4: return launch_solo_t<OpI64, 8>(p, nlocal, sm_count, pf, s);
+      case 1: return launch_solo_t<OpF32, 4>(p, nlocal, s);
+      case 2: return launch_solo_t<OpBF16, 2>(p, nlocal, s);
+      case 3: return launch_solo_t<OpI32, 4>(p, nlocal, s);
+      case 4: return launch_solo_t<OpI64, 8>(p, nlocal, s);
       default: return cudaErrorInvalidValue;
     }
   }
-  if (dtype == 2 && td == 1) return launch_solo_t<OpBF16, 4>(p, nlocal, sm_count, pf, s);
-  if (dtype == 1 && td == 2) return launch_solo_t<OpF32, 2>(p, nlocal, sm_count, pf, s);
+  if (dtype == 2 && td == 1) return launch_solo_t<OpBF16, 4>(p, nlocal, s);
+  if (dtype == 1 && td == 2) return launch_solo_t<OpF32, 2>(p, nlocal, s);
   return cudaErrorInvalidValue;
 }
 

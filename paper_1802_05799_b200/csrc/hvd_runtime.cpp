@@ -98,7 +98,6 @@ struct hvd_comm {
   unsigned long long ll_epoch = 0;  // LL launches issued (flag value = epoch)
   int64_t ll_max = (int64_t)kLLMaxBytes;  // HVD_CFG_LL_MAX_BYTES
   int ll_ctas = 1;                         // co-resident LL CTAs per local rank
-  int solo_pf = 2;                         // HVD_CFG_SOLO_PREFETCH
   int protocol = 1;                 // 0: pull (receiver-initiated TMA loads), 1: push (SM stores)
   unsigned long long pbase[kMaxChannels] = {};  // pull-protocol progress counter bases
   int pull_calls = 0;
@@ -592,7 +591,7 @@ int enqueue_fused_multi(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStrea
   F.cache_segs = maxseg <= kFusedSmemSegs ? (maxseg + 1) / 2 * 2 : 0;
   if (N == 1) {  // no ring: the in-place gather x (1/N) -> scatter stream (solo_kernel)
     if (c->tl) c->tl_slices = 0;  // the solo kernel records no timeline
-    return launch_counted(c, HVD_KERNEL_SOLO, s, [&] { return launch_solo(F, dtype, c->nlocal, c->sm_count, c->solo_pf, s); });
+    return launch_counted(c, HVD_KERNEL_SOLO, s, [&] { return launch_solo(F, dtype, c->nlocal, s); });
   }
   const int tdt = F.tdtype;
   F.ring.epoch = ++c->hs_epoch;
@@ -1252,10 +1251,6 @@ int hvd_set_config(hvd_comm* c, int key, int64_t value) {
       if (value < 0 || value > (int64_t)kLLLimitBytes) return HVD_ERR_INVALID;
       c->ll_max = value;
       return HVD_OK;
-    case HVD_CFG_SOLO_PREFETCH:
-      if (value < 0 || value > 16) return HVD_ERR_INVALID;
-      c->solo_pf = (int)value;
-      return HVD_OK;
     case HVD_CFG_MULTI_BUFFERS:
       if (value < 1 || value > kMaxMultiBufs) return HVD_ERR_INVALID;
       c->multi_bufs = (int)value;
@@ -1307,7 +1302,6 @@ int64_t hvd_get_config(const hvd_comm* c, int key) {
     case HVD_CFG_PROTOCOL: return c->protocol;
     case HVD_CFG_MULTI_BUFFERS: return c->multi_bufs;
     case HVD_CFG_LL_MAX_BYTES: return c->ll_max;
-    case HVD_CFG_SOLO_PREFETCH: return c->solo_pf;
     case HVD_CFG_FIN_LAG: return c->fin_lag;
     default: return -1;
   }
