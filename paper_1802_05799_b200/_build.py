@@ -48,7 +48,9 @@ def build(force: bool = False, verbose: bool = False) -> pathlib.Path:
     objs = []
     for src in SOURCES:
         obj = objdir / (src + ".o")
-        cmd = [nvcc, *ARCH, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-c", str(CSRC / src), "-o", str(obj)]
+        # HVD_NVCC_EXTRA: tuning experiments only (e.g. -DHVD_SOLO_U=8); the product build sets none
+        extra = os.environ.get("HVD_NVCC_EXTRA", "").split()
+        cmd = [nvcc, *ARCH, *NVCC_FLAGS, *extra, "-I", str(ROOT / "include"), "-c", str(CSRC / src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)

@@ -1551,13 +1551,20 @@ cudaError_t launch_ring(const RingParams& p, int dtype, int nch, int nlocal, int
 // tail; a persistent grid-stride walk left the SMs idle 28 % of the kernel in
 // ncu).  A tile inside one member with aligned addresses (the common case)
 // issues its U independent 16 B loads off one pointer, then its U stores.
-constexpr int kSoloThreads = 128;
+#ifndef HVD_SOLO_THREADS
+#define HVD_SOLO_THREADS 128
+#endif
+#ifndef HVD_SOLO_U
+#define HVD_SOLO_U 8
+#endif
+constexpr int kSoloThreads = HVD_SOLO_THREADS;
+constexpr int kSoloU = HVD_SOLO_U;  // 16 B wire vectors per thread (same-dtype wire)
 
 template <class Op, int TESZ>
 __global__ void __launch_bounds__(kSoloThreads) solo_kernel(const __grid_constant__ FusedParams P) {
   constexpr int ESZ = Op::kEsz;
   constexpr int VEL = 16 / ESZ;
-  constexpr int U = TESZ > ESZ ? 2 : 4;  // wider tensor vectors (fp32 tensor, bf16 wire): 32 B each
+  constexpr int U = TESZ > ESZ ? (kSoloU + 1) / 2 : kSoloU;  // fp32 tensor, bf16 wire: 32 B of tensor each
   constexpr unsigned long long TILE = (unsigned long long)kSoloThreads * U;
   using Cvt = WireCvt<ESZ, TESZ>;
   const unsigned tid = threadIdx.x;
@@ -1627,7 +1634,7 @@ __global__ void __launch_bounds__(kSoloThreads) solo_kernel(const __grid_constan
 template <class Op, int TESZ>
 static cudaError_t launch_solo_t(const FusedParams& p, int nlocal, cudaStream_t s) {
   constexpr int VEL = 16 / Op::kEsz;
-  constexpr unsigned long long TILE = (unsigned long long)kSoloThreads * (TESZ > Op::kEsz ? 2 : 4);
+  constexpr unsigned long long TILE = (unsigned long long)kSoloThreads * (TESZ > Op::kEsz ? (kSoloU + 1) / 2 : kSoloU);
   unsigned long long tiles = 0;
   for (int b = 0; b < p.nbuf; ++b) tiles += ((p.bufs[b].L + VEL - 1) / VEL + TILE - 1) / TILE;
   if (tiles == 0) return cudaSuccess;

@@ -37,6 +37,13 @@ def main():
     rows = []
     us = timeit(lambda i: comm.allreduce_average(regs[i]), nsets)
     rows.append({"variant": "hvd solo", "us": us})
+    comm.set_config(hvd._lib.HVD_CFG_PROFILE, 1)
+    comm.kernel_stats()
+    us = timeit(lambda i: comm.allreduce_average(regs[i]), nsets)
+    ks = comm.kernel_stats()
+    comm.set_config(hvd._lib.HVD_CFG_PROFILE, 0)
+    rows.append({"variant": "hvd solo, HVD_CFG_PROFILE=1 (events around each launch)", "us": us,
+                 "kernel_avg_us": ks["solo"][1] / ks["solo"][0] * 1e3})
     rows.append({"variant": "torch x.mul_(1.0)", "us": timeit(lambda i: xs[i].mul_(1.0), nsets)})
     rows.append({"variant": "torch y.copy_(x)", "us": timeit(lambda i: ys[i].copy_(xs[i]), nsets)})
     rows.append({"variant": "torch x.mul_(1.0) warm (1 set)", "us": timeit(lambda i: xs[0].mul_(1.0), 1)})
