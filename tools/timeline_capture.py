@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--out", default="gpurun_out/timeline.json")
     ap.add_argument("--channels", type=int, default=0)
     ap.add_argument("--slice-kib", type=int, default=0)
+    ap.add_argument("--registered", action="store_true", help="registered tensor (the bench's path)")
     a = ap.parse_args()
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
     dist.init_process_group("gloo")
@@ -33,11 +34,12 @@ def main():
         comm.set_config(L.HVD_CFG_SLICE_BYTES, a.slice_kib << 10)
     comm.set_config(L.HVD_CFG_TIMELINE, 1024)
     x = torch.randn((a.mib << 20) // 4, device="cuda")
+    h = comm.register([x]) if a.registered else [x]
     for _ in range(5):
-        comm.allreduce_average([x])
+        comm.allreduce_average(h)
     torch.cuda.synchronize()
     dist.barrier()
-    comm.allreduce_average([x])
+    comm.allreduce_average(h)
     torch.cuda.synchronize()
     tl = comm.timeline()
     allt = [None] * dist.get_world_size()
