@@ -39,6 +39,7 @@ def main():
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--out", default="gpurun_out/sweep.json")
     ap.add_argument("--nccl", action="store_true")
+    ap.add_argument("--ll-max", type=int, default=-1, help="HVD_CFG_LL_MAX_BYTES (-1: library default)")
     ap.add_argument("--mode", default="ring", choices=["ring", "fused", "three", "registered"],
                     help="ring: hvd_allreduce_buffer; fused/three: hvd_allreduce_average of one tensor")
     a = ap.parse_args()
@@ -57,6 +58,8 @@ def main():
              for mib in a.mib}
     comm.set_config(L.HVD_CFG_FUSED, (1 if a.mode in ("fused", "registered") else 0) if a.fused < 0 else a.fused)
     comm.set_config(L.HVD_CFG_PROTOCOL, a.protocol)
+    if a.ll_max >= 0:
+        comm.set_config(L.HVD_CFG_LL_MAX_BYTES, a.ll_max)
 
     regs = {mib: comm.register([grads[mib]]) for mib in a.mib} if a.mode == "registered" else {}
 
