@@ -275,6 +275,54 @@ int hvd_plan(const uint64_t* counts, const int32_t* dtypes, int n, uint64_t fusi
  * ("chunks of the data buffer"; R2): out[0..size] boundaries. */
 int hvd_chunk_bounds(uint64_t length, int size, int dtype, uint64_t* out);
 
+/* ---------------------------------------------------------------- readiness negotiation
+ * Tensor Fusion step 1, "Determine which tensors are ready to be reduced" and
+ * step 6, "Repeat until there are no more tensors to reduce in the cycle"
+ * (P:L366).  The paper does not say how ranks agree on readiness;
+ * DESIGN.md R15 takes SPEC's reading: a tensor is globally ready
+ * when every rank has reported it; globally ready tensors are reduced in rank
+ * 0's submission order; the others stay pending for a later cycle.
+ *
+ * Host-only control plane (no GPU needed).  Tensors are named by dense ids
+ * 0..max_tensors-1 (e.g. registration order).  Ranks of one node share a POSIX
+ * shared-memory segment `shm_name` ("/name"; created by rank 0, opened by the
+ * others, retried until it exists): per rank and cycle parity, the ordered
+ * pending list {id, dtype, count}.  A cycle publishes this process's lists, waits
+ * until every rank has published the same cycle, and intersects — every rank
+ * computes the same answer, so no coordinator round trip is needed.  Parities
+ * alternate: a rank cannot overwrite cycle k's list before every rank has
+ * finished reading it (it must first see all ranks publish cycle k+1).
+ * shm_name == NULL: process-private segment for `nlocal` ranks rank..rank+nlocal-1
+ * of a virtual communicator (hvd_init_virtual); otherwise nlocal must be 1. */
+typedef struct hvd_negotiator hvd_negotiator;
+/* Errors: INVALID (arguments), TIMEOUT (segment never appeared), UNSUPPORTED (shm). */
+int hvd_negotiator_create(const char* shm_name, int rank, int size, int nlocal, uint32_t max_tensors,
+                          uint64_t timeout_ms, hvd_negotiator** out);
+/* Mark tensor `id` ready on local rank `local` (count elements of dtype); it joins
+ * the end of that rank's pending list.  Errors: INVALID (id out of range, already
+ * pending, bad dtype). */
+int hvd_negotiator_ready(hvd_negotiator* g, int local, uint32_t id, uint64_t count, int dtype);
+/* One negotiation cycle (collective over all ranks): ids_out[0..*n_out) = the
+ * globally ready ids in rank 0's submission order, removed from every rank's
+ * pending list.  ids_out has room for max_tensors ids.  Errors: TIMEOUT (a rank
+ * did not publish within timeout_ms), INVALID (the same id reported with a
+ * different dtype or count by two ranks: the protocol error of S:L299; the id is
+ * returned in *n_out). */
+int hvd_negotiator_cycle(hvd_negotiator* g, uint32_t* ids_out, uint32_t* n_out);
+/* Pending ids of local rank `local` (in submission order; ids_out may be NULL). */
+int hvd_negotiator_pending(const hvd_negotiator* g, int local, uint32_t* ids_out, uint32_t* n_out);
+/* Unmap (rank 0 also unlinks the segment).  Idempotent on NULL. */
+int hvd_negotiator_destroy(hvd_negotiator* g);
+
+/* One cycle, then the allreduce of the agreed tensors (P:L366-373 in full):
+ * tensors[l * n + id] is local rank l's tensor `id` (n = the id space used);
+ * the agreed ids (ids_out, capacity n) are reduced in that order through the
+ * same Tensor Fusion plan and ring as hvd_allreduce.  Errors: those of
+ * hvd_negotiator_cycle and hvd_allreduce; INVALID if an agreed tensor's count or
+ * dtype differs from what was reported ready. */
+int hvd_allreduce_negotiated(hvd_comm* c, hvd_negotiator* g, const hvd_tensor* tensors, uint32_t n, int op,
+                             uint64_t fusion_threshold, void* stream, uint32_t* ids_out, uint32_t* n_out);
+
 #ifdef __cplusplus
 }
 #endif

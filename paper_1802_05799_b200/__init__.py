@@ -177,6 +177,18 @@ class Comm:
               "hvd_allreduce_average")
         return tensors
 
+    def allreduce_negotiated(self, neg: "Negotiator", tensors, op: str = "average",
+                             fusion_threshold: int = DEFAULT_FUSION_BYTES, stream=None):
+        """One negotiation cycle, then the allreduce of the tensors ready on every rank
+        (P:L366-373).  ``tensors``: indexed by id (a virtual comm: per-rank lists); returns
+        the ids reduced, in order."""
+        arr, n = self._marshal(tensors)
+        ids = (C.c_uint32 * max(1, n))()
+        m = C.c_uint32(0)
+        check(lib.hvd_allreduce_negotiated(self._h, neg._h, arr, n, _OPS[op], int(fusion_threshold),
+                                           _stream_handle(stream), ids, C.byref(m)), "hvd_allreduce_negotiated")
+        return list(ids[:m.value])
+
     def allreduce_buffer(self, count: int, dtype: int = HVD_FLOAT32, op: str = "sum", stream=None):
         """Raw ring on the registered fusion buffer (headline measurement)."""
         check(lib.hvd_allreduce_buffer(self._h, int(count), int(dtype), _OPS[op], _stream_handle(stream)),
@@ -302,6 +314,60 @@ def chunk_bounds(length, size, dtype):
     check(lib.hvd_chunk_bounds(int(length), int(size), _DT_CODE[dtype] if isinstance(dtype, str) else dtype, out),
           "hvd_chunk_bounds")
     return list(out)
+
+
+class Negotiator:
+    """Readiness negotiation ("Determine which tensors are ready"; R15):
+    ``ready(id)`` as tensors become ready, ``cycle()`` (collective) returns the ids ready on
+    every rank, in rank 0's submission order.  Host-only (``hvd_negotiator_*``)."""
+
+    def __init__(self, shm_name, rank: int, size: int, nlocal: int = 1, max_tensors: int = 4096,
+                 timeout_ms: int = 60000):
+        h = C.c_void_p()
+        nm = shm_name.encode() if shm_name else None
+        check(lib.hvd_negotiator_create(nm, int(rank), int(size), int(nlocal), int(max_tensors), int(timeout_ms),
+                                        C.byref(h)), "hvd_negotiator_create")
+        self._h, self.size, self.nlocal, self.max_tensors = h, size, nlocal, max_tensors
+        self._ids = (C.c_uint32 * max_tensors)()
+
+    def ready(self, tid: int, count: int, dtype, local: int = 0):
+        code = _DT_CODE[dtype] if isinstance(dtype, str) else (dtype if isinstance(dtype, int) else _dtype_code(dtype))
+        check(lib.hvd_negotiator_ready(self._h, int(local), int(tid), int(count), code), "hvd_negotiator_ready")
+
+    def ready_tensor(self, tid: int, t, local: int = 0):
+        self.ready(tid, t.numel(), _dtype_code(t), local)
+
+    def cycle(self):
+        n = C.c_uint32(0)
+        check(lib.hvd_negotiator_cycle(self._h, self._ids, C.byref(n)), "hvd_negotiator_cycle")
+        return list(self._ids[:n.value])
+
+    def pending(self, local: int = 0):
+        n = C.c_uint32(0)
+        check(lib.hvd_negotiator_pending(self._h, int(local), self._ids, C.byref(n)), "hvd_negotiator_pending")
+        return list(self._ids[:n.value])
+
+    def close(self):
+        if self._h:
+            lib.hvd_negotiator_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def negotiator(comm: "Comm", max_tensors: int = 4096, timeout_ms: int = 60000, group=None) -> Negotiator:
+    """A negotiator for ``comm``'s ranks: a process-private one for a virtual comm, else a
+    shared-memory segment named by rank 0 and passed over ``group`` (one node)."""
+    if comm.local_ranks > 1 or comm.size == 1:
+        return Negotiator(None, 0, comm.size, comm.local_ranks, max_tensors, timeout_ms)
+    import torch.distributed as dist
+    name = [f"/hvd_neg_{os.getpid()}_{os.urandom(4).hex()}" if comm.rank == 0 else None]
+    dist.broadcast_object_list(name, src=0, group=group)
+    return Negotiator(name[0], comm.rank, comm.size, 1, max_tensors, timeout_ms)
 
 
 def init_virtual(size: int, device: int = 0, fusion_bytes: int = DEFAULT_FUSION_BYTES) -> Comm:

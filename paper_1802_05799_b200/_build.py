@@ -15,8 +15,8 @@ PKG = pathlib.Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libhvd_b200.so"
-SOURCES = ["hvd_kernels.cu", "hvd_runtime.cpp", "hvd_plan.cpp"]
-HEADERS = ["hvd_internal.h", "hvd_plan.h"]
+SOURCES = ["hvd_kernels.cu", "hvd_runtime.cpp", "hvd_plan.cpp", "hvd_negotiate.cpp"]
+HEADERS = ["hvd_internal.h", "hvd_plan.h", "hvd_negotiate.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # -fmad=false: no FMA contraction anywhere (bit parity with the oracle, SURVEY §7 hard part 5)

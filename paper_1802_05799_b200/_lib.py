@@ -108,6 +108,14 @@ def _load():
         "hvd_chunk_bounds": (C.c_int, [C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_uint64)]),
         "hvd_kernel_stats": (C.c_int, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_double)]),
         "hvd_timeline": (C.c_int, [P, C.c_int, C.POINTER(C.c_uint64), C.c_uint64, C.POINTER(hvd_timeline_info)]),
+        "hvd_negotiator_create": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_uint32, C.c_uint64,
+                                            C.POINTER(P)]),
+        "hvd_negotiator_ready": (C.c_int, [P, C.c_int, C.c_uint32, C.c_uint64, C.c_int]),
+        "hvd_negotiator_cycle": (C.c_int, [P, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
+        "hvd_negotiator_pending": (C.c_int, [P, C.c_int, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
+        "hvd_negotiator_destroy": (C.c_int, [P]),
+        "hvd_allreduce_negotiated": (C.c_int, [P, P, C.POINTER(hvd_tensor), C.c_uint32, C.c_int, C.c_uint64, P,
+                                               C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -125,7 +133,8 @@ EXPORTS = sorted([
     "hvd_fusion_buffer", "hvd_fusion_capacity", "hvd_broadcast", "hvd_allgather", "hvd_poll_error",
     "hvd_strerror", "hvd_traffic", "hvd_set_config", "hvd_get_config", "hvd_plan", "hvd_chunk_bounds",
     "hvd_kernel_stats", "hvd_timeline", "hvd_allreduce_ex", "hvd_register_blob", "hvd_register",
-    "hvd_allreduce_registered", "hvd_deregister",
+    "hvd_allreduce_registered", "hvd_deregister", "hvd_negotiator_create", "hvd_negotiator_ready",
+    "hvd_negotiator_cycle", "hvd_negotiator_pending", "hvd_negotiator_destroy", "hvd_allreduce_negotiated",
 ])
 
 

@@ -19,6 +19,7 @@
 #include "../../include/hvd.h"
 #include "hvd_internal.h"
 #include "hvd_plan.h"
+#include "hvd_negotiate.h"
 
 using namespace hvd;
 
@@ -1006,6 +1007,39 @@ int hvd_allreduce_registered(hvd_comm* c, int reg_id, int op, uint64_t fusion_th
   const Registration& R = c->regs[reg_id];
   return do_allreduce(c, R.own.data(), R.n, op, fusion_threshold, static_cast<cudaStream_t>(stream), 0,
                       c->size > 1 ? &R : nullptr);
+}
+
+int hvd_allreduce_negotiated(hvd_comm* c, hvd_negotiator* g, const hvd_tensor* tensors, uint32_t n, int op,
+                             uint64_t fusion_threshold, void* stream, uint32_t* ids_out, uint32_t* n_out) {
+  int st = check_live(c);
+  if (st != HVD_OK) return st;
+  if (!g || !ids_out || !n_out || (n > 0 && !tensors)) return HVD_ERR_INVALID;
+  if (hvd_neg::size_of(g) != c->size || hvd_neg::nlocal_of(g) != c->nlocal) return HVD_ERR_INVALID;
+  std::vector<uint32_t> ids(hvd_neg::max_of(g));
+  uint32_t m = 0;
+  st = hvd_negotiator_cycle(g, ids.data(), &m);  // step 1: what is ready on every rank
+  if (st != HVD_OK) {
+    *n_out = m;
+    return st;
+  }
+  std::vector<hvd_tensor> list((size_t)c->nlocal * m);
+  for (uint32_t i = 0; i < m; ++i) {
+    uint32_t id = 0;
+    uint64_t count = 0;
+    int dtype = 0;
+    hvd_neg::agreed_meta(g, i, &id, &count, &dtype);
+    if (id >= n) return HVD_ERR_INVALID;
+    for (int l = 0; l < c->nlocal; ++l) {
+      const hvd_tensor& t = tensors[(size_t)l * n + id];
+      if (t.count != count || t.dtype != dtype) return HVD_ERR_INVALID;
+      list[(size_t)l * m + i] = t;
+    }
+    ids_out[i] = id;
+  }
+  *n_out = m;
+  if (m == 0) return HVD_OK;
+  // steps 2-6 on the agreed tensors, in rank 0's submission order
+  return do_allreduce(c, list.data(), (int)m, op, fusion_threshold, static_cast<cudaStream_t>(stream));
 }
 
 int hvd_deregister(hvd_comm* c, int reg_id) {

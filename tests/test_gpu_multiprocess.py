@@ -5,6 +5,7 @@ collective on its seeded inputs; the parent compares every rank's output with
 the oracle element by element and checks cross-rank bitwise agreement.
 """
 import os
+import random
 import socket
 
 import numpy as np
@@ -57,6 +58,20 @@ def _worker(rank, world, port, cases, q, protocol):
                     torch.cuda.synchronize()
                     res_its.append([from_torch(t, "f32") for t in ts])
                 out.append(res_its)
+            elif kind == "negotiated":
+                # every rank reports the same ids in its own order over 3 cycles (R15)
+                g = hvd.negotiator(comm, max_tensors=64)
+                ts = [to_torch(workloads.rank_tensor(c, dtype, rank, k, "normal"), dtype) for k, c in enumerate(counts)]
+                order = list(range(len(counts)))
+                random.Random(1000 + rank).shuffle(order)
+                got_ids = []
+                for cyc in range(3):
+                    for tid in order[cyc::3]:
+                        g.ready(tid, counts[tid], dtype)
+                    got_ids.append(comm.allreduce_negotiated(g, ts, op="average", fusion_threshold=thr))
+                torch.cuda.synchronize()
+                g.close()
+                out.append([[from_torch(t, dtype) for t in ts], got_ids])
             elif kind == "bcast":
                 xs = [workloads.rank_tensor(c, dtype, rank, k, "specials") for k, c in enumerate(counts)]
                 ts = [to_torch(x, dtype) for x in xs]
@@ -98,6 +113,7 @@ CASES = [
     ("buffer", [16 << 20], "f32", "sum", 0),
     ("buffer", [(1 << 20) + 3], "bf16", "average", 0),
     ("bcast", [5, 1 << 20, 333], "f32", 1, 0),
+    ("negotiated", [5, 1 << 20, 333, 70_001, 2_000_003, 17, 4096], "f32", None, 4 << 20),
     ("registered", [17, 3_000_001, 64, 500_000], "f32", "average", 8 << 20),
     ("allgather", [100_003], "f32", None, 0),
     ("allgather", [8_000_001], "bf16", None, 0),
@@ -133,6 +149,26 @@ def test_multiprocess_ring_matches_oracle(protocol):
                 for r in range(n):
                     for k in range(len(counts)):
                         assert_same(res[r][0][ci][it][k], ref[r][k], "f32", f"registered it={it} r={r} k={k}")
+        elif kind == "negotiated":
+            from oracle import negotiation as neg
+            reports = [[[] for _ in range(n)] for _ in range(3)]
+            for r in range(n):
+                order = list(range(len(counts)))
+                random.Random(1000 + r).shuffle(order)
+                for cyc in range(3):
+                    reports[cyc][r] = [(t, 1, counts[t]) for t in order[cyc::3]]
+            expect = neg.simulate(reports)
+            xs = [[workloads.rank_tensor(c, dtype, r, k, "normal") for k, c in enumerate(counts)] for r in range(n)]
+            for r in range(n):
+                assert res[r][0][ci][1] == expect
+            for ids in expect:
+                if not ids:
+                    continue
+                ref, _, _ = oracle.allreduce([[xs[r][i] for i in ids] for r in range(n)], [dtype] * len(ids),
+                                             "average", threshold=thr)
+                for r in range(n):
+                    for j, i in enumerate(ids):
+                        assert_same(res[r][0][ci][0][i], ref[r][j], dtype, f"negotiated id {i} rank {r}")
         elif kind == "bcast":
             xs = [[workloads.rank_tensor(c, dtype, r, k, "specials") for k, c in enumerate(counts)] for r in range(n)]
             ref, _ = oracle.broadcast(xs, op)

@@ -529,3 +529,52 @@ def test_solo_stream_n1(hvd):
                 assert_same(from_torch(ts[0][k], dt), ref[0][k], dt, f"{dt} k={k}")
     finally:
         comm.finalize()
+
+
+@pytest.mark.parametrize("n", [2, 3, 4])
+def test_negotiated_allreduce_cycles(hvd, n):
+    """Readiness negotiation + Tensor Fusion (R15): each cycle reduces exactly the
+    tensors every rank has reported, in rank 0's submission order (which fixes the fusion plan),
+    bit-exact; the others stay untouched until their cycle."""
+    import random
+    from oracle import negotiation as neg
+    comm = comm_for(hvd, n)
+    g = hvd.negotiator(comm, max_tensors=32)
+    try:
+        rng = random.Random(55 + n)
+        counts = [rng.choice([1, 7, 1000, 4096, 70_001, 262_144]) for _ in range(12)]
+        xs = workloads.all_ranks(counts, "f32", n, seed=66)
+        ts = [[to_torch(x, "f32") for x in xs[r]] for r in range(n)]
+        reports = [[[] for _ in range(n)] for _ in range(4)]
+        for t in range(len(counts)):
+            for r in range(n):
+                if t == 11 and r == n - 1:
+                    continue  # never reported by the last rank: never reduced
+                reports[rng.randrange(4)][r].append((t, 1, counts[t]))
+        for c in range(4):
+            for r in range(n):
+                rng.shuffle(reports[c][r])
+        expect = neg.simulate(reports)
+        done = set()
+        for c in range(4):
+            for r in range(n):
+                for tid, dt, cnt in reports[c][r]:
+                    g.ready(tid, cnt, "f32", local=r)
+            ids = comm.allreduce_negotiated(g, ts, op="average", fusion_threshold=1 << 20)
+            torch.cuda.synchronize()
+            assert comm.poll_error() == 0
+            assert ids == expect[c]
+            if ids:
+                ref, _, _ = oracle.allreduce([[xs[r][i] for i in ids] for r in range(n)], ["f32"] * len(ids),
+                                             "average", threshold=1 << 20)
+                for r in range(n):
+                    for j, i in enumerate(ids):
+                        assert_same(from_torch(ts[r][i], "f32"), ref[r][j], "f32", f"cycle {c} id {i} r={r}")
+            done |= set(ids)
+            for r in range(n):
+                for i in range(len(counts)):
+                    if i not in done:
+                        assert_same(from_torch(ts[r][i], "f32"), xs[r][i], "f32", f"pending id {i}")
+        assert 11 not in done and g.pending(0) == [11]
+    finally:
+        g.close()
