@@ -50,10 +50,20 @@ def _tensor_array(tensors):
     return arr
 
 
+_RAW_STREAM = None
+
+
 def _stream_handle(stream):
-    import torch
-    s = torch.cuda.current_stream() if stream is None else stream
-    return C.c_void_p(s.cuda_stream)
+    """The caller's stream (default: torch's current stream on the current device)."""
+    global _RAW_STREAM
+    if stream is not None:
+        return C.c_void_p(stream.cuda_stream)
+    if _RAW_STREAM is None:
+        import torch
+        raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)  # ~0.3 us vs ~3 us for current_stream()
+        _RAW_STREAM = (lambda: raw(torch.cuda.current_device())) if raw else \
+            (lambda: torch.cuda.current_stream().cuda_stream)
+    return C.c_void_p(_RAW_STREAM())
 
 
 _OPS = {"sum": HVD_SUM, "average": HVD_AVERAGE}

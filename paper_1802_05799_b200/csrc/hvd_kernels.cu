@@ -702,10 +702,22 @@ template <> struct WireCvt<4, 2> {  // bf16 tensor, fp32 wire
 
 // One slice [lo, hi) of the fused kernel by the data threads.  Row j of the
 // slice is vector v = v_lo + j*nthr + tid.  slots0/slots1: [kPipe][nthr] uint4.
+// Handshake to complete inside a slice (the launch's first remote push): the
+// slice's first loads are issued, then the leader waits for the successor's
+// ready flag while they fly.
+struct Handshake {
+  const unsigned long long* flag;  // nullptr: none
+  unsigned long long epoch;
+  int* err;
+  unsigned long long timeout_ns;
+  int* abort;                      // shared abort flag of the CTA
+};
+
 template <class Op, int KIND, int TESZ = Op::kEsz>
 __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& me, unsigned long long lo,
                                             unsigned long long hi, unsigned tid, unsigned nthr, SegCache& sc,
-                                            Raw32* slots0, uint4* slots1, long long pv = 0) {
+                                            Raw32* slots0, uint4* slots1, long long pv = 0,
+                                            const Handshake* hs = nullptr) {
   // pv: shift from a buffer vector index to its slot in the channel-private layout of
   // the scratch / fusion-buffer regions (0: buffer order)
   constexpr int ESZ = Op::kEsz;  // wire element size
@@ -722,8 +734,8 @@ __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& m
   constexpr bool TO_NBUF = KIND == kF_AG0 || KIND == kF_AG || KIND == kF_G2B || KIND == kF_G2BS;
   const unsigned long long v_lo = lo / VEL;
   const unsigned long long v_hi = (hi + VEL - 1) / VEL;
-  if (v_hi <= v_lo + tid) return;
-  const int rows = (int)((v_hi - v_lo - tid + nthr - 1) / nthr);  // rows this thread owns
+  if (!hs && v_hi <= v_lo + tid) return;  // (with a handshake every thread reaches its barrier)
+  const int rows = v_hi <= v_lo + tid ? 0 : (int)((v_hi - v_lo - tid + nthr - 1) / nthr);  // rows this thread owns
   SegCache ci = sc;  // issue-side cache (runs kPipe-1 rows ahead of the consume side)
   auto issue = [&](int j) {
     if (j < rows) {
@@ -744,7 +756,13 @@ __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& m
   };
 #pragma unroll
   for (int j = 0; j < kPipe - 1; ++j) issue(j);
-  for (int j = 0; j < rows; ++j) {
+  int nrows = rows;
+  if (hs) {
+    if (tid == 0 && !spin_until(hs->flag, hs->epoch, hs->err, hs->timeout_ns)) *(volatile int*)hs->abort = 1;
+    bar_sync(kBarData, nthr);
+    if (*(volatile int*)hs->abort) nrows = 0;
+  }
+  for (int j = 0; j < nrows; ++j) {
     issue(j + kPipe - 1);
     cp_async_wait<kPipe - 1>();  // row j has landed in this thread's slots
     const unsigned long long v = v_lo + (unsigned long long)j * nthr + tid;
@@ -878,6 +896,10 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
   unsigned long long bbase = base0;  // counter base of the current buffer
   bool first = true;
   int bpar = 0;  // receive half of this channel's next buffer
+  // the launch's first remote push waits for the successor's handshake (inside the slice,
+  // after its first loads are issued)
+  const Handshake hs0 = {me.rflags + ch, R.epoch, R.err, R.timeout_ns, &s_abort};
+  bool hs_pending = true;
   for (int b = 0; b < P.nbuf; ++b) {
     const BufDesc& D = P.bufs[b];
     if (D.owner >= 0 && D.owner != ch) continue;  // a small buffer run by another channel
@@ -885,8 +907,6 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
     const int K = D.K;
     const bool cache = D.nseg <= P.cache_segs;
     if (!first) bar_sync(kBarData, nd);  // every data warp is done with the previous member table
-    // before the first push of the launch: the successor's handshake for this epoch
-    if (first && tid == 0 && !spin_until(me.rflags + ch, R.epoch, R.err, R.timeout_ns)) s_abort = 1;
     first = false;
     if (cache)
       for (int j = tid; j < D.nseg; j += nd) s_vbeg[j] = D.vbeg[j];
@@ -935,17 +955,22 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
       }
       const unsigned long long tb = tl_d ? globaltimer() : 0;
       if (hi > lo && !s_abort) {
+        const Handshake* hs = nullptr;
+        if (hs_pending && t < T) {  // every op but the final local scatter pushes
+          hs = &hs0;
+          hs_pending = false;
+        }
         if (P.registered) {
-          if (rs && s == 0) fused_slice<Op, kF_RS0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv);
-          else if (rs) fused_slice<Op, kF_RS, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv);
-          else if (s == 0) fused_slice<Op, kF_RAG0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv);
-          else fused_slice<Op, kF_RAG, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv);
+          if (rs && s == 0) fused_slice<Op, kF_RS0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs);
+          else if (rs) fused_slice<Op, kF_RS, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs);
+          else if (s == 0) fused_slice<Op, kF_RAG0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs);
+          else fused_slice<Op, kF_RAG, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs);
         } else {
           if (t == T) fused_slice<Op, kF_FIN, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv);
-          else if (rs && s == 0) fused_slice<Op, kF_RS0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv);
-          else if (rs) fused_slice<Op, kF_RS, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv);
-          else if (s == 0) fused_slice<Op, kF_AG0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv);
-          else fused_slice<Op, kF_AG, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv);
+          else if (rs && s == 0) fused_slice<Op, kF_RS0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs);
+          else if (rs) fused_slice<Op, kF_RS, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs);
+          else if (s == 0) fused_slice<Op, kF_AG0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs);
+          else fused_slice<Op, kF_AG, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs);
         }
         if (t < T) sent += (hi - lo) * Op::kEsz;
       }
