@@ -275,6 +275,17 @@ int hvd_plan(const uint64_t* counts, const int32_t* dtypes, int n, uint64_t fusi
  * ("chunks of the data buffer"; R2): out[0..size] boundaries. */
 int hvd_chunk_bounds(uint64_t length, int size, int dtype, uint64_t* out);
 
+/* Allreduce of `count` elements held in HOST memory (pinned for overlap):
+ * in[l] -> out[l] for each local rank l (in and out may alias).  The buffer is
+ * cut into chunks of `chunk_bytes` (0 = 8 MiB); chunk i is copied to the device
+ * on one copy stream, reduced on `stream` exactly as hvd_allreduce reduces one
+ * tensor (so same bits), and copied back on another copy stream while chunk
+ * i+1 is copied in: PCIe in, the ring and PCIe out overlap (3 device staging
+ * slots, library-owned).  Completion: `stream`.  Host buffers must stay valid
+ * until then.  Errors: INVALID, UNSUPPORTED (dtype / AVERAGE on integers), CUDA. */
+int hvd_allreduce_host(hvd_comm* c, const void* const* in, void* const* out, uint64_t count, int dtype, int op,
+                       uint64_t chunk_bytes, void* stream);
+
 /* ---------------------------------------------------------------- readiness negotiation
  * Tensor Fusion step 1, "Determine which tensors are ready to be reduced" and
  * step 6, "Repeat until there are no more tensors to reduce in the cycle"

@@ -199,6 +199,24 @@ class Comm:
                                            _stream_handle(stream), ids, C.byref(m)), "hvd_allreduce_negotiated")
         return list(ids[:m.value])
 
+    def allreduce_host(self, inputs, outputs=None, op: str = "average", chunk_bytes: int = 0, stream=None):
+        """Allreduce of HOST tensors (pinned CPU tensors for overlap; one per local rank on a virtual
+        comm): chunked H2D -> ring -> D2H, pipelined (``hvd_allreduce_host``).  In place when
+        ``outputs`` is None.  Completes on ``stream``."""
+        ins = list(inputs) if isinstance(inputs, (list, tuple)) else [inputs]
+        outs = ins if outputs is None else (list(outputs) if isinstance(outputs, (list, tuple)) else [outputs])
+        if len(ins) != self.local_ranks or len(outs) != self.local_ranks:
+            raise HvdError(_lib.HVD_ERR_INVALID, "one host tensor per local rank")
+        for x in ins + outs:
+            if x.device.type != "cpu" or not x.is_contiguous():
+                raise HvdError(_lib.HVD_ERR_INVALID, "host tensors must be contiguous CPU tensors")
+        n, code = ins[0].numel(), _dtype_code(ins[0])
+        pin = (C.c_void_p * len(ins))(*[x.data_ptr() for x in ins])
+        pout = (C.c_void_p * len(outs))(*[x.data_ptr() for x in outs])
+        check(lib.hvd_allreduce_host(self._h, pin, pout, n, code, _OPS[op], int(chunk_bytes),
+                                     _stream_handle(stream)), "hvd_allreduce_host")
+        return outs
+
     def allreduce_buffer(self, count: int, dtype: int = HVD_FLOAT32, op: str = "sum", stream=None):
         """Raw ring on the registered fusion buffer (headline measurement)."""
         check(lib.hvd_allreduce_buffer(self._h, int(count), int(dtype), _OPS[op], _stream_handle(stream)),

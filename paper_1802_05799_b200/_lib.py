@@ -108,6 +108,8 @@ def _load():
         "hvd_chunk_bounds": (C.c_int, [C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_uint64)]),
         "hvd_kernel_stats": (C.c_int, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_double)]),
         "hvd_timeline": (C.c_int, [P, C.c_int, C.POINTER(C.c_uint64), C.c_uint64, C.POINTER(hvd_timeline_info)]),
+        "hvd_allreduce_host": (C.c_int, [P, C.POINTER(P), C.POINTER(P), C.c_uint64, C.c_int, C.c_int, C.c_uint64,
+                                         P]),
         "hvd_negotiator_create": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_uint32, C.c_uint64,
                                             C.POINTER(P)]),
         "hvd_negotiator_ready": (C.c_int, [P, C.c_int, C.c_uint32, C.c_uint64, C.c_int]),
@@ -135,6 +137,7 @@ EXPORTS = sorted([
     "hvd_kernel_stats", "hvd_timeline", "hvd_allreduce_ex", "hvd_register_blob", "hvd_register",
     "hvd_allreduce_registered", "hvd_deregister", "hvd_negotiator_create", "hvd_negotiator_ready",
     "hvd_negotiator_cycle", "hvd_negotiator_pending", "hvd_negotiator_destroy", "hvd_allreduce_negotiated",
+    "hvd_allreduce_host",
 ])
 
 

@@ -1379,9 +1379,10 @@ __global__ void __launch_bounds__(416, 1) pull_allreduce_kernel(const __grid_con
 // barriers — each thread only waits for the words it consumes.  Same ring, same
 // chunks, same reduction order as the fused kernel (bit-identical); the wire
 // carries 2x the bytes, which does not matter at these sizes.
-// LL region of a rank: [parity 2][step 2N-2][chunk slot q] words, written by the
-// predecessor.  Parity = epoch & 1: a sender reuses a parity two launches later,
-// when (stream order + the all-gather chain) its successor has finished with it.
+// LL region of a rank: two fixed halves (parity = epoch & 1), each [step 2N-2][chunk
+// slot q] words, written by the predecessor.  A sender reuses a parity two launches
+// later, when (stream order + the all-gather chain) its successor has finished with
+// it; the halves are fixed so that launches of different sizes never overlap.
 __device__ __forceinline__ void ll_store(unsigned long long* p, uint4 x, unsigned flag) {
   const unsigned long long f = (unsigned long long)flag << 32;
   asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1,%2};" ::"l"(p), "l"(f | x.x), "l"(f | x.y) : "memory");
@@ -1427,8 +1428,11 @@ __global__ void __launch_bounds__(256) ll_allreduce_kernel(const __grid_constant
   const unsigned flag = (unsigned)R.epoch;
   const int par = (int)(R.epoch & 1);
   const unsigned long long slot_words = D.q / VEL * 4;  // words per chunk slot
-  unsigned long long* const in_ll = me.ll + (unsigned long long)par * T * slot_words;
-  unsigned long long* const out_ll = me.nll + (unsigned long long)par * T * slot_words;
+  // each parity owns a FIXED half of the region: a launch of another size must not reach
+  // into the other parity, which the successor may still be reading (previous launch)
+  constexpr unsigned long long kHalfWords = kLLRegionBytes / 2 / 8;
+  unsigned long long* const in_ll = me.ll + (unsigned long long)par * kHalfWords;
+  unsigned long long* const out_ll = me.nll + (unsigned long long)par * kHalfWords;
   FusedCtx F;
   F.segs = D.segs;
   F.src = D.src + (size_t)blockIdx.y * D.nseg;

@@ -117,6 +117,13 @@ struct hvd_comm {
   struct Timed { int kind; cudaEvent_t a, b; };
   std::vector<Timed> timed;
   std::vector<cudaEvent_t> event_pool;
+  // host-buffer allreduce (hvd_allreduce_host): device staging slots + copy streams
+  static constexpr int kHostSlots = 3;
+  char* stage[kMaxLocal] = {};
+  uint64_t stage_chunk = 0;  // bytes per slot
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_in[kHostSlots] = {}, ev_red[kHostSlots] = {}, ev_out[kHostSlots] = {};
+  cudaEvent_t ev_start = nullptr, ev_done = nullptr;
 };
 
 namespace {
@@ -639,7 +646,7 @@ int enqueue_ll(hvd_comm* c, DevPlanBuffer& b, cudaStream_t s) {
   D.slice_el = std::max<uint64_t>(D.ch_el, g);
   D.K = 1;
   D.owner = -1;
-  if ((uint64_t)8 * (N - 1) * D.q * esz > kLLRegionBytes) return HVD_ERR_INVALID;  // 2 par x T x 2 q esz
+  if ((uint64_t)4 * (N - 1) * D.q * esz > kLLRegionBytes / 2) return HVD_ERR_INVALID;  // T x 2 q esz per half
   F.nbuf = 1;
   F.scale_on = b.pp.scale_on;
   F.scale = b.pp.scale;
@@ -857,6 +864,17 @@ int hvd_finalize(hvd_comm* c) {
       cudaEventDestroy(t.b);
     }
     for (auto e : c->event_pool) cudaEventDestroy(e);
+    for (int k = 0; k < hvd_comm::kHostSlots; ++k) {
+      if (c->ev_in[k]) cudaEventDestroy(c->ev_in[k]);
+      if (c->ev_red[k]) cudaEventDestroy(c->ev_red[k]);
+      if (c->ev_out[k]) cudaEventDestroy(c->ev_out[k]);
+    }
+    if (c->ev_start) cudaEventDestroy(c->ev_start);
+    if (c->ev_done) cudaEventDestroy(c->ev_done);
+    if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
+    if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
+    for (int l = 0; l < kMaxLocal; ++l)
+      if (c->stage[l]) cudaFree(c->stage[l]);
     c->cache.clear();
     for (auto& kv : c->ipc_maps) cudaIpcCloseMemHandle(kv.second);
     if (c->peer_region) cudaIpcCloseMemHandle(c->peer_region);
@@ -877,6 +895,82 @@ int hvd_local_ranks(const hvd_comm* c) { return c ? c->nlocal : -1; }
 
 int hvd_allreduce(hvd_comm* c, const hvd_tensor* t, int n, int op, uint64_t fusion_threshold, void* stream) {
   return do_allreduce(c, t, n, op, fusion_threshold, static_cast<cudaStream_t>(stream));
+}
+
+// Host-buffer allreduce: chunk i is copied in (copy stream 1), reduced on the
+// caller's stream by the same path as hvd_allreduce, and copied out (copy
+// stream 2) while chunk i+1 is copied in — PCIe in, the ring, and PCIe out
+// overlap through kHostSlots device staging slots.
+int hvd_allreduce_host(hvd_comm* c, const void* const* in, void* const* out, uint64_t count, int dtype, int op,
+                       uint64_t chunk_bytes, void* stream) {
+  int st = check_live(c);
+  if (st != HVD_OK) return st;
+  const int esz = elem_size(dtype);
+  if (esz == 0) return HVD_ERR_UNSUPPORTED;
+  if (!in || !out) return HVD_ERR_INVALID;
+  for (int l = 0; l < c->nlocal; ++l)
+    if (count && (!in[l] || !out[l])) return HVD_ERR_INVALID;
+  if (count == 0) return HVD_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(c->device));
+  uint64_t chunk = chunk_bytes ? chunk_bytes : (8ull << 20);
+  chunk = std::max<uint64_t>(kChunkQuantum, chunk / kChunkQuantum * kChunkQuantum);
+  chunk = std::min<uint64_t>(chunk, c->cap);
+  if (c->stage_chunk < chunk) {  // (re)allocate the staging slots
+    CK(cudaDeviceSynchronize());
+    for (int l = 0; l < c->nlocal; ++l) {
+      if (c->stage[l]) CK(cudaFree(c->stage[l]));
+      c->stage[l] = nullptr;
+      CK(cudaMalloc(reinterpret_cast<void**>(&c->stage[l]), chunk * hvd_comm::kHostSlots));
+    }
+    c->stage_chunk = chunk;
+  }
+  if (!c->s_h2d) {
+    CK(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
+    for (int k = 0; k < hvd_comm::kHostSlots; ++k) {
+      CK(cudaEventCreateWithFlags(&c->ev_in[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_red[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_out[k], cudaEventDisableTiming));
+    }
+    CK(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming));
+  }
+  // the copies start after everything already on the caller's stream (earlier calls'
+  // staging use included: their copy-outs were joined into it)
+  CK(cudaEventRecord(c->ev_start, s));
+  CK(cudaStreamWaitEvent(c->s_h2d, c->ev_start, 0));
+  CK(cudaStreamWaitEvent(c->s_d2h, c->ev_start, 0));
+  const uint64_t ce = chunk / esz;  // elements per chunk (slots are c->stage_chunk bytes apart)
+  const uint64_t nchunks = (count + ce - 1) / ce;
+  std::vector<hvd_tensor> t(c->nlocal);
+  for (uint64_t i = 0; i < nchunks; ++i) {
+    const int k = (int)(i % hvd_comm::kHostSlots);
+    const uint64_t off = i * ce;
+    const uint64_t n = std::min<uint64_t>(ce, count - off);
+    if (i >= (uint64_t)hvd_comm::kHostSlots) CK(cudaStreamWaitEvent(c->s_h2d, c->ev_out[k], 0));  // slot free
+    for (int l = 0; l < c->nlocal; ++l)
+      CK(cudaMemcpyAsync(c->stage[l] + (uint64_t)k * c->stage_chunk, static_cast<const char*>(in[l]) + off * esz,
+                         n * esz, cudaMemcpyHostToDevice, c->s_h2d));
+    CK(cudaEventRecord(c->ev_in[k], c->s_h2d));
+    CK(cudaStreamWaitEvent(s, c->ev_in[k], 0));
+    for (int l = 0; l < c->nlocal; ++l) {
+      t[l].data = c->stage[l] + (uint64_t)k * c->stage_chunk;
+      t[l].count = n;
+      t[l].dtype = (hvd_dtype)dtype;
+    }
+    st = do_allreduce(c, t.data(), 1, op, c->cap, s);
+    if (st != HVD_OK) return st;
+    CK(cudaEventRecord(c->ev_red[k], s));
+    CK(cudaStreamWaitEvent(c->s_d2h, c->ev_red[k], 0));
+    for (int l = 0; l < c->nlocal; ++l)
+      CK(cudaMemcpyAsync(static_cast<char*>(out[l]) + off * esz, c->stage[l] + (uint64_t)k * c->stage_chunk,
+                         n * esz, cudaMemcpyDeviceToHost, c->s_d2h));
+    CK(cudaEventRecord(c->ev_out[k], c->s_d2h));
+  }
+  CK(cudaEventRecord(c->ev_done, c->s_d2h));
+  CK(cudaStreamWaitEvent(s, c->ev_done, 0));  // completion = the caller's stream
+  return HVD_OK;
 }
 
 int hvd_allreduce_ex(hvd_comm* c, const hvd_tensor* t, int n, int op, uint64_t fusion_threshold, int wire_dtype,

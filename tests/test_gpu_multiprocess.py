@@ -58,6 +58,24 @@ def _worker(rank, world, port, cases, q, protocol):
                     torch.cuda.synchronize()
                     res_its.append([from_torch(t, "f32") for t in ts])
                 out.append(res_its)
+            elif kind == "mixed_sizes":
+                # back-to-back calls of alternating sizes, no host sync in between: LL and fused
+                # launches of different geometry reuse receive regions (DESIGN.md Hazards)
+                res_its = []
+                for it in range(16):
+                    c = counts[it % len(counts)]
+                    t = to_torch(workloads.rank_tensor(c, dtype, rank, it, "normal"), dtype)
+                    comm.allreduce_average([t])
+                    res_its.append(t)
+                torch.cuda.synchronize()
+                out.append([from_torch(t, dtype) for t in res_its])
+            elif kind == "host":
+                x = workloads.rank_tensor(counts[0], dtype, rank, 5, "normal")
+                hin = to_torch(x, dtype, device="cpu").pin_memory()
+                hout = torch.empty_like(hin).pin_memory()
+                comm.allreduce_host(hin, hout, op=op, chunk_bytes=thr)
+                torch.cuda.synchronize()
+                out.append([from_torch(hout, dtype)])
             elif kind == "negotiated":
                 # every rank reports the same ids in its own order over 3 cycles (R15)
                 g = hvd.negotiator(comm, max_tensors=64)
@@ -114,6 +132,8 @@ CASES = [
     ("buffer", [(1 << 20) + 3], "bf16", "average", 0),
     ("bcast", [5, 1 << 20, 333], "f32", 1, 0),
     ("negotiated", [5, 1 << 20, 333, 70_001, 2_000_003, 17, 4096], "f32", None, 4 << 20),
+    ("host", [3_000_001], "f32", "average", 1 << 20),
+    ("mixed_sizes", [262_144, 5_000, 786_432, 25, 3_000_000, 1_048_576, 777], "f32", "average", 0),
     ("registered", [17, 3_000_001, 64, 500_000], "f32", "average", 8 << 20),
     ("allgather", [100_003], "f32", None, 0),
     ("allgather", [8_000_001], "bf16", None, 0),
@@ -149,6 +169,20 @@ def test_multiprocess_ring_matches_oracle(protocol):
                 for r in range(n):
                     for k in range(len(counts)):
                         assert_same(res[r][0][ci][it][k], ref[r][k], "f32", f"registered it={it} r={r} k={k}")
+        elif kind == "mixed_sizes":
+            for it in range(16):
+                c = counts[it % len(counts)]
+                xs = [[workloads.rank_tensor(c, dtype, r, it, "normal")] for r in range(n)]
+                ref, _, _ = oracle.allreduce(xs, [dtype], "average")
+                for r in range(n):
+                    assert_same(res[r][0][ci][it], ref[r][0], dtype, f"mixed call {it} rank {r}")
+        elif kind == "host":
+            xs = [workloads.rank_tensor(counts[0], dtype, r, 5, "normal") for r in range(n)]
+            ce = thr // oracle.ELEM_SIZE[dtype]
+            for off in range(0, counts[0], ce):
+                ref, _, _ = oracle.allreduce([[x[off:off + ce]] for x in xs], [dtype], op)
+                for r in range(n):
+                    assert_same(res[r][0][ci][0][off:off + ce], ref[r][0], dtype, f"host chunk@{off} rank {r}")
         elif kind == "negotiated":
             from oracle import negotiation as neg
             reports = [[[] for _ in range(n)] for _ in range(3)]

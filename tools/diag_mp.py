@@ -85,6 +85,33 @@ def main():
                         print(f"   first bad {i}: got {g[i]} want {ref[rank][k][i]} own {own[i]} "
                               f"succ {xs[(rank + 1) % n][k][i]} ptr {hex(ts[k].data_ptr())}", flush=True)
             comm.deregister(reg)
+        elif kind == "negotiated":
+            import random
+            g = hvd.negotiator(comm, max_tensors=64)
+            ts = [to_torch(workloads.rank_tensor(c, dtype, rank, k, "normal"), dtype) for k, c in enumerate(counts)]
+            order = list(range(len(counts)))
+            random.Random(1000 + rank).shuffle(order)
+            for cyc in range(3):
+                for tid in order[cyc::3]:
+                    g.ready(tid, counts[tid], dtype)
+                ids = comm.allreduce_negotiated(g, ts, op="average", fusion_threshold=thr)
+                print(f"rank {rank} case {ci} cycle {cyc} ids {ids}", flush=True)
+            torch.cuda.synchronize()
+            g.close()
+        elif kind == "host":
+            x = workloads.rank_tensor(counts[0], dtype, rank, 5, "normal")
+            hin = to_torch(x, dtype, device="cpu").pin_memory()
+            hout = torch.empty_like(hin).pin_memory()
+            comm.allreduce_host(hin, hout, op=op, chunk_bytes=thr)
+            torch.cuda.synchronize()
+            xs = [workloads.rank_tensor(counts[0], dtype, r, 5, "normal") for r in range(n)]
+            ce = thr // oracle.ELEM_SIZE[dtype]
+            bad = 0
+            for off in range(0, counts[0], ce):
+                ref, _, _ = oracle.allreduce([[xx[off:off + ce]] for xx in xs], [dtype], op)
+                b = diff(from_torch(hout[off:off + ce], dtype), ref[rank][0])
+                bad += len(b)
+            print(f"rank {rank} case {ci} host: {bad} bad, err {comm.poll_error()}", flush=True)
         elif kind == "buffer":
             L = counts[0]
             x = workloads.rank_tensor(L, dtype, rank, 9, "normal" if dtype in ("f32", "bf16") else "int_uniform")
