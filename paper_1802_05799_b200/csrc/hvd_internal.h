@@ -129,7 +129,10 @@ struct BufDesc {
   unsigned long long L, q, ch_el, slice_el;
   int nseg, K;
   int owner;                         // -1: every channel takes a share; else the one channel
-  int pad;                           //  that runs this (small) buffer alone
+                                     //  that runs this (small) buffer alone
+  int nch;                           // LL: CTAs (channels) of this buffer
+  unsigned ll_off;                   // LL: word offset of this buffer's slots in a parity half
+  int pad;
 };
 constexpr int kMaxMultiBufs = 96;    // fusion buffers per fused launch (kernel parameter space)
 

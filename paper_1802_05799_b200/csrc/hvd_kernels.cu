@@ -841,6 +841,14 @@ __device__ __forceinline__ void slice_range_d(const BufDesc& D, int c, int ch, i
   hi = hi < h_hi ? hi : h_hi;
 }
 
+// Channel ch's index among the channels of buffer D (D.owner < 0: all of them; else the
+// D.nch channels owner, owner+1, ... mod nch), or -1 if it takes no part.
+__device__ __forceinline__ int chan_of(const BufDesc& D, int ch, int nch) {
+  if (D.owner < 0) return ch;
+  const int d = (ch - D.owner + nch) % nch;
+  return d < D.nch ? d : -1;
+}
+
 // Every fusion buffer of a call (up to kMaxMultiBufs) in ONE persistent launch:
 // each channel walks the buffers in order with no grid-wide barrier between
 // them, so buffer b+1's first pushes overlap buffer b's tail.  That is safe
@@ -881,7 +889,7 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
     if (threadIdx.x == nd) st_relaxed_sys(me.pready + ch, R.epoch);
     int total = 0;
     for (int b = 0; b < P.nbuf; ++b)
-      if (P.bufs[b].owner < 0 || P.bufs[b].owner == ch) total += T * P.bufs[b].K;
+      if (chan_of(P.bufs[b], ch, gridDim.x) >= 0) total += T * P.bufs[b].K;
     if (threadIdx.x == nd && total > 0)
       signal_loop(&s_done, total, me.nflags + ch, base0, R.sig_mode, &s_pub,
                   R.tl ? R.tl + tl_words(R.tl_max) * blockIdx.y + ((size_t)kMaxChannels + ch) * R.tl_max * 2 : nullptr,
@@ -902,8 +910,8 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
   bool hs_pending = true;
   for (int b = 0; b < P.nbuf; ++b) {
     const BufDesc& D = P.bufs[b];
-    if (D.owner >= 0 && D.owner != ch) continue;  // a small buffer run by another channel
-    const int cg = D.owner >= 0 ? 0 : ch;         // this channel's index in the buffer's geometry
+    const int cg = chan_of(D, ch, gridDim.x);  // this channel's index in the buffer's geometry
+    if (cg < 0) continue;                       // a buffer run by other channels
     const int K = D.K;
     const bool cache = D.nseg <= P.cache_segs;
     if (!first) bar_sync(kBarData, nd);  // every data warp is done with the previous member table
@@ -1420,19 +1428,21 @@ __global__ void __launch_bounds__(256) ll_allreduce_kernel(const __grid_constant
   constexpr int VEL = 16 / ESZ;
   const RingParams& R = P.ring;
   const RingRank& me = R.rk[blockIdx.y];
-  const int ch = blockIdx.x;
+  int ch = blockIdx.x;  // -> (buffer b, channel ch of b): the buffers of a call share one launch
+  int b = 0;
+  while (b + 1 < P.nbuf && ch >= P.bufs[b].nch) ch -= P.bufs[b++].nch;
   const int N = R.N;
   const int r = me.rank;
   const int T = 2 * (N - 1);
-  const BufDesc& D = P.bufs[0];
+  const BufDesc& D = P.bufs[b];
   const unsigned flag = (unsigned)R.epoch;
   const int par = (int)(R.epoch & 1);
   const unsigned long long slot_words = D.q / VEL * 4;  // words per chunk slot
   // each parity owns a FIXED half of the region: a launch of another size must not reach
   // into the other parity, which the successor may still be reading (previous launch)
   constexpr unsigned long long kHalfWords = kLLRegionBytes / 2 / 8;
-  unsigned long long* const in_ll = me.ll + (unsigned long long)par * kHalfWords;
-  unsigned long long* const out_ll = me.nll + (unsigned long long)par * kHalfWords;
+  unsigned long long* const in_ll = me.ll + (unsigned long long)par * kHalfWords + D.ll_off;
+  unsigned long long* const out_ll = me.nll + (unsigned long long)par * kHalfWords + D.ll_off;
   FusedCtx F;
   F.segs = D.segs;
   F.src = D.src + (size_t)blockIdx.y * D.nseg;

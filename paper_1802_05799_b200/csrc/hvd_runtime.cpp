@@ -578,13 +578,18 @@ int enqueue_fused_multi(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStrea
     D.nseg = b.pp.nseg;
     D.L = b.L;
     D.q = chunk_len(b.L, N, dtype);
-    // A buffer too small to give every channel 32 KiB per chunk runs whole on one
-    // channel (round robin), so many small buffers of one call proceed in parallel.
-    const bool small = nb > 1 && nch > 1 && D.q * esz < (uint64_t)nch * (32 << 10) &&
-                       (uint64_t)N * ((D.q + g - 1) / g * g) <= F.region_el;  // fits one channel's region
-    D.owner = small ? (next_owner++ % nch) : -1;
-    const int geo_ch = small ? 1 : nch;
-    D.ch_el = (D.q + (uint64_t)geo_ch * g - 1) / ((uint64_t)geo_ch * g) * g;
+    // In a multi-buffer call a buffer runs on k consecutive channels (round robin), about
+    // 64 KiB of every chunk per channel, so many small and medium buffers proceed in
+    // parallel; k grows until the buffer's slots fit the channels' private regions.
+    int k = nch;
+    if (nb > 1 && nch > 1) {
+      k = (int)std::min<uint64_t>((uint64_t)nch, std::max<uint64_t>(1, (D.q * esz + (64 << 10) - 1) / (64 << 10)));
+      while (k < nch && (uint64_t)N * ((D.q + (uint64_t)k * g - 1) / ((uint64_t)k * g) * g) > F.region_el) ++k;
+    }
+    D.owner = k < nch ? next_owner : -1;  // first channel of the range
+    D.nch = k;
+    if (k < nch) next_owner = (next_owner + k) % nch;
+    D.ch_el = (D.q + (uint64_t)k * g - 1) / ((uint64_t)k * g) * g;
     uint64_t sb = (uint64_t)c->slice_bytes;
     if (sb == 0) sb = std::min<uint64_t>(128 << 10, std::max<uint64_t>(32 << 10, D.ch_el * esz / 2));
     D.slice_el = std::min<uint64_t>(std::max<uint64_t>(g, sb / esz / g * g), std::max<uint64_t>(D.ch_el, g));
@@ -593,8 +598,7 @@ int enqueue_fused_multi(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStrea
     if ((uint64_t)N * D.ch_el > F.region_el) return HVD_ERR_INVALID;  // region slack exhausted
     maxseg = std::max(maxseg, D.nseg);
     const unsigned long long inc = (unsigned long long)(N > 1 ? 2 * (N - 1) : 0) * D.K;
-    if (small) signals[D.owner] += inc;
-    else for (int ch = 0; ch < nch; ++ch) signals[ch] += inc;
+    for (int j = 0; j < k; ++j) signals[D.owner < 0 ? j : (D.owner + j) % nch] += inc;
   }
   F.cache_segs = maxseg <= kFusedSmemSegs ? (maxseg + 1) / 2 * 2 : 0;
   if (N == 1) {  // no ring: the in-place gather x (1/N) -> scatter stream (solo_kernel)
@@ -620,52 +624,106 @@ int enqueue_fused_multi(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStrea
   return HVD_OK;
 }
 
-// LL protocol for one small buffer (ll_allreduce_kernel).
-int enqueue_ll(hvd_comm* c, DevPlanBuffer& b, cudaStream_t s) {
-  const int dtype = b.dtype;
+// LL protocol (ll_allreduce_kernel) for a group of small buffers of one dtype in
+// one cooperative launch: buffer i gets nch_i CTAs (one 16 B vector per thread per
+// step where the co-resident budget allows) and its own slot area in each parity half.
+int ll_want(const hvd_comm* c, const DevPlanBuffer& b, uint64_t cta_bytes) {
+  const uint64_t q = chunk_len(b.L, c->size, b.dtype);
+  const uint64_t qb = q * elem_size(b.dtype);
+  return (int)std::min<uint64_t>((uint64_t)c->ll_ctas, std::max<uint64_t>(1, (qb + cta_bytes - 1) / cta_bytes));
+}
+
+// cta_bytes: chunk bytes per CTA (4 KiB = one 16 B vector per thread per step for a lone
+// buffer; 16 KiB when many buffers share the launch)
+int enqueue_ll(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStream_t s, uint64_t cta_bytes = 4096) {
+  const int dtype = bs[0]->dtype;
   const int esz = elem_size(dtype);
   const uint64_t g = kChunkQuantum / esz;
   const int N = c->size;
   FusedParams F;
   std::memset(&F, 0, sizeof(F));
-  int nch = 0;
-  int st = make_ring_params(c, b.L, dtype, true, &F.ring, &nch);
+  int nch_unused = 0;
+  int st = make_ring_params(c, bs[0]->L, dtype, true, &F.ring, &nch_unused);
   if (st != HVD_OK) return st;
-  BufDesc& D = F.bufs[0];
-  D.q = chunk_len(b.L, N, dtype);
-  // one 16 B vector per thread per step where possible (each vector costs a full
-  // NVLink round of polling), at most ll_ctas co-resident CTAs per rank
-  nch = (int)std::min<uint64_t>((uint64_t)c->ll_ctas, std::max<uint64_t>(1, (D.q * esz + 4095) / 4096));
-  D.segs = b.pp.segs;
-  D.src = b.pp.src;
-  D.dst = b.dst ? b.dst : b.pp.src;
-  D.vbeg = b.vbeg;
-  D.nseg = b.pp.nseg;
-  D.L = b.L;
-  D.ch_el = (D.q + (uint64_t)nch * g - 1) / ((uint64_t)nch * g) * g;
-  D.slice_el = std::max<uint64_t>(D.ch_el, g);
-  D.K = 1;
-  D.owner = -1;
-  if ((uint64_t)4 * (N - 1) * D.q * esz > kLLRegionBytes / 2) return HVD_ERR_INVALID;  // T x 2 q esz per half
-  F.nbuf = 1;
-  F.scale_on = b.pp.scale_on;
-  F.scale = b.pp.scale;
+  int ctas = 0;
+  uint64_t words = 0;
+  for (int i = 0; i < nb; ++i) {
+    const DevPlanBuffer& b = *bs[i];
+    BufDesc& D = F.bufs[i];
+    D.q = chunk_len(b.L, N, dtype);
+    D.nch = ll_want(c, b, cta_bytes);
+    ctas += D.nch;
+    D.segs = b.pp.segs;
+    D.src = b.pp.src;
+    D.dst = b.dst ? b.dst : b.pp.src;
+    D.vbeg = b.vbeg;
+    D.nseg = b.pp.nseg;
+    D.L = b.L;
+    D.ch_el = (D.q + (uint64_t)D.nch * g - 1) / ((uint64_t)D.nch * g) * g;
+    D.slice_el = std::max<uint64_t>(D.ch_el, g);
+    D.K = 1;
+    D.owner = -1;
+    D.ll_off = (unsigned)words;
+    words += (uint64_t)2 * (N - 1) * (D.q * esz / 16 * 4);  // T steps x slot (8 B word per 4 B of data)
+  }
+  if (ctas > c->ll_ctas || words * 8 > kLLRegionBytes / 2) return HVD_ERR_INVALID;
+  F.nbuf = nb;
+  F.scale_on = bs[0]->pp.scale_on;
+  F.scale = bs[0]->pp.scale;
   F.dtype = dtype;
   F.tdtype = dtype;
   F.ring.epoch = ++c->ll_epoch;
   if (c->tl) c->tl_slices = 0;  // the LL kernel records no timeline
-  return launch_counted(c, HVD_KERNEL_LL, s, [&] { return launch_ll(F, dtype, nch, c->nlocal, s); });
+  return launch_counted(c, HVD_KERNEL_LL, s, [&] { return launch_ll(F, dtype, ctas, c->nlocal, s); });
 }
 
-// The fused path for a whole plan: pull protocol per buffer, else multi-buffer launches.
+// LL for a lone buffer up to ll_max; inside a multi-buffer plan only for buffers of at
+// most kLLMultiBytes (larger ones pipeline better inside the multi-buffer fused launch)
+constexpr int64_t kLLMultiBytes = 256 << 10;
+bool ll_eligible(const hvd_comm* c, const DevPlanBuffer& b, bool multi) {
+  const int esz = elem_size(b.dtype);
+  const int64_t lim = multi ? std::min<int64_t>(c->ll_max, kLLMultiBytes) : c->ll_max;
+  return c->size > 1 && c->protocol == 1 && b.L > 0 && b.tdtype == b.dtype && b.dtype != HVD_INT64 &&
+         (int64_t)(b.L * esz) <= lim;
+}
+
+// The fused path for a whole plan: small buffers through the LL protocol (grouped),
+// the rest through multi-buffer fused launches (or the pull protocol per buffer).
 int enqueue_fused_plan(hvd_comm* c, CachedPlan* plan, cudaStream_t s) {
-  if (plan->bufs.size() == 1 && c->size > 1 && c->protocol == 1) {  // one small buffer: LL protocol
-    DevPlanBuffer& b = plan->bufs[0];
-    const int esz = elem_size(b.dtype);
-    if (b.L > 0 && b.tdtype == b.dtype && b.dtype != HVD_INT64 && (int64_t)(b.L * esz) <= c->ll_max)
-      return enqueue_ll(c, b, s);
-  }
   std::vector<DevPlanBuffer*> group;
+  const bool multi = plan->bufs.size() > 1;
+  const uint64_t cta_bytes = multi ? (16 << 10) : 4096;
+  // 1. LL groups: same dtype, <= kMaxMultiBufs buffers, CTA and region budgets
+  {
+    int ctas = 0;
+    uint64_t words = 0;
+    auto flush = [&]() -> int {
+      int st = HVD_OK;
+      if (!group.empty()) st = enqueue_ll(c, group.data(), (int)group.size(), s, cta_bytes);
+      group.clear();
+      ctas = 0;
+      words = 0;
+      return st;
+    };
+    for (DevPlanBuffer& b : plan->bufs) {
+      if (!ll_eligible(c, b, multi)) continue;
+      const int esz = elem_size(b.dtype);
+      const uint64_t q = chunk_len(b.L, c->size, b.dtype);
+      const int want = ll_want(c, b, cta_bytes);
+      const uint64_t w = (uint64_t)2 * (c->size - 1) * (q * esz / 16 * 4);
+      if (!group.empty() && (group[0]->dtype != b.dtype || (int)group.size() >= kMaxMultiBufs ||
+                             ctas + want > c->ll_ctas || (words + w) * 8 > kLLRegionBytes / 2)) {
+        int st = flush();
+        if (st != HVD_OK) return st;
+      }
+      group.push_back(&b);
+      ctas += want;
+      words += w;
+    }
+    int st = flush();
+    if (st != HVD_OK) return st;
+  }
+  // 2. everything else
   auto flush = [&]() -> int {
     int st = HVD_OK;
     if (!group.empty()) st = enqueue_fused_multi(c, group.data(), (int)group.size(), s);
@@ -673,7 +731,7 @@ int enqueue_fused_plan(hvd_comm* c, CachedPlan* plan, cudaStream_t s) {
     return st;
   };
   for (DevPlanBuffer& b : plan->bufs) {
-    if (b.L == 0) continue;
+    if (b.L == 0 || ll_eligible(c, b, multi)) continue;
     if (c->protocol == 0 && c->size > 1 && b.tdtype == b.dtype && !b.rdst) {
       int st = flush();
       if (st != HVD_OK) return st;

@@ -369,6 +369,7 @@ def test_both_protocols_bitexact(hvd, n, protocol):
     comm = hvd.init_virtual(n, 0, 2 << 20)
     try:
         comm.set_config(hvd._lib.HVD_CFG_PROTOCOL, protocol)
+        comm.set_config(hvd._lib.HVD_CFG_LL_MAX_BYTES, 0)  # small buffers would take the LL protocol
         counts = [3, 1000, 262_149, 5, 77_777, 400_000]
         for it, dtype in enumerate(["f32", "bf16", "f32"]):
             xs = workloads.all_ranks(counts, dtype, n, seed=500 + it)
@@ -458,15 +459,21 @@ def test_many_small_buffers_one_launch(hvd, n):
     xs = workloads.all_ranks(counts, "f32", n, seed=31)
     ref, _, plan = oracle.allreduce(xs, ["f32"] * len(counts), "average", threshold=0)
     assert len(plan) == 200
-    ts = [[to_torch(x, "f32") for x in xs[r]] for r in range(n)]
-    comm.kernel_stats()
-    comm.allreduce(ts, op="average", fusion_threshold=0)
-    torch.cuda.synchronize()
-    assert comm.poll_error() == 0
-    assert comm.kernel_stats()["fused"][0] == 3
-    for r in range(n):
-        for k in range(len(counts)):
-            assert_same(from_torch(ts[r][k], "f32"), ref[r][k], "f32", f"r={r} k={k}")
+    ll_default = comm.get_config(hvd._lib.HVD_CFG_LL_MAX_BYTES)
+    # fused multi-buffer launches (LL off), then grouped LL launches (the default for small buffers)
+    for ll_max, kind in ((0, "fused"), (ll_default, "ll")):
+        comm.set_config(hvd._lib.HVD_CFG_LL_MAX_BYTES, ll_max)
+        ts = [[to_torch(x, "f32") for x in xs[r]] for r in range(n)]
+        comm.kernel_stats()
+        comm.allreduce(ts, op="average", fusion_threshold=0)
+        torch.cuda.synchronize()
+        assert comm.poll_error() == 0
+        st = comm.kernel_stats()
+        assert st[kind][0] == 3 and sum(v[0] for v in st.values()) == 3  # 96 + 96 + 8 buffers
+        for r in range(n):
+            for k in range(len(counts)):
+                assert_same(from_torch(ts[r][k], "f32"), ref[r][k], "f32", f"{kind} r={r} k={k}")
+    comm.set_config(hvd._lib.HVD_CFG_LL_MAX_BYTES, ll_default)
 
 
 @pytest.mark.parametrize("n", [2, 3, 4, 5, 8])
@@ -609,3 +616,29 @@ def test_allreduce_host_pipelined_chunks(hvd, n):
         torch.cuda.synchronize()
         for r in range(n):
             assert np.array_equal(from_torch(hin[r], dt).view(np.uint8), from_torch(hout[r], dt).view(np.uint8))
+
+
+@pytest.mark.parametrize("n", [2, 3, 4])
+def test_fusion_off_mixed_sizes_channel_ranges(hvd, n):
+    """Fusion off over tensors from 1 element to ~6 MB: buffers <= 256 KiB take grouped LL
+    launches, the others share multi-buffer fused launches, each on a range of ~q/64 KiB
+    channels (round robin); with LL off every buffer takes the channel-range path.  Bit-exact."""
+    comm = comm_for(hvd, n)
+    rng = np.random.default_rng(90 + n)
+    counts = [int(c) for c in rng.choice([1, 37, 1000, 40_000, 65_536, 300_001, 1_500_000], size=40)]
+    xs = workloads.all_ranks(counts, "f32", n, seed=91)
+    ref, _, plan = oracle.allreduce(xs, ["f32"] * len(counts), "average", threshold=0)
+    ll_default = comm.get_config(hvd._lib.HVD_CFG_LL_MAX_BYTES)
+    for ll_max in (ll_default, 0):
+        comm.set_config(hvd._lib.HVD_CFG_LL_MAX_BYTES, ll_max)
+        ts = [[to_torch(x, "f32") for x in xs[r]] for r in range(n)]
+        comm.kernel_stats()
+        comm.allreduce(ts, op="average", fusion_threshold=0)
+        torch.cuda.synchronize()
+        assert comm.poll_error() == 0
+        st = comm.kernel_stats()
+        assert (st["ll"][0] > 0) == (ll_max > 0) and st["fused"][0] >= 1
+        for r in range(n):
+            for k in range(len(counts)):
+                assert_same(from_torch(ts[r][k], "f32"), ref[r][k], "f32", f"ll={ll_max} r={r} k={k}")
+    comm.set_config(hvd._lib.HVD_CFG_LL_MAX_BYTES, ll_default)
