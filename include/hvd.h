@@ -199,8 +199,10 @@ typedef enum {
                                 fusion buffer; 0: three kernels (pack, ring, unpack)       */
   HVD_CFG_TIMELINE = 9,      /* > 0: record a device timeline of every fused launch with up to
                                 this many slice records per channel; 0: off (default)      */
-  HVD_CFG_WINDOW = 10,       /* fused: max slices per channel pushed but not yet fenced (0 = no
-                                limit): bounds the NVLink backlog and so the signal latency */
+  HVD_CFG_WINDOW = 10,       /* fused: max slices per channel pushed but not yet published,
+                                the one being pushed included (default 2; 0 = no limit; 1 = a slice
+                                starts only after the previous one's signal is out): bounds
+                                the NVLink backlog a fence waits for, so the signal latency */
   HVD_CFG_FIN_LAG = 11,      /* fused: slices by which the final local scatter trails the last
                                 all-gather iteration (>= K-1: scatter after all of it)     */
   HVD_CFG_LL_MAX_BYTES = 14, /* a call that is one fusion buffer of at most this many bytes

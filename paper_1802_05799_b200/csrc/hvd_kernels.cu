@@ -956,9 +956,9 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
           (long long)(((unsigned long long)ch * P.region_el + (unsigned long long)c * D.ch_el +
                        (lo - (unsigned long long)c * D.q - (unsigned long long)cg * D.ch_el)) / VEL) -
           (long long)(lo / VEL);
-      if (R.window > 0 && t < T && i > R.window) {
+      if (R.window > 0 && t < T && i + 1 > R.window) {  // at most `window` pushed-unpublished ops
         if (tid == 0)
-          while (ld_acquire_cta_shared(&s_pub) < i - R.window) __nanosleep(64);
+          while (ld_acquire_cta_shared(&s_pub) < i + 1 - R.window) __nanosleep(32);
         bar_sync(kBarData, nd);
       }
       const unsigned long long tb = tl_d ? globaltimer() : 0;

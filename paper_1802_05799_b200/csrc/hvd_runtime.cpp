@@ -93,7 +93,7 @@ struct hvd_comm {
   int sig_mode = 1;
   int fused = 1;
   int multi_bufs = kMaxMultiBufs;  // fusion buffers per fused launch
-  int window = 0;
+  int window = 2;  // HVD_CFG_WINDOW (measured: N = 4 +5-8 %, N = 2 neutral)
   int fin_lag = 1;
   unsigned long long hs_epoch = 0;  // copy-collective handshake epochs issued
   unsigned long long ll_epoch = 0;  // LL launches issued (flag value = epoch)
