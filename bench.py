@@ -184,9 +184,16 @@ def run_ours(args):
         step(i)
     _barrier(world)
     # every rank must make the same number of collective calls: the pre-load
-    # count is derived from the warm-up time and agreed on (max over ranks)
-    per_step = (time.perf_counter() - w0) / args.warmup
-    n_load = int(_max_over_ranks(min(50000.0, args.clock_window / max(per_step, 1e-6)), world))
+    # count is derived from a calibration run (the warm-up includes first-call
+    # costs such as plan uploads) and agreed on (max over ranks)
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    ncal = 50
+    for i in range(ncal):
+        step(i)
+    torch.cuda.synchronize()
+    per_step = (time.perf_counter() - w0) / ncal
+    n_load = int(_max_over_ranks(min(200000.0, args.clock_window / max(per_step, 1e-6)), world))
     comm.kernel_stats()  # reset counters
     t_load0 = time.time()
     if True:
