@@ -57,7 +57,10 @@ typedef enum {
   HVD_ERR_CUDA = -3,           /* a CUDA runtime call failed                              */
   HVD_ERR_NOT_CONNECTED = -4,  /* size > 1 and hvd_connect() has not completed            */
   HVD_ERR_TIMEOUT = -5,        /* a device spin-wait exceeded the watchdog (async)        */
-  HVD_ERR_CLOSED = -6          /* comm already finalized                                  */
+  HVD_ERR_CLOSED = -6,         /* comm already finalized                                  */
+  HVD_ERR_MISMATCH = -7        /* ranks made different collective calls (async): the launch
+                                  handshake carries a hash of the call's geometry and the
+                                  successor's must equal this rank's                       */
 } hvd_status;
 
 typedef enum { HVD_FLOAT32 = 1, HVD_BFLOAT16 = 2, HVD_INT32 = 3, HVD_INT64 = 4 } hvd_dtype;

@@ -17,6 +17,7 @@ HVD_ERR_CUDA = -3
 HVD_ERR_NOT_CONNECTED = -4
 HVD_ERR_TIMEOUT = -5
 HVD_ERR_CLOSED = -6
+HVD_ERR_MISMATCH = -7
 
 HVD_FLOAT32, HVD_BFLOAT16, HVD_INT32, HVD_INT64 = 1, 2, 3, 4
 HVD_SUM, HVD_AVERAGE = 0, 1

@@ -40,6 +40,8 @@ struct RingRank {
   unsigned long long* nflags;    // successor's flags
   unsigned long long* rflags;    // [kMaxChannels] ready flags, written by the successor (handshake)
   unsigned long long* pready;    // predecessor's ready flags (this rank writes them)
+  unsigned long long* rhash;     // [kMaxChannels] call hashes, written by the successor
+  unsigned long long* phash;     // predecessor's call hashes (this rank writes them)
   // pull protocol (pull_allreduce_kernel)
   char* pull[2];                 // own pull buffers (call parity), read by the successor
   const char* ppull[2];          // predecessor's pull buffers
@@ -79,6 +81,7 @@ struct RingParams {
   int window;                   // fused: max pushed-but-unfenced slices per channel (0 = no limit)
   int fin_lag;                  // fused: final-scatter interleave lag in slices
   unsigned long long epoch;     // ring/fused/copy: handshake epoch of this launch (LL: flag)
+  unsigned long long hash;      // ring/fused: hash of the call's geometry (HVD_ERR_MISMATCH)
   int parity;                   // pull protocol: pull buffer of this call
   int call;                     // pull protocol: 1-based call index
   unsigned long long exits_target;  // pull protocol: cumulative CTA exits after this call

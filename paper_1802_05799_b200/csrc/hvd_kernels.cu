@@ -18,7 +18,8 @@
 namespace hvd {
 namespace {
 
-constexpr int kHvdErrTimeout = -5;  // HVD_ERR_TIMEOUT
+constexpr int kHvdErrTimeout = -5;   // HVD_ERR_TIMEOUT
+constexpr int kHvdErrMismatch = -7;  // HVD_ERR_MISMATCH
 
 // ------------------------------------------------------------------ memory helpers
 struct V32 { uint32_t w[8]; };
@@ -295,7 +296,8 @@ __global__ void __launch_bounds__(416, 1) ring_allreduce_kernel(const __grid_con
 
   if (threadIdx.x >= nd) {  // ---- signal warp
     if (threadIdx.x == nd) {
-      st_relaxed_sys(me.pready + ch, P.epoch);  // handshake: previous launch done with the regions
+      st_relaxed_sys(me.phash + ch, P.hash);     // handshake: previous launch done with the regions,
+      st_release_sys(me.pready + ch, P.epoch);   // and this launch's geometry
       signal_loop(&s_done, T * K, me.nflags + ch, base, P.sig_mode);
     }
     return;
@@ -303,7 +305,14 @@ __global__ void __launch_bounds__(416, 1) ring_allreduce_kernel(const __grid_con
 
   // ---- data warps
   const unsigned tid = threadIdx.x;
-  if (tid == 0 && !spin_until(me.rflags + ch, P.epoch, P.err, P.timeout_ns)) s_abort = 1;
+  if (tid == 0) {
+    if (!spin_until(me.rflags + ch, P.epoch, P.err, P.timeout_ns)) {
+      s_abort = 1;
+    } else if (*(volatile const unsigned long long*)(me.rhash + ch) != P.hash) {
+      *(volatile int*)P.err = kHvdErrMismatch;
+      s_abort = 1;
+    }
+  }
   bar_sync(kBarData, nd);  // no push before the successor's handshake
   unsigned long long sent = 0;
   int i = 0;
@@ -707,6 +716,8 @@ template <> struct WireCvt<4, 2> {  // bf16 tensor, fp32 wire
 // ready flag while they fly.
 struct Handshake {
   const unsigned long long* flag;  // nullptr: none
+  const unsigned long long* hash_flag;  // the successor's call hash, written before its flag
+  unsigned long long hash;              // this rank's call hash
   unsigned long long epoch;
   int* err;
   unsigned long long timeout_ns;
@@ -758,7 +769,14 @@ __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& m
   for (int j = 0; j < kPipe - 1; ++j) issue(j);
   int nrows = rows;
   if (hs) {
-    if (tid == 0 && !spin_until(hs->flag, hs->epoch, hs->err, hs->timeout_ns)) *(volatile int*)hs->abort = 1;
+    if (tid == 0) {
+      if (!spin_until(hs->flag, hs->epoch, hs->err, hs->timeout_ns)) {
+        *(volatile int*)hs->abort = 1;
+      } else if (*(volatile const unsigned long long*)hs->hash_flag != hs->hash) {  // ordered by the acquire
+        *(volatile int*)hs->err = kHvdErrMismatch;
+        *(volatile int*)hs->abort = 1;
+      }
+    }
     bar_sync(kBarData, nthr);
     if (*(volatile int*)hs->abort) nrows = 0;
   }
@@ -886,7 +904,10 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
   if (threadIdx.x >= nd) {  // ---- signal warp
     // handshake: this launch started, so this rank's previous launch has finished with
     // its receive regions — the predecessor may push (relaxed: the kernel boundary orders it)
-    if (threadIdx.x == nd) st_relaxed_sys(me.pready + ch, R.epoch);
+    if (threadIdx.x == nd) {  // the call hash first, then the epoch (release orders the two)
+      st_relaxed_sys(me.phash + ch, R.hash);
+      st_release_sys(me.pready + ch, R.epoch);
+    }
     int total = 0;
     for (int b = 0; b < P.nbuf; ++b)
       if (chan_of(P.bufs[b], ch, gridDim.x) >= 0) total += T * P.bufs[b].K;
@@ -906,7 +927,7 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
   int bpar = 0;  // receive half of this channel's next buffer
   // the launch's first remote push waits for the successor's handshake (inside the slice,
   // after its first loads are issued)
-  const Handshake hs0 = {me.rflags + ch, R.epoch, R.err, R.timeout_ns, &s_abort};
+  const Handshake hs0 = {me.rflags + ch, me.rhash + ch, R.hash, R.epoch, R.err, R.timeout_ns, &s_abort};
   bool hs_pending = true;
   for (int b = 0; b < P.nbuf; ++b) {
     const BufDesc& D = P.bufs[b];

@@ -159,6 +159,7 @@ unsigned long long* tail_of(char* region, uint64_t cap) {
   return reinterpret_cast<unsigned long long*>(region + kNumBufs * cap);
 }
 unsigned long long* rflags_of(char* region, uint64_t cap) { return tail_of(region, cap) + 512; }
+unsigned long long* rhash_of(char* region, uint64_t cap) { return tail_of(region, cap) + 768; }
 unsigned long long* pflags_of(char* region, uint64_t cap) { return tail_of(region, cap) + 1024; }
 unsigned long long* done_of(char* region, uint64_t cap) { return tail_of(region, cap) + 1536; }
 unsigned long long* exits_of(char* region, uint64_t cap) { return tail_of(region, cap) + 1537; }
@@ -187,6 +188,7 @@ int common_init(hvd_comm* c, uint64_t fusion_bytes) {
     r.flags = flags_of(c->region[l], bz);
     r.stats = stats_of(c->region[l], bz);
     r.rflags = rflags_of(c->region[l], bz);
+    r.rhash = rhash_of(c->region[l], bz);
     r.pull[0] = pull_of(c->region[l], bz, 0);
     r.pull[1] = pull_of(c->region[l], bz, 1);
     r.pflags_own = pflags_of(c->region[l], bz);
@@ -210,6 +212,7 @@ void set_neighbours(RingRank& r, char* succ_region, char* pred_region, uint64_t 
   r.nscratch1 = scratch1_of(succ_region, cap);
   r.nflags = flags_of(succ_region, cap);
   r.pready = rflags_of(pred_region, cap);
+  r.phash = rhash_of(pred_region, cap);
   r.ppull[0] = pull_of(pred_region, cap, 0);
   r.ppull[1] = pull_of(pred_region, cap, 1);
   r.pflags_pred = pflags_of(pred_region, cap);
@@ -495,6 +498,17 @@ void advance_base(hvd_comm* c, const RingParams& P, int nch) {
   for (int ch = 0; ch < nch; ++ch) c->base[ch] += inc;
 }
 
+// Hash of a launch's geometry: both ends of every ring link must agree on it.
+struct CallHash {
+  uint64_t h = 0x9e3779b97f4a7c15ull;
+  void add(uint64_t v) {
+    uint64_t z = (h ^ v) + 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    h = z ^ (z >> 31);
+  }
+};
+
 int enqueue_ring(hvd_comm* c, uint64_t L, int dtype, cudaStream_t s) {
   if (c->size <= 1 || L == 0) return HVD_OK;
   RingParams P;
@@ -502,6 +516,11 @@ int enqueue_ring(hvd_comm* c, uint64_t L, int dtype, cudaStream_t s) {
   int st = make_ring_params(c, L, dtype, false, &P, &nch);
   if (st != HVD_OK) return st;
   P.epoch = ++c->hs_epoch;
+  {
+    CallHash ch;
+    for (uint64_t v : {(uint64_t)1, L, (uint64_t)dtype, (uint64_t)nch, (uint64_t)P.K, (uint64_t)c->size}) ch.add(v);
+    P.hash = ch.h;
+  }
   st = launch_counted(c, HVD_KERNEL_RING, s, [&] { return launch_ring(P, dtype, nch, c->nlocal, c->threads, s); });
   if (st != HVD_OK) return st;
   advance_base(c, P, nch);
@@ -607,6 +626,16 @@ int enqueue_fused_multi(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStrea
   }
   const int tdt = F.tdtype;
   F.ring.epoch = ++c->hs_epoch;
+  {
+    CallHash h;
+    for (uint64_t v : {(uint64_t)2, (uint64_t)N, (uint64_t)dtype, (uint64_t)F.tdtype, (uint64_t)F.registered,
+                       (uint64_t)F.scale_on, (uint64_t)nb, (uint64_t)nch})
+      h.add(v);
+    for (int i = 0; i < nb; ++i)
+      for (uint64_t v : {(uint64_t)F.bufs[i].L, (uint64_t)F.bufs[i].K, (uint64_t)(int64_t)F.bufs[i].owner, (uint64_t)F.bufs[i].nch})
+        h.add(v);
+    F.ring.hash = h.h;
+  }
   st = launch_counted(c, HVD_KERNEL_FUSED, s, [&] { return launch_fused(F, dtype, nch, c->nlocal, c->threads, s); });
   (void)tdt;
   if (st != HVD_OK) return st;
@@ -1383,6 +1412,7 @@ const char* hvd_strerror(int status) {
     case HVD_ERR_NOT_CONNECTED: return "communicator not connected";
     case HVD_ERR_TIMEOUT: return "device watchdog timeout (a peer did not signal)";
     case HVD_ERR_CLOSED: return "communicator finalized";
+    case HVD_ERR_MISMATCH: return "ranks made different collective calls";
     default: return "unknown status";
   }
 }

@@ -281,3 +281,44 @@ def test_watchdog_turns_a_missing_peer_into_an_error():
     err, elapsed, again = res[0]
     assert err == -5 and again == -5, res  # HVD_ERR_TIMEOUT
     assert 1.0 < elapsed < 60.0
+
+
+def _mismatch_worker(rank, world, port, q):
+    os.environ.update(RANK=str(rank), WORLD_SIZE=str(world), LOCAL_RANK=str(rank),
+                      MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import paper_1802_05799_b200 as hvd
+    import torch.distributed as dist
+    try:
+        comm = hvd.init()
+        comm.set_config(hvd._lib.HVD_CFG_TIMEOUT_MS, 3000)
+        dist.barrier()
+        # the collective contract broken: rank 0 reduces 3M elements, rank 1 5M (both fused)
+        x = torch.ones(3_000_000 if rank == 0 else 5_000_000, device="cuda")
+        comm.allreduce_average([x])
+        torch.cuda.synchronize()
+        q.put((rank, comm.poll_error()))
+        dist.barrier()
+        comm.finalize()
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e)))
+
+
+def test_mismatched_calls_are_detected():
+    """Ranks calling with different sizes: the launch handshake compares call hashes and
+    latches HVD_ERR_MISMATCH (or the watchdog times out) instead of corrupting or hanging."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_mismatch_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=120)
+    assert all(isinstance(v, int) for v in res.values()), res
+    assert -7 in res.values() and set(res.values()) <= {-7, -5}, res
