@@ -135,6 +135,7 @@ CASES = [
     ("host", [3_000_001], "f32", "average", 1 << 20),
     ("mixed_sizes", [262_144, 5_000, 786_432, 25, 3_000_000, 1_048_576, 777], "f32", "average", 0),
     ("registered", [17, 3_000_001, 64, 500_000], "f32", "average", 8 << 20),
+    ("registered", [16 << 20], "f32", "average", 64 << 20),  # bench.py's step: one registered 64 MiB gradient
     ("allgather", [100_003], "f32", None, 0),
     ("allgather", [8_000_001], "bf16", None, 0),
 ]
