@@ -1412,6 +1412,9 @@ __global__ void __launch_bounds__(416, 1) pull_allreduce_kernel(const __grid_con
 // slot q] words, written by the predecessor.  A sender reuses a parity two launches
 // later, when (stream order + the all-gather chain) its successor has finished with
 // it; the halves are fixed so that launches of different sizes never overlap.
+#ifndef HVD_LL_BACKOFF
+#define HVD_LL_BACKOFF 0
+#endif
 __device__ __forceinline__ void ll_store(unsigned long long* p, uint4 x, unsigned flag) {
   const unsigned long long f = (unsigned long long)flag << 32;
   asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1,%2};" ::"l"(p), "l"(f | x.x), "l"(f | x.y) : "memory");
@@ -1438,6 +1441,9 @@ __device__ __forceinline__ bool ll_load(const unsigned long long* p, unsigned fl
         return false;
       }
     }
+#if HVD_LL_BACKOFF > 0
+    if (spins > 8) __nanosleep(HVD_LL_BACKOFF);  // fewer polls in flight while the words travel
+#endif
   }
   x = make_uint4((uint32_t)a, (uint32_t)b, (uint32_t)c, (uint32_t)d);
   return true;
@@ -1617,6 +1623,9 @@ cudaError_t launch_ring(const RingParams& p, int dtype, int nch, int nlocal, int
 #ifndef HVD_SOLO_U
 #define HVD_SOLO_U 8
 #endif
+#ifndef HVD_SOLO_TMA
+#define HVD_SOLO_TMA 1
+#endif
 constexpr int kSoloThreads = HVD_SOLO_THREADS;
 constexpr int kSoloU = HVD_SOLO_U;  // 16 B wire vectors per thread (same-dtype wire)
 
@@ -1655,8 +1664,40 @@ __global__ void __launch_bounds__(kSoloThreads) solo_kernel(const __grid_constan
   const unsigned long long e0 = base * VEL;
   const char* g0 = reinterpret_cast<const char*>(sc.g + e0 * TESZ);
   char* d0 = reinterpret_cast<char*>(sc.d + e0 * TESZ);
-  if (t_end * VEL <= sc.end_el && t_end <= sc.vhi &&
-      ((reinterpret_cast<uintptr_t>(g0) | reinterpret_cast<uintptr_t>(d0)) & 15) == 0) {
+  const bool fast = t_end * VEL <= sc.end_el && t_end <= sc.vhi &&
+                    ((reinterpret_cast<uintptr_t>(g0) | reinterpret_cast<uintptr_t>(d0)) & 15) == 0;
+#if HVD_SOLO_TMA
+  if constexpr (TESZ == ESZ) {
+    // same dtype: the tile moves HBM -> shared -> HBM by bulk copies (TMA engine), the
+    // threads only scale it in shared memory; in-flight bytes cost shared memory, not
+    // registers (~14 CTAs x 16 KiB per SM)
+    __shared__ __align__(128) uint4 s_tile[TILE];
+    __shared__ __align__(8) unsigned long long s_bar;
+    if (fast) {
+      const unsigned bytes = (unsigned)((t_end - base) * 16);
+      if (tid == 0) {
+        mbar_init(&s_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_expect_tx(&s_bar, bytes);
+        tma_load(s_tile, g0, bytes, &s_bar);
+      }
+      __syncthreads();
+      mbar_wait(&s_bar, 0);
+      for (unsigned long long v = tid; v < t_end - base; v += kSoloThreads)
+        s_tile[v] = Pack16<ESZ>::conv(s_tile[v], F.scale, F.scale_on, F.dtype);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async-proxy reads
+      __syncthreads();
+      if (tid == 0) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                     ::"l"(d0), "r"(smem_u32(s_tile)), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // shared memory read before exit
+      }
+      return;
+    }
+  }
+#endif
+  if (fast) {
     constexpr unsigned long long VB = (unsigned long long)VEL * TESZ;  // tensor bytes per wire vector
     const char* gp = g0 + tid * VB;
     char* dp = d0 + tid * VB;
