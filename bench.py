@@ -13,8 +13,19 @@ per-rank ring traffic of P:L197-204).  At N = 1 the ring has no iterations
 (factor 0), so ``value`` is the algorithmic bandwidth payload_bytes / t of the
 N = 1 path (pack/scale + unpack) and ``value_kind`` says so.
 
+Timed region: K steps between barriers, CUDA events on the stream, max over
+ranks, no per-launch events; inputs are registered gradient tensors rotated
+over > 2 x L2.  ``roofline``: the dominant kernel (here the only kernel of a
+step) with its algorithmic bytes per launch over its average launch duration
+in the timed region; a second, profiled pass (events around every launch)
+gives ``achieved_profiled`` and ``share_of_step``.  ``e2e``: the same metric
+through ``comm.allreduce_host`` with pinned host gradients in and the averaged
+result out (H2D / ring / D2H pipelined in 8 MiB chunks).  ``cpu_baseline``:
+the oracle on a bounded sample, rank 0, N = 1 only.
+
 ``--impl reference`` times the CPU oracle (``oracle/``) — the only reference
-this tier has — on the same workload, on rank 0 only.
+this tier has — on the same workload, on rank 0 only: W warm-up + K steps of a
+bounded per-step sample.
 """
 from __future__ import annotations
 
