@@ -143,6 +143,7 @@ int cuda_fail(cudaError_t e, const char* what) {
 // buffer is `bufsz` = capacity + slack bytes (the slack absorbs the quantum rounding
 // of the channel-private layout).  `cap` arguments below are bufsz.
 constexpr uint64_t kRegionSlack = 2ull << 20;
+constexpr uint64_t kRegionFactor = 3;
 // [buf][scratch][pull0][pull1][scratch1][tail][LL]: scratch1 is the second
 // reduce-scatter receive half (a channel alternates halves buffer by buffer).
 constexpr uint64_t kNumBufs = 5;
@@ -170,7 +171,9 @@ unsigned long long* ll_of(char* region, uint64_t cap) {
 
 int common_init(hvd_comm* c, uint64_t fusion_bytes) {
   c->cap = ((fusion_bytes ? fusion_bytes : kDefaultFusionBytes) + 4095) / 4096 * 4096;
-  c->bufsz = c->cap + kRegionSlack;
+  // region buffers hold kRegionFactor fusion buffers: the buffers of a multi-buffer call
+  // then fit side by side in the channel-private layout and run concurrently
+  c->bufsz = kRegionFactor * c->cap + kRegionSlack;
   CK(cudaSetDevice(c->device));
   CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device));
   CK(cudaHostAlloc(reinterpret_cast<void**>(&c->err_host), sizeof(int), cudaHostAllocMapped));
@@ -585,7 +588,65 @@ int enqueue_fused_multi(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStrea
   F.nbuf = nb;
   int maxseg = 0;
   std::vector<unsigned long long> signals(nch, 0);
-  int next_owner = 0;
+  // Channels per buffer.  One buffer: all.  Several: ~64 KiB of every chunk per channel
+  // (want), at least enough channels for the buffer's slots to fit their private regions
+  // (need).  When every buffer's need fits, the channels are split into disjoint ranges
+  // in proportion to the buffers' sizes, so all buffers of the call run at once;
+  // otherwise ranges of `want` channels are assigned round robin (they overlap and a
+  // channel runs its buffers in order).
+  // (disjoint ranges only for a few buffers: with many, one channel minimum per buffer
+  // would leave the large buffers too few channels)
+  constexpr int kDisjointMaxBufs = 16;
+  std::vector<int> kk(nb, nch), first(nb, -1);
+  if (nb > 1 && nch > 1) {
+    std::vector<int> want(nb), need(nb);
+    std::vector<uint64_t> qs(nb);
+    long sum_want = 0, sum_need = 0;
+    for (int i = 0; i < nb; ++i) {
+      qs[i] = chunk_len(bs[i]->L, N, dtype);
+      want[i] = (int)std::min<uint64_t>((uint64_t)nch, std::max<uint64_t>(1, (qs[i] * esz + (64 << 10) - 1) / (64 << 10)));
+      int k = 1;
+      while (k < nch && (uint64_t)N * ((qs[i] + (uint64_t)k * g - 1) / ((uint64_t)k * g) * g) > F.region_el) ++k;
+      need[i] = k;
+      sum_want += want[i];
+      sum_need += need[i];
+    }
+    if (sum_need <= nch && nb <= kDisjointMaxBufs) {
+      int used = 0;
+      for (int i = 0; i < nb; ++i) {
+        kk[i] = sum_want <= nch ? std::max(want[i], need[i])
+                                : std::max(need[i], (int)((long)nch * want[i] / sum_want));
+        used += kk[i];
+      }
+      while (used > nch) {  // trim the buffer with the most channels above its need
+        int j = -1;
+        for (int i = 0; i < nb; ++i)
+          if (kk[i] > need[i] && (j < 0 || kk[i] > kk[j])) j = i;
+        --kk[j];
+        --used;
+      }
+      if (sum_want > nch)
+        while (used < nch) {  // spare channels to the buffer with the most data per channel
+          int j = 0;
+          for (int i = 1; i < nb; ++i)
+            if (qs[i] * kk[j] > qs[j] * kk[i]) j = i;
+          ++kk[j];
+          ++used;
+        }
+      int f = 0;
+      for (int i = 0; i < nb; ++i) {
+        first[i] = kk[i] < nch ? f : -1;
+        f += kk[i];
+      }
+    } else {
+      int next_owner = 0;
+      for (int i = 0; i < nb; ++i) {
+        kk[i] = std::max(want[i], need[i]);
+        first[i] = kk[i] < nch ? next_owner : -1;
+        if (kk[i] < nch) next_owner = (next_owner + kk[i]) % nch;
+      }
+    }
+  }
   for (int i = 0; i < nb; ++i) {
     const DevPlanBuffer& b = *bs[i];
     BufDesc& D = F.bufs[i];
@@ -597,17 +658,9 @@ int enqueue_fused_multi(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStrea
     D.nseg = b.pp.nseg;
     D.L = b.L;
     D.q = chunk_len(b.L, N, dtype);
-    // In a multi-buffer call a buffer runs on k consecutive channels (round robin), about
-    // 64 KiB of every chunk per channel, so many small and medium buffers proceed in
-    // parallel; k grows until the buffer's slots fit the channels' private regions.
-    int k = nch;
-    if (nb > 1 && nch > 1) {
-      k = (int)std::min<uint64_t>((uint64_t)nch, std::max<uint64_t>(1, (D.q * esz + (64 << 10) - 1) / (64 << 10)));
-      while (k < nch && (uint64_t)N * ((D.q + (uint64_t)k * g - 1) / ((uint64_t)k * g) * g) > F.region_el) ++k;
-    }
-    D.owner = k < nch ? next_owner : -1;  // first channel of the range
+    const int k = kk[i];
+    D.owner = first[i];  // first channel of the range (-1: all channels)
     D.nch = k;
-    if (k < nch) next_owner = (next_owner + k) % nch;
     D.ch_el = (D.q + (uint64_t)k * g - 1) / ((uint64_t)k * g) * g;
     uint64_t sb = (uint64_t)c->slice_bytes;
     if (sb == 0) sb = std::min<uint64_t>(128 << 10, std::max<uint64_t>(32 << 10, D.ch_el * esz / 2));
