@@ -173,7 +173,7 @@ int common_init(hvd_comm* c, uint64_t fusion_bytes) {
   c->cap = ((fusion_bytes ? fusion_bytes : kDefaultFusionBytes) + 4095) / 4096 * 4096;
   // region buffers hold kRegionFactor fusion buffers: the buffers of a multi-buffer call
   // then fit side by side in the channel-private layout and run concurrently
-  c->bufsz = kRegionFactor * c->cap + kRegionSlack;
+  c->bufsz = (c->cap <= (256ull << 20) ? kRegionFactor : 1) * c->cap + kRegionSlack;
   CK(cudaSetDevice(c->device));
   CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device));
   CK(cudaHostAlloc(reinterpret_cast<void**>(&c->err_host), sizeof(int), cudaHostAllocMapped));
