@@ -209,7 +209,7 @@ typedef enum {
   HVD_CFG_FIN_LAG = 11,      /* fused: slices by which the final local scatter trails the last
                                 all-gather iteration (>= K-1: scatter after all of it)     */
   HVD_CFG_LL_MAX_BYTES = 14, /* a call that is one fusion buffer of at most this many bytes
-                                (default 4 MiB at N = 2, 8 MiB at N > 2; max 8 MiB; 0 = never)
+                                (default 2 MiB at N = 2, 4 MiB at N > 2; max 8 MiB; 0 = never)
                                 uses the LL protocol: {epoch, data} words, no fences or
                                 counters (fp32/bf16/i32) */
   HVD_CFG_MULTI_BUFFERS = 13, /* fusion buffers per fused launch (1..96, default 96): the

@@ -176,7 +176,7 @@ cudaError_t launch_fused(const FusedParams& p, int dtype, int nch, int nlocal, i
 cudaError_t launch_copy(const FusedParams& p, int dtype, int nch, int nlocal, int threads, cudaStream_t s);
 cudaError_t launch_pull(const FusedParams& p, int dtype, int nch, int nlocal, int threads, cudaStream_t s);
 cudaError_t launch_ll(const FusedParams& p, int dtype, int nch, int nlocal, cudaStream_t s);
-constexpr unsigned long long kLLMaxBytes = 4ull << 20;    // default LL payload limit at N = 2 (N > 2: kLLLimitBytes)
+constexpr unsigned long long kLLMaxBytes = 2ull << 20;    // default LL payload limit at N = 2 (N > 2: twice that)
 constexpr unsigned long long kLLLimitBytes = 8ull << 20;  // largest HVD_CFG_LL_MAX_BYTES accepted
 // 2 parities x (2N-2) steps x chunk slot of 2 q esz bytes (8 B word per 4 B of data)
 // = 8 (N-1) q esz < 8 L + 8 (N-1) N 256 for L <= kLLLimitBytes.

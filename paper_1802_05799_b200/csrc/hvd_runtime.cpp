@@ -203,8 +203,8 @@ int common_init(hvd_comm* c, uint64_t fusion_bytes) {
   int ll_per_sm = 0;
   CK(ll_max_ctas_per_sm(&ll_per_sm));
   c->ll_ctas = std::max(1, std::min(ll_per_sm, 4) * c->sm_count / c->nlocal);
-  // LL beats the fenced push up to ~4 MiB at N = 2 and ~8 MiB at N = 4 (profiles/r01_c5_*)
-  c->ll_max = (int64_t)(c->size <= 2 ? kLLMaxBytes : kLLLimitBytes);
+  // LL beats the fused push up to 2 MiB at N = 2 and 4 MiB at N = 4 (profiles/r01_ll_vs_fused_*)
+  c->ll_max = (int64_t)(c->size <= 2 ? kLLMaxBytes : 2 * kLLMaxBytes);
   CK(cudaDeviceSynchronize());
   return HVD_OK;
 }
