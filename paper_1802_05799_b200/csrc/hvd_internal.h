@@ -131,9 +131,9 @@ struct BufDesc {
   const unsigned long long* vbeg;    // [nseg] member start vectors
   unsigned long long L, q, ch_el, slice_el;
   int nseg, K;
-  int owner;                         // -1: every channel takes a share; else the one channel
-                                     //  that runs this (small) buffer alone
-  int nch;                           // LL: CTAs (channels) of this buffer
+  int owner;                         // fused: -1 = every channel takes a share; else the first
+                                     //  of the nch consecutive channels (mod grid) that run it
+  int nch;                           // fused: channels of this buffer; LL: its CTAs
   unsigned ll_off;                   // LL: word offset of this buffer's slots in a parity half
   int pad;
 };

@@ -496,7 +496,7 @@ __global__ void __launch_bounds__(256) pack_kernel(const __grid_constant__ PackP
 // exactly once before it is scattered (same CTA, program order), so the
 // in-place update of the caller's tensors is safe.  Results are bit-identical
 // to pack -> ring -> unpack: same per-element operations in the same order.
-enum FusedKind { kF_RS0 = 0, kF_RS = 1, kF_AG0 = 2, kF_AG = 3, kF_FIN = 4, kF_SOLO = 5,
+enum FusedKind { kF_RS0 = 0, kF_RS = 1, kF_AG0 = 2, kF_AG = 3, kF_FIN = 4,
                  kF_RAG0 = 8,   // registered all-gather step 0: final -> own tensors + successor's tensors
                  kF_RAG = 9,    // registered all-gather step s >= 1: own tensors -> successor's tensors
                  kF_G2B = 6,    // broadcast root:        nbuf <- gather(x)
@@ -734,10 +734,10 @@ __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& m
   constexpr int ESZ = Op::kEsz;  // wire element size
   constexpr int VEL = 16 / ESZ;
   using Cvt = WireCvt<ESZ, TESZ>;
-  constexpr bool GATHER = KIND == kF_RS0 || KIND == kF_RS || KIND == kF_AG0 || KIND == kF_SOLO ||
+  constexpr bool GATHER = KIND == kF_RS0 || KIND == kF_RS || KIND == kF_AG0 ||
                           KIND == kF_G2B || KIND == kF_G2BS || KIND == kF_RAG0 || KIND == kF_RAG;
   constexpr bool SCALE = KIND != kF_RAG;  // the registered forward reads final values: no prescale
-  constexpr bool SCATTER = KIND == kF_AG0 || KIND == kF_AG || KIND == kF_FIN || KIND == kF_SOLO || KIND == kF_G2BS ||
+  constexpr bool SCATTER = KIND == kF_AG0 || KIND == kF_AG || KIND == kF_FIN || KIND == kF_G2BS ||
                            KIND == kF_RAG0;
   constexpr bool RSCATTER = KIND == kF_RAG0 || KIND == kF_RAG;  // into the successor's tensors
   constexpr bool ADD = KIND == kF_RS || KIND == kF_AG0 || KIND == kF_RAG0;
