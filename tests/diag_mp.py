@@ -10,7 +10,7 @@ import torch.distributed as dist
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-sys.path.insert(0, os.path.join(ROOT, "tests"))
+sys.path.insert(0, os.path.join(ROOT, "tests"))  # (this script lives in tests/: it calls the oracle)
 import oracle  # noqa: E402
 import paper_1802_05799_b200 as hvd  # noqa: E402
 import workloads  # noqa: E402
