@@ -327,6 +327,12 @@ int hvd_negotiator_ready(hvd_negotiator* g, int local, uint32_t id, uint64_t cou
 int hvd_negotiator_cycle(hvd_negotiator* g, uint32_t* ids_out, uint32_t* n_out);
 /* Pending ids of local rank `local` (in submission order; ids_out may be NULL). */
 int hvd_negotiator_pending(const hvd_negotiator* g, int local, uint32_t* ids_out, uint32_t* n_out);
+/* Negotiation records for the Horovod Timeline (P:L326-349 shows each tensor's
+ * negotiation phase): for every id agreed since the last read, out[3i..3i+2] =
+ * {id, ns when local rank `local` reported it ready, ns when the cycle agreed
+ * it} (CLOCK_REALTIME, comparable across the processes of a node).  out = NULL:
+ * *n_out = records available.  Records read are dropped.  Errors: INVALID. */
+int hvd_negotiator_trace(hvd_negotiator* g, int local, uint64_t* out, uint32_t cap, uint32_t* n_out);
 /* Unmap (rank 0 also unlinks the segment).  Idempotent on NULL. */
 int hvd_negotiator_destroy(hvd_negotiator* g);
 

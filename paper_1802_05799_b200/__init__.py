@@ -375,6 +375,14 @@ class Negotiator:
         check(lib.hvd_negotiator_pending(self._h, int(local), self._ids, C.byref(n)), "hvd_negotiator_pending")
         return list(self._ids[:n.value])
 
+    def trace(self, local: int = 0):
+        """Negotiation records since the last call: [(id, t_ready_ns, t_agreed_ns)] (Timeline)."""
+        n = C.c_uint32(0)
+        check(lib.hvd_negotiator_trace(self._h, int(local), None, 0, C.byref(n)), "hvd_negotiator_trace")
+        buf = (C.c_uint64 * max(1, 3 * n.value))()
+        check(lib.hvd_negotiator_trace(self._h, int(local), buf, n.value, C.byref(n)), "hvd_negotiator_trace")
+        return [(int(buf[3 * i]), int(buf[3 * i + 1]), int(buf[3 * i + 2])) for i in range(n.value)]
+
     def close(self):
         if self._h:
             lib.hvd_negotiator_destroy(self._h)

@@ -117,6 +117,7 @@ def _load():
         "hvd_negotiator_cycle": (C.c_int, [P, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
         "hvd_negotiator_pending": (C.c_int, [P, C.c_int, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
         "hvd_negotiator_destroy": (C.c_int, [P]),
+        "hvd_negotiator_trace": (C.c_int, [P, C.c_int, C.POINTER(C.c_uint64), C.c_uint32, C.POINTER(C.c_uint32)]),
         "hvd_allreduce_negotiated": (C.c_int, [P, P, C.POINTER(hvd_tensor), C.c_uint32, C.c_int, C.c_uint64, P,
                                                C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
     }
@@ -138,7 +139,7 @@ EXPORTS = sorted([
     "hvd_kernel_stats", "hvd_timeline", "hvd_allreduce_ex", "hvd_register_blob", "hvd_register",
     "hvd_allreduce_registered", "hvd_deregister", "hvd_negotiator_create", "hvd_negotiator_ready",
     "hvd_negotiator_cycle", "hvd_negotiator_pending", "hvd_negotiator_destroy", "hvd_allreduce_negotiated",
-    "hvd_allreduce_host",
+    "hvd_allreduce_host", "hvd_negotiator_trace",
 ])
 
 

@@ -17,6 +17,9 @@
 #include <sys/stat.h>
 #include <unistd.h>
 
+#include <time.h>
+
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstdlib>
@@ -53,6 +56,18 @@ struct SlotHead {
 
 bool valid_dtype(int d) { return d >= 1 && d <= 4; }
 
+uint64_t now_ns() {  // CLOCK_REALTIME: comparable across the processes of one node
+  timespec ts;
+  clock_gettime(CLOCK_REALTIME, &ts);
+  return (uint64_t)ts.tv_sec * 1000000000ull + (uint64_t)ts.tv_nsec;
+}
+
+constexpr size_t kTraceCap = 8192;  // negotiation records kept per local rank
+
+struct TraceRec {
+  uint64_t id, t_ready, t_agreed;
+};
+
 }  // namespace
 
 struct hvd_negotiator {
@@ -72,6 +87,8 @@ struct hvd_negotiator {
   std::vector<uint32_t> nranks;
   std::vector<Entry> meta;
   std::vector<Entry> agreed;  // last cycle's agreed entries, in order
+  std::vector<std::vector<uint64_t>> t_ready;   // [nlocal][max] when each pending id was reported
+  std::vector<std::vector<TraceRec>> trace;     // [nlocal] (id, reported, agreed) since the last read
 
   size_t slot_bytes() const { return sizeof(SlotHead) + (size_t)max * sizeof(Entry); }
   char* slot(int r, int par) const { return base + sizeof(Header) + ((size_t)r * 2 + par) * slot_bytes(); }
@@ -111,6 +128,8 @@ int hvd_negotiator_create(const char* shm_name, int rank, int size, int nlocal, 
   g->stamp.assign(max_tensors, 0);
   g->nranks.assign(max_tensors, 0);
   g->meta.assign(max_tensors, Entry{0, 0, 0});
+  g->t_ready.assign(nlocal, std::vector<uint64_t>(max_tensors, 0));
+  g->trace.assign(nlocal, {});
   Header* h = nullptr;
   if (!shm_name) {  // process-private: every rank lives in this process
     g->priv = true;
@@ -192,6 +211,7 @@ int hvd_negotiator_ready(hvd_negotiator* g, int local, uint32_t id, uint64_t cou
   if (!g || local < 0 || local >= g->nlocal || id >= g->max || !valid_dtype(dtype)) return HVD_ERR_INVALID;
   if (g->is_pending[local][id]) return HVD_ERR_INVALID;
   g->is_pending[local][id] = 1;
+  g->t_ready[local][id] = now_ns();
   g->pending[local].push_back(Entry{id, dtype, count});
   return HVD_OK;
 }
@@ -257,7 +277,10 @@ int hvd_negotiator_cycle(hvd_negotiator* g, uint32_t* ids_out, uint32_t* n_out) 
   for (size_t i = 0; i < g->agreed.size(); ++i) ids_out[i] = g->agreed[i].id;
   *n_out = (uint32_t)g->agreed.size();
   // drop the agreed ids from the local pending lists (order of the rest kept)
+  const uint64_t t_agreed = now_ns();
   for (int l = 0; l < g->nlocal; ++l) {
+    for (const Entry& a : g->agreed)
+      if (g->trace[l].size() < kTraceCap) g->trace[l].push_back(TraceRec{a.id, g->t_ready[l][a.id], t_agreed});
     for (const Entry& a : g->agreed) g->is_pending[l][a.id] = 2;  // mark for removal
     std::vector<Entry>& p = g->pending[l];
     size_t w = 0;
@@ -279,6 +302,24 @@ int hvd_negotiator_pending(const hvd_negotiator* g, int local, uint32_t* ids_out
   if (ids_out)
     for (size_t i = 0; i < p.size(); ++i) ids_out[i] = p[i].id;
   *n_out = (uint32_t)p.size();
+  return HVD_OK;
+}
+
+int hvd_negotiator_trace(hvd_negotiator* g, int local, uint64_t* out, uint32_t cap, uint32_t* n_out) {
+  if (!g || !n_out || local < 0 || local >= g->nlocal) return HVD_ERR_INVALID;
+  std::vector<TraceRec>& t = g->trace[local];
+  if (!out) {
+    *n_out = (uint32_t)t.size();
+    return HVD_OK;
+  }
+  const uint32_t n = (uint32_t)std::min<size_t>(t.size(), cap);
+  for (uint32_t i = 0; i < n; ++i) {
+    out[3 * i] = t[i].id;
+    out[3 * i + 1] = t[i].t_ready;
+    out[3 * i + 2] = t[i].t_agreed;
+  }
+  *n_out = n;
+  t.erase(t.begin(), t.begin() + n);
   return HVD_OK;
 }
 

@@ -91,9 +91,31 @@ def chrome_trace(timelines, align: str = "per_rank") -> dict:
     return {"traceEvents": events, "displayTimeUnit": "ns"}
 
 
-def write_chrome_trace(path: str, timelines) -> None:
+def negotiation_events(traces, names=None) -> list:
+    """Chrome events for ``Negotiator.trace()`` records, one list per rank: each agreed tensor
+    as a NEGOTIATE span from its ready report to the cycle that agreed it (Horovod Timeline's
+    negotiation phase).  Host CLOCK_REALTIME, so ranks of a node line up; shown
+    on a "negotiation" lane of each rank, relative to the earliest report."""
+    recs = [(r, rec) for r, tr in enumerate(traces) for rec in (tr or [])]
+    if not recs:
+        return []
+    t0 = min(rec[1] for _, rec in recs)
+    ev = []
+    for r in sorted({r for r, _ in recs}):
+        ev.append({"name": "thread_name", "ph": "M", "pid": r, "tid": "negotiation", "args": {"name": "negotiation"}})
+    for r, (tid, tr, ta) in recs:
+        nm = names[tid] if names and tid < len(names) else f"tensor {tid}"
+        ev.append({"name": f"NEGOTIATE {nm}", "cat": "NEGOTIATE", "ph": "X", "pid": r, "tid": "negotiation",
+                   "ts": (tr - t0) / 1e3, "dur": max(ta - tr, 1) / 1e3})
+    return ev
+
+
+def write_chrome_trace(path: str, timelines, negotiation=None, names=None) -> None:
+    tr = chrome_trace(timelines)
+    if negotiation:
+        tr["traceEvents"] += negotiation_events(negotiation, names)
     with open(path, "w") as f:
-        json.dump(chrome_trace(timelines), f)
+        json.dump(tr, f)
 
 
 def summarize(tl) -> dict:

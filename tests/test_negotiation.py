@@ -190,3 +190,31 @@ def test_c_negotiator_timeout_when_a_rank_is_absent():
     res = _run_shm(2, reports, skip_cycles=True)
     err = res[0][0]
     assert err[0] == "error" and err[1] == -5 and 1.0 <= err[2] <= 30.0
+
+
+def test_negotiation_trace_and_timeline_events(hvd):
+    """Timeline records of the negotiation phase: one (id, reported, agreed) per
+    agreed tensor and rank, agreed >= reported; exported as NEGOTIATE spans per rank."""
+    from paper_1802_05799_b200 import timeline
+    g = hvd.Negotiator(None, 0, 2, 2, 16, 1000)
+    try:
+        g.ready(3, 10, "f32", local=0)
+        g.ready(5, 20, "f32", local=0)
+        g.ready(5, 20, "f32", local=1)
+        time.sleep(0.002)
+        assert g.cycle() == [5]
+        g.ready(3, 10, "f32", local=1)
+        assert g.cycle() == [3]
+        tr = [g.trace(0), g.trace(1)]
+        assert [t[0] for t in tr[0]] == [5, 3] and [t[0] for t in tr[1]] == [5, 3]
+        for recs in tr:
+            for tid, t_ready, t_agreed in recs:
+                assert t_ready > 0 and t_agreed >= t_ready
+        assert tr[0][1][1] < tr[1][1][1]  # rank 0 reported tensor 3 before rank 1 did
+        assert g.trace(0) == []            # records are consumed
+        ev = timeline.negotiation_events(tr, names=[f"grad{i}" for i in range(16)])
+        spans = [e for e in ev if e.get("cat") == "NEGOTIATE"]
+        assert len(spans) == 4 and {e["name"] for e in spans} == {"NEGOTIATE grad5", "NEGOTIATE grad3"}
+        assert all(e["dur"] > 0 and e["ts"] >= 0 for e in spans)
+    finally:
+        g.close()
