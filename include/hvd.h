@@ -29,7 +29,10 @@
  *     allocated"), all released by hvd_finalize.
  *   - Collective contract: every rank makes the same sequence of collective
  *     calls with identical tensor counts, dtypes, op, threshold and root.  A
- *     mismatch is undefined behaviour (it can hang until the watchdog fires).
+ *     ring launch whose geometry differs between neighbours is caught by the
+ *     launch handshake (HVD_ERR_MISMATCH, async); other mismatches wait until
+ *     the watchdog fires (HVD_ERR_TIMEOUT).  Neither corrupts memory silently
+ *     nor hangs the GPU.
  *   - A comm is not thread-safe; use one comm per thread.
  *
  * Virtual ranks: hvd_init_virtual() creates a comm that simulates all N ranks
@@ -80,8 +83,12 @@ typedef struct hvd_comm hvd_comm; /* opaque */
 
 /* Create the comm of ring rank `rank` of `size` on CUDA device `device` and
  * allocate its fusion buffer of `fusion_bytes` (0 = default 64 MiB, P:L368-369;
- * rounded up to 4 KiB) plus an equal-size reduce-scatter scratch and the signal
- * flags.  For size > 1 the comm must then exchange blobs and hvd_connect().
+ * rounded up to 4 KiB).  One device region holds it together with two
+ * reduce-scatter scratch halves, two pull-protocol buffers, the signal / ready
+ * / hash words and the LL region.  Each region buffer is sized 3x the capacity
+ * (capacity <= 256 MiB) so that the buffers of a multi-buffer call fit side by
+ * side; that is about 1 GB at the default.  For size > 1 the comm must then
+ * exchange blobs and hvd_connect().
  * Errors: INVALID (size < 1, rank out of range, null out), CUDA. */
 int hvd_init(int rank, int size, int device, uint64_t fusion_bytes, hvd_comm** out);
 
@@ -116,10 +123,14 @@ int hvd_local_ranks(const hvd_comm* c); /* ranks driven by this comm (1 or N)   
  * aligned members, same dtype; fusion_threshold == 0 turns fusion off; a tensor
  * larger than the limit is split into limit-sized segments — DESIGN.md R6-R8).
  * Per buffer: pack (with x * fl32(1/N) for AVERAGE, R1) -> ring reduce-scatter
- * + all-gather -> unpack, all enqueued on `stream`.
+ * + all-gather -> unpack, all enqueued on `stream`.  How (same
+ * bits every way): by default one persistent launch per call gathers in the
+ * first ring step and scatters in the all-gather steps (zero-copy, all buffers
+ * of the call pipelined); buffers up to HVD_CFG_LL_MAX_BYTES (or 256 KiB in a
+ * multi-buffer call) take the LL latency protocol; at N = 1 a plain HBM stream.
  * op: HVD_SUM (all dtypes) or HVD_AVERAGE (float dtypes only).
  * Errors: INVALID (null/size), UNSUPPORTED (AVERAGE on integers, bad dtype),
- * NOT_CONNECTED, TIMEOUT (latched), CUDA. */
+ * NOT_CONNECTED, TIMEOUT / MISMATCH (latched), CUDA. */
 int hvd_allreduce(hvd_comm* c, const hvd_tensor* t, int n, int op, uint64_t fusion_threshold,
                   void* stream);
 
