@@ -429,17 +429,21 @@ cudaEvent_t pool_event(hvd_comm* c) {
 }
 
 // Wraps one kernel launch: counts it and, when profiling, brackets it with events.
+constexpr size_t kMaxTimed = 1 << 16;
 template <class F>
 int launch_counted(hvd_comm* c, int kind, cudaStream_t s, F&& launch) {
   hvd_comm::Timed t = {kind, nullptr, nullptr};
-  if (c->profile) {
+  // per-launch events until hvd_kernel_stats collects them (bounded: a caller that
+  // never collects stops being profiled instead of growing without limit)
+  const bool prof = c->profile && c->timed.size() < kMaxTimed;
+  if (prof) {
     t.a = pool_event(c);
     t.b = pool_event(c);
     CK(cudaEventRecord(t.a, s));
   }
   CK(launch());
   c->launches[kind] += 1;
-  if (c->profile) {
+  if (prof) {
     CK(cudaEventRecord(t.b, s));
     c->timed.push_back(t);
   }
