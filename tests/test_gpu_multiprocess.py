@@ -58,6 +58,23 @@ def _worker(rank, world, port, cases, q, protocol):
                     torch.cuda.synchronize()
                     res_its.append([from_torch(t, "f32") for t in ts])
                 out.append(res_its)
+            elif kind == "mixed_collectives":
+                # allreduce (fused), broadcast, allgather and a small (LL) allreduce back to back,
+                # no host sync: every kernel kind's launch handshake against every other's
+                res_its = []
+                for it in range(4):
+                    big = to_torch(workloads.rank_tensor(counts[0], dtype, rank, it, "normal"), dtype)
+                    small = to_torch(workloads.rank_tensor(counts[1], dtype, rank, 10 + it, "normal"), dtype)
+                    bc = to_torch(workloads.rank_tensor(counts[2], dtype, rank, 20 + it, "normal"), dtype)
+                    ag_in = to_torch(workloads.rank_tensor(counts[3], dtype, rank, 30 + it, "normal"), dtype)
+                    ag_out = torch.empty(world * counts[3], dtype=ag_in.dtype, device="cuda")
+                    comm.allreduce_average([big])
+                    comm.broadcast([bc], root=it % world)
+                    comm.allgather(ag_in, ag_out)
+                    comm.allreduce_average([small])
+                    res_its.append([big, small, bc, ag_out])
+                torch.cuda.synchronize()
+                out.append([[from_torch(t, dtype) for t in r] for r in res_its])
             elif kind == "mixed_sizes":
                 # back-to-back calls of alternating sizes, no host sync in between: LL and fused
                 # launches of different geometry reuse receive regions (DESIGN.md Hazards)
@@ -134,6 +151,7 @@ CASES = [
     ("negotiated", [5, 1 << 20, 333, 70_001, 2_000_003, 17, 4096], "f32", None, 4 << 20),
     ("host", [3_000_001], "f32", "average", 1 << 20),
     ("mixed_sizes", [262_144, 5_000, 786_432, 25, 3_000_000, 1_048_576, 777], "f32", "average", 0),
+    ("mixed_collectives", [4_000_000, 3_000, 100_001, 50_000], "f32", None, 0),
     ("registered", [17, 3_000_001, 64, 500_000], "f32", "average", 8 << 20),
     ("registered", [16 << 20], "f32", "average", 64 << 20),  # bench.py's step: one registered 64 MiB gradient
     ("allgather", [100_003], "f32", None, 0),
@@ -170,6 +188,22 @@ def test_multiprocess_ring_matches_oracle(protocol):
                 for r in range(n):
                     for k in range(len(counts)):
                         assert_same(res[r][0][ci][it][k], ref[r][k], "f32", f"registered it={it} r={r} k={k}")
+        elif kind == "mixed_collectives":
+            for it in range(4):
+                big = [[workloads.rank_tensor(counts[0], dtype, r, it, "normal")] for r in range(n)]
+                small = [[workloads.rank_tensor(counts[1], dtype, r, 10 + it, "normal")] for r in range(n)]
+                bc = [[workloads.rank_tensor(counts[2], dtype, r, 20 + it, "normal")] for r in range(n)]
+                ag = [workloads.rank_tensor(counts[3], dtype, r, 30 + it, "normal") for r in range(n)]
+                rb, _, _ = oracle.allreduce(big, [dtype], "average")
+                rs, _, _ = oracle.allreduce(small, [dtype], "average")
+                rc, _ = oracle.broadcast(bc, it % n)
+                ra, _ = oracle.allgather(ag)
+                for r in range(n):
+                    got = res[r][0][ci][it]
+                    assert_same(got[0], rb[r][0], dtype, f"mixed big it={it} rank {r}")
+                    assert_same(got[1], rs[r][0], dtype, f"mixed small it={it} rank {r}")
+                    assert np.array_equal(got[2].view(np.uint8), rc[r][0].view(np.uint8)), f"bcast it={it} r={r}"
+                    assert_same(got[3], ra[r], dtype, f"mixed allgather it={it} rank {r}")
         elif kind == "mixed_sizes":
             for it in range(16):
                 c = counts[it % len(counts)]
