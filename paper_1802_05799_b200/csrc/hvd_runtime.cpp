@@ -86,7 +86,7 @@ struct hvd_comm {
   // tuning (hvd_set_config)
   int channels = 128;
   int64_t slice_bytes = 0;  // 0 = auto: about half of a channel's share of a chunk, 32..128 KiB
-  int threads = 384;
+  int threads = 256;  // HVD_CFG_THREADS (256 vs 384: 0.5-1 % faster at N = 2, 4; 98 vs 147 KB smem)
   int64_t timeout_ms = 30000;
   int pack_ctas_per_sm = 8;
   int profile = 0;
