@@ -1712,23 +1712,36 @@ __global__ void __launch_bounds__(kSoloThreads) solo_kernel(const __grid_constan
         Cvt::put(dp + (unsigned long long)u * kSoloThreads * VB, VEL, Cvt::take(raw[u], F.scale, F.scale_on, F.dtype));
     return;
   }
-  for (int u = 0; u < U; ++u) {  // member boundary, ragged end or misaligned tensor
-    const unsigned long long v = base + (unsigned long long)u * kSoloThreads + tid;
-    if (v >= t_end) break;
-    seg_lookup<TESZ>(F, v, sc);
-    const unsigned long long e = v * VEL;
-    const unsigned long long left = sc.end_el > e ? sc.end_el - e : 0;
-    if (left == 0) continue;  // padding after a member
-    const char* gp = reinterpret_cast<const char*>(sc.g + e * TESZ);
-    uint4 x;
-    if (Cvt::fast(gp, left)) {
-      Raw32 raw;
-      Cvt::load(raw, gp);
-      x = Cvt::take(raw, F.scale, F.scale_on, F.dtype);
-    } else {
-      x = Cvt::slow(gp, left, F.scale, F.scale_on, F.dtype);
+  // member boundary, ragged end or misaligned tensor: per-vector member lookup, the
+  // loads of each group of H vectors issued together (memory-level parallelism)
+  constexpr int H = U / 4 > 0 ? U / 4 : 1;
+  for (int u0 = 0; u0 < U; u0 += H) {
+    Raw32 raw[H];
+    uintptr_t gp[H], dp[H];
+    unsigned long long left[H];
+    bool fast[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const unsigned long long v = base + (unsigned long long)(u0 + h) * kSoloThreads + tid;
+      left[h] = 0;
+      fast[h] = false;
+      if (v < t_end) {
+        seg_lookup<TESZ>(F, v, sc);
+        const unsigned long long e = v * VEL;
+        left[h] = sc.end_el > e ? sc.end_el - e : 0;  // 0: padding after a member
+        gp[h] = sc.g + e * TESZ;
+        dp[h] = sc.d + e * TESZ;
+        fast[h] = left[h] && Cvt::fast(reinterpret_cast<const char*>(gp[h]), left[h]);
+        if (fast[h]) Cvt::load(raw[h], reinterpret_cast<const char*>(gp[h]));
+      }
     }
-    Cvt::put(reinterpret_cast<char*>(sc.d + e * TESZ), left, x);
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      if (left[h] == 0) continue;
+      const uint4 x = fast[h] ? Cvt::take(raw[h], F.scale, F.scale_on, F.dtype)
+                              : Cvt::slow(reinterpret_cast<const char*>(gp[h]), left[h], F.scale, F.scale_on, F.dtype);
+      Cvt::put(reinterpret_cast<char*>(dp[h]), left[h], x);
+    }
   }
 }
 
