@@ -10,7 +10,11 @@ The paper's user-facing calls:
     hvd.init()                              -> ``init()``
     hvd.DistributedOptimizer (averaging)    -> ``Comm.allreduce_average(grads)``
     hvd.broadcast_global_variables(0)       -> ``Comm.broadcast(tensors, root=0)``
-plus ``Comm.allgather`` (north_star).
+plus ``Comm.allgather`` (north_star).  Also: ``Comm.register`` (zero-copy
+gradients), ``Comm.allreduce(..., wire="bf16")`` (wire dtype, R14),
+``negotiator`` / ``Comm.allreduce_negotiated`` (readiness cycle),
+``Comm.allreduce_host`` (pinned host gradients), ``Comm.timeline`` and
+``timeline.write_chrome_trace`` (Horovod Timeline).
 """
 from __future__ import annotations
 
