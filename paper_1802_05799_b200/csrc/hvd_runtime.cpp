@@ -765,10 +765,13 @@ int enqueue_ll(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStream_t s, ui
 
 // LL for a lone buffer up to ll_max; inside a multi-buffer plan only for buffers of at
 // most kLLMultiBytes (larger ones pipeline better inside the multi-buffer fused launch)
-constexpr int64_t kLLMultiBytes = 256 << 10;
+// (measured on Inception V3 with fusion off, profiles/r01_ll_multi_limit.json: at N = 2
+// 256 KiB is best; at N = 4 1 MiB cuts bf16 from 679 to 413 us and fp32 from 686 to 649 us)
+constexpr int64_t kLLMultiBytes = 256 << 10;     // N = 2
+constexpr int64_t kLLMultiBytesN4 = 1 << 20;     // N > 2
 bool ll_eligible(const hvd_comm* c, const DevPlanBuffer& b, bool multi) {
   const int esz = elem_size(b.dtype);
-  const int64_t lim = multi ? std::min<int64_t>(c->ll_max, kLLMultiBytes) : c->ll_max;
+  const int64_t lim = multi ? std::min<int64_t>(c->ll_max, c->size <= 2 ? kLLMultiBytes : kLLMultiBytesN4) : c->ll_max;
   return c->size > 1 && c->protocol == 1 && b.L > 0 && b.tdtype == b.dtype && b.dtype != HVD_INT64 &&
          (int64_t)(b.L * esz) <= lim;
 }
