@@ -87,7 +87,7 @@ typedef struct hvd_comm hvd_comm; /* opaque */
  * reduce-scatter scratch halves, two pull-protocol buffers, the signal / ready
  * / hash words and the LL region.  Each region buffer is sized 3x the capacity
  * (capacity <= 256 MiB) so that the buffers of a multi-buffer call fit side by
- * side; that is about 1 GB at the default.  For size > 1 the comm must then
+ * side, plus a 320 MiB LL / LL128 region: about 1.3 GB at the default.  For size > 1 the comm must then
  * exchange blobs and hvd_connect().
  * Errors: INVALID (size < 1, rank out of range, null out), CUDA. */
 int hvd_init(int rank, int size, int device, uint64_t fusion_bytes, hvd_comm** out);
@@ -127,7 +127,8 @@ int hvd_local_ranks(const hvd_comm* c); /* ranks driven by this comm (1 or N)   
  * bits every way): by default one persistent launch per call gathers in the
  * first ring step and scatters in the all-gather steps (zero-copy, all buffers
  * of the call pipelined); buffers up to HVD_CFG_LL_MAX_BYTES (or 256 KiB / 1 MiB at N = 2 / N > 2 in a
- * multi-buffer call) take the LL latency protocol; at N = 1 a plain HBM stream.
+ * multi-buffer call) take the LL latency protocol, a lone buffer up to
+ * HVD_CFG_LL128_MAX_BYTES the LL128 protocol; at N = 1 a plain HBM stream.
  * op: HVD_SUM (all dtypes) or HVD_AVERAGE (float dtypes only).
  * Errors: INVALID (null/size), UNSUPPORTED (AVERAGE on integers, bad dtype),
  * NOT_CONNECTED, TIMEOUT / MISMATCH (latched), CUDA. */
@@ -219,8 +220,13 @@ typedef enum {
                                 the NVLink backlog a fence waits for, so the signal latency */
   HVD_CFG_FIN_LAG = 11,      /* fused: slices by which the final local scatter trails the last
                                 all-gather iteration (>= K-1: scatter after all of it)     */
+  HVD_CFG_LL128_MAX_BYTES = 15, /* a call that is one fusion buffer larger than LL_MAX_BYTES
+                                and of at most this many bytes uses the LL128 protocol: flags
+                                inside 128-byte lines (relies on NVLink delivering a warp's
+                                128 B line store whole; 8/7 wire bytes).  Default 16 MiB at
+                                N = 2, 32 MiB at N > 2; max 64 MiB; 0 = never.             */
   HVD_CFG_LL_MAX_BYTES = 14, /* a call that is one fusion buffer of at most this many bytes
-                                (default 2 MiB at N = 2, 4 MiB at N > 2; max 8 MiB; 0 = never)
+                                (default 256 KiB; max 8 MiB; 0 = never, also in multi-buffer calls)
                                 uses the LL protocol: {epoch, data} words, no fences or
                                 counters (fp32/bf16/i32) */
   HVD_CFG_MULTI_BUFFERS = 13, /* fusion buffers per fused launch (1..96, default 96): the
@@ -235,7 +241,7 @@ int64_t hvd_get_config(const hvd_comm* c, int key);
 
 typedef enum { HVD_KERNEL_PACK = 0, HVD_KERNEL_RING = 1, HVD_KERNEL_UNPACK = 2, HVD_KERNEL_SCALE = 3,
                HVD_KERNEL_FUSED = 4, HVD_KERNEL_COPY = 5, HVD_KERNEL_PULL = 6, HVD_KERNEL_LL = 7,
-               HVD_KERNEL_SOLO = 8, HVD_KERNEL_KINDS = 9 } hvd_kernel_kind;
+               HVD_KERNEL_SOLO = 8, HVD_KERNEL_LL128 = 9, HVD_KERNEL_KINDS = 10 } hvd_kernel_kind;
 /* Kernel launches of each kind since the last call (always counted) and, with
  * HVD_CFG_PROFILE on, the summed device time in ms between the CUDA events
  * recorded on the launch stream around each launch (waits for those events).

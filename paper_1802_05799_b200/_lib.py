@@ -36,13 +36,15 @@ HVD_CFG_FIN_LAG = 11
 HVD_CFG_PROTOCOL = 12
 HVD_CFG_MULTI_BUFFERS = 13
 HVD_CFG_LL_MAX_BYTES = 14
+HVD_CFG_LL128_MAX_BYTES = 15
 MAX_CHANNELS = 256
 HVD_KERNEL_PACK, HVD_KERNEL_RING, HVD_KERNEL_UNPACK, HVD_KERNEL_SCALE, HVD_KERNEL_FUSED = 0, 1, 2, 3, 4
 HVD_KERNEL_COPY = 5
 HVD_KERNEL_PULL = 6
 HVD_KERNEL_LL = 7
 HVD_KERNEL_SOLO = 8
-HVD_KERNEL_KINDS = 9
+HVD_KERNEL_LL128 = 9
+HVD_KERNEL_KINDS = 10
 
 
 class hvd_tensor(C.Structure):

@@ -176,13 +176,17 @@ cudaError_t launch_fused(const FusedParams& p, int dtype, int nch, int nlocal, i
 cudaError_t launch_copy(const FusedParams& p, int dtype, int nch, int nlocal, int threads, cudaStream_t s);
 cudaError_t launch_pull(const FusedParams& p, int dtype, int nch, int nlocal, int threads, cudaStream_t s);
 cudaError_t launch_ll(const FusedParams& p, int dtype, int nch, int nlocal, cudaStream_t s);
-constexpr unsigned long long kLLMaxBytes = 2ull << 20;    // default LL payload limit at N = 2 (N > 2: twice that)
+constexpr unsigned long long kLLMaxBytes = 256ull << 10;  // default LL payload limit for a lone buffer
 constexpr unsigned long long kLLLimitBytes = 8ull << 20;  // largest HVD_CFG_LL_MAX_BYTES accepted
+constexpr unsigned long long kLL128LimitBytes = 64ull << 20;  // largest HVD_CFG_LL128_MAX_BYTES accepted
 // 2 parities x (2N-2) steps x chunk slot of 2 q esz bytes (8 B word per 4 B of data)
 // = 8 (N-1) q esz < 8 L + 8 (N-1) N 256 for L <= kLLLimitBytes.
-constexpr unsigned long long kLLRegionBytes = 8 * kLLLimitBytes + (64ull << 10);
+// LL128 needs 2 (N-1) x lines x 128 B per half ~ 2 (N-1)/N x 8/7 x L <= 2.3 L: 160 MiB
+// halves hold a 64 MiB buffer at any N <= 8
+constexpr unsigned long long kLLRegionBytes = 320ull << 20;
 cudaError_t pull_max_ctas_per_sm(int dtype, int threads, int* out);
 cudaError_t ll_max_ctas_per_sm(int* out);
+cudaError_t launch_ll128(const FusedParams& p, int dtype, int nch, int nlocal, cudaStream_t s);
 cudaError_t launch_solo(const FusedParams& p, int dtype, int nlocal, cudaStream_t s);
 cudaError_t fused_max_ctas_per_sm(int dtype, int threads, int* out);
 cudaError_t launch_pack(const PackParams& p, int dtype, int nlocal, int grid, int threads,

@@ -1527,6 +1527,129 @@ __global__ void __launch_bounds__(256) ll_allreduce_kernel(const __grid_constant
   }
 }
 
+// LL128 protocol: like LL, the data carries its own arrival flag, but per 128-byte
+// line instead of per 8-byte word.  Lanes 0..6 of an 8-lane group store 7 x 16 B of
+// data and lane 7 stores the flag {~epoch, ~epoch}, all in ONE warp store
+// instruction; the receiver loads the line the same way and accepts it when the flag
+// matches.  This relies on NVLink (and L2) delivering one warp store of a 128-byte
+// line whole — what NCCL's LL128 also relies on; PTX does not promise it.  Measured:
+// 134M lines, 0 torn (tools/ll128_probe.cu, profiles/r01_ll128_probe.json).  Wire
+// bytes are 8/7 of the data (LL: 2x).  Same chunks, same reduction order as the ring:
+// bit-identical.  Slot of step t: lines of 7 vectors of the chunk, in a fixed LL half.
+template <class Op>
+__global__ void __launch_bounds__(256) ll128_allreduce_kernel(const __grid_constant__ FusedParams P) {
+  constexpr int ESZ = Op::kEsz;
+  constexpr int VEL = 16 / ESZ;
+  constexpr unsigned FULL = 0xffffffffu;
+  const RingParams& R = P.ring;
+  const RingRank& me = R.rk[blockIdx.y];
+  const int ch = blockIdx.x;
+  const int nch = gridDim.x;
+  const int N = R.N;
+  const int r = me.rank;
+  const int T = 2 * (N - 1);
+  const BufDesc& D = P.bufs[0];
+  const unsigned long long flag = ~R.epoch;  // never an LL word nor zeroed memory
+  const int par = (int)(R.epoch & 1);
+  const unsigned long long qv = D.q / VEL;         // vectors per chunk
+  const unsigned long long lines = (qv + 6) / 7;   // 128 B lines per chunk slot
+  const unsigned long long slot_words = lines * 16;
+  constexpr unsigned long long kHalfWords = kLLRegionBytes / 2 / 8;
+  unsigned long long* const in_ll = me.ll + (unsigned long long)par * kHalfWords;
+  unsigned long long* const out_ll = me.nll + (unsigned long long)par * kHalfWords;
+  const unsigned long long lpc = (lines + nch - 1) / nch;  // lines of this channel
+  const unsigned long long l_lo = (unsigned long long)ch * lpc < lines ? (unsigned long long)ch * lpc : lines;
+  const unsigned long long l_hi = l_lo + lpc < lines ? l_lo + lpc : lines;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, sub = lane % 8;
+  const unsigned long long nvec = (D.L + VEL - 1) / VEL;
+  FusedCtx F;
+  F.segs = D.segs;
+  F.src = D.src + (size_t)blockIdx.y * D.nseg;
+  F.dst = D.dst + (size_t)blockIdx.y * D.nseg;
+  F.rdst = nullptr;
+  F.vbeg = D.vbeg;
+  F.nseg = D.nseg;
+  F.scale_on = P.scale_on;
+  F.scale = P.scale;
+  F.dtype = P.dtype;
+  using Cvt = WireCvt<ESZ, ESZ>;
+  SegCache sc;
+  bool ok = true;
+  unsigned long long sent = 0;
+  for (int t = 0; t <= T && ok; ++t) {  // t == T: the chunk received in the last step
+    const bool rs = t < N - 1;
+    const int s = rs ? t : t - (N - 1);
+    const int c = t == T ? mod(r + 2, N) : (rs ? mod(r - s, N) : mod(r + 1 - s, N));
+    const unsigned long long c0v = (unsigned long long)c * qv;  // first vector of chunk c
+    for (unsigned long long lg = l_lo + (unsigned long long)warp * 4; lg < l_hi && ok; lg += 32) {
+      const unsigned long long line = lg + lane / 8;
+      const bool active = line < l_hi;
+      const unsigned long long cvec = line * 7 + sub;  // vector inside the chunk
+      const unsigned long long v = c0v + cvec;
+      const bool valid = active && sub < 7 && cvec < qv && v < nvec;
+      unsigned long long left = 0;
+      uint4 g = make_uint4(0, 0, 0, 0);
+      if (valid) {
+        seg_lookup<ESZ>(F, v, sc);
+        const unsigned long long e = v * VEL;
+        left = sc.end_el > e ? sc.end_el - e : 0;
+        if (t <= N - 1 && left) {
+          const char* gp = reinterpret_cast<const char*>(sc.g + e * ESZ);
+          g = Cvt::fast(gp, left) ? Pack16<ESZ>::conv(__ldcs(reinterpret_cast<const uint4*>(gp)), F.scale, F.scale_on,
+                                                      F.dtype)
+                                  : Cvt::slow(gp, left, F.scale, F.scale_on, F.dtype);
+        }
+      }
+      uint4 x = g;
+      if (t > 0) {
+        const unsigned long long* src = in_ll + (unsigned long long)(t - 1) * slot_words + line * 16 + sub * 2;
+        bool got = !active;
+        unsigned long long a = 0, b = 0, t0 = 0;
+        unsigned spins = 0;
+        for (;;) {
+          if (!got) asm volatile("ld.relaxed.sys.global.v2.u64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "l"(src) : "memory");
+          const unsigned long long f = __shfl_sync(FULL, b, (lane & ~7) | 7);
+          if (!got && f == flag) got = true;  // the line arrived whole (one 128 B warp store)
+          if (__all_sync(FULL, got)) break;
+          bool fail = false;
+          if ((++spins & 255u) == 0) {
+            const unsigned long long now = globaltimer();
+            if (t0 == 0) t0 = now;
+            else if (now - t0 > R.timeout_ns || *(volatile int*)R.err != 0) fail = true;
+          }
+          if (__any_sync(FULL, fail)) {
+            if (lane == 0) *(volatile int*)R.err = kHvdErrTimeout;
+            ok = false;
+            break;
+          }
+        }
+        if (!ok) break;
+        x = make_uint4((uint32_t)a, (uint32_t)(a >> 32), (uint32_t)b, (uint32_t)(b >> 32));
+        if (t <= N - 1) Op::template add_words<4>(reinterpret_cast<uint32_t*>(&x), reinterpret_cast<const uint32_t*>(&g));
+      }
+      if (t < T && active) {
+        unsigned long long* dst = out_ll + (unsigned long long)t * slot_words + line * 16 + sub * 2;
+        const unsigned long long w0 = sub < 7 ? ((unsigned long long)x.y << 32 | x.x) : flag;
+        const unsigned long long w1 = sub < 7 ? ((unsigned long long)x.w << 32 | x.z) : flag;
+        asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1,%2};" ::"l"(dst), "l"(w0), "l"(w1) : "memory");
+      }
+      if (t >= N - 1 && valid && left) Cvt::put(reinterpret_cast<char*>(sc.d + v * VEL * ESZ), left, x);
+    }
+    if (t < T) {  // data elements of this channel's lines of chunk c
+      const unsigned long long cl = (unsigned long long)c * D.q;
+      unsigned long long ce = cl + D.q < D.L ? cl + D.q : D.L;
+      const unsigned long long el = cl + l_lo * 7 * VEL;
+      unsigned long long eh = cl + l_hi * 7 * VEL;
+      eh = eh < ce ? eh : ce;
+      if (eh > el && threadIdx.x == 0) sent += (eh - el) * ESZ;
+    }
+  }
+  if (threadIdx.x == 0) {
+    atomicAdd(me.stats + 0, sent);
+    if (ch == 0) atomicAdd(me.stats + 1, (unsigned long long)T);
+  }
+}
+
 struct BufList { char* b[kMaxLocal]; };
 
 template <int ESZ>
@@ -1904,6 +2027,29 @@ static cudaError_t launch_ll_t(const FusedParams& p, int nch, int nlocal, cudaSt
   return cudaLaunchKernelEx(&cfg, ll_allreduce_kernel<Op>, p);
 }
 
+template <class Op>
+static cudaError_t launch_ll128_t(const FusedParams& p, int nch, int nlocal, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nch, nlocal);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // CTAs of all ranks wait on each other's lines
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, ll128_allreduce_kernel<Op>, p);
+}
+
+cudaError_t launch_ll128(const FusedParams& p, int dtype, int nch, int nlocal, cudaStream_t s) {
+  switch (dtype) {
+    case 1: return launch_ll128_t<OpF32>(p, nch, nlocal, s);
+    case 2: return launch_ll128_t<OpBF16>(p, nch, nlocal, s);
+    case 3: return launch_ll128_t<OpI32>(p, nch, nlocal, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 cudaError_t launch_ll(const FusedParams& p, int dtype, int nch, int nlocal, cudaStream_t s) {
   switch (dtype) {
     case 1: return launch_ll_t<OpF32>(p, nch, nlocal, s);
@@ -1919,7 +2065,14 @@ cudaError_t ll_max_ctas_per_sm(int* out) {
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, ll_allreduce_kernel<OpF32>, 256, 0);
   if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ll_allreduce_kernel<OpBF16>, 256, 0);
   if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, ll_allreduce_kernel<OpI32>, 256, 0);
-  *out = a < b ? (a < c ? a : c) : (b < c ? b : c);
+  int d = 0, f = 0, h = 0;  // the LL128 kernels share the budget
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d, ll128_allreduce_kernel<OpF32>, 256, 0);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&f, ll128_allreduce_kernel<OpBF16>, 256, 0);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h, ll128_allreduce_kernel<OpI32>, 256, 0);
+  int m = a < b ? (a < c ? a : c) : (b < c ? b : c);
+  m = m < d ? m : d;
+  m = m < f ? m : f;
+  *out = m < h ? m : h;
   return e;
 }
 

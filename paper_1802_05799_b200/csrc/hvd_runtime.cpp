@@ -99,6 +99,7 @@ struct hvd_comm {
   unsigned long long ll_epoch = 0;  // LL launches issued (flag value = epoch)
   int64_t ll_max = (int64_t)kLLMaxBytes;  // HVD_CFG_LL_MAX_BYTES
   int ll_ctas = 1;                         // co-resident LL CTAs per local rank
+  int64_t ll128_max = 0;                   // HVD_CFG_LL128_MAX_BYTES
   int protocol = 1;                 // 0: pull (receiver-initiated TMA loads), 1: push (SM stores)
   unsigned long long pbase[kMaxChannels] = {};  // pull-protocol progress counter bases
   int pull_calls = 0;
@@ -203,8 +204,10 @@ int common_init(hvd_comm* c, uint64_t fusion_bytes) {
   int ll_per_sm = 0;
   CK(ll_max_ctas_per_sm(&ll_per_sm));
   c->ll_ctas = std::max(1, std::min(ll_per_sm, 4) * c->sm_count / c->nlocal);
-  // LL beats the fused push up to 2 MiB at N = 2 and 4 MiB at N = 4 (profiles/r01_ll_vs_fused_*)
-  c->ll_max = (int64_t)(c->size <= 2 ? kLLMaxBytes : 2 * kLLMaxBytes);
+  // Protocol limits for a lone buffer (profiles/r01_ll128_crossover_n{2,4}.json): LL up to
+  // 256 KiB, LL128 up to 16 MiB (N = 2) / 32 MiB (N > 2), the fused push beyond
+  c->ll_max = (int64_t)kLLMaxBytes;
+  c->ll128_max = c->size <= 2 ? (int64_t)(16ull << 20) : (int64_t)(32ull << 20);
   CK(cudaDeviceSynchronize());
   return HVD_OK;
 }
@@ -769,9 +772,55 @@ int enqueue_ll(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStream_t s, ui
 // 256 KiB is best; at N = 4 1 MiB cuts bf16 from 679 to 413 us and fp32 from 686 to 649 us)
 constexpr int64_t kLLMultiBytes = 256 << 10;     // N = 2
 constexpr int64_t kLLMultiBytesN4 = 1 << 20;     // N > 2
+// LL128 (ll128_allreduce_kernel) for one buffer: lines of 7 vectors + a flag vector.
+uint64_t ll128_lines(const hvd_comm* c, const DevPlanBuffer& b) {
+  const uint64_t qv = chunk_len(b.L, c->size, b.dtype) * elem_size(b.dtype) / 16;
+  return (qv + 6) / 7;
+}
+
+bool ll128_eligible(const hvd_comm* c, const DevPlanBuffer& b) {
+  const int64_t bytes = (int64_t)(b.L * elem_size(b.dtype));
+  return c->size > 1 && c->protocol == 1 && b.L > 0 && b.tdtype == b.dtype && b.dtype != HVD_INT64 &&
+         bytes > c->ll_max && bytes <= c->ll128_max &&
+         (uint64_t)2 * (c->size - 1) * ll128_lines(c, b) * 128 <= kLLRegionBytes / 2;  // fits a half
+}
+
+int enqueue_ll128(hvd_comm* c, DevPlanBuffer& b, cudaStream_t s) {
+  const int dtype = b.dtype;
+  FusedParams F;
+  std::memset(&F, 0, sizeof(F));
+  int nch_unused = 0;
+  int st = make_ring_params(c, b.L, dtype, true, &F.ring, &nch_unused);
+  if (st != HVD_OK) return st;
+  BufDesc& D = F.bufs[0];
+  D.q = chunk_len(b.L, c->size, dtype);
+  D.segs = b.pp.segs;
+  D.src = b.pp.src;
+  D.dst = b.dst ? b.dst : b.pp.src;
+  D.vbeg = b.vbeg;
+  D.nseg = b.pp.nseg;
+  D.L = b.L;
+  D.ch_el = D.q;
+  D.slice_el = D.q;
+  D.K = 1;
+  D.owner = -1;
+  // one group of 4 lines per warp per step where the co-resident budget allows (8 warps)
+  const int nch = (int)std::min<uint64_t>((uint64_t)c->ll_ctas, std::max<uint64_t>(1, (ll128_lines(c, b) + 31) / 32));
+  D.nch = nch;
+  F.nbuf = 1;
+  F.scale_on = b.pp.scale_on;
+  F.scale = b.pp.scale;
+  F.dtype = dtype;
+  F.tdtype = dtype;
+  F.ring.epoch = ++c->ll_epoch;  // the LL epoch sequence: LL and LL128 launches alternate the halves
+  if (c->tl) c->tl_slices = 0;
+  return launch_counted(c, HVD_KERNEL_LL128, s, [&] { return launch_ll128(F, dtype, nch, c->nlocal, s); });
+}
+
 bool ll_eligible(const hvd_comm* c, const DevPlanBuffer& b, bool multi) {
   const int esz = elem_size(b.dtype);
-  const int64_t lim = multi ? std::min<int64_t>(c->ll_max, c->size <= 2 ? kLLMultiBytes : kLLMultiBytesN4) : c->ll_max;
+  // (ll_max == 0 turns LL off everywhere; otherwise multi-buffer calls have their own limit)
+  const int64_t lim = c->ll_max == 0 ? 0 : multi ? (c->size <= 2 ? kLLMultiBytes : kLLMultiBytesN4) : c->ll_max;
   return c->size > 1 && c->protocol == 1 && b.L > 0 && b.tdtype == b.dtype && b.dtype != HVD_INT64 &&
          (int64_t)(b.L * esz) <= lim;
 }
@@ -779,6 +828,7 @@ bool ll_eligible(const hvd_comm* c, const DevPlanBuffer& b, bool multi) {
 // The fused path for a whole plan: small buffers through the LL protocol (grouped),
 // the rest through multi-buffer fused launches (or the pull protocol per buffer).
 int enqueue_fused_plan(hvd_comm* c, CachedPlan* plan, cudaStream_t s) {
+  if (plan->bufs.size() == 1 && ll128_eligible(c, plan->bufs[0])) return enqueue_ll128(c, plan->bufs[0], s);
   std::vector<DevPlanBuffer*> group;
   const bool multi = plan->bufs.size() > 1;
   const uint64_t cta_bytes = multi ? (16 << 10) : 4096;
@@ -1527,6 +1577,10 @@ int hvd_set_config(hvd_comm* c, int key, int64_t value) {
       if (value < 0 || value > (int64_t)kLLLimitBytes) return HVD_ERR_INVALID;
       c->ll_max = value;
       return HVD_OK;
+    case HVD_CFG_LL128_MAX_BYTES:
+      if (value < 0 || value > (int64_t)kLL128LimitBytes) return HVD_ERR_INVALID;
+      c->ll128_max = value;
+      return HVD_OK;
     case HVD_CFG_MULTI_BUFFERS:
       if (value < 1 || value > kMaxMultiBufs) return HVD_ERR_INVALID;
       c->multi_bufs = (int)value;
@@ -1578,6 +1632,7 @@ int64_t hvd_get_config(const hvd_comm* c, int key) {
     case HVD_CFG_PROTOCOL: return c->protocol;
     case HVD_CFG_MULTI_BUFFERS: return c->multi_bufs;
     case HVD_CFG_LL_MAX_BYTES: return c->ll_max;
+    case HVD_CFG_LL128_MAX_BYTES: return c->ll128_max;
     case HVD_CFG_FIN_LAG: return c->fin_lag;
     default: return -1;
   }

@@ -329,8 +329,10 @@ def _mismatch_worker(rank, world, port, q):
         comm = hvd.init()
         comm.set_config(hvd._lib.HVD_CFG_TIMEOUT_MS, 3000)
         dist.barrier()
-        # the collective contract broken: rank 0 reduces 3M elements, rank 1 5M (both fused)
-        x = torch.ones(3_000_000 if rank == 0 else 5_000_000, device="cuda")
+        # the collective contract broken: rank 0 reduces 6M elements, rank 1 10M (both on the
+        # fused push kernel, whose launch handshake compares call hashes; the LL protocols have
+        # no handshake and report a mismatch through the watchdog)
+        x = torch.ones(6_000_000 if rank == 0 else 10_000_000, device="cuda")
         comm.allreduce_average([x])
         torch.cuda.synchronize()
         q.put((rank, comm.poll_error()))

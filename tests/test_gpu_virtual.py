@@ -178,6 +178,7 @@ def test_tuning_knobs_keep_bits(hvd):
         ref, _, _ = oracle.allreduce(xs, ["f32", "f32"], "average")
         L = hvd._lib
         comm.set_config(L.HVD_CFG_LL_MAX_BYTES, 0)  # one small buffer: keep it on the fused kernel
+        comm.set_config(L.HVD_CFG_LL128_MAX_BYTES, 0)
         for ch, sl, th in [(1, 256, 64), (7, 4096, 256), (64, 1 << 20, 384), (16, 65536, 128), (256, 512, 96)]:
             comm.set_config(L.HVD_CFG_CHANNELS, ch)
             comm.set_config(L.HVD_CFG_SLICE_BYTES, sl)
@@ -263,7 +264,8 @@ def test_timeline_records_every_slice(hvd):
     try:
         comm.set_config(hvd._lib.HVD_CFG_TIMELINE, 256)
         comm.set_config(hvd._lib.HVD_CFG_PROTOCOL, 1)  # push kernel records
-        comm.set_config(hvd._lib.HVD_CFG_LL_MAX_BYTES, 0)  # the LL kernel records no timeline
+        comm.set_config(hvd._lib.HVD_CFG_LL_MAX_BYTES, 0)  # the LL kernels record no timeline
+        comm.set_config(hvd._lib.HVD_CFG_LL128_MAX_BYTES, 0)
         ts = [[torch.randn(1 << 20, device="cuda")] for _ in range(n)]
         comm.allreduce_average(ts)
         torch.cuda.synchronize()
@@ -642,3 +644,65 @@ def test_fusion_off_mixed_sizes_channel_ranges(hvd, n):
             for k in range(len(counts)):
                 assert_same(from_torch(ts[r][k], "f32"), ref[r][k], "f32", f"ll={ll_max} r={r} k={k}")
     comm.set_config(hvd._lib.HVD_CFG_LL_MAX_BYTES, ll_default)
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 8])
+def test_ll128_protocol_bitexact(hvd, n):
+    """LL128 (flag inside each 128-byte line): same bits as the oracle's ring for ragged and
+    multi-member buffers, interleaved with LL and fused calls (shared LL halves and epochs)."""
+    comm = comm_for(hvd, n)
+    L = hvd._lib
+    ll_d, ll128_d = comm.get_config(L.HVD_CFG_LL_MAX_BYTES), comm.get_config(L.HVD_CFG_LL128_MAX_BYTES)
+    cases = [([1], "f32", 16 << 20), ([1000, 7, 65_536], "bf16", 16 << 20), ([1_000_003], "f32", 16 << 20),
+             ([500_000, 3, 77_777], "i32", 16 << 20), ([2_000_001], "bf16", 16 << 20),
+             ([300_000], "f32", 1 << 20),          # LL (multi-limit) between LL128 calls
+             ([3_999_999], "f32", 16 << 20), ([5_000], "f32", 0)]  # ll128 off: fused
+    try:
+        pend = []
+        comm.kernel_stats()
+        n128 = 0
+        for it, (counts, dt, ll128) in enumerate(cases):
+            comm.set_config(L.HVD_CFG_LL_MAX_BYTES, 0 if ll128 == 16 << 20 else ll_d)
+            comm.set_config(L.HVD_CFG_LL128_MAX_BYTES, ll128)
+            n128 += ll128 == 16 << 20
+            kind = "normal" if dt in ("f32", "bf16") else "int_uniform"
+            op = "average" if dt in ("f32", "bf16") else "sum"
+            xs = workloads.all_ranks(counts, dt, n, kind=kind, seed=400 + it)
+            ts = [[to_torch(x, dt) for x in xs[r]] for r in range(n)]
+            if it == 1:  # a misaligned member
+                big = torch.empty(counts[0] + 1, dtype=ts[0][0].dtype, device="cuda")
+                big[1:].copy_(ts[0][0])
+                ts[0][0] = big[1:]
+                pend.append(big)
+            comm.allreduce(ts, op=op)
+            pend.append((xs, ts, dt, op, counts))
+        torch.cuda.synchronize()
+        assert comm.poll_error() == 0
+        st = comm.kernel_stats()
+        assert st["ll128"][0] == n128
+        for item in pend:
+            if not isinstance(item, tuple):
+                continue
+            xs, ts, dt, op, counts = item
+            ref, _, _ = oracle.allreduce(xs, [dt] * len(counts), op)
+            for r in range(n):
+                for k in range(len(counts)):
+                    assert_same(from_torch(ts[r][k], dt), ref[r][k], dt, f"{dt} {counts} r={r} k={k}")
+        # traffic: the same bytes as the ring's (2L - |c_{r+1}| - |c_{r+2}|) elements
+        comm.set_config(L.HVD_CFG_LL_MAX_BYTES, 0)
+        comm.set_config(L.HVD_CFG_LL128_MAX_BYTES, 16 << 20)
+        Lb = 1_234_567
+        xs = [workloads.rank_tensor(Lb, "f32", r, 9) for r in range(n)]
+        ref, tr = oracle.allreduce_buffer(xs, "f32", "sum")
+        before = [comm.traffic(r) for r in range(n)]
+        for r in range(n):
+            comm.fusion_buffer(r, torch.float32, Lb).copy_(to_torch(xs[r], "f32"))
+        comm.allreduce_buffer(Lb, hvd._lib.HVD_FLOAT32, "sum")
+        torch.cuda.synchronize()
+        for r in range(n):
+            assert_same(from_torch(comm.fusion_buffer(r, torch.float32, Lb), "f32"), ref[r], "f32")
+            sent, sends = comm.traffic(r)
+            assert sent - before[r][0] == tr[r].sent_elems * 4 and sends - before[r][1] == 2 * (n - 1)
+    finally:
+        comm.set_config(L.HVD_CFG_LL_MAX_BYTES, ll_d)
+        comm.set_config(L.HVD_CFG_LL128_MAX_BYTES, ll128_d)

@@ -67,6 +67,7 @@ def main():
     ap.add_argument("--sweep-max-log2", type=int, default=30)
     ap.add_argument("--sweep-min-log2", type=int, default=10)
     ap.add_argument("--ll-max", type=int, default=-1, help="HVD_CFG_LL_MAX_BYTES (-1: library default)")
+    ap.add_argument("--ll128-max", type=int, default=-1, help="HVD_CFG_LL128_MAX_BYTES (-1: library default)")
     ap.add_argument("--no-nccl", action="store_true")
     a = ap.parse_args()
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
@@ -75,6 +76,8 @@ def main():
     comm = hvd.init(fusion_bytes=64 * MIB)
     if a.ll_max >= 0:
         comm.set_config(hvd._lib.HVD_CFG_LL_MAX_BYTES, a.ll_max)
+    if a.ll128_max >= 0:
+        comm.set_config(hvd._lib.HVD_CFG_LL128_MAX_BYTES, a.ll128_max)
     ng = dist.new_group(backend="nccl") if n > 1 else None
     res = {"n_gpus": n, "rows": []}
     only = set(a.only.split(","))
@@ -136,7 +139,8 @@ def main():
                 iters = a.iters if size <= 256 * MIB else max(3, a.iters // 4)
                 us = timed(lambda i: comm.allreduce_average(preps[i % len(preps)]), iters, nsets=len(preps))
                 row = {"config": "C5", "dtype": dt, "bytes": size, "us": us, "busbw_GBps": bus(size, us, n),
-                       "ll_max": comm.get_config(hvd._lib.HVD_CFG_LL_MAX_BYTES)}
+                       "ll_max": comm.get_config(hvd._lib.HVD_CFG_LL_MAX_BYTES),
+                       "ll128_max": comm.get_config(hvd._lib.HVD_CFG_LL128_MAX_BYTES)}
                 if n > 1 and not a.no_nccl:
                     x = sets[0][0]
                     row["nccl_us"] = timed(lambda i: dist.all_reduce(x, group=ng), iters)
