@@ -1543,20 +1543,22 @@ __global__ void __launch_bounds__(256) ll128_allreduce_kernel(const __grid_const
   constexpr unsigned FULL = 0xffffffffu;
   const RingParams& R = P.ring;
   const RingRank& me = R.rk[blockIdx.y];
-  const int ch = blockIdx.x;
-  const int nch = gridDim.x;
+  int ch = blockIdx.x;  // -> (buffer b, channel ch of b): a group of buffers may share a launch
+  int b = 0;
+  while (b + 1 < P.nbuf && ch >= P.bufs[b].nch) ch -= P.bufs[b++].nch;
+  const BufDesc& D = P.bufs[b];
+  const int nch = D.nch;
   const int N = R.N;
   const int r = me.rank;
   const int T = 2 * (N - 1);
-  const BufDesc& D = P.bufs[0];
   const unsigned long long flag = ~R.epoch;  // never an LL word nor zeroed memory
   const int par = (int)(R.epoch & 1);
   const unsigned long long qv = D.q / VEL;         // vectors per chunk
   const unsigned long long lines = (qv + 6) / 7;   // 128 B lines per chunk slot
   const unsigned long long slot_words = lines * 16;
   constexpr unsigned long long kHalfWords = kLLRegionBytes / 2 / 8;
-  unsigned long long* const in_ll = me.ll + (unsigned long long)par * kHalfWords;
-  unsigned long long* const out_ll = me.nll + (unsigned long long)par * kHalfWords;
+  unsigned long long* const in_ll = me.ll + (unsigned long long)par * kHalfWords + D.ll_off;
+  unsigned long long* const out_ll = me.nll + (unsigned long long)par * kHalfWords + D.ll_off;
   const unsigned long long lpc = (lines + nch - 1) / nch;  // lines of this channel
   const unsigned long long l_lo = (unsigned long long)ch * lpc < lines ? (unsigned long long)ch * lpc : lines;
   const unsigned long long l_hi = l_lo + lpc < lines ? l_lo + lpc : lines;

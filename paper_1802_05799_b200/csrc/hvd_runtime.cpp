@@ -573,6 +573,11 @@ int enqueue_pull(hvd_comm* c, DevPlanBuffer& b, cudaStream_t s) {
 }
 
 // One fused launch for consecutive fusion buffers of one dtype (<= kMaxMultiBufs).
+// multi-buffer calls with at most this many buffers run them concurrently (disjoint
+// channel ranges); with more, one channel minimum per buffer would leave the large
+// buffers too few channels
+constexpr int kDisjointMaxBufs = 16;
+
 int enqueue_fused_multi(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStream_t s) {
   const int dtype = bs[0]->dtype;
   const int esz = elem_size(dtype);
@@ -603,7 +608,6 @@ int enqueue_fused_multi(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStrea
   // channel runs its buffers in order).
   // (disjoint ranges only for a few buffers: with many, one channel minimum per buffer
   // would leave the large buffers too few channels)
-  constexpr int kDisjointMaxBufs = 16;
   std::vector<int> kk(nb, nch), first(nb, -1);
   if (nb > 1 && nch > 1) {
     std::vector<int> want(nb), need(nb);
@@ -785,36 +789,55 @@ bool ll128_eligible(const hvd_comm* c, const DevPlanBuffer& b) {
          (uint64_t)2 * (c->size - 1) * ll128_lines(c, b) * 128 <= kLLRegionBytes / 2;  // fits a half
 }
 
-int enqueue_ll128(hvd_comm* c, DevPlanBuffer& b, cudaStream_t s) {
-  const int dtype = b.dtype;
+int ll128_want(const hvd_comm* c, const DevPlanBuffer& b, uint64_t lines_per_cta = 32) {
+  // lone buffer: one group of 4 lines per warp per step where the co-resident budget
+  // allows (8 warps, 32 lines); in a group of buffers, 4 groups per warp (128 lines)
+  return (int)std::min<uint64_t>((uint64_t)c->ll_ctas,
+                                 std::max<uint64_t>(1, (ll128_lines(c, b) + lines_per_cta - 1) / lines_per_cta));
+}
+uint64_t ll128_words(const hvd_comm* c, const DevPlanBuffer& b) {
+  return (uint64_t)2 * (c->size - 1) * ll128_lines(c, b) * 16;
+}
+
+// A group of buffers of one dtype in one LL128 launch: buffer i gets its own CTAs and
+// its own slot area in the launch's half.
+int enqueue_ll128(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStream_t s) {
+  const int dtype = bs[0]->dtype;
   FusedParams F;
   std::memset(&F, 0, sizeof(F));
   int nch_unused = 0;
-  int st = make_ring_params(c, b.L, dtype, true, &F.ring, &nch_unused);
+  int st = make_ring_params(c, bs[0]->L, dtype, true, &F.ring, &nch_unused);
   if (st != HVD_OK) return st;
-  BufDesc& D = F.bufs[0];
-  D.q = chunk_len(b.L, c->size, dtype);
-  D.segs = b.pp.segs;
-  D.src = b.pp.src;
-  D.dst = b.dst ? b.dst : b.pp.src;
-  D.vbeg = b.vbeg;
-  D.nseg = b.pp.nseg;
-  D.L = b.L;
-  D.ch_el = D.q;
-  D.slice_el = D.q;
-  D.K = 1;
-  D.owner = -1;
-  // one group of 4 lines per warp per step where the co-resident budget allows (8 warps)
-  const int nch = (int)std::min<uint64_t>((uint64_t)c->ll_ctas, std::max<uint64_t>(1, (ll128_lines(c, b) + 31) / 32));
-  D.nch = nch;
-  F.nbuf = 1;
-  F.scale_on = b.pp.scale_on;
-  F.scale = b.pp.scale;
+  int ctas = 0;
+  uint64_t words = 0;
+  for (int i = 0; i < nb; ++i) {
+    const DevPlanBuffer& b = *bs[i];
+    BufDesc& D = F.bufs[i];
+    D.q = chunk_len(b.L, c->size, dtype);
+    D.segs = b.pp.segs;
+    D.src = b.pp.src;
+    D.dst = b.dst ? b.dst : b.pp.src;
+    D.vbeg = b.vbeg;
+    D.nseg = b.pp.nseg;
+    D.L = b.L;
+    D.ch_el = D.q;
+    D.slice_el = D.q;
+    D.K = 1;
+    D.owner = -1;
+    D.nch = ll128_want(c, b, nb > 1 ? 128 : 32);
+    D.ll_off = (unsigned)words;
+    ctas += D.nch;
+    words += ll128_words(c, b);
+  }
+  if (ctas > c->ll_ctas || words * 8 > kLLRegionBytes / 2) return HVD_ERR_INVALID;
+  F.nbuf = nb;
+  F.scale_on = bs[0]->pp.scale_on;
+  F.scale = bs[0]->pp.scale;
   F.dtype = dtype;
   F.tdtype = dtype;
   F.ring.epoch = ++c->ll_epoch;  // the LL epoch sequence: LL and LL128 launches alternate the halves
   if (c->tl) c->tl_slices = 0;
-  return launch_counted(c, HVD_KERNEL_LL128, s, [&] { return launch_ll128(F, dtype, nch, c->nlocal, s); });
+  return launch_counted(c, HVD_KERNEL_LL128, s, [&] { return launch_ll128(F, dtype, ctas, c->nlocal, s); });
 }
 
 bool ll_eligible(const hvd_comm* c, const DevPlanBuffer& b, bool multi) {
@@ -828,9 +851,21 @@ bool ll_eligible(const hvd_comm* c, const DevPlanBuffer& b, bool multi) {
 // The fused path for a whole plan: small buffers through the LL protocol (grouped),
 // the rest through multi-buffer fused launches (or the pull protocol per buffer).
 int enqueue_fused_plan(hvd_comm* c, CachedPlan* plan, cudaStream_t s) {
-  if (plan->bufs.size() == 1 && ll128_eligible(c, plan->bufs[0])) return enqueue_ll128(c, plan->bufs[0], s);
+  if (plan->bufs.size() == 1 && ll128_eligible(c, plan->bufs[0])) {
+    DevPlanBuffer* b0 = &plan->bufs[0];
+    return enqueue_ll128(c, &b0, 1, s);
+  }
   std::vector<DevPlanBuffer*> group;
   const bool multi = plan->bufs.size() > 1;
+  // many buffers (fusion off) at N > 2: the mid-size ones (above the LL limit, <= 16 MiB)
+  // go to grouped LL128 launches; with few buffers they run concurrently in the fused
+  // launch, and at N = 2 the fused ring's two steps are short enough
+  const bool many = (int)plan->bufs.size() > kDisjointMaxBufs;
+  auto ll128_multi = [&](const DevPlanBuffer& b) {
+    return many && !ll_eligible(c, b, multi) && c->ll128_max > 0 && c->size > 2 && c->protocol == 1 && b.L > 0 &&
+           b.tdtype == b.dtype && b.dtype != HVD_INT64 && (int64_t)(b.L * elem_size(b.dtype)) <= (16ll << 20) &&
+           ll128_words(c, b) * 8 <= kLLRegionBytes / 2;
+  };
   const uint64_t cta_bytes = multi ? (16 << 10) : 4096;
   // 1. LL groups: same dtype, <= kMaxMultiBufs buffers, CTA and region budgets
   {
@@ -862,6 +897,34 @@ int enqueue_fused_plan(hvd_comm* c, CachedPlan* plan, cudaStream_t s) {
     int st = flush();
     if (st != HVD_OK) return st;
   }
+  // 1b. LL128 groups (fusion off): same dtype, <= kMaxMultiBufs, CTA and region budgets
+  {
+    int ctas = 0;
+    uint64_t words = 0;
+    auto flush = [&]() -> int {
+      int st = HVD_OK;
+      if (!group.empty()) st = enqueue_ll128(c, group.data(), (int)group.size(), s);
+      group.clear();
+      ctas = 0;
+      words = 0;
+      return st;
+    };
+    for (DevPlanBuffer& b : plan->bufs) {
+      if (!ll128_multi(b)) continue;
+      const int want = ll128_want(c, b, 128);
+      const uint64_t w = ll128_words(c, b);
+      if (!group.empty() && (group[0]->dtype != b.dtype || (int)group.size() >= kMaxMultiBufs ||
+                             ctas + want > c->ll_ctas || (words + w) * 8 > kLLRegionBytes / 2)) {
+        int st = flush();
+        if (st != HVD_OK) return st;
+      }
+      group.push_back(&b);
+      ctas += want;
+      words += w;
+    }
+    int st = flush();
+    if (st != HVD_OK) return st;
+  }
   // 2. everything else
   auto flush = [&]() -> int {
     int st = HVD_OK;
@@ -870,7 +933,7 @@ int enqueue_fused_plan(hvd_comm* c, CachedPlan* plan, cudaStream_t s) {
     return st;
   };
   for (DevPlanBuffer& b : plan->bufs) {
-    if (b.L == 0 || ll_eligible(c, b, multi)) continue;
+    if (b.L == 0 || ll_eligible(c, b, multi) || ll128_multi(b)) continue;
     if (c->protocol == 0 && c->size > 1 && b.tdtype == b.dtype && !b.rdst) {
       int st = flush();
       if (st != HVD_OK) return st;

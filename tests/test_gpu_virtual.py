@@ -461,10 +461,17 @@ def test_many_small_buffers_one_launch(hvd, n):
     xs = workloads.all_ranks(counts, "f32", n, seed=31)
     ref, _, plan = oracle.allreduce(xs, ["f32"] * len(counts), "average", threshold=0)
     assert len(plan) == 200
-    ll_default = comm.get_config(hvd._lib.HVD_CFG_LL_MAX_BYTES)
-    # fused multi-buffer launches (LL off), then grouped LL launches (the default for small buffers)
-    for ll_max, kind in ((0, "fused"), (ll_default, "ll")):
-        comm.set_config(hvd._lib.HVD_CFG_LL_MAX_BYTES, ll_max)
+    L = hvd._lib
+    ll_default = comm.get_config(L.HVD_CFG_LL_MAX_BYTES)
+    ll128_default = comm.get_config(L.HVD_CFG_LL128_MAX_BYTES)
+    # fused multi-buffer launches (LL and LL128 off), grouped LL128 launches (LL off), then
+    # grouped LL launches (the default for small buffers)
+    passes = [(0, 0, "fused"), (ll_default, ll128_default, "ll")]
+    if n > 2:  # grouped LL128 for buffers above the LL limit: N > 2 only
+        passes.insert(1, (0, ll128_default, "ll128"))
+    for ll_max, ll128_max, kind in passes:
+        comm.set_config(L.HVD_CFG_LL_MAX_BYTES, ll_max)
+        comm.set_config(L.HVD_CFG_LL128_MAX_BYTES, ll128_max)
         ts = [[to_torch(x, "f32") for x in xs[r]] for r in range(n)]
         comm.kernel_stats()
         comm.allreduce(ts, op="average", fusion_threshold=0)
@@ -475,7 +482,8 @@ def test_many_small_buffers_one_launch(hvd, n):
         for r in range(n):
             for k in range(len(counts)):
                 assert_same(from_torch(ts[r][k], "f32"), ref[r][k], "f32", f"{kind} r={r} k={k}")
-    comm.set_config(hvd._lib.HVD_CFG_LL_MAX_BYTES, ll_default)
+    comm.set_config(L.HVD_CFG_LL_MAX_BYTES, ll_default)
+    comm.set_config(L.HVD_CFG_LL128_MAX_BYTES, ll128_default)
 
 
 @pytest.mark.parametrize("n", [2, 3, 4, 5, 8])
@@ -630,20 +638,29 @@ def test_fusion_off_mixed_sizes_channel_ranges(hvd, n):
     counts = [int(c) for c in rng.choice([1, 37, 1000, 40_000, 65_536, 300_001, 1_500_000], size=40)]
     xs = workloads.all_ranks(counts, "f32", n, seed=91)
     ref, _, plan = oracle.allreduce(xs, ["f32"] * len(counts), "average", threshold=0)
-    ll_default = comm.get_config(hvd._lib.HVD_CFG_LL_MAX_BYTES)
-    for ll_max in (ll_default, 0):
-        comm.set_config(hvd._lib.HVD_CFG_LL_MAX_BYTES, ll_max)
+    L = hvd._lib
+    ll_default = comm.get_config(L.HVD_CFG_LL_MAX_BYTES)
+    ll128_default = comm.get_config(L.HVD_CFG_LL128_MAX_BYTES)
+    # defaults: small buffers in LL groups, mid-size ones in LL128 groups, the rest fused;
+    # then every buffer on the fused kernel's channel ranges
+    for ll_max, ll128_max in ((ll_default, ll128_default), (0, 0)):
+        comm.set_config(L.HVD_CFG_LL_MAX_BYTES, ll_max)
+        comm.set_config(L.HVD_CFG_LL128_MAX_BYTES, ll128_max)
         ts = [[to_torch(x, "f32") for x in xs[r]] for r in range(n)]
         comm.kernel_stats()
         comm.allreduce(ts, op="average", fusion_threshold=0)
         torch.cuda.synchronize()
         assert comm.poll_error() == 0
         st = comm.kernel_stats()
-        assert (st["ll"][0] > 0) == (ll_max > 0) and st["fused"][0] >= 1
+        if ll_max:
+            assert st["ll"][0] > 0 and (st["ll128"][0] > 0) == (n > 2)
+        else:
+            assert st["ll"][0] == 0 and st["ll128"][0] == 0 and st["fused"][0] >= 1
         for r in range(n):
             for k in range(len(counts)):
                 assert_same(from_torch(ts[r][k], "f32"), ref[r][k], "f32", f"ll={ll_max} r={r} k={k}")
-    comm.set_config(hvd._lib.HVD_CFG_LL_MAX_BYTES, ll_default)
+    comm.set_config(L.HVD_CFG_LL_MAX_BYTES, ll_default)
+    comm.set_config(L.HVD_CFG_LL128_MAX_BYTES, ll128_default)
 
 
 @pytest.mark.parametrize("n", [2, 3, 4, 8])
