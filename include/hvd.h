@@ -231,9 +231,19 @@ typedef enum {
                                 counters (fp32/bf16/i32) */
   HVD_CFG_MULTI_BUFFERS = 13, /* fusion buffers per fused launch (1..96, default 96): the
                                 buffers of one call pipeline inside one persistent launch  */
-  HVD_CFG_PROTOCOL = 12      /* allreduce data movement: 1 (default) push — SM stores into the
-                                successor's HBM; 0 pull — each rank TMA-loads its
-                                predecessor's partials.  Same ring order, same bits.       */
+  HVD_CFG_PROTOCOL = 12,     /* allreduce data movement for buffers above the LL / LL128
+                                limits: 2 bulk push — the TMA engine moves every stage
+                                through shared memory (cp.async.bulk loads and stores into
+                                the successor's HBM), only for calls whose tensors share the
+                                wire dtype; 1 push — SM stores into the successor's HBM;
+                                0 pull — each rank TMA-loads its predecessor's partials.
+                                Same ring order, same bits.                                 */
+  HVD_CFG_BULK_STAGES = 16,  /* bulk push: shared-memory stages per CTA (3..8, > BULK_DEPTH + 1) */
+  HVD_CFG_BULK_STAGE_BYTES = 17, /* bulk push: bytes per stage (4 KiB..64 KiB, multiple of 1 KiB) */
+  HVD_CFG_BULK_DEPTH = 18,   /* bulk push: bulk-store groups a CTA leaves incomplete before it
+                                retires (publishes) a stage (0..3)                          */
+  HVD_CFG_BULK_CHANNELS = 19, /* bulk push: CTAs per rank (1..256; capped by co-residency)  */
+  HVD_CFG_BULK_SLICE_BYTES = 20 /* bulk push: signal slice per channel (multiple of 256 B)  */
 } hvd_config_key;
 /* Set a tuning knob; every rank must set identical values.  Errors: INVALID. */
 int hvd_set_config(hvd_comm* c, int key, int64_t value);
@@ -241,7 +251,8 @@ int64_t hvd_get_config(const hvd_comm* c, int key);
 
 typedef enum { HVD_KERNEL_PACK = 0, HVD_KERNEL_RING = 1, HVD_KERNEL_UNPACK = 2, HVD_KERNEL_SCALE = 3,
                HVD_KERNEL_FUSED = 4, HVD_KERNEL_COPY = 5, HVD_KERNEL_PULL = 6, HVD_KERNEL_LL = 7,
-               HVD_KERNEL_SOLO = 8, HVD_KERNEL_LL128 = 9, HVD_KERNEL_KINDS = 10 } hvd_kernel_kind;
+               HVD_KERNEL_SOLO = 8, HVD_KERNEL_LL128 = 9, HVD_KERNEL_BULK = 10,
+               HVD_KERNEL_KINDS = 11 } hvd_kernel_kind;
 /* Kernel launches of each kind since the last call (always counted) and, with
  * HVD_CFG_PROFILE on, the summed device time in ms between the CUDA events
  * recorded on the launch stream around each launch (waits for those events).

@@ -272,7 +272,7 @@ class Comm:
         n = _lib.HVD_KERNEL_KINDS
         la, ms = (C.c_uint64 * n)(), (C.c_double * n)()
         check(lib.hvd_kernel_stats(self._h, la, ms), "hvd_kernel_stats")
-        names = ["pack", "ring", "unpack", "scale", "fused", "copy", "pull", "ll", "solo", "ll128"]
+        names = ["pack", "ring", "unpack", "scale", "fused", "copy", "pull", "ll", "solo", "ll128", "bulk"]
         return {names[i]: (la[i], ms[i]) for i in range(n)}
 
     def timeline(self, local: int = 0):

@@ -37,6 +37,11 @@ HVD_CFG_PROTOCOL = 12
 HVD_CFG_MULTI_BUFFERS = 13
 HVD_CFG_LL_MAX_BYTES = 14
 HVD_CFG_LL128_MAX_BYTES = 15
+HVD_CFG_BULK_STAGES = 16
+HVD_CFG_BULK_STAGE_BYTES = 17
+HVD_CFG_BULK_DEPTH = 18
+HVD_CFG_BULK_CHANNELS = 19
+HVD_CFG_BULK_SLICE_BYTES = 20
 MAX_CHANNELS = 256
 HVD_KERNEL_PACK, HVD_KERNEL_RING, HVD_KERNEL_UNPACK, HVD_KERNEL_SCALE, HVD_KERNEL_FUSED = 0, 1, 2, 3, 4
 HVD_KERNEL_COPY = 5
@@ -44,7 +49,8 @@ HVD_KERNEL_PULL = 6
 HVD_KERNEL_LL = 7
 HVD_KERNEL_SOLO = 8
 HVD_KERNEL_LL128 = 9
-HVD_KERNEL_KINDS = 10
+HVD_KERNEL_BULK = 10
+HVD_KERNEL_KINDS = 11
 
 
 class hvd_tensor(C.Structure):

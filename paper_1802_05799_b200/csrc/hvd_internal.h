@@ -168,6 +168,11 @@ struct FusedParams {
   int nbuf;
   int cache_segs;                    // member-offset cache entries in shared memory
   unsigned long long region_el;      // channel-private region of scratch / buffer, elements
+  // bulk-copy push kernel (bulk_allreduce_kernel)
+  int bulk_stages;                   // shared-memory stages per CTA
+  int bulk_stage_bytes;              // bytes per stage (multiple of 16)
+  int bulk_depth;                    // bulk store groups left incomplete before retiring a stage
+  int pad2;
   BufDesc bufs[kMaxMultiBufs];
 };
 
@@ -187,6 +192,9 @@ constexpr unsigned long long kLLRegionBytes = 320ull << 20;
 cudaError_t pull_max_ctas_per_sm(int dtype, int threads, int* out);
 cudaError_t ll_max_ctas_per_sm(int* out);
 cudaError_t launch_ll128(const FusedParams& p, int dtype, int nch, int nlocal, cudaStream_t s);
+cudaError_t launch_bulk(const FusedParams& p, int dtype, int nch, int nlocal, cudaStream_t s);
+cudaError_t bulk_max_ctas_per_sm(int dtype, int stages, int stage_bytes, int* out);
+size_t bulk_smem_bytes(int stages, int stage_bytes);
 cudaError_t launch_solo(const FusedParams& p, int dtype, int nlocal, cudaStream_t s);
 cudaError_t fused_max_ctas_per_sm(int dtype, int threads, int* out);
 cudaError_t launch_pack(const PackParams& p, int dtype, int nlocal, int grid, int threads,

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 
 #include "hvd_internal.h"
 
@@ -1652,6 +1653,539 @@ __global__ void __launch_bounds__(256) ll128_allreduce_kernel(const __grid_const
   }
 }
 
+// ------------------------------------------------------------------ bulk-copy push ring
+// The same ring, chunks, slices, reduction order and signal counters as
+// fused_allreduce_kernel, but every byte moves through shared memory by the TMA
+// engine's bulk copies (cp.async.bulk) instead of per-thread loads and NVLink
+// stores.  Warp roles per CTA (one channel):
+//   warp 0  loader      walks the channel's ops, cuts each slice into stages of at
+//                       most `stage` bytes, writes a stage descriptor and issues the
+//                       bulk loads (gathered gradient pieces -> A, received partial
+//                       or forwarded values -> B / A), mbarrier transaction counts;
+//                       before the first load of data the predecessor wrote it waits
+//                       for the predecessor's counter (acquire, system scope)
+//   warps 3+ compute    x = fl32(x * s) (+ partial) in shared memory (the same
+//                       per-element operations as the fused kernel: bit-identical),
+//                       plus the element-by-element pieces a bulk copy cannot move
+//                       (a member's ragged last vector, misaligned tensors)
+//   warp 1  storer      issues the stage's bulk stores (successor's scratch / fusion
+//                       buffer / tensors over NVLink, own tensors locally), one bulk
+//                       group per stage; a stage is retired (its shared memory given
+//                       back to the loader, its op published) once its group is
+//                       COMPLETE (cp.async.bulk.wait_group)
+//   warp 2  signaller   turns the retired op count into the successor's counter with
+//                       fence.acq_rel.sys + a relaxed store (the fence is needed:
+//                       bulk-group completion alone does not make the writes visible
+//                       to the peer, profiles/r02_arrival_probe.json), off the data path
+// The storer never waits for the signaller and the loader only for real data
+// dependencies, so slices can be small (a fence under load takes ~15 us, which the
+// next slices' transfers hide).
+constexpr int kBulkComputeWarps = 4;
+constexpr int kBulkThreads = (3 + kBulkComputeWarps) * 32;
+constexpr int kBulkMaxExc = 16;    // element-wise pieces per stage (the loader cuts the stage when full)
+constexpr int kBulkEnd = 15;       // descriptor kind: no more stages
+constexpr int kBarCompute = 3;     // named barrier of the compute warps
+
+struct BulkExc {
+  unsigned a, n;  // vectors [a, a+n) of the stage (offsets from v0)
+  int s, pad;     // member
+};
+struct StageDesc {
+  unsigned long long v0;  // first buffer vector of the stage
+  long long pv;           // buffer vector -> channel-private slot shift
+  int n;                  // vectors (0: an op without data on this channel)
+  int kind;               // FusedKind or kBulkEnd
+  int pub;                // ring ops to publish once this stage is complete (-1: none)
+  int b;                  // fusion buffer of the call
+  int half;               // receive half (scratch / scratch1)
+  int nexc;
+  int op;                 // op index of this channel (timeline)
+  int last;               // last stage of its op
+  unsigned long long e_hi;  // end element of the slice (traffic count of a ragged end)
+  BulkExc exc[kBulkMaxExc];
+};
+
+__host__ __device__ constexpr bool bk_gathers(int k) {
+  return k == kF_RS0 || k == kF_RS || k == kF_AG0 || k == kF_RAG0 || k == kF_RAG;
+}
+__host__ __device__ constexpr bool bk_scales(int k) { return k == kF_RS0 || k == kF_RS || k == kF_AG0 || k == kF_RAG0; }
+__host__ __device__ constexpr bool bk_adds(int k) { return k == kF_RS || k == kF_AG0 || k == kF_RAG0; }
+__host__ __device__ constexpr bool bk_from_buf(int k) { return k == kF_AG || k == kF_FIN; }
+__host__ __device__ constexpr bool bk_to_nscr(int k) { return k == kF_RS0 || k == kF_RS; }
+__host__ __device__ constexpr bool bk_to_nbuf(int k) { return k == kF_AG0 || k == kF_AG; }
+__host__ __device__ constexpr bool bk_scatters(int k) { return k == kF_AG0 || k == kF_AG || k == kF_FIN || k == kF_RAG0; }
+__host__ __device__ constexpr bool bk_rscatters(int k) { return k == kF_RAG0 || k == kF_RAG; }
+__host__ __device__ constexpr bool bk_members(int k) { return bk_gathers(k) || bk_scatters(k) || bk_rscatters(k); }
+
+__device__ __forceinline__ void mbar_expect_tx_only(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait(int d) {  // until at most d bulk groups are incomplete
+  switch (d) {
+    case 0: asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.bulk.wait_group 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.bulk.wait_group 2;" ::: "memory"); break;
+    default: asm volatile("cp.async.bulk.wait_group 3;" ::: "memory"); break;
+  }
+}
+
+// One member's address for this local rank (gather / scatter / successor's scatter).
+struct BulkTabs {
+  const PackSeg* segs;
+  const unsigned long long* vbeg;
+  char* const* src;
+  char* const* dst;
+  char* const* rdst;  // nullptr unless registered
+  int nseg;
+};
+__device__ __forceinline__ BulkTabs bulk_tabs(const FusedParams& P, int b) {
+  const BufDesc& D = P.bufs[b];
+  BulkTabs T;
+  T.segs = D.segs;
+  T.vbeg = D.vbeg;
+  T.src = D.src + (size_t)blockIdx.y * D.nseg;
+  T.dst = D.dst + (size_t)blockIdx.y * D.nseg;
+  T.rdst = P.registered ? D.rdst + (size_t)blockIdx.y * D.nseg : nullptr;
+  T.nseg = D.nseg;
+  return T;
+}
+
+// Member of buffer vector v (largest s with vbeg[s] <= v).
+__device__ __forceinline__ int bulk_find(const BulkTabs& T, unsigned long long v) {
+  int lo = 0, hi = T.nseg - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(T.vbeg + mid) <= v) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// Walk the members covering buffer vectors [v, vend): f(a, e, s, exc) is called for
+// each piece [a, e) of member s; exc: the piece goes element by element (a ragged last
+// vector, or a member whose tensor address is not 16 B aligned on this rank).  `s` is
+// a cursor (the member of v or one before it).  The loader and the storer make the
+// same calls for the same range, so they agree on which pieces are bulk copies.
+template <class Fn>
+__device__ __forceinline__ void bulk_walk(const BulkTabs& T, int VEL, unsigned long long v, unsigned long long vend,
+                                          int& s, Fn&& f) {
+  while (s + 1 < T.nseg && __ldg(T.vbeg + s + 1) <= v) ++s;
+  while (v < vend && s < T.nseg) {
+    const unsigned long long vb = __ldg(T.vbeg + s);
+    const unsigned long long cnt = __ldg(&T.segs[s].count);
+    const unsigned long long vn = vb + (cnt + VEL - 1) / VEL;  // members are packed on 16 B
+    if (vn <= v) {
+      ++s;
+      continue;
+    }
+    const unsigned long long e = vend < vn ? vend : vn;
+    const uintptr_t al = reinterpret_cast<uintptr_t>(T.src[s]) | reinterpret_cast<uintptr_t>(T.dst[s]) |
+                         (T.rdst ? reinterpret_cast<uintptr_t>(T.rdst[s]) : 0);
+    const unsigned long long full = vb + cnt / VEL;
+    if (al & 15) {
+      if (!f(v, e, s, true)) return;
+    } else {
+      const unsigned long long fe = e < full ? e : full;
+      if (fe > v && !f(v, fe, s, false)) return;
+      if (e > fe && !f(fe > v ? fe : v, e, s, true)) return;
+    }
+    v = e;
+    if (v >= vn) ++s;
+  }
+}
+
+// Element-by-element move of one 16 B buffer vector whose member piece cannot be a
+// bulk copy: `left` valid elements (the rest of the vector is zero padding).
+template <int ESZ>
+__device__ __forceinline__ uint4 bulk_gather_elem(const char* p, unsigned long long left) {
+  constexpr int VEL = 16 / ESZ;
+  alignas(16) unsigned char tmp[16];
+#pragma unroll
+  for (int i = 0; i < VEL; ++i)
+#pragma unroll
+    for (int b = 0; b < ESZ; ++b)
+      tmp[i * ESZ + b] = (unsigned long long)i < left ? *reinterpret_cast<const volatile unsigned char*>(p + i * ESZ + b) : 0;
+  return *reinterpret_cast<const uint4*>(tmp);
+}
+
+__device__ __forceinline__ bool mbar_test(unsigned long long* bar, unsigned parity) {
+  unsigned done;
+  asm volatile("{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+               : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  return done != 0;
+}
+
+// mbarrier wait with the watchdog: a stage that never completes (a protocol bug, a
+// peer that died) latches HVD_ERR_TIMEOUT and traps instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait_wd(unsigned long long* bar, unsigned parity, int* err,
+                                             unsigned long long timeout_ns) {
+  unsigned done = 0, spins = 0;
+  unsigned long long t0 = 0;
+  for (;;) {
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    if (done) return;
+    if ((++spins & 255u) == 0) {
+      const unsigned long long now = globaltimer();
+      if (t0 == 0) {
+        t0 = now;
+      } else if (now - t0 > timeout_ns + 1000000000ull) {  // after the spin watchdogs had their chance
+        *(volatile int*)err = kHvdErrTimeout;
+        __threadfence_system();
+        asm volatile("trap;");
+      }
+    }
+  }
+}
+
+template <class Op>
+__global__ void __launch_bounds__(kBulkThreads, 1) bulk_allreduce_kernel(const __grid_constant__ FusedParams P) {
+  extern __shared__ __align__(1024) unsigned char s_bulk[];
+  constexpr int ESZ = Op::kEsz;
+  constexpr int VEL = 16 / ESZ;
+  const RingParams& R = P.ring;
+  const RingRank& me = R.rk[blockIdx.y];
+  const int ch = blockIdx.x;
+  const int N = R.N;
+  const int r = me.rank;
+  const int T = 2 * (N - 1);
+  const int S = P.bulk_stages;
+  const unsigned stage_vecs = (unsigned)(P.bulk_stage_bytes / 16);
+  const unsigned long long base0 = R.base[ch];
+  // shared memory: [A stages][B stages][descriptors][mbarriers full, comp, empty]
+  uint4* sA = reinterpret_cast<uint4*>(s_bulk);
+  uint4* sB = sA + (size_t)S * stage_vecs;
+  StageDesc* desc = reinterpret_cast<StageDesc*>(sB + (size_t)S * stage_vecs);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(desc + S);
+  unsigned long long* comp = full + S;
+  unsigned long long* empty = comp + S;
+  __shared__ int s_abort, s_done;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    s_abort = 0;
+    s_done = 0;
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&comp[i], kBulkComputeWarps);
+      mbar_init(&empty[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // ring ops this channel publishes over the whole call
+  int total = 0;
+  for (int b = 0; b < P.nbuf; ++b)
+    if (chan_of(P.bufs[b], ch, gridDim.x) >= 0) total += T * P.bufs[b].K;
+
+  if (warp == 2) {  // ---- signaller: handshake to the predecessor, then publish retired ops
+    if (lane == 0) {
+      st_relaxed_sys(me.phash + ch, R.hash);
+      st_release_sys(me.pready + ch, R.epoch);
+      if (total > 0)
+        signal_loop(&s_done, total, me.nflags + ch, base0, R.sig_mode, nullptr,
+                    R.tl ? R.tl + tl_words(R.tl_max) * blockIdx.y + ((size_t)kMaxChannels + ch) * R.tl_max * 2 : nullptr,
+                    R.tl_max);
+    }
+    return;
+  }
+  unsigned long long* tl_d = R.tl ? R.tl + tl_words(R.tl_max) * blockIdx.y + (size_t)ch * R.tl_max * 2 : nullptr;
+
+  if (warp == 0) {  // ---- loader
+    if (lane != 0) return;
+    unsigned long long seq = 0;
+    unsigned long long bbase = base0;
+    int ring_i = 0, bpar = 0, nop = 0;
+    bool abort = false;
+    auto acquire_slot = [&](unsigned long long q) -> int {
+      const int slot = (int)(q % S);
+      if (q >= (unsigned long long)S) mbar_wait_wd(&empty[slot], (unsigned)((q / S - 1) & 1), R.err, R.timeout_ns);
+      return slot;
+    };
+    for (int b = 0; b < P.nbuf; ++b) {
+      const BufDesc& D = P.bufs[b];
+      const int cg = chan_of(D, ch, gridDim.x);
+      if (cg < 0) continue;
+      const int K = D.K;
+      const int half = bpar;
+      bpar ^= 1;
+      const BulkTabs TB = bulk_tabs(P, b);
+      const char* scr = half ? me.scratch1 : me.scratch;
+      const int nops = P.registered ? T * K : (T + 1) * K;
+      int cur = 0;  // member cursor (ranges grow within a slice)
+      for (int j = 0; j < nops; ++j, ++nop) {
+        int t, k;
+        if (P.registered) {
+          t = j / K;
+          k = j - t * K;
+        } else {
+          fused_op(j, K, T, R.fin_lag, t, k);
+        }
+        const bool rs = t < N - 1;
+        const int s_ = rs ? t : t - (N - 1);
+        const int c = t == T ? mod(r + 2, N) : (rs ? mod(r - s_, N) : mod(r + 1 - s_, N));
+        int kind;
+        if (P.registered) kind = t == 0 ? kF_RS0 : (rs ? kF_RS : (s_ == 0 ? kF_RAG0 : kF_RAG));
+        else kind = t == T ? kF_FIN : (t == 0 ? kF_RS0 : (rs ? kF_RS : (s_ == 0 ? kF_AG0 : kF_AG)));
+        unsigned long long lo, hi;
+        slice_range_d(D, c, cg, k, lo, hi);
+        const long long pv =
+            (long long)(((unsigned long long)ch * P.region_el + (unsigned long long)c * D.ch_el +
+                         (lo - (unsigned long long)c * D.q - (unsigned long long)cg * D.ch_el)) / VEL) -
+            (long long)(lo / VEL);
+        const unsigned long long vlo = lo / VEL, vhi = hi > lo ? (hi + VEL - 1) / VEL : vlo;
+        const int pub = t < T ? ++ring_i : -1;
+        const unsigned long long target = t > 0 ? bbase + (unsigned long long)(t - 1) * K + k + 1 : 0;
+        if (tl_d && nop < R.tl_max) tl_d[2 * nop] = globaltimer();
+        bool dep_done = target == 0;
+        auto wait_dep = [&]() {
+          if (dep_done) return;
+          dep_done = true;
+          if (!abort && !spin_until(me.flags + ch, target, R.err, R.timeout_ns)) {
+            abort = true;
+            s_abort = 1;
+#ifdef HVD_BULK_DEBUG
+            printf("bulk dep timeout r=%d ch=%d kind=%d t=%d k=%d target=%llu have=%llu base0=%llu\n", r, ch, kind, t, k,
+                   target, *(volatile unsigned long long*)(me.flags + ch), base0);
+#endif
+          }
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // the acquire covers the async-proxy loads
+        };
+        if (vhi <= vlo) {  // no data on this channel: an empty stage keeps the publish order
+          const int slot = acquire_slot(seq);
+          StageDesc& sd = desc[slot];
+          sd.v0 = vlo;
+          sd.pv = pv;
+          sd.n = 0;
+          sd.kind = kind;
+          sd.pub = pub;
+          sd.b = b;
+          sd.half = half;
+          sd.nexc = 0;
+          sd.op = nop;
+          sd.last = 1;
+          sd.e_hi = hi;
+          mbar_arrive(&full[slot]);
+          ++seq;
+          continue;
+        }
+        cur = bk_members(kind) ? bulk_find(TB, vlo) : 0;
+        for (unsigned long long v0 = vlo; v0 < vhi;) {
+          const int slot = acquire_slot(seq);
+          StageDesc& sd = desc[slot];
+          uint4* A = sA + (size_t)slot * stage_vecs;
+          uint4* B = sB + (size_t)slot * stage_vecs;
+          unsigned long long v1 = v0 + stage_vecs < vhi ? v0 + stage_vecs : vhi;
+          int nexc = 0;
+          const bool dep_gather = kind == kF_RAG;  // own tensors written by the predecessor
+          if (dep_gather) wait_dep();
+          if (bk_members(kind)) {
+            // member pieces: bulk-load the gathered ones, list the element-wise ones; the
+            // stage ends early when the list is full
+            unsigned long long cut = v1;
+            bulk_walk(TB, VEL, v0, v1, cur, [&](unsigned long long a, unsigned long long e, int s, bool exc) -> bool {
+              if (exc) {
+                if (nexc == kBulkMaxExc) {
+                  cut = a;
+                  return false;
+                }
+                sd.exc[nexc].a = (unsigned)(a - v0);
+                sd.exc[nexc].n = (unsigned)(e - a);
+                sd.exc[nexc].s = s;
+                ++nexc;
+              } else if (bk_gathers(kind) && !abort) {
+                const unsigned bytes = (unsigned)((e - a) * 16);
+                mbar_expect_tx_only(&full[slot], bytes);
+                tma_load(A + (a - v0), TB.src[s] + (a - __ldg(TB.vbeg + s)) * 16, bytes, &full[slot]);
+              }
+              return true;
+            });
+            v1 = cut;
+          }
+          if (bk_adds(kind) || bk_from_buf(kind)) {
+            wait_dep();
+            if (!abort) {
+              const unsigned bytes = (unsigned)((v1 - v0) * 16);
+              mbar_expect_tx_only(&full[slot], bytes);
+              if (bk_adds(kind)) tma_load(B, scr + (v0 + pv) * 16, bytes, &full[slot]);
+              else tma_load(A, me.buf + (v0 + pv) * 16, bytes, &full[slot]);
+            }
+          }
+          sd.v0 = v0;
+          sd.pv = pv;
+          sd.n = (int)(v1 - v0);
+          sd.kind = kind;
+          sd.pub = v1 >= vhi ? pub : -1;
+          sd.b = b;
+          sd.half = half;
+          sd.nexc = nexc;
+          sd.op = nop;
+          sd.last = v1 >= vhi;
+          sd.e_hi = hi;
+          if (nexc) wait_dep();  // element-wise gathers of RAG data by the compute warps
+          mbar_arrive(&full[slot]);
+          ++seq;
+          v0 = v1;
+        }
+      }
+      bbase += (unsigned long long)T * K;
+    }
+    const int slot = acquire_slot(seq);
+    desc[slot].kind = kBulkEnd;
+    mbar_arrive(&full[slot]);
+    // registered: the predecessor's last all-gather stores land in this rank's tensors;
+    // the kernel completes only when they have arrived
+    if (P.registered && total > 0 && !abort) spin_until(me.flags + ch, bbase, R.err, R.timeout_ns);
+    return;
+  }
+
+  if (warp == 1) {  // ---- storer
+    if (lane != 0) return;
+    unsigned long long seq = 0, retired = 0;
+    unsigned long long sent = 0;
+    bool ready = false;
+    const int depth = P.bulk_depth;
+    auto retire = [&](unsigned long long upto) {  // stages < upto are complete
+      for (; retired < upto; ++retired) {
+        const int slot = (int)(retired % S);
+        const int pub = desc[slot].pub;
+        const int op = desc[slot].op;
+        const bool last = desc[slot].last;
+        mbar_arrive(&empty[slot]);
+        if (pub >= 0) st_release_cta_shared(&s_done, pub);
+        if (last && tl_d && op < R.tl_max) tl_d[2 * op + 1] = globaltimer();
+      }
+    };
+    for (;; ++seq) {
+      const int slot = (int)(seq % S);
+      // the next stage may wait on the successor's progress, which may wait on a stage
+      // published here: never leave issued stages unretired while waiting for it
+      if (retired < seq && !mbar_test(&comp[slot], (unsigned)((seq / S) & 1))) {
+        bulk_wait(0);
+        retire(seq);
+      }
+      mbar_wait_wd(&comp[slot], (unsigned)((seq / S) & 1), R.err, R.timeout_ns);
+      const StageDesc& sd = desc[slot];
+      const int kind = sd.kind;
+      if (kind == kBulkEnd) break;
+      const uint4* A = sA + (size_t)slot * stage_vecs;
+      if (sd.n > 0 && !s_abort) {
+        const bool remote = bk_to_nscr(kind) || bk_to_nbuf(kind) || bk_rscatters(kind);
+        if (remote && !ready) {  // the launch's first remote store waits for the successor
+          ready = true;
+          if (!spin_until(me.rflags + ch, R.epoch, R.err, R.timeout_ns)) {
+            s_abort = 1;
+#ifdef HVD_BULK_DEBUG
+            printf("bulk handshake timeout r=%d ch=%d epoch=%llu have=%llu\n", r, ch, R.epoch,
+                   *(volatile unsigned long long*)(me.rflags + ch));
+#endif
+          } else if (*(volatile const unsigned long long*)(me.rhash + ch) != R.hash) {
+            *(volatile int*)R.err = kHvdErrMismatch;
+            s_abort = 1;
+          }
+        }
+        if (!s_abort) {
+          const unsigned bytes = (unsigned)sd.n * 16;
+          if (bk_to_nscr(kind)) bulk_store((sd.half ? me.nscratch1 : me.nscratch) + (sd.v0 + sd.pv) * 16, A, bytes);
+          if (bk_to_nbuf(kind)) bulk_store(me.nbuf + (sd.v0 + sd.pv) * 16, A, bytes);
+          if (remote) {
+            const unsigned long long eh = (sd.v0 + sd.n) * VEL < sd.e_hi ? (sd.v0 + sd.n) * VEL : sd.e_hi;
+            sent += (eh - sd.v0 * VEL) * ESZ;
+          }
+          if (bk_scatters(kind) || bk_rscatters(kind)) {
+            const BulkTabs TB = bulk_tabs(P, sd.b);
+            int cur = bulk_find(TB, sd.v0);
+            bulk_walk(TB, VEL, sd.v0, sd.v0 + sd.n, cur,
+                      [&](unsigned long long a, unsigned long long e, int s, bool exc) -> bool {
+                        if (!exc) {
+                          const unsigned long long off = (a - __ldg(TB.vbeg + s)) * 16;
+                          if (bk_scatters(kind)) bulk_store(TB.dst[s] + off, A + (a - sd.v0), (unsigned)((e - a) * 16));
+                          if (bk_rscatters(kind)) bulk_store(TB.rdst[s] + off, A + (a - sd.v0), (unsigned)((e - a) * 16));
+                        }
+                        return true;
+                      });
+          }
+        }
+      }
+      bulk_commit();
+      bulk_wait(depth);
+      if (seq + 1 > (unsigned long long)depth) retire(seq + 1 - depth);
+    }
+    bulk_wait(0);
+    retire(seq);
+    atomicAdd(me.stats + 0, sent);
+    if (ch == 0) atomicAdd(me.stats + 1, (unsigned long long)T * P.nbuf);
+    return;
+  }
+
+  // ---- compute warps
+  const int ctid = threadIdx.x - 96;
+  constexpr int CT = kBulkComputeWarps * 32;
+  const float scale = P.scale;
+  const int scale_on = P.scale_on;
+  for (unsigned long long seq = 0;; ++seq) {
+    const int slot = (int)(seq % S);
+    mbar_wait_wd(&full[slot], (unsigned)((seq / S) & 1), R.err, R.timeout_ns);
+    const StageDesc& sd = desc[slot];
+    const int kind = sd.kind;
+    if (kind == kBulkEnd) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&comp[slot]);
+      break;
+    }
+    uint4* A = sA + (size_t)slot * stage_vecs;
+    const uint4* B = sB + (size_t)slot * stage_vecs;
+    const int n = sd.n;
+    const int nexc = sd.nexc;
+    if (nexc && bk_gathers(kind)) {
+      const BulkTabs TB = bulk_tabs(P, sd.b);
+      for (int x = 0; x < nexc; ++x) {
+        const BulkExc ex = sd.exc[x];
+        const unsigned long long dst_off = TB.segs[ex.s].dst_off;
+        const unsigned long long end_el = dst_off + TB.segs[ex.s].count;
+        for (unsigned i = ctid; i < ex.n; i += CT) {
+          const unsigned long long e = (sd.v0 + ex.a + i) * VEL;
+          A[ex.a + i] = bulk_gather_elem<ESZ>(TB.src[ex.s] + (e - dst_off) * ESZ, end_el - e);
+        }
+      }
+      bar_sync(kBarCompute, CT);
+    }
+    if (bk_scales(kind) || bk_adds(kind)) {
+      const int on = bk_scales(kind) ? scale_on : 0;
+      for (int v = ctid; v < n; v += CT) {
+        uint4 x = A[v];
+        if (on) x = Pack16<ESZ>::conv(x, scale, 1, P.dtype);
+        if (bk_adds(kind)) {
+          const uint4 y = B[v];
+          Op::template add_words<4>(reinterpret_cast<uint32_t*>(&x), reinterpret_cast<const uint32_t*>(&y));
+        }
+        A[v] = x;
+      }
+    }
+    if (nexc && (bk_scatters(kind) || bk_rscatters(kind))) {
+      bar_sync(kBarCompute, CT);
+      const BulkTabs TB = bulk_tabs(P, sd.b);
+      for (int x = 0; x < nexc; ++x) {
+        const BulkExc ex = sd.exc[x];
+        const unsigned long long dst_off = TB.segs[ex.s].dst_off;
+        const unsigned long long end_el = dst_off + TB.segs[ex.s].count;
+        for (unsigned i = ctid; i < ex.n; i += CT) {
+          const unsigned long long e = (sd.v0 + ex.a + i) * VEL;
+          const uint4 val = A[ex.a + i];
+          if (bk_scatters(kind)) scatter_slow<ESZ>(TB.dst[ex.s] + (e - dst_off) * ESZ, end_el - e, val);
+          if (bk_rscatters(kind)) scatter_slow<ESZ>(TB.rdst[ex.s] + (e - dst_off) * ESZ, end_el - e, val);
+        }
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> bulk-store reads
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&comp[slot]);
+  }
+}
+
 struct BufList { char* b[kMaxLocal]; };
 
 template <int ESZ>
@@ -2095,6 +2629,64 @@ cudaError_t ring_max_ctas_per_sm(int dtype, int threads, int* out) {
     case 2: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, ring_allreduce_kernel<OpBF16>, threads + 32, 0);
     case 3: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, ring_allreduce_kernel<OpI32>, threads + 32, 0);
     case 4: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, ring_allreduce_kernel<OpI64>, threads + 32, 0);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+
+// ------------------------------------------------------------------ bulk-copy push ring launchers
+size_t bulk_smem_bytes(int stages, int stage_bytes) {
+  return (size_t)stages * (2 * (size_t)stage_bytes + sizeof(StageDesc) + 3 * sizeof(unsigned long long));
+}
+
+template <class Op>
+static cudaError_t launch_bulk_t(const FusedParams& p, int nch, int nlocal, cudaStream_t s) {
+  const size_t smem = bulk_smem_bytes(p.bulk_stages, p.bulk_stage_bytes);
+  cudaError_t e = cudaFuncSetAttribute(bulk_allreduce_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nch, nlocal);
+  cfg.blockDim = dim3(kBulkThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (they wait on each other)
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, bulk_allreduce_kernel<Op>, p);
+}
+
+cudaError_t launch_bulk(const FusedParams& p, int dtype, int nch, int nlocal, cudaStream_t s) {
+  switch (dtype) {
+    case 1: return launch_bulk_t<OpF32>(p, nch, nlocal, s);
+    case 2: return launch_bulk_t<OpBF16>(p, nch, nlocal, s);
+    case 3: return launch_bulk_t<OpI32>(p, nch, nlocal, s);
+    case 4: return launch_bulk_t<OpI64>(p, nch, nlocal, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t bulk_max_ctas_per_sm(int dtype, int stages, int stage_bytes, int* out) {
+  const size_t smem = bulk_smem_bytes(stages, stage_bytes);
+  cudaError_t e = cudaSuccess;
+  switch (dtype) {
+    case 1:
+      e = cudaFuncSetAttribute(bulk_allreduce_kernel<OpF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, bulk_allreduce_kernel<OpF32>, kBulkThreads, smem);
+      return e;
+    case 2:
+      e = cudaFuncSetAttribute(bulk_allreduce_kernel<OpBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, bulk_allreduce_kernel<OpBF16>, kBulkThreads, smem);
+      return e;
+    case 3:
+      e = cudaFuncSetAttribute(bulk_allreduce_kernel<OpI32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, bulk_allreduce_kernel<OpI32>, kBulkThreads, smem);
+      return e;
+    case 4:
+      e = cudaFuncSetAttribute(bulk_allreduce_kernel<OpI64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, bulk_allreduce_kernel<OpI64>, kBulkThreads, smem);
+      return e;
     default: return cudaErrorInvalidValue;
   }
 }

@@ -29,6 +29,7 @@ constexpr uint64_t kDefaultFusionBytes = 64ull << 20;  // P:L368-369 "Default ..
 constexpr uint64_t kTailBytes = 16384;  // flags, stats, ready flags, pull progress, done/exit counters
 constexpr uint32_t kBlobMagic = 0x48564442u;            // "HVDB"
 constexpr int kPackThreads = 256;
+constexpr size_t kBulkMaxSmem = 227 << 10;  // dynamic shared memory of one bulk-push CTA
 constexpr int kPackVecsPerThread = 8;
 constexpr size_t kPlanCacheSize = 32;
 
@@ -100,7 +101,13 @@ struct hvd_comm {
   int64_t ll_max = (int64_t)kLLMaxBytes;  // HVD_CFG_LL_MAX_BYTES
   int ll_ctas = 1;                         // co-resident LL CTAs per local rank
   int64_t ll128_max = 0;                   // HVD_CFG_LL128_MAX_BYTES
-  int protocol = 1;                 // 0: pull (receiver-initiated TMA loads), 1: push (SM stores)
+  int protocol = 1;                 // 0: pull (receiver-initiated TMA loads), 1: push (SM stores),
+                                    // 2: bulk push (TMA bulk loads / stores through shared memory)
+  int bulk_stages = 6;              // HVD_CFG_BULK_STAGES
+  int bulk_stage_bytes = 16 << 10;  // HVD_CFG_BULK_STAGE_BYTES
+  int bulk_depth = 1;               // HVD_CFG_BULK_DEPTH
+  int bulk_channels = 148;          // HVD_CFG_BULK_CHANNELS
+  int64_t bulk_slice = 64 << 10;    // HVD_CFG_BULK_SLICE_BYTES
   unsigned long long pbase[kMaxChannels] = {};  // pull-protocol progress counter bases
   int pull_calls = 0;
   unsigned long long pull_exits = 0;  // cumulative CTA exits of the pull kernel (per rank)
@@ -458,7 +465,7 @@ int launch_counted(hvd_comm* c, int kind, cudaStream_t s, F&& launch) {
 // Split one buffer of L elements into chunks / channels / slices (R2) for the
 // ring or fused kernel.  Returns the channel count.
 int make_ring_params(hvd_comm* c, uint64_t L, int dtype, bool fused, RingParams* P, int* nch_out,
-                     uint64_t q_override = 0, bool pull = false) {
+                     uint64_t q_override = 0, bool pull = false, bool bulk = false) {
   const int esz = elem_size(dtype);
   const uint64_t g = kChunkQuantum / esz;
   std::memset(P, 0, sizeof(*P));
@@ -470,22 +477,25 @@ int make_ring_params(hvd_comm* c, uint64_t L, int dtype, bool fused, RingParams*
   // what stays co-resident (the CTAs of all ranks wait on each other)
   const int threads = pull ? std::max(256, c->threads) : c->threads;
   // occupancy of (kernel, dtype, threads), cached: a driver query per launch costs microseconds
-  const int okey = (pull ? 2 : fused ? 1 : 0) * 100000 + dtype * 10000 + threads;
+  const int okey = bulk ? 300000000 + dtype * 10000000 + c->bulk_stages * 1000000 + (c->bulk_stage_bytes >> 10)
+                       : (pull ? 2 : fused ? 1 : 0) * 100000 + dtype * 10000 + threads;
   int max_per_sm = 0;
   for (auto& kv : c->occ_cache)
     if (kv.first == okey) max_per_sm = kv.second;
   if (max_per_sm == 0) {
-    CK(pull ? pull_max_ctas_per_sm(dtype, threads, &max_per_sm)
+    CK(bulk ? bulk_max_ctas_per_sm(dtype, c->bulk_stages, c->bulk_stage_bytes, &max_per_sm)
+       : pull ? pull_max_ctas_per_sm(dtype, threads, &max_per_sm)
             : fused ? fused_max_ctas_per_sm(dtype, threads, &max_per_sm) : ring_max_ctas_per_sm(dtype, threads, &max_per_sm));
     max_per_sm = std::max(1, max_per_sm);
     c->occ_cache.push_back({okey, max_per_sm});
   }
   const int resident = std::max(1, c->sm_count * max_per_sm / c->nlocal);
   const uint64_t qbytes = P->q * esz;
-  int nch = (int)std::min<uint64_t>((uint64_t)c->channels, std::max<uint64_t>(1, qbytes / (32 << 10)));
+  int nch = (int)std::min<uint64_t>((uint64_t)(bulk ? c->bulk_channels : c->channels),
+                                    std::max<uint64_t>(1, qbytes / (32 << 10)));
   nch = std::min(nch, std::min(resident, kMaxChannels));
   P->ch_el = (P->q + (uint64_t)nch * g - 1) / ((uint64_t)nch * g) * g;
-  uint64_t sb = (uint64_t)c->slice_bytes;
+  uint64_t sb = bulk ? (uint64_t)c->bulk_slice : (uint64_t)c->slice_bytes;
   if (sb == 0) sb = std::min<uint64_t>(128 << 10, std::max<uint64_t>(32 << 10, P->ch_el * esz / 2));
   const uint64_t slice_el = std::max<uint64_t>(g, sb / esz / g * g);
   P->slice_el = std::min<uint64_t>(slice_el, P->ch_el);
@@ -588,10 +598,16 @@ int enqueue_fused_multi(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStrea
   // channels: sized by the largest buffer, like a single-buffer launch
   uint64_t maxL = 0;
   for (int i = 0; i < nb; ++i) maxL = std::max<uint64_t>(maxL, bs[i]->L);
+  // bulk push (bulk_allreduce_kernel): same-dtype calls only (the wire conversions stay in
+  // the fused kernel); the decision depends only on rank-independent call properties
+  const bool bulk = c->protocol == 2 && N > 1 && bs[0]->tdtype == dtype;
   int nch = 0;
-  int st = make_ring_params(c, maxL, dtype, true, &F.ring, &nch);
+  int st = make_ring_params(c, maxL, dtype, true, &F.ring, &nch, 0, false, bulk);
   if (st != HVD_OK) return st;
   F.region_el = c->bufsz / esz / nch / g * g;
+  F.bulk_stages = c->bulk_stages;
+  F.bulk_stage_bytes = c->bulk_stage_bytes;
+  F.bulk_depth = c->bulk_depth;
   F.scale_on = bs[0]->pp.scale_on;
   F.scale = bs[0]->pp.scale;
   F.dtype = dtype;
@@ -673,7 +689,7 @@ int enqueue_fused_multi(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStrea
     D.owner = first[i];  // first channel of the range (-1: all channels)
     D.nch = k;
     D.ch_el = (D.q + (uint64_t)k * g - 1) / ((uint64_t)k * g) * g;
-    uint64_t sb = (uint64_t)c->slice_bytes;
+    uint64_t sb = bulk ? (uint64_t)c->bulk_slice : (uint64_t)c->slice_bytes;
     if (sb == 0) sb = std::min<uint64_t>(128 << 10, std::max<uint64_t>(32 << 10, D.ch_el * esz / 2));
     D.slice_el = std::min<uint64_t>(std::max<uint64_t>(g, sb / esz / g * g), std::max<uint64_t>(D.ch_el, g));
     D.K = (int)((D.ch_el + D.slice_el - 1) / D.slice_el);
@@ -692,15 +708,18 @@ int enqueue_fused_multi(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStrea
   F.ring.epoch = ++c->hs_epoch;
   {
     CallHash h;
-    for (uint64_t v : {(uint64_t)2, (uint64_t)N, (uint64_t)dtype, (uint64_t)F.tdtype, (uint64_t)F.registered,
-                       (uint64_t)F.scale_on, (uint64_t)nb, (uint64_t)nch})
+    for (uint64_t v : {(uint64_t)(bulk ? 3 : 2), (uint64_t)N, (uint64_t)dtype, (uint64_t)F.tdtype,
+                       (uint64_t)F.registered, (uint64_t)F.scale_on, (uint64_t)nb, (uint64_t)nch})
       h.add(v);
     for (int i = 0; i < nb; ++i)
       for (uint64_t v : {(uint64_t)F.bufs[i].L, (uint64_t)F.bufs[i].K, (uint64_t)(int64_t)F.bufs[i].owner, (uint64_t)F.bufs[i].nch})
         h.add(v);
     F.ring.hash = h.h;
   }
-  st = launch_counted(c, HVD_KERNEL_FUSED, s, [&] { return launch_fused(F, dtype, nch, c->nlocal, c->threads, s); });
+  if (bulk)
+    st = launch_counted(c, HVD_KERNEL_BULK, s, [&] { return launch_bulk(F, dtype, nch, c->nlocal, s); });
+  else
+    st = launch_counted(c, HVD_KERNEL_FUSED, s, [&] { return launch_fused(F, dtype, nch, c->nlocal, c->threads, s); });
   (void)tdt;
   if (st != HVD_OK) return st;
   if (c->tl) {
@@ -784,7 +803,7 @@ uint64_t ll128_lines(const hvd_comm* c, const DevPlanBuffer& b) {
 
 bool ll128_eligible(const hvd_comm* c, const DevPlanBuffer& b) {
   const int64_t bytes = (int64_t)(b.L * elem_size(b.dtype));
-  return c->size > 1 && c->protocol == 1 && b.L > 0 && b.tdtype == b.dtype && b.dtype != HVD_INT64 &&
+  return c->size > 1 && c->protocol >= 1 && b.L > 0 && b.tdtype == b.dtype && b.dtype != HVD_INT64 &&
          bytes > c->ll_max && bytes <= c->ll128_max &&
          (uint64_t)2 * (c->size - 1) * ll128_lines(c, b) * 128 <= kLLRegionBytes / 2;  // fits a half
 }
@@ -844,7 +863,7 @@ bool ll_eligible(const hvd_comm* c, const DevPlanBuffer& b, bool multi) {
   const int esz = elem_size(b.dtype);
   // (ll_max == 0 turns LL off everywhere; otherwise multi-buffer calls have their own limit)
   const int64_t lim = c->ll_max == 0 ? 0 : multi ? (c->size <= 2 ? kLLMultiBytes : kLLMultiBytesN4) : c->ll_max;
-  return c->size > 1 && c->protocol == 1 && b.L > 0 && b.tdtype == b.dtype && b.dtype != HVD_INT64 &&
+  return c->size > 1 && c->protocol >= 1 && b.L > 0 && b.tdtype == b.dtype && b.dtype != HVD_INT64 &&
          (int64_t)(b.L * esz) <= lim;
 }
 
@@ -862,7 +881,7 @@ int enqueue_fused_plan(hvd_comm* c, CachedPlan* plan, cudaStream_t s) {
   // launch, and at N = 2 the fused ring's two steps are short enough
   const bool many = (int)plan->bufs.size() > kDisjointMaxBufs;
   auto ll128_multi = [&](const DevPlanBuffer& b) {
-    return many && !ll_eligible(c, b, multi) && c->ll128_max > 0 && c->size > 2 && c->protocol == 1 && b.L > 0 &&
+    return many && !ll_eligible(c, b, multi) && c->ll128_max > 0 && c->size > 2 && c->protocol >= 1 && b.L > 0 &&
            b.tdtype == b.dtype && b.dtype != HVD_INT64 && (int64_t)(b.L * elem_size(b.dtype)) <= (16ll << 20) &&
            ll128_words(c, b) * 8 <= kLLRegionBytes / 2;
   };
@@ -1649,8 +1668,32 @@ int hvd_set_config(hvd_comm* c, int key, int64_t value) {
       c->multi_bufs = (int)value;
       return HVD_OK;
     case HVD_CFG_PROTOCOL:
-      if (value != 0 && value != 1) return HVD_ERR_INVALID;
+      if (value < 0 || value > 2) return HVD_ERR_INVALID;
       c->protocol = (int)value;
+      return HVD_OK;
+    case HVD_CFG_BULK_STAGES:
+      if (value < 3 || value > 8 || value <= c->bulk_depth + 1 ||
+          bulk_smem_bytes((int)value, c->bulk_stage_bytes) > kBulkMaxSmem)
+        return HVD_ERR_INVALID;
+      c->bulk_stages = (int)value;
+      return HVD_OK;
+    case HVD_CFG_BULK_STAGE_BYTES:
+      if (value < (4 << 10) || value > (64 << 10) || value % 1024 ||
+          bulk_smem_bytes(c->bulk_stages, (int)value) > kBulkMaxSmem)
+        return HVD_ERR_INVALID;
+      c->bulk_stage_bytes = (int)value;
+      return HVD_OK;
+    case HVD_CFG_BULK_DEPTH:
+      if (value < 0 || value > 3 || value + 1 >= c->bulk_stages) return HVD_ERR_INVALID;
+      c->bulk_depth = (int)value;
+      return HVD_OK;
+    case HVD_CFG_BULK_CHANNELS:
+      if (value < 1 || value > kMaxChannels) return HVD_ERR_INVALID;
+      c->bulk_channels = (int)value;
+      return HVD_OK;
+    case HVD_CFG_BULK_SLICE_BYTES:
+      if (value < kChunkQuantum || value % kChunkQuantum) return HVD_ERR_INVALID;
+      c->bulk_slice = value;
       return HVD_OK;
     case HVD_CFG_WINDOW:
       if (value < 0 || value > 1024) return HVD_ERR_INVALID;
@@ -1697,6 +1740,11 @@ int64_t hvd_get_config(const hvd_comm* c, int key) {
     case HVD_CFG_LL_MAX_BYTES: return c->ll_max;
     case HVD_CFG_LL128_MAX_BYTES: return c->ll128_max;
     case HVD_CFG_FIN_LAG: return c->fin_lag;
+    case HVD_CFG_BULK_STAGES: return c->bulk_stages;
+    case HVD_CFG_BULK_STAGE_BYTES: return c->bulk_stage_bytes;
+    case HVD_CFG_BULK_DEPTH: return c->bulk_depth;
+    case HVD_CFG_BULK_CHANNELS: return c->bulk_channels;
+    case HVD_CFG_BULK_SLICE_BYTES: return c->bulk_slice;
     default: return -1;
   }
 }
