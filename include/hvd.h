@@ -238,12 +238,15 @@ typedef enum {
                                 wire dtype; 1 push — SM stores into the successor's HBM;
                                 0 pull — each rank TMA-loads its predecessor's partials.
                                 Same ring order, same bits.                                 */
-  HVD_CFG_BULK_STAGES = 16,  /* bulk push: shared-memory stages per CTA (3..8, > BULK_DEPTH + 1) */
+  HVD_CFG_BULK_STAGES = 16,  /* bulk push: shared-memory stages per CTA (2..8)                */
   HVD_CFG_BULK_STAGE_BYTES = 17, /* bulk push: bytes per stage (4 KiB..64 KiB, multiple of 1 KiB) */
   HVD_CFG_BULK_DEPTH = 18,   /* bulk push: bulk-store groups a CTA leaves incomplete before it
-                                retires (publishes) a stage (0..3)                          */
+                                publishes a stage's op (0..3); a stage's shared memory is
+                                reused as soon as its stores have read it                   */
   HVD_CFG_BULK_CHANNELS = 19, /* bulk push: CTAs per rank (1..256; capped by co-residency)  */
-  HVD_CFG_BULK_SLICE_BYTES = 20 /* bulk push: signal slice per channel (multiple of 256 B)  */
+  HVD_CFG_BULK_SLICE_BYTES = 20, /* bulk push: signal slice per channel (multiple of 256 B) */
+  HVD_CFG_SIGNAL_WARPS = 21  /* fused push: signal warps per CTA (1..4; THREADS + 32 x this
+                                <= 416): each fences and publishes with a max, so fences overlap */
 } hvd_config_key;
 /* Set a tuning knob; every rank must set identical values.  Errors: INVALID. */
 int hvd_set_config(hvd_comm* c, int key, int64_t value);

@@ -76,6 +76,7 @@ struct RingParams {
   int* err;                     // host-mapped error word (device address)
   unsigned long long timeout_ns;
   int sig_mode;                 // signal fence variant (hvd_kernels.cu signal_loop)
+  int sig_warps;                // fused: signal warps per CTA (1: signal_loop, > 1: signal_loop_multi)
   int tl_max;                   // timeline: slice records per channel (0 = timeline off)
   unsigned long long* tl;       // timeline records of this launch (per local rank, see tl_words)
   int window;                   // fused: max pushed-but-unfenced slices per channel (0 = no limit)

@@ -278,6 +278,28 @@ __device__ __forceinline__ void signal_loop(const int* done, int total, unsigned
   }
 }
 
+// Several signal warps (HVD_CFG_SIGNAL_WARPS): a fence under NVLink load takes ~15 us
+// (profiles/r02_arrival_probe.json), so one signal lane publishes at most one batch per
+// fence.  Here each warp's lane 0 claims the slices done so far, fences and raises the
+// successor's counter with a max (publishes may land out of order; the counter stays
+// monotone), so fences overlap and a slice waits for at most one fence, not two.
+__device__ __forceinline__ void signal_loop_multi(const int* done, int* claimed, int total,
+                                                  unsigned long long* nflag, unsigned long long base, int* pub) {
+  for (;;) {
+    const int c = *(volatile int*)claimed;
+    if (c >= total) return;
+    const int d = ld_acquire_cta_shared(done);
+    if (d <= c) {
+      __nanosleep(32);
+      continue;
+    }
+    if (atomicCAS(claimed, c, d) != c) continue;
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    asm volatile("red.relaxed.sys.global.max.u64 [%0], %1;" ::"l"(nflag), "l"(base + (unsigned long long)d) : "memory");
+    if (pub) atomicMax(pub, d);
+  }
+}
+
 template <class Op>
 __global__ void __launch_bounds__(416, 1) ring_allreduce_kernel(const __grid_constant__ RingParams P) {
   const RingRank& me = P.rk[blockIdx.y];
@@ -890,8 +912,8 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
   const int r = me.rank;
   const unsigned long long base0 = R.base[ch];
   const int T = N > 1 ? 2 * (N - 1) : 0;
-  const int nd = blockDim.x - 32;
-  __shared__ int s_abort, s_done, s_pub;
+  const int nd = blockDim.x - 32 * R.sig_warps;
+  __shared__ int s_abort, s_done, s_pub, s_claim;
   unsigned long long* s_vbeg = s_dyn;
   Raw32* slots0 = reinterpret_cast<Raw32*>(s_dyn + P.cache_segs);
   uint4* slots1 = reinterpret_cast<uint4*>(slots0 + kPipe * nd);
@@ -899,6 +921,7 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
     s_abort = 0;
     s_done = 0;
     s_pub = 0;
+    s_claim = 0;
   }
   __syncthreads();
   if (N == 1) return;  // N = 1 runs solo_kernel
@@ -912,6 +935,11 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
     int total = 0;
     for (int b = 0; b < P.nbuf; ++b)
       if (chan_of(P.bufs[b], ch, gridDim.x) >= 0) total += T * P.bufs[b].K;
+    if (R.sig_warps > 1) {
+      if ((threadIdx.x - nd) % 32 == 0 && total > 0)
+        signal_loop_multi(&s_done, &s_claim, total, me.nflags + ch, base0, &s_pub);
+      return;
+    }
     if (threadIdx.x == nd && total > 0)
       signal_loop(&s_done, total, me.nflags + ch, base0, R.sig_mode, &s_pub,
                   R.tl ? R.tl + tl_words(R.tl_max) * blockIdx.y + ((size_t)kMaxChannels + ch) * R.tl_max * 2 : nullptr,
@@ -2048,21 +2076,29 @@ __global__ void __launch_bounds__(kBulkThreads, 1) bulk_allreduce_kernel(const _
     unsigned long long sent = 0;
     bool ready = false;
     const int depth = P.bulk_depth;
+    // A stage's shared memory goes back to the loader as soon as its bulk stores have READ
+    // it (cp.async.bulk.wait_group.read); its op is published once the stores are COMPLETE
+    // (cp.async.bulk.wait_group), `depth` groups behind the newest.  The publish data of
+    // a stage is kept here because its descriptor slot is reused after the release.
+    constexpr int kRing = 8;
+    int r_pub[kRing], r_op[kRing];
+    bool r_last[kRing];
+    unsigned long long released = 0;
+    auto release = [&](unsigned long long upto) {  // stages < upto have been read
+      for (; released < upto; ++released) mbar_arrive(&empty[(int)(released % S)]);
+    };
     auto retire = [&](unsigned long long upto) {  // stages < upto are complete
+      release(upto);
       for (; retired < upto; ++retired) {
-        const int slot = (int)(retired % S);
-        const int pub = desc[slot].pub;
-        const int op = desc[slot].op;
-        const bool last = desc[slot].last;
-        mbar_arrive(&empty[slot]);
-        if (pub >= 0) st_release_cta_shared(&s_done, pub);
-        if (last && tl_d && op < R.tl_max) tl_d[2 * op + 1] = globaltimer();
+        const int i = (int)(retired % kRing);
+        if (r_pub[i] >= 0) st_release_cta_shared(&s_done, r_pub[i]);
+        if (r_last[i] && tl_d && r_op[i] < R.tl_max) tl_d[2 * r_op[i] + 1] = globaltimer();
       }
     };
     for (;; ++seq) {
       const int slot = (int)(seq % S);
       // the next stage may wait on the successor's progress, which may wait on a stage
-      // published here: never leave issued stages unretired while waiting for it
+      // published here: never leave issued stages unpublished while waiting for it
       if (retired < seq && !mbar_test(&comp[slot], (unsigned)((seq / S) & 1))) {
         bulk_wait(0);
         retire(seq);
@@ -2111,6 +2147,11 @@ __global__ void __launch_bounds__(kBulkThreads, 1) bulk_allreduce_kernel(const _
         }
       }
       bulk_commit();
+      r_pub[seq % kRing] = sd.pub;
+      r_op[seq % kRing] = sd.op;
+      r_last[seq % kRing] = sd.last != 0;
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      if (seq > 0) release(seq);  // all but the newest stage have been read
       bulk_wait(depth);
       if (seq + 1 > (unsigned long long)depth) retire(seq + 1 - depth);
     }
@@ -2444,7 +2485,7 @@ static cudaError_t launch_fused_t(const FusedParams& p, int nch, int nlocal, int
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nch, nlocal);
-  cfg.blockDim = dim3(threads + 32);
+  cfg.blockDim = dim3(threads + 32 * p.ring.sig_warps);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];

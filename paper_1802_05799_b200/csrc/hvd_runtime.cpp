@@ -92,6 +92,7 @@ struct hvd_comm {
   int pack_ctas_per_sm = 8;
   int profile = 0;
   int sig_mode = 1;
+  int sig_warps = 1;  // HVD_CFG_SIGNAL_WARPS (fused kernel)
   int fused = 1;
   int multi_bufs = kMaxMultiBufs;  // fusion buffers per fused launch
   int window = 2;  // HVD_CFG_WINDOW (measured: N = 4 +5-8 %, N = 2 neutral)
@@ -504,6 +505,7 @@ int make_ring_params(hvd_comm* c, uint64_t L, int dtype, bool fused, RingParams*
   P->err = c->err_dev;
   P->timeout_ns = (unsigned long long)c->timeout_ms * 1000000ull;
   P->sig_mode = c->sig_mode;
+  P->sig_warps = fused ? c->sig_warps : 1;
   P->tl = c->tl;
   P->window = c->window;
   P->fin_lag = c->fin_lag;
@@ -1632,7 +1634,8 @@ int hvd_set_config(hvd_comm* c, int key, int64_t value) {
       c->slice_bytes = value;
       return HVD_OK;
     case HVD_CFG_THREADS:
-      if (value < 64 || value > 384 || value % 32) return HVD_ERR_INVALID;
+      if (value < 64 || value > 384 || value % 32 || value + 32 * c->sig_warps > kMaxRingThreads + 32)
+        return HVD_ERR_INVALID;
       c->threads = (int)value;
       return HVD_OK;
     case HVD_CFG_TIMEOUT_MS:
@@ -1671,8 +1674,12 @@ int hvd_set_config(hvd_comm* c, int key, int64_t value) {
       if (value < 0 || value > 2) return HVD_ERR_INVALID;
       c->protocol = (int)value;
       return HVD_OK;
+    case HVD_CFG_SIGNAL_WARPS:
+      if (value < 1 || value > 4 || c->threads + 32 * value > kMaxRingThreads + 32) return HVD_ERR_INVALID;
+      c->sig_warps = (int)value;
+      return HVD_OK;
     case HVD_CFG_BULK_STAGES:
-      if (value < 3 || value > 8 || value <= c->bulk_depth + 1 ||
+      if (value < 2 || value > 8 ||
           bulk_smem_bytes((int)value, c->bulk_stage_bytes) > kBulkMaxSmem)
         return HVD_ERR_INVALID;
       c->bulk_stages = (int)value;
@@ -1684,7 +1691,7 @@ int hvd_set_config(hvd_comm* c, int key, int64_t value) {
       c->bulk_stage_bytes = (int)value;
       return HVD_OK;
     case HVD_CFG_BULK_DEPTH:
-      if (value < 0 || value > 3 || value + 1 >= c->bulk_stages) return HVD_ERR_INVALID;
+      if (value < 0 || value > 3) return HVD_ERR_INVALID;
       c->bulk_depth = (int)value;
       return HVD_OK;
     case HVD_CFG_BULK_CHANNELS:
@@ -1740,6 +1747,7 @@ int64_t hvd_get_config(const hvd_comm* c, int key) {
     case HVD_CFG_LL_MAX_BYTES: return c->ll_max;
     case HVD_CFG_LL128_MAX_BYTES: return c->ll128_max;
     case HVD_CFG_FIN_LAG: return c->fin_lag;
+    case HVD_CFG_SIGNAL_WARPS: return c->sig_warps;
     case HVD_CFG_BULK_STAGES: return c->bulk_stages;
     case HVD_CFG_BULK_STAGE_BYTES: return c->bulk_stage_bytes;
     case HVD_CFG_BULK_DEPTH: return c->bulk_depth;
