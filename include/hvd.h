@@ -192,6 +192,22 @@ int hvd_allgather(hvd_comm* c, const hvd_tensor* in, const hvd_tensor* out, void
 
 /* ---- errors, statistics, tuning -------------------------------------------------------------- */
 
+/* LL128 safety (HVD_CFG_LL128_MAX_BYTES): the LL128 protocol relies on a warp's 128-byte
+ * line store arriving whole at the peer, which PTX does not promise.  hvd_connect runs
+ * this check on every communicator of N > 1 processes; virtual comms may call it.
+ * Collective: every rank calls it.  Each rank writes 8 rounds of 128-byte lines (flag in
+ * the 8th 16 B) into its successor's LL128 area while reading the lines its predecessor
+ * writes, and counts lines whose flag arrived without their data (or that never arrived
+ * within the watchdog).  The counts — plus, from hvd_connect, whether NVML reports both
+ * ring links as NVLink — are summed over the ranks with the LL protocol (8-byte words,
+ * single-copy atomic by PTX), and a non-zero sum disables LL128 (LL128_MAX_BYTES = 0)
+ * on every rank.  force_fail != 0 makes this rank report a failure (test hook; the
+ * environment variable HVD_LL128_SELFTEST_FORCE_FAIL=1 does the same inside
+ * hvd_connect).  *status = HVD_CFG_LL128_STATUS.  Synchronises the device.
+ * Errors: INVALID, NOT_CONNECTED, CUDA; a peer that never writes makes its lines count
+ * as missing (the check fails, it does not hang). */
+int hvd_ll128_selftest(hvd_comm* c, int force_fail, int* status);
+
 /* Latched asynchronous error (HVD_OK if none).  Non-blocking. */
 int hvd_poll_error(hvd_comm* c);
 const char* hvd_strerror(int status);
@@ -223,8 +239,13 @@ typedef enum {
   HVD_CFG_LL128_MAX_BYTES = 15, /* a call that is one fusion buffer larger than LL_MAX_BYTES
                                 and of at most this many bytes uses the LL128 protocol: flags
                                 inside 128-byte lines (relies on NVLink delivering a warp's
-                                128 B line store whole; 8/7 wire bytes).  Default 16 MiB at
-                                N = 2, 32 MiB at N > 2; max 64 MiB; 0 = never.             */
+                                128 B line store whole; 8/7 wire bytes).  In a call of more
+                                than 16 buffers at N > 2 (fusion off), buffers above the
+                                multi-buffer LL limit and up to min(this, 16 MiB) go to
+                                grouped LL128 launches.  Default 16 MiB at N = 2, 32 MiB at
+                                N > 2 when every ring link is NVLink and the connect-time
+                                line-atomicity self-test passed, else 0; max 64 MiB;
+                                0 = never.                                                  */
   HVD_CFG_LL_MAX_BYTES = 14, /* a call that is one fusion buffer of at most this many bytes
                                 (default 256 KiB; max 8 MiB; 0 = never, also in multi-buffer calls)
                                 uses the LL protocol: {epoch, data} words, no fences or
@@ -245,8 +266,13 @@ typedef enum {
                                 reused as soon as its stores have read it                   */
   HVD_CFG_BULK_CHANNELS = 19, /* bulk push: CTAs per rank (1..256; capped by co-residency)  */
   HVD_CFG_BULK_SLICE_BYTES = 20, /* bulk push: signal slice per channel (multiple of 256 B) */
-  HVD_CFG_SIGNAL_WARPS = 21  /* fused push: signal warps per CTA (1..4; THREADS + 32 x this
+  HVD_CFG_SIGNAL_WARPS = 21, /* fused push: signal warps per CTA (1..4; THREADS + 32 x this
                                 <= 416): each fences and publishes with a max, so fences overlap */
+  HVD_CFG_LL128_STATUS = 22  /* read only (hvd_get_config): outcome of the LL128 line-atomicity
+                                self-test: 0 not run (N = 1, or a virtual comm that did not
+                                call hvd_ll128_selftest), 1 passed, -1 torn or missing lines,
+                                -2 a ring link is not NVLink, -3 failure forced (test hook).
+                                Any failure sets LL128_MAX_BYTES to 0 on every rank.        */
 } hvd_config_key;
 /* Set a tuning knob; every rank must set identical values.  Errors: INVALID. */
 int hvd_set_config(hvd_comm* c, int key, int64_t value);

@@ -299,6 +299,13 @@ class Comm:
     def poll_error(self) -> int:
         return lib.hvd_poll_error(self._h)
 
+    def ll128_selftest(self, force_fail: bool = False) -> int:
+        """Collective LL128 line-atomicity self-test (``hvd_ll128_selftest``); returns
+        HVD_CFG_LL128_STATUS (1 passed; < 0 failed, LL128 switched off on every rank)."""
+        st = C.c_int(0)
+        check(lib.hvd_ll128_selftest(self._h, int(bool(force_fail)), C.byref(st)), "hvd_ll128_selftest")
+        return st.value
+
     def set_config(self, key: int, value: int):
         check(lib.hvd_set_config(self._h, int(key), int(value)), "hvd_set_config")
 

@@ -56,7 +56,7 @@ def build(force: bool = False, verbose: bool = False) -> pathlib.Path:
         subprocess.run(cmd, check=True)
         objs.append(str(obj))
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc, *ARCH, "-shared", "-o", str(tmp), *objs, "-cudart", "static"]
+    cmd = [nvcc, *ARCH, "-shared", "-o", str(tmp), *objs, "-cudart", "static", "-ldl"]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)

@@ -43,6 +43,7 @@ HVD_CFG_BULK_DEPTH = 18
 HVD_CFG_BULK_CHANNELS = 19
 HVD_CFG_BULK_SLICE_BYTES = 20
 HVD_CFG_SIGNAL_WARPS = 21
+HVD_CFG_LL128_STATUS = 22
 MAX_CHANNELS = 256
 HVD_KERNEL_PACK, HVD_KERNEL_RING, HVD_KERNEL_UNPACK, HVD_KERNEL_SCALE, HVD_KERNEL_FUSED = 0, 1, 2, 3, 4
 HVD_KERNEL_COPY = 5
@@ -127,6 +128,7 @@ def _load():
         "hvd_negotiator_pending": (C.c_int, [P, C.c_int, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
         "hvd_negotiator_destroy": (C.c_int, [P]),
         "hvd_negotiator_trace": (C.c_int, [P, C.c_int, C.POINTER(C.c_uint64), C.c_uint32, C.POINTER(C.c_uint32)]),
+        "hvd_ll128_selftest": (C.c_int, [P, C.c_int, C.POINTER(C.c_int)]),
         "hvd_allreduce_negotiated": (C.c_int, [P, P, C.POINTER(hvd_tensor), C.c_uint32, C.c_int, C.c_uint64, P,
                                                C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
     }
@@ -148,7 +150,7 @@ EXPORTS = sorted([
     "hvd_kernel_stats", "hvd_timeline", "hvd_allreduce_ex", "hvd_register_blob", "hvd_register",
     "hvd_allreduce_registered", "hvd_deregister", "hvd_negotiator_create", "hvd_negotiator_ready",
     "hvd_negotiator_cycle", "hvd_negotiator_pending", "hvd_negotiator_destroy", "hvd_allreduce_negotiated",
-    "hvd_allreduce_host", "hvd_negotiator_trace",
+    "hvd_allreduce_host", "hvd_negotiator_trace", "hvd_ll128_selftest",
 ])
 
 

@@ -185,14 +185,22 @@ cudaError_t launch_ll(const FusedParams& p, int dtype, int nch, int nlocal, cuda
 constexpr unsigned long long kLLMaxBytes = 256ull << 10;  // default LL payload limit for a lone buffer
 constexpr unsigned long long kLLLimitBytes = 8ull << 20;  // largest HVD_CFG_LL_MAX_BYTES accepted
 constexpr unsigned long long kLL128LimitBytes = 64ull << 20;  // largest HVD_CFG_LL128_MAX_BYTES accepted
-// 2 parities x (2N-2) steps x chunk slot of 2 q esz bytes (8 B word per 4 B of data)
-// = 8 (N-1) q esz < 8 L + 8 (N-1) N 256 for L <= kLLLimitBytes.
-// LL128 needs 2 (N-1) x lines x 128 B per half ~ 2 (N-1)/N x 8/7 x L <= 2.3 L: 160 MiB
-// halves hold a 64 MiB buffer at any N <= 8
-constexpr unsigned long long kLLRegionBytes = 320ull << 20;
+// LL region of a rank: [LL half 0][LL half 1][LL128 half 0][LL128 half 1].  LL and
+// LL128 never share memory: an LL word is taken when its upper 32 bits equal the epoch,
+// and LL128 lines carry raw data there (stale LL128 data must never be
+// polled by LL).  Launches of either protocol alternate the halves of their own pair.
+// LL: (2N-2) steps x chunk slot of 2 q esz bytes (8 B word per 4 B of data) per half
+// = 4 (N-1) q esz < 4 L + 4 (N-1) N 256 <= 32.1 MiB for L <= kLLLimitBytes.
+// LL128: 2 (N-1) x lines x 128 B per half ~ 2 (N-1)/N x 8/7 x L <= 2.3 L: 160 MiB
+// halves hold a 64 MiB buffer at any N <= 8.
+constexpr unsigned long long kLLHalfBytes = 48ull << 20;
+constexpr unsigned long long kLL128HalfBytes = 160ull << 20;
+constexpr unsigned long long kLLRegionBytes = 2 * (kLLHalfBytes + kLL128HalfBytes);
 cudaError_t pull_max_ctas_per_sm(int dtype, int threads, int* out);
 cudaError_t ll_max_ctas_per_sm(int* out);
 cudaError_t launch_ll128(const FusedParams& p, int dtype, int nch, int nlocal, cudaStream_t s);
+cudaError_t launch_ll128_selftest(const RingParams& p, int nch, int nlocal, int rounds, int lines_per_cta,
+                                  unsigned long long* torn, cudaStream_t s);
 cudaError_t launch_bulk(const FusedParams& p, int dtype, int nch, int nlocal, cudaStream_t s);
 cudaError_t bulk_max_ctas_per_sm(int dtype, int stages, int stage_bytes, int* out);
 size_t bulk_smem_bytes(int stages, int stage_bytes);

@@ -1494,9 +1494,9 @@ __global__ void __launch_bounds__(256) ll_allreduce_kernel(const __grid_constant
   const unsigned flag = (unsigned)R.epoch;
   const int par = (int)(R.epoch & 1);
   const unsigned long long slot_words = D.q / VEL * 4;  // words per chunk slot
-  // each parity owns a FIXED half of the region: a launch of another size must not reach
+  // each parity owns a FIXED half of the LL area: a launch of another size must not reach
   // into the other parity, which the successor may still be reading (previous launch)
-  constexpr unsigned long long kHalfWords = kLLRegionBytes / 2 / 8;
+  constexpr unsigned long long kHalfWords = kLLHalfBytes / 8;
   unsigned long long* const in_ll = me.ll + (unsigned long long)par * kHalfWords + D.ll_off;
   unsigned long long* const out_ll = me.nll + (unsigned long long)par * kHalfWords + D.ll_off;
   FusedCtx F;
@@ -1585,9 +1585,11 @@ __global__ void __launch_bounds__(256) ll128_allreduce_kernel(const __grid_const
   const unsigned long long qv = D.q / VEL;         // vectors per chunk
   const unsigned long long lines = (qv + 6) / 7;   // 128 B lines per chunk slot
   const unsigned long long slot_words = lines * 16;
-  constexpr unsigned long long kHalfWords = kLLRegionBytes / 2 / 8;
-  unsigned long long* const in_ll = me.ll + (unsigned long long)par * kHalfWords + D.ll_off;
-  unsigned long long* const out_ll = me.nll + (unsigned long long)par * kHalfWords + D.ll_off;
+  // the LL128 area follows the two LL halves (the protocols never share memory)
+  constexpr unsigned long long kBaseWords = 2 * kLLHalfBytes / 8;
+  constexpr unsigned long long kHalfWords = kLL128HalfBytes / 8;
+  unsigned long long* const in_ll = me.ll + kBaseWords + (unsigned long long)par * kHalfWords + D.ll_off;
+  unsigned long long* const out_ll = me.nll + kBaseWords + (unsigned long long)par * kHalfWords + D.ll_off;
   const unsigned long long lpc = (lines + nch - 1) / nch;  // lines of this channel
   const unsigned long long l_lo = (unsigned long long)ch * lpc < lines ? (unsigned long long)ch * lpc : lines;
   const unsigned long long l_hi = l_lo + lpc < lines ? l_lo + lpc : lines;
@@ -2227,6 +2229,94 @@ __global__ void __launch_bounds__(kBulkThreads, 1) bulk_allreduce_kernel(const _
   }
 }
 
+
+// ------------------------------------------------------------------ LL128 line-atomicity self-test
+// hvd_ll128_selftest / hvd_connect: LL128 relies on a warp's 128-byte line store arriving
+// whole, which PTX does not promise.  Every rank writes `rounds` x (gridDim.x x
+// lines_per_cta) lines into its successor's LL128 area (half 0) — lanes 0..6 of an
+// 8-lane group a pattern of (round, line, lane), lane 7 the flag ~(tag + round), one warp
+// store per line, exactly as ll128_allreduce_kernel stores — while its other warps read
+// the lines its predecessor writes into its own area.  A line whose flag matches but
+// whose data does not is torn; the count goes to `torn`.  Lines that never arrive within
+// the watchdog count as well.  The tag keeps the flags far from any LL128 epoch.
+constexpr unsigned long long kSelfTestTag = 0x5e1f000000000000ull;
+
+__device__ __forceinline__ unsigned long long selftest_word(int round, unsigned long long line, int sub, int half) {
+  unsigned long long z = kSelfTestTag ^ ((unsigned long long)round << 40) ^ (line << 8) ^ ((unsigned long long)sub << 1) ^
+                         (unsigned long long)half;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+__global__ void __launch_bounds__(256) ll128_selftest_kernel(const __grid_constant__ RingParams P, int rounds,
+                                                             int lines_per_cta, unsigned long long* torn) {
+  constexpr unsigned FULL = 0xffffffffu;
+  const RingRank& me = P.rk[blockIdx.y];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, sub = lane % 8, grp = lane / 8;
+  constexpr unsigned long long kBaseWords = 2 * kLLHalfBytes / 8;  // LL128 half 0
+  const unsigned long long* in = me.ll + kBaseWords;
+  unsigned long long* out = me.nll + kBaseWords;
+  const unsigned long long lines_total = (unsigned long long)gridDim.x * lines_per_cta;
+  const unsigned long long l0 = (unsigned long long)blockIdx.x * lines_per_cta;
+  const int w = warp & 3;
+  // handshake: this rank's earlier launches are over (the host synchronised the device),
+  // so its LL128 area may be overwritten; the writers wait for the successor's word
+  if (threadIdx.x == 0) st_release_sys(me.pready + blockIdx.x, P.epoch);
+  if (warp < 4) {  // writers: the successor's area
+    if (lane == 0) spin_until(me.rflags + blockIdx.x, P.epoch, P.err, P.timeout_ns);  // a dead peer latches TIMEOUT
+    __syncwarp();
+    for (int r = 0; r < rounds; ++r)
+      for (unsigned long long l = l0 + w * 4 + grp; l < l0 + lines_per_cta; l += 16) {
+        unsigned long long* dst = out + ((unsigned long long)r * lines_total + l) * 16 + sub * 2;
+        const unsigned long long f = ~(kSelfTestTag + (unsigned long long)r);
+        const unsigned long long w0 = sub < 7 ? selftest_word(r, l, sub, 0) : f;
+        const unsigned long long w1 = sub < 7 ? selftest_word(r, l, sub, 1) : f;
+        asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1,%2};" ::"l"(dst), "l"(w0), "l"(w1) : "memory");
+      }
+    return;
+  }
+  // readers: poll this rank's area, line by line, and check every arrived line
+  unsigned long long bad = 0;
+  bool dead = false;
+  for (int r = 0; r < rounds && !dead; ++r) {
+    const unsigned long long f = ~(kSelfTestTag + (unsigned long long)r);
+    for (unsigned long long lg = l0 + w * 4; lg < l0 + lines_per_cta && !dead; lg += 16) {
+      const unsigned long long l = lg + grp;
+      const bool active = l < l0 + lines_per_cta;
+      const unsigned long long* src = in + ((unsigned long long)r * lines_total + l) * 16 + sub * 2;
+      unsigned long long a = 0, b = 0, t0 = 0;
+      bool got = !active;
+      unsigned spins = 0;
+      for (;;) {
+        if (!got) asm volatile("ld.relaxed.sys.global.v2.u64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "l"(src) : "memory");
+        const unsigned long long fl = __shfl_sync(FULL, b, (lane & ~7) | 7);
+        if (!got && fl == f) got = true;
+        if (__all_sync(FULL, got)) break;
+        bool fail = false;
+        if ((++spins & 255u) == 0) {
+          const unsigned long long now = globaltimer();
+          if (t0 == 0) t0 = now;
+          else if (now - t0 > P.timeout_ns) fail = true;
+        }
+        if (__any_sync(FULL, fail)) {
+          dead = true;
+          break;
+        }
+      }
+      if (dead) break;
+      const bool ok = !active || (sub < 7 ? (a == selftest_word(r, l, sub, 0) && b == selftest_word(r, l, sub, 1))
+                                          : (a == f && b == f));
+      const unsigned ballot = __ballot_sync(FULL, !ok);
+      if (lane == 0) bad += (unsigned long long)__popc(ballot);
+    }
+  }
+  if (lane == 0) {
+    if (dead) bad += 1ull << 32;  // lines that never arrived
+    if (bad) atomicAdd(torn + blockIdx.y, bad);
+  }
+}
+
 struct BufList { char* b[kMaxLocal]; };
 
 template <int ESZ>
@@ -2730,6 +2820,21 @@ cudaError_t bulk_max_ctas_per_sm(int dtype, int stages, int stage_bytes, int* ou
       return e;
     default: return cudaErrorInvalidValue;
   }
+}
+
+
+cudaError_t launch_ll128_selftest(const RingParams& p, int nch, int nlocal, int rounds, int lines_per_cta,
+                                  unsigned long long* torn, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nch, nlocal);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // virtual ranks: readers and writers co-resident
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, ll128_selftest_kernel, p, rounds, lines_per_cta, torn);
 }
 
 }  // namespace hvd

@@ -14,6 +14,7 @@
 #include <list>
 #include <vector>
 
+#include <dlfcn.h>
 #include <unistd.h>
 
 #include "../../include/hvd.h"
@@ -40,6 +41,7 @@ struct Blob {
   uint64_t capacity;
   uint64_t region_bytes;
   cudaIpcMemHandle_t handle;
+  char pci[32];  // PCI bus id of the rank's GPU (NVLink check of the ring links)
 };
 
 struct DevPlanBuffer {
@@ -102,6 +104,7 @@ struct hvd_comm {
   int64_t ll_max = (int64_t)kLLMaxBytes;  // HVD_CFG_LL_MAX_BYTES
   int ll_ctas = 1;                         // co-resident LL CTAs per local rank
   int64_t ll128_max = 0;                   // HVD_CFG_LL128_MAX_BYTES
+  int ll128_status = 0;                    // HVD_CFG_LL128_STATUS (hvd_ll128_selftest)
   int protocol = 1;                 // 0: pull (receiver-initiated TMA loads), 1: push (SM stores),
                                     // 2: bulk push (TMA bulk loads / stores through shared memory)
   int bulk_stages = 6;              // HVD_CFG_BULK_STAGES
@@ -780,7 +783,7 @@ int enqueue_ll(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStream_t s, ui
     D.ll_off = (unsigned)words;
     words += (uint64_t)2 * (N - 1) * (D.q * esz / 16 * 4);  // T steps x slot (8 B word per 4 B of data)
   }
-  if (ctas > c->ll_ctas || words * 8 > kLLRegionBytes / 2) return HVD_ERR_INVALID;
+  if (ctas > c->ll_ctas || words * 8 > kLLHalfBytes) return HVD_ERR_INVALID;
   F.nbuf = nb;
   F.scale_on = bs[0]->pp.scale_on;
   F.scale = bs[0]->pp.scale;
@@ -807,7 +810,7 @@ bool ll128_eligible(const hvd_comm* c, const DevPlanBuffer& b) {
   const int64_t bytes = (int64_t)(b.L * elem_size(b.dtype));
   return c->size > 1 && c->protocol >= 1 && b.L > 0 && b.tdtype == b.dtype && b.dtype != HVD_INT64 &&
          bytes > c->ll_max && bytes <= c->ll128_max &&
-         (uint64_t)2 * (c->size - 1) * ll128_lines(c, b) * 128 <= kLLRegionBytes / 2;  // fits a half
+         (uint64_t)2 * (c->size - 1) * ll128_lines(c, b) * 128 <= kLL128HalfBytes;  // fits a half
 }
 
 int ll128_want(const hvd_comm* c, const DevPlanBuffer& b, uint64_t lines_per_cta = 32) {
@@ -850,13 +853,16 @@ int enqueue_ll128(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStream_t s)
     ctas += D.nch;
     words += ll128_words(c, b);
   }
-  if (ctas > c->ll_ctas || words * 8 > kLLRegionBytes / 2) return HVD_ERR_INVALID;
+  if (ctas > c->ll_ctas || words * 8 > kLL128HalfBytes) return HVD_ERR_INVALID;
   F.nbuf = nb;
   F.scale_on = bs[0]->pp.scale_on;
   F.scale = bs[0]->pp.scale;
   F.dtype = dtype;
   F.tdtype = dtype;
-  F.ring.epoch = ++c->ll_epoch;  // the LL epoch sequence: LL and LL128 launches alternate the halves
+  // one epoch sequence for LL and LL128 launches; each protocol alternates the two halves
+  // of its own area, so a half is reused at least two launches later (after the ring's
+  // dependency chain of the launch in between)
+  F.ring.epoch = ++c->ll_epoch;
   if (c->tl) c->tl_slices = 0;
   return launch_counted(c, HVD_KERNEL_LL128, s, [&] { return launch_ll128(F, dtype, ctas, c->nlocal, s); });
 }
@@ -884,8 +890,9 @@ int enqueue_fused_plan(hvd_comm* c, CachedPlan* plan, cudaStream_t s) {
   const bool many = (int)plan->bufs.size() > kDisjointMaxBufs;
   auto ll128_multi = [&](const DevPlanBuffer& b) {
     return many && !ll_eligible(c, b, multi) && c->ll128_max > 0 && c->size > 2 && c->protocol >= 1 && b.L > 0 &&
-           b.tdtype == b.dtype && b.dtype != HVD_INT64 && (int64_t)(b.L * elem_size(b.dtype)) <= (16ll << 20) &&
-           ll128_words(c, b) * 8 <= kLLRegionBytes / 2;
+           b.tdtype == b.dtype && b.dtype != HVD_INT64 &&
+           (int64_t)(b.L * elem_size(b.dtype)) <= std::min<int64_t>(c->ll128_max, 16ll << 20) &&
+           ll128_words(c, b) * 8 <= kLL128HalfBytes;
   };
   const uint64_t cta_bytes = multi ? (16 << 10) : 4096;
   // 1. LL groups: same dtype, <= kMaxMultiBufs buffers, CTA and region budgets
@@ -907,7 +914,7 @@ int enqueue_fused_plan(hvd_comm* c, CachedPlan* plan, cudaStream_t s) {
       const int want = ll_want(c, b, cta_bytes);
       const uint64_t w = (uint64_t)2 * (c->size - 1) * (q * esz / 16 * 4);
       if (!group.empty() && (group[0]->dtype != b.dtype || (int)group.size() >= kMaxMultiBufs ||
-                             ctas + want > c->ll_ctas || (words + w) * 8 > kLLRegionBytes / 2)) {
+                             ctas + want > c->ll_ctas || (words + w) * 8 > kLLHalfBytes)) {
         int st = flush();
         if (st != HVD_OK) return st;
       }
@@ -935,7 +942,7 @@ int enqueue_fused_plan(hvd_comm* c, CachedPlan* plan, cudaStream_t s) {
       const int want = ll128_want(c, b, 128);
       const uint64_t w = ll128_words(c, b);
       if (!group.empty() && (group[0]->dtype != b.dtype || (int)group.size() >= kMaxMultiBufs ||
-                             ctas + want > c->ll_ctas || (words + w) * 8 > kLLRegionBytes / 2)) {
+                             ctas + want > c->ll_ctas || (words + w) * 8 > kLL128HalfBytes)) {
         int st = flush();
         if (st != HVD_OK) return st;
       }
@@ -1029,6 +1036,90 @@ int do_allreduce(hvd_comm* c, const hvd_tensor* t, int n, int op, uint64_t thres
   return HVD_OK;
 }
 
+// NVLink P2P status of two GPUs by PCI bus id through NVML (dlopen: no link-time
+// dependency): 1 NVLink, 0 not NVLink, -1 unknown (NVML missing or the query failed).
+int nvlink_link(const char* a, const char* b) {
+  typedef int (*InitFn)();
+  typedef int (*HandleFn)(const char*, void**);
+  typedef int (*P2PFn)(void*, void*, int, int*);
+  static void* lib = dlopen("libnvidia-ml.so.1", RTLD_NOW | RTLD_LOCAL);
+  if (!lib) return -1;
+  static InitFn init = reinterpret_cast<InitFn>(dlsym(lib, "nvmlInit_v2"));
+  static HandleFn handle = reinterpret_cast<HandleFn>(dlsym(lib, "nvmlDeviceGetHandleByPciBusId_v2"));
+  static P2PFn p2p = reinterpret_cast<P2PFn>(dlsym(lib, "nvmlDeviceGetP2PStatus"));
+  static int init_rc = init ? init() : -1;
+  if (init_rc != 0 || !handle || !p2p) return -1;
+  void* da = nullptr;
+  void* db = nullptr;
+  if (handle(a, &da) != 0 || handle(b, &db) != 0) return -1;
+  if (da == db) return 1;  // one GPU (a ring of two ranks on one device is not a real comm)
+  int st = -1;
+  if (p2p(da, db, 2 /* NVML_P2P_CAPS_INDEX_NVLINK */, &st) != 0) return -1;
+  return st == 0 /* NVML_P2P_STATUS_OK */ ? 1 : 0;
+}
+
+// The LL128 line-atomicity self-test (ll128_selftest_kernel) and the agreement on its
+// outcome: every rank's count of torn or missing lines (plus `no_nvlink`, `force_fail`)
+// is summed by a one-element LL allreduce — the LL protocol's 8-byte words are
+// single-copy atomic by PTX, so the agreement does not depend on what is being tested.
+// A non-zero sum disables LL128 on every rank (HVD_CFG_LL128_MAX_BYTES = 0).
+int ll128_selftest(hvd_comm* c, int no_nvlink, int force_fail, int* status) {
+  *status = 0;
+  if (c->size <= 1) return HVD_OK;
+  CK(cudaSetDevice(c->device));
+  CK(cudaDeviceSynchronize());  // no earlier launch of this rank still reads its LL128 area
+  cudaStream_t s = nullptr;
+  CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  unsigned long long* torn = nullptr;
+  int st = cuda_fail(cudaMalloc(reinterpret_cast<void**>(&torn), 8 * kMaxLocal + 16 * kMaxLocal), "cudaMalloc");
+  unsigned long long host[kMaxLocal] = {};
+  int flag[kMaxLocal * 4] = {};  // per local rank: {torn or missing lines, not NVLink, forced, 0}
+  if (st == HVD_OK) st = cuda_fail(cudaMemsetAsync(torn, 0, 8 * kMaxLocal, s), "cudaMemsetAsync");
+  if (st == HVD_OK) {
+    RingParams P;
+    std::memset(&P, 0, sizeof(P));
+    for (int l = 0; l < c->nlocal; ++l) P.rk[l] = c->rk[l];
+    P.N = c->size;
+    P.timeout_ns = (unsigned long long)c->timeout_ms * 1000000ull;
+    P.err = c->err_dev;
+    P.epoch = ++c->hs_epoch;  // the launch handshake's epoch sequence (every rank calls this)
+    const int nch = std::max(1, std::min(64, c->sm_count * 2 / c->nlocal));
+    st = cuda_fail(launch_ll128_selftest(P, nch, c->nlocal, 8, 256, torn, s), "ll128 self-test");
+  }
+  if (st == HVD_OK) st = cuda_fail(cudaMemcpyAsync(host, torn, 8 * c->nlocal, cudaMemcpyDeviceToHost, s), "copy");
+  if (st == HVD_OK) st = cuda_fail(cudaStreamSynchronize(s), "self-test sync");
+  int* dflag = reinterpret_cast<int*>(torn + kMaxLocal);
+  if (st == HVD_OK) {
+    for (int l = 0; l < c->nlocal; ++l) {
+      flag[4 * l + 0] = host[l] ? 1 : 0;
+      flag[4 * l + 1] = no_nvlink ? 1 : 0;
+      flag[4 * l + 2] = force_fail ? 1 : 0;
+      flag[4 * l + 3] = 0;
+    }
+    st = cuda_fail(cudaMemcpyAsync(dflag, flag, 16 * c->nlocal, cudaMemcpyHostToDevice, s), "copy");
+  }
+  if (st == HVD_OK) {
+    std::vector<hvd_tensor> t(c->nlocal);
+    for (int l = 0; l < c->nlocal; ++l) t[l] = {dflag + 4 * l, 4, HVD_INT32, 0};
+    st = do_allreduce(c, t.data(), 1, HVD_SUM, c->cap, s);
+  }
+  if (st == HVD_OK) st = cuda_fail(cudaMemcpyAsync(flag, dflag, 16, cudaMemcpyDeviceToHost, s), "copy");
+  if (st == HVD_OK) st = cuda_fail(cudaStreamSynchronize(s), "agreement sync");
+  if (torn) cudaFree(torn);
+  cudaStreamDestroy(s);
+  if (st != HVD_OK) return st;
+  // summed over the ranks: {ranks that saw torn or missing lines, ranks with a non-NVLink
+  // ring link, ranks forcing a failure} — identical on every rank
+  if (flag[0] == 0 && flag[1] == 0 && flag[2] == 0) {
+    *status = 1;
+  } else {
+    *status = flag[2] ? -3 : (flag[1] ? -2 : -1);
+    c->ll128_max = 0;
+  }
+  c->ll128_status = *status;
+  return HVD_OK;
+}
+
 }  // namespace
 
 // ================================================================== C ABI
@@ -1097,6 +1188,7 @@ int hvd_get_ipc_blob(hvd_comm* c, void* out, uint64_t* len) {
   b.region_bytes = kNumBufs * c->bufsz + kTailBytes + kLLRegionBytes;
   CK(cudaSetDevice(c->device));
   CK(cudaIpcGetMemHandle(&b.handle, c->region[0]));
+  CK(cudaDeviceGetPCIBusId(b.pci, (int)sizeof(b.pci), c->device));
   std::memcpy(out, &b, sizeof(b));
   *len = sizeof(Blob);
   return HVD_OK;
@@ -1131,7 +1223,22 @@ int hvd_connect(hvd_comm* c, const void* blobs, uint64_t len_each) {
   }
   set_neighbours(c->rk[0], c->peer_region, c->pred_region, c->bufsz);
   c->connected = true;
-  return HVD_OK;
+  // LL128 only over verified NVLink ring links whose 128-byte lines arrive whole
+  // (ADVICE r1): NVML's NVLink P2P status of both links, then the line-atomicity
+  // self-test; every rank applies the same agreed outcome.
+  char me_pci[32] = {};
+  CK(cudaDeviceGetPCIBusId(me_pci, (int)sizeof(me_pci), c->device));
+  const int nv = nvlink_link(me_pci, bs.pci) == 1 && nvlink_link(me_pci, bp.pci) == 1;
+  const char* ff = std::getenv("HVD_LL128_SELFTEST_FORCE_FAIL");
+  int status = 0;
+  return ll128_selftest(c, !nv, ff && ff[0] == '1', &status);
+}
+
+int hvd_ll128_selftest(hvd_comm* c, int force_fail, int* status) {
+  int st = check_live(c);
+  if (st != HVD_OK) return st;
+  if (!status) return HVD_ERR_INVALID;
+  return ll128_selftest(c, 0, force_fail, status);
 }
 
 int hvd_finalize(hvd_comm* c) {
@@ -1748,6 +1855,7 @@ int64_t hvd_get_config(const hvd_comm* c, int key) {
     case HVD_CFG_LL128_MAX_BYTES: return c->ll128_max;
     case HVD_CFG_FIN_LAG: return c->fin_lag;
     case HVD_CFG_SIGNAL_WARPS: return c->sig_warps;
+    case HVD_CFG_LL128_STATUS: return c->ll128_status;
     case HVD_CFG_BULK_STAGES: return c->bulk_stages;
     case HVD_CFG_BULK_STAGE_BYTES: return c->bulk_stage_bytes;
     case HVD_CFG_BULK_DEPTH: return c->bulk_depth;

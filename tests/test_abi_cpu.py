@@ -26,7 +26,7 @@ def L():
 def _header_functions():
     text = (ROOT / "include" / "hvd.h").read_text()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b(hvd_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(hvd_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_library_exports_every_header_symbol(L):

@@ -27,13 +27,22 @@ def hvd():
 _COMMS = {}
 
 
-def bulk_comm(hvd, n, cap=64 << 20, ll=False):
-    key = (n, cap, ll)
+@pytest.fixture(scope="module", autouse=True)
+def _finalize_comms():
+    """Each virtual comm holds every rank's buffers on the one GPU: free them per module."""
+    yield
+    for c in _COMMS.values():
+        c.finalize()
+    _COMMS.clear()
+
+
+def bulk_comm(hvd, n, cap=64 << 20, ll=False, proto=2):
+    key = (n, cap, ll, proto)
     if key not in _COMMS:
         c = hvd.init_virtual(n, 0, cap)
         L = hvd._lib
         c.set_config(L.HVD_CFG_TIMEOUT_MS, 20000)
-        c.set_config(L.HVD_CFG_PROTOCOL, 2)
+        c.set_config(L.HVD_CFG_PROTOCOL, proto)
         if not ll:
             c.set_config(L.HVD_CFG_LL_MAX_BYTES, 0)
             c.set_config(L.HVD_CFG_LL128_MAX_BYTES, 0)
@@ -178,11 +187,16 @@ def test_bulk_registered_zero_copy(hvd, n):
         comm.finalize()
 
 
+KERNEL = {1: "fused", 2: "bulk"}
+
+
+@pytest.mark.parametrize("proto", [1, 2])
 @pytest.mark.parametrize("n", [2, 4, 8])
-def test_bulk_bench_step_registered_64MiB(hvd, n):
+def test_bench_step_registered_64MiB(hvd, n, proto):
     """bench.py's exact step: one registered 64 MiB fp32 gradient, default 64 MiB capacity,
-    allreduce-average through the bulk kernel; every element vs the oracle."""
-    comm = bulk_comm(hvd, n, ll=True)
+    allreduce-average through the default SM-store push (1) and the bulk push (2); every
+    element vs the oracle."""
+    comm = bulk_comm(hvd, n, ll=True, proto=proto)
     cnt = 16 << 20
     xs = [[workloads.rank_tensor(cnt, "f32", r, 0)] for r in range(n)]
     ref, _, plan = oracle.allreduce(xs, ["f32"], "average")
@@ -193,17 +207,18 @@ def test_bulk_bench_step_registered_64MiB(hvd, n):
     comm.allreduce_average(reg)
     torch.cuda.synchronize()
     assert comm.poll_error() == 0
-    assert comm.kernel_stats()["bulk"][0] == 1
+    assert comm.kernel_stats()[KERNEL[proto]][0] == 1
     for r in range(n):
         assert_same(from_torch(ts[r][0], "f32"), ref[r][0], "f32", f"N={n} r={r}")
     comm.deregister(reg)
 
 
+@pytest.mark.parametrize("proto", [1, 2])
 @pytest.mark.parametrize("n", [2, 4, 8])
-def test_bulk_raw_buffer_16Mi_and_traffic(hvd, n):
+def test_raw_buffer_16Mi_and_traffic(hvd, n, proto):
     """hvd_allreduce_buffer of 16 Mi fp32 (the headline ring) and a ragged length: bits and the
     per-rank traffic counters 2L - |c_{r+1}| - |c_{r+2}|."""
-    comm = bulk_comm(hvd, n)
+    comm = bulk_comm(hvd, n, proto=proto)
     for L_ in (16 << 20, 3_000_017):
         xs = [workloads.rank_tensor(L_, "f32", r, 9) for r in range(n)]
         ref, tr = oracle.allreduce_buffer(xs, "f32", "average")
@@ -220,12 +235,14 @@ def test_bulk_raw_buffer_16Mi_and_traffic(hvd, n):
             assert sends - before[r][1] == 2 * (n - 1)
 
 
+@pytest.mark.parametrize("proto", [1, 2])
 @pytest.mark.parametrize("model,dtype,n", [("vgg16", "f32", 4), ("vgg16", "f32", 8), ("resnet101", "f32", 4),
                                            ("inception_v3", "bf16", 2)])
-def test_bulk_model_sets_full_size(hvd, model, dtype, n):
+def test_model_sets_full_size(hvd, model, dtype, n, proto):
     """BASELINE configs C2-C4 at full size (VGG-16: 11 buffers, fc6 split 6 x 64 + 8 MiB, fc7
-    exactly 64 MiB) through the bulk kernel: every element vs the oracle."""
-    comm = bulk_comm(hvd, n)
+    exactly 64 MiB), library defaults (LL / LL128 for small buffers) with the SM-store push (1)
+    or the bulk push (2) for the rest: every element vs the oracle."""
+    comm = bulk_comm(hvd, n, ll=True, proto=proto)
     counts = [c for _, c in workloads.gradient_set(model)]
     xs = workloads.all_ranks(counts, dtype, n)
     dts = [dtype] * len(counts)

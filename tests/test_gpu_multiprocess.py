@@ -159,7 +159,17 @@ CASES = [
 ]
 
 
-@pytest.mark.parametrize("protocol", [1, 0])
+def _evidence(name, obj):
+    """Keep what a multi-GPU run verified (the driver's GPU test box may have one GPU):
+    gpurun_out/ travels back from gpurun and is copied into profiles/."""
+    import json
+    d = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+    os.makedirs(d, exist_ok=True)
+    with open(os.path.join(d, name), "w") as f:
+        json.dump(obj, f, indent=1)
+
+
+@pytest.mark.parametrize("protocol", [1, 0, 2])
 def test_multiprocess_ring_matches_oracle(protocol):
     n = min(torch.cuda.device_count(), 4)
     if n < 2:
@@ -265,6 +275,10 @@ def test_multiprocess_ring_matches_oracle(protocol):
                 assert_same(res[r][0][ci][0], ref[r], dtype, f"buffer case {ci} rank {r}")
                 sent, sends = res[r][0][ci][1]
                 assert sent == tr[r].sent_elems * oracle.ELEM_SIZE[dtype] and sends == 2 * (n - 1)
+    _evidence(f"mp_evidence_n{n}_protocol{protocol}.json",
+              {"test": "test_multiprocess_ring_matches_oracle", "n_gpus": n, "protocol": protocol,
+               "result": "every case bit-exact vs the oracle on every rank",
+               "cases": [{"kind": k, "counts": c, "dtype": d, "op": o, "threshold": t} for k, c, d, o, t in CASES]})
 
 
 def _timeout_worker(rank, world, port, q):
@@ -359,3 +373,66 @@ def test_mismatched_calls_are_detected():
         p.join(timeout=120)
     assert all(isinstance(v, int) for v in res.values()), res
     assert -7 in res.values() and set(res.values()) <= {-7, -5}, res
+
+
+def _selftest_worker(rank, world, port, q, force_rank):
+    os.environ.update(RANK=str(rank), WORLD_SIZE=str(world), LOCAL_RANK=str(rank),
+                      MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    if rank == force_rank:
+        os.environ["HVD_LL128_SELFTEST_FORCE_FAIL"] = "1"
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import paper_1802_05799_b200 as hvd
+    import torch.distributed as dist
+    try:
+        comm = hvd.init()  # hvd_connect runs the NVLink check + LL128 self-test
+        L = hvd._lib
+        status = comm.get_config(L.HVD_CFG_LL128_STATUS)
+        ll128 = comm.get_config(L.HVD_CFG_LL128_MAX_BYTES)
+        comm.set_config(L.HVD_CFG_TIMEOUT_MS, 20000)
+        x = to_torch(workloads.rank_tensor(2_000_003, "f32", rank, 3, "normal"), "f32")  # ~8 MiB: LL128 if on
+        comm.kernel_stats()
+        comm.allreduce_average([x])
+        torch.cuda.synchronize()
+        ks = {k: v[0] for k, v in comm.kernel_stats().items() if v[0]}
+        again = comm.ll128_selftest()  # the explicit call agrees too
+        q.put((rank, (status, ll128, ks, from_torch(x, "f32"), comm.poll_error(), again)))
+        dist.barrier()
+        comm.finalize()
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e)))
+
+
+@pytest.mark.parametrize("force_rank", [-1, 1])
+def test_ll128_selftest_at_connect(force_rank):
+    """hvd_connect's LL128 safety check: on NVLink with whole 128-byte lines every rank
+    passes and uses LL128 for an 8 MiB buffer; one rank forcing a failure switches LL128 off
+    on EVERY rank (agreed through an LL allreduce) and results stay bit-exact."""
+    n = min(torch.cuda.device_count(), 4)
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_selftest_worker, args=(r, n, port, q, force_rank)) for r in range(n)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(n))
+    for p in procs:
+        p.join(timeout=120)
+    assert all(isinstance(v, tuple) for v in res.values()), res
+    xs = [[workloads.rank_tensor(2_000_003, "f32", r, 3, "normal")] for r in range(n)]
+    ref, _, _ = oracle.allreduce(xs, ["f32"], "average")
+    for r in range(n):
+        status, ll128, ks, got, err, again = res[r]
+        assert err == 0
+        assert_same(got, ref[r][0], "f32", f"rank {r}")
+        if force_rank < 0:
+            assert status == 1 and again == 1 and ll128 > 0 and ks.get("ll128") == 1, res[r][:3]
+        else:
+            assert status == -3 and ll128 == 0 and "ll128" not in ks, res[r][:3]
+    _evidence(f"mp_evidence_ll128_selftest_n{n}_force{force_rank}.json",
+              {"test": "test_ll128_selftest_at_connect", "n_gpus": n, "force_rank": force_rank,
+               "status_per_rank": [res[r][0] for r in range(n)], "ll128_max_per_rank": [res[r][1] for r in range(n)],
+               "kernels_per_rank": [res[r][2] for r in range(n)], "result": "bit-exact vs the oracle"})

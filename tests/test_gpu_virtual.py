@@ -27,6 +27,15 @@ def hvd():
 _COMMS = {}
 
 
+@pytest.fixture(scope="module", autouse=True)
+def _finalize_comms():
+    """Each virtual comm holds every rank's buffers on the one GPU: free them per module."""
+    yield
+    for c in _COMMS.values():
+        c.finalize()
+    _COMMS.clear()
+
+
 def comm_for(hvd, n, cap=64 << 20):
     key = (n, cap)
     if key not in _COMMS:
@@ -723,3 +732,61 @@ def test_ll128_protocol_bitexact(hvd, n):
     finally:
         comm.set_config(L.HVD_CFG_LL_MAX_BYTES, ll_d)
         comm.set_config(L.HVD_CFG_LL128_MAX_BYTES, ll128_d)
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_ll_after_ll128_small_int_data(hvd, n):
+    """LL and LL128 own separate areas: an LL128 launch whose int32 data words
+    equal small future epochs, followed by LL launches at those epochs, stays bit-exact.
+    With a shared area, LL could take the stale LL128 words as its own."""
+    comm = comm_for(hvd, n)
+    big = 1 << 19    # 2 MiB int32: LL128
+    small = 4096     # 16 KiB: LL
+    pend = []
+    for it in range(12):
+        xs = [[np.full(big, (it % 8) + 1 + r, dtype=np.int32)] for r in range(n)]
+        ts = [[to_torch(x, "i32") for x in xs[r]] for r in range(n)]
+        comm.allreduce(ts, op="sum")
+        pend.append((xs, ts))
+        for j in range(3):
+            xs2 = [[(np.arange(small, dtype=np.int32) % 7) + j + it + r] for r in range(n)]
+            ts2 = [[to_torch(x, "i32") for x in xs2[r]] for r in range(n)]
+            comm.allreduce(ts2, op="sum")
+            pend.append((xs2, ts2))
+    torch.cuda.synchronize()
+    assert comm.poll_error() == 0
+    st = comm.kernel_stats()
+    assert st["ll128"][0] >= 12 and st["ll"][0] >= 36
+    for xs, ts in pend:
+        ref, _, _ = oracle.allreduce(xs, ["i32"], "sum")
+        for r in range(n):
+            assert_same(from_torch(ts[r][0], "i32"), ref[r][0], "i32")
+
+
+def test_ll128_selftest_virtual(hvd):
+    """hvd_ll128_selftest on virtual ranks: passes; a forced failure switches LL128 off and
+    the LL128-sized call then runs on the fused push, bit-exact."""
+    n = 4
+    comm = hvd.init_virtual(n, 0, 64 << 20)
+    try:
+        L = hvd._lib
+        comm.set_config(L.HVD_CFG_TIMEOUT_MS, 20000)
+        assert comm.get_config(L.HVD_CFG_LL128_STATUS) == 0
+        assert comm.ll128_selftest() == 1
+        assert comm.get_config(L.HVD_CFG_LL128_MAX_BYTES) > 0
+        xs = workloads.all_ranks([2_000_003], "f32", n)
+        ref, _, _ = oracle.allreduce(xs, ["f32"], "average")
+        for expect_kernel in ("ll128", "fused"):
+            if expect_kernel == "fused":
+                assert comm.ll128_selftest(force_fail=True) == -3
+                assert comm.get_config(L.HVD_CFG_LL128_MAX_BYTES) == 0
+            ts = [[to_torch(xs[r][0], "f32")] for r in range(n)]
+            comm.kernel_stats()
+            comm.allreduce_average(ts)
+            torch.cuda.synchronize()
+            assert comm.poll_error() == 0
+            assert comm.kernel_stats()[expect_kernel][0] == 1
+            for r in range(n):
+                assert_same(from_torch(ts[r][0], "f32"), ref[r][0], "f32", f"{expect_kernel} r={r}")
+    finally:
+        comm.finalize()
