@@ -268,11 +268,20 @@ typedef enum {
   HVD_CFG_BULK_SLICE_BYTES = 20, /* bulk push: signal slice per channel (multiple of 256 B) */
   HVD_CFG_SIGNAL_WARPS = 21, /* fused push: signal warps per CTA (1..4; THREADS + 32 x this
                                 <= 416): each fences and publishes with a max, so fences overlap */
-  HVD_CFG_LL128_STATUS = 22  /* read only (hvd_get_config): outcome of the LL128 line-atomicity
+  HVD_CFG_LL128_STATUS = 22, /* read only (hvd_get_config): outcome of the LL128 line-atomicity
                                 self-test: 0 not run (N = 1, or a virtual comm that did not
                                 call hvd_ll128_selftest), 1 passed, -1 torn or missing lines,
                                 -2 a ring link is not NVLink, -3 failure forced (test hook).
                                 Any failure sets LL128_MAX_BYTES to 0 on every rank.        */
+  HVD_CFG_SOLO_KERNEL = 23,  /* N = 1 (gather x 1/N -> scatter, an HBM stream): 0 (default)
+                                one CTA per 16 KiB tile; 1 persistent bulk-copy kernel (one
+                                CTA per SM streaming tiles through shared-memory stages: each
+                                byte holds shared memory from load issue to store read, which
+                                measured slower).  Both use programmatic dependent launch.
+                                Tensors whose dtype differs from the wire dtype always take
+                                the tile kernel.                                            */
+  HVD_CFG_SOLO_STAGES = 24,  /* N = 1 bulk kernel: shared-memory stages per CTA (2..8)      */
+  HVD_CFG_SOLO_STAGE_BYTES = 25 /* N = 1 bulk kernel: bytes per stage (4..64 KiB, x 1 KiB)   */
 } hvd_config_key;
 /* Set a tuning knob; every rank must set identical values.  Errors: INVALID. */
 int hvd_set_config(hvd_comm* c, int key, int64_t value);

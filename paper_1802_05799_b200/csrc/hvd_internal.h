@@ -202,8 +202,8 @@ cudaError_t launch_ll128(const FusedParams& p, int dtype, int nch, int nlocal, c
 cudaError_t launch_ll128_selftest(const RingParams& p, int nch, int nlocal, int rounds, int lines_per_cta,
                                   unsigned long long* torn, cudaStream_t s);
 cudaError_t launch_bulk(const FusedParams& p, int dtype, int nch, int nlocal, cudaStream_t s);
-cudaError_t bulk_max_ctas_per_sm(int dtype, int stages, int stage_bytes, int* out);
-size_t bulk_smem_bytes(int stages, int stage_bytes);
+cudaError_t bulk_max_ctas_per_sm(int dtype, int stages, int stage_bytes, int* out, bool two = true);
+size_t bulk_smem_bytes(int stages, int stage_bytes, bool two = true);  // two: A and B stages (N > 1)
 cudaError_t launch_solo(const FusedParams& p, int dtype, int nlocal, cudaStream_t s);
 cudaError_t fused_max_ctas_per_sm(int dtype, int threads, int* out);
 cudaError_t launch_pack(const PackParams& p, int dtype, int nlocal, int grid, int threads,

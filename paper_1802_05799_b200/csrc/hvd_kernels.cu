@@ -523,7 +523,8 @@ enum FusedKind { kF_RS0 = 0, kF_RS = 1, kF_AG0 = 2, kF_AG = 3, kF_FIN = 4,
                  kF_RAG0 = 8,   // registered all-gather step 0: final -> own tensors + successor's tensors
                  kF_RAG = 9,    // registered all-gather step s >= 1: own tensors -> successor's tensors
                  kF_G2B = 6,    // broadcast root:        nbuf <- gather(x)
-                 kF_G2BS = 7 }; // allgather own block:   nbuf <- gather(in); out <- same
+                 kF_G2BS = 7,   // allgather own block:   nbuf <- gather(in); out <- same
+                 kF_SOLO = 10 };// N = 1 (bulk kernel): x <- gather(x) * s
 
 struct FusedCtx {
   const PackSeg* segs;
@@ -1736,14 +1737,18 @@ struct StageDesc {
 };
 
 __host__ __device__ constexpr bool bk_gathers(int k) {
-  return k == kF_RS0 || k == kF_RS || k == kF_AG0 || k == kF_RAG0 || k == kF_RAG;
+  return k == kF_RS0 || k == kF_RS || k == kF_AG0 || k == kF_RAG0 || k == kF_RAG || k == kF_SOLO;
 }
-__host__ __device__ constexpr bool bk_scales(int k) { return k == kF_RS0 || k == kF_RS || k == kF_AG0 || k == kF_RAG0; }
+__host__ __device__ constexpr bool bk_scales(int k) {
+  return k == kF_RS0 || k == kF_RS || k == kF_AG0 || k == kF_RAG0 || k == kF_SOLO;
+}
 __host__ __device__ constexpr bool bk_adds(int k) { return k == kF_RS || k == kF_AG0 || k == kF_RAG0; }
 __host__ __device__ constexpr bool bk_from_buf(int k) { return k == kF_AG || k == kF_FIN; }
 __host__ __device__ constexpr bool bk_to_nscr(int k) { return k == kF_RS0 || k == kF_RS; }
 __host__ __device__ constexpr bool bk_to_nbuf(int k) { return k == kF_AG0 || k == kF_AG; }
-__host__ __device__ constexpr bool bk_scatters(int k) { return k == kF_AG0 || k == kF_AG || k == kF_FIN || k == kF_RAG0; }
+__host__ __device__ constexpr bool bk_scatters(int k) {
+  return k == kF_AG0 || k == kF_AG || k == kF_FIN || k == kF_RAG0 || k == kF_SOLO;
+}
 __host__ __device__ constexpr bool bk_rscatters(int k) { return k == kF_RAG0 || k == kF_RAG; }
 __host__ __device__ constexpr bool bk_members(int k) { return bk_gathers(k) || bk_scatters(k) || bk_rscatters(k); }
 
@@ -1886,10 +1891,10 @@ __global__ void __launch_bounds__(kBulkThreads, 1) bulk_allreduce_kernel(const _
   const int S = P.bulk_stages;
   const unsigned stage_vecs = (unsigned)(P.bulk_stage_bytes / 16);
   const unsigned long long base0 = R.base[ch];
-  // shared memory: [A stages][B stages][descriptors][mbarriers full, comp, empty]
+  // shared memory: [A stages][B stages (N > 1)][descriptors][mbarriers full, comp, empty]
   uint4* sA = reinterpret_cast<uint4*>(s_bulk);
   uint4* sB = sA + (size_t)S * stage_vecs;
-  StageDesc* desc = reinterpret_cast<StageDesc*>(sB + (size_t)S * stage_vecs);
+  StageDesc* desc = reinterpret_cast<StageDesc*>(sA + (size_t)(N > 1 ? 2 : 1) * S * stage_vecs);
   unsigned long long* full = reinterpret_cast<unsigned long long*>(desc + S);
   unsigned long long* comp = full + S;
   unsigned long long* empty = comp + S;
@@ -1904,6 +1909,9 @@ __global__ void __launch_bounds__(kBulkThreads, 1) bulk_allreduce_kernel(const _
       mbar_init(&empty[i], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // programmatic dependent launch (N = 1 launches): the next kernel on the stream may
+    // start launching now; it waits for this grid's completion before touching memory
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   }
   __syncthreads();
   // ring ops this channel publishes over the whole call
@@ -1935,6 +1943,68 @@ __global__ void __launch_bounds__(kBulkThreads, 1) bulk_allreduce_kernel(const _
       if (q >= (unsigned long long)S) mbar_wait_wd(&empty[slot], (unsigned)((q / S - 1) & 1), R.err, R.timeout_ns);
       return slot;
     };
+    // member pieces of stage [v0, v1): bulk-load the gathered ones into A, list the
+    // element-wise ones; the stage ends early (returned end) when the list is full
+    auto walk_stage = [&](StageDesc& sd, int slot, unsigned long long v0, unsigned long long v1, int kind,
+                          const BulkTabs& TB, int& cur) -> unsigned long long {
+      uint4* A = sA + (size_t)slot * stage_vecs;
+      unsigned long long cut = v1;
+      int nexc = 0;
+      bulk_walk(TB, VEL, v0, v1, cur, [&](unsigned long long a, unsigned long long e, int s, bool exc) -> bool {
+        if (exc) {
+          if (nexc == kBulkMaxExc) {
+            cut = a;
+            return false;
+          }
+          sd.exc[nexc].a = (unsigned)(a - v0);
+          sd.exc[nexc].n = (unsigned)(e - a);
+          sd.exc[nexc].s = s;
+          ++nexc;
+        } else if (bk_gathers(kind) && !abort) {
+          const unsigned bytes = (unsigned)((e - a) * 16);
+          mbar_expect_tx_only(&full[slot], bytes);
+          tma_load(A + (a - v0), TB.src[s] + (a - __ldg(TB.vbeg + s)) * 16, bytes, &full[slot]);
+        }
+        return true;
+      });
+      sd.nexc = nexc;
+      return cut;
+    };
+    if (N == 1) {  // no ring: tiles of `stage` bytes round robin over the channels
+      asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous grid on the stream is complete
+      for (int b = 0; b < P.nbuf; ++b) {
+        const BufDesc& D = P.bufs[b];
+        const BulkTabs TB = bulk_tabs(P, b);
+        const unsigned long long nvec = (D.L + VEL - 1) / VEL;
+        for (unsigned long long vlo = (unsigned long long)ch * stage_vecs; vlo < nvec;
+             vlo += (unsigned long long)gridDim.x * stage_vecs) {
+          const unsigned long long vhi = vlo + stage_vecs < nvec ? vlo + stage_vecs : nvec;
+          int cur = bulk_find(TB, vlo);
+          for (unsigned long long v0 = vlo; v0 < vhi;) {
+            const int slot = acquire_slot(seq);
+            StageDesc& sd = desc[slot];
+            const unsigned long long v1 = walk_stage(sd, slot, v0, vhi, kF_SOLO, TB, cur);
+            sd.v0 = v0;
+            sd.pv = 0;
+            sd.n = (int)(v1 - v0);
+            sd.kind = kF_SOLO;
+            sd.pub = -1;
+            sd.b = b;
+            sd.half = 0;
+            sd.op = 0;
+            sd.last = 0;
+            sd.e_hi = D.L;
+            mbar_arrive(&full[slot]);
+            ++seq;
+            v0 = v1;
+          }
+        }
+      }
+      const int slot = acquire_slot(seq);
+      desc[slot].kind = kBulkEnd;
+      mbar_arrive(&full[slot]);
+      return;
+    }
     for (int b = 0; b < P.nbuf; ++b) {
       const BufDesc& D = P.bufs[b];
       const int cg = chan_of(D, ch, gridDim.x);
@@ -2009,32 +2079,11 @@ __global__ void __launch_bounds__(kBulkThreads, 1) bulk_allreduce_kernel(const _
           uint4* A = sA + (size_t)slot * stage_vecs;
           uint4* B = sB + (size_t)slot * stage_vecs;
           unsigned long long v1 = v0 + stage_vecs < vhi ? v0 + stage_vecs : vhi;
-          int nexc = 0;
           const bool dep_gather = kind == kF_RAG;  // own tensors written by the predecessor
           if (dep_gather) wait_dep();
-          if (bk_members(kind)) {
-            // member pieces: bulk-load the gathered ones, list the element-wise ones; the
-            // stage ends early when the list is full
-            unsigned long long cut = v1;
-            bulk_walk(TB, VEL, v0, v1, cur, [&](unsigned long long a, unsigned long long e, int s, bool exc) -> bool {
-              if (exc) {
-                if (nexc == kBulkMaxExc) {
-                  cut = a;
-                  return false;
-                }
-                sd.exc[nexc].a = (unsigned)(a - v0);
-                sd.exc[nexc].n = (unsigned)(e - a);
-                sd.exc[nexc].s = s;
-                ++nexc;
-              } else if (bk_gathers(kind) && !abort) {
-                const unsigned bytes = (unsigned)((e - a) * 16);
-                mbar_expect_tx_only(&full[slot], bytes);
-                tma_load(A + (a - v0), TB.src[s] + (a - __ldg(TB.vbeg + s)) * 16, bytes, &full[slot]);
-              }
-              return true;
-            });
-            v1 = cut;
-          }
+          sd.nexc = 0;
+          if (bk_members(kind)) v1 = walk_stage(sd, slot, v0, v1, kind, TB, cur);
+          const int nexc = sd.nexc;
           if (bk_adds(kind) || bk_from_buf(kind)) {
             wait_dep();
             if (!abort) {
@@ -2051,7 +2100,6 @@ __global__ void __launch_bounds__(kBulkThreads, 1) bulk_allreduce_kernel(const _
           sd.pub = v1 >= vhi ? pub : -1;
           sd.b = b;
           sd.half = half;
-          sd.nexc = nexc;
           sd.op = nop;
           sd.last = v1 >= vhi;
           sd.e_hi = hi;
@@ -2101,7 +2149,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1) bulk_allreduce_kernel(const _
       const int slot = (int)(seq % S);
       // the next stage may wait on the successor's progress, which may wait on a stage
       // published here: never leave issued stages unpublished while waiting for it
-      if (retired < seq && !mbar_test(&comp[slot], (unsigned)((seq / S) & 1))) {
+      if (N > 1 && retired < seq && !mbar_test(&comp[slot], (unsigned)((seq / S) & 1))) {
         bulk_wait(0);
         retire(seq);
       }
@@ -2154,6 +2202,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1) bulk_allreduce_kernel(const _
       r_last[seq % kRing] = sd.last != 0;
       asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
       if (seq > 0) release(seq);  // all but the newest stage have been read
+      if (N == 1) continue;       // nothing to publish: the stores complete with the grid
       bulk_wait(depth);
       if (seq + 1 > (unsigned long long)depth) retire(seq + 1 - depth);
     }
@@ -2427,6 +2476,12 @@ __global__ void __launch_bounds__(kSoloThreads) solo_kernel(const __grid_constan
   constexpr unsigned long long TILE = (unsigned long long)kSoloThreads * U;
   using Cvt = WireCvt<ESZ, TESZ>;
   const unsigned tid = threadIdx.x;
+  // programmatic dependent launch: the next kernel on the stream may be launched as soon
+  // as every CTA of this grid has started; this grid's own memory work waits for the
+  // previous grid's completion (griddepcontrol.wait), so back-to-back calls overlap only
+  // the launch, never the data
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   unsigned long long t = blockIdx.x;  // -> (buffer b, tile t of b)
   int b = 0;
   for (; b < P.nbuf; ++b) {
@@ -2543,8 +2598,16 @@ static cudaError_t launch_solo_t(const FusedParams& p, int nlocal, cudaStream_t 
   for (int b = 0; b < p.nbuf; ++b) tiles += ((p.bufs[b].L + VEL - 1) / VEL + TILE - 1) / TILE;
   if (tiles == 0) return cudaSuccess;
   if (tiles > 0x7fffffffull) return cudaErrorInvalidValue;
-  solo_kernel<Op, TESZ><<<dim3((unsigned)tiles, nlocal), kSoloThreads, 0, s>>>(p);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)tiles, nlocal);
+  cfg.blockDim = dim3(kSoloThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, solo_kernel<Op, TESZ>, p);
 }
 
 cudaError_t launch_solo(const FusedParams& p, int dtype, int nlocal, cudaStream_t s) {
@@ -2766,13 +2829,14 @@ cudaError_t ring_max_ctas_per_sm(int dtype, int threads, int* out) {
 
 
 // ------------------------------------------------------------------ bulk-copy push ring launchers
-size_t bulk_smem_bytes(int stages, int stage_bytes) {
-  return (size_t)stages * (2 * (size_t)stage_bytes + sizeof(StageDesc) + 3 * sizeof(unsigned long long));
+size_t bulk_smem_bytes(int stages, int stage_bytes, bool two) {
+  return (size_t)stages * ((two ? 2 : 1) * (size_t)stage_bytes + sizeof(StageDesc) + 3 * sizeof(unsigned long long));
 }
 
 template <class Op>
 static cudaError_t launch_bulk_t(const FusedParams& p, int nch, int nlocal, cudaStream_t s) {
-  const size_t smem = bulk_smem_bytes(p.bulk_stages, p.bulk_stage_bytes);
+  const bool ring = p.ring.N > 1;
+  const size_t smem = bulk_smem_bytes(p.bulk_stages, p.bulk_stage_bytes, ring);
   cudaError_t e = cudaFuncSetAttribute(bulk_allreduce_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -2781,8 +2845,14 @@ static cudaError_t launch_bulk_t(const FusedParams& p, int nch, int nlocal, cuda
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (they wait on each other)
-  attr[0].val.cooperative = 1;
+  if (ring) {
+    attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (they wait on each other)
+    attr[0].val.cooperative = 1;
+  } else {
+    // N = 1: CTAs wait on nothing but the previous grid (griddepcontrol.wait)
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+  }
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, bulk_allreduce_kernel<Op>, p);
@@ -2798,8 +2868,8 @@ cudaError_t launch_bulk(const FusedParams& p, int dtype, int nch, int nlocal, cu
   }
 }
 
-cudaError_t bulk_max_ctas_per_sm(int dtype, int stages, int stage_bytes, int* out) {
-  const size_t smem = bulk_smem_bytes(stages, stage_bytes);
+cudaError_t bulk_max_ctas_per_sm(int dtype, int stages, int stage_bytes, int* out, bool two) {
+  const size_t smem = bulk_smem_bytes(stages, stage_bytes, two);
   cudaError_t e = cudaSuccess;
   switch (dtype) {
     case 1:

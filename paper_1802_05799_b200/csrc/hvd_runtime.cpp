@@ -112,6 +112,9 @@ struct hvd_comm {
   int bulk_depth = 1;               // HVD_CFG_BULK_DEPTH
   int bulk_channels = 148;          // HVD_CFG_BULK_CHANNELS
   int64_t bulk_slice = 64 << 10;    // HVD_CFG_BULK_SLICE_BYTES
+  int solo_kernel = 0;              // HVD_CFG_SOLO_KERNEL: 1 persistent bulk kernel, 0 tile-per-CTA kernel
+  int solo_stages = 6;              // HVD_CFG_SOLO_STAGES
+  int solo_stage_bytes = 32 << 10;  // HVD_CFG_SOLO_STAGE_BYTES
   unsigned long long pbase[kMaxChannels] = {};  // pull-protocol progress counter bases
   int pull_calls = 0;
   unsigned long long pull_exits = 0;  // cumulative CTA exits of the pull kernel (per rank)
@@ -705,8 +708,20 @@ int enqueue_fused_multi(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStrea
     for (int j = 0; j < k; ++j) signals[D.owner < 0 ? j : (D.owner + j) % nch] += inc;
   }
   F.cache_segs = maxseg <= kFusedSmemSegs ? (maxseg + 1) / 2 * 2 : 0;
-  if (N == 1) {  // no ring: the in-place gather x (1/N) -> scatter stream (solo_kernel)
-    if (c->tl) c->tl_slices = 0;  // the solo kernel records no timeline
+  if (N == 1) {  // no ring: the in-place gather x (1/N) -> scatter stream
+    if (c->tl) c->tl_slices = 0;  // the solo kernels record no timeline
+    if (c->solo_kernel == 1 && F.tdtype == dtype) {
+      // persistent bulk kernel (N = 1 branch of bulk_allreduce_kernel): every SM streams
+      // tiles HBM -> shared -> HBM by bulk copies, launched with programmatic dependent
+      // launch so that back-to-back calls do not pay the launch gap
+      F.bulk_stages = c->solo_stages;
+      F.bulk_stage_bytes = c->solo_stage_bytes;
+      F.bulk_depth = 1;
+      int per_sm = 0;
+      CK(bulk_max_ctas_per_sm(dtype, c->solo_stages, c->solo_stage_bytes, &per_sm, false));
+      const int grid = std::max(1, std::max(1, per_sm) * c->sm_count / c->nlocal);
+      return launch_counted(c, HVD_KERNEL_SOLO, s, [&] { return launch_bulk(F, dtype, grid, c->nlocal, s); });
+    }
     return launch_counted(c, HVD_KERNEL_SOLO, s, [&] { return launch_solo(F, dtype, c->nlocal, s); });
   }
   const int tdt = F.tdtype;
@@ -1781,6 +1796,21 @@ int hvd_set_config(hvd_comm* c, int key, int64_t value) {
       if (value < 0 || value > 2) return HVD_ERR_INVALID;
       c->protocol = (int)value;
       return HVD_OK;
+    case HVD_CFG_SOLO_KERNEL:
+      if (value != 0 && value != 1) return HVD_ERR_INVALID;
+      c->solo_kernel = (int)value;
+      return HVD_OK;
+    case HVD_CFG_SOLO_STAGES:
+      if (value < 2 || value > 8 || bulk_smem_bytes((int)value, c->solo_stage_bytes, false) > kBulkMaxSmem)
+        return HVD_ERR_INVALID;
+      c->solo_stages = (int)value;
+      return HVD_OK;
+    case HVD_CFG_SOLO_STAGE_BYTES:
+      if (value < (4 << 10) || value > (64 << 10) || value % 1024 ||
+          bulk_smem_bytes(c->solo_stages, (int)value, false) > kBulkMaxSmem)
+        return HVD_ERR_INVALID;
+      c->solo_stage_bytes = (int)value;
+      return HVD_OK;
     case HVD_CFG_SIGNAL_WARPS:
       if (value < 1 || value > 4 || c->threads + 32 * value > kMaxRingThreads + 32) return HVD_ERR_INVALID;
       c->sig_warps = (int)value;
@@ -1856,6 +1886,9 @@ int64_t hvd_get_config(const hvd_comm* c, int key) {
     case HVD_CFG_FIN_LAG: return c->fin_lag;
     case HVD_CFG_SIGNAL_WARPS: return c->sig_warps;
     case HVD_CFG_LL128_STATUS: return c->ll128_status;
+    case HVD_CFG_SOLO_KERNEL: return c->solo_kernel;
+    case HVD_CFG_SOLO_STAGES: return c->solo_stages;
+    case HVD_CFG_SOLO_STAGE_BYTES: return c->solo_stage_bytes;
     case HVD_CFG_BULK_STAGES: return c->bulk_stages;
     case HVD_CFG_BULK_STAGE_BYTES: return c->bulk_stage_bytes;
     case HVD_CFG_BULK_DEPTH: return c->bulk_depth;
