@@ -426,7 +426,27 @@ def cpu_baseline(args, counts, dt, n, budget_s=10.0):
     return {"value": alg * _bus_factor(n) if n > 1 else alg, "unit": "GB/s", "cores": 1, "kind": "oracle",
             "sample": f"oracle.allreduce of {len(sample)} tensor(s), {payload / MIB:.0f} MiB {dt} per rank, "
                       f"{n} simulated rank(s), {reps} reps in {reps * t:.1f} s (numpy, single thread)",
-            "c1_seconds_median5": statistics.median(c1), "host_cpus": os.cpu_count()}
+            "c1_seconds_median5": statistics.median(c1), **_host_info()}
+
+
+def _host_info():
+    """Host metadata BASELINE.md §4 asks for next to the oracle timing."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        aff = sorted(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        aff = None
+    return {"host_cpus": os.cpu_count(), "sched_getaffinity": len(aff) if aff is not None else None,
+            "cpu_model": model, "threads_used": 1,
+            "omp_num_threads": os.environ.get("OMP_NUM_THREADS")}
 
 
 def run_reference(args, budget_s=120.0):
@@ -463,7 +483,8 @@ def run_reference(args, budget_s=120.0):
             "config": {"workload": args.workload, "payload_bytes": payload, "simulated_ranks": n},
             "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle",
                              "sample": f"{len(sample)} tensor(s), {payload / MIB:.2f} MiB per rank of the "
-                                       f"workload, {n} simulated rank(s), per step; numpy single thread"},
+                                       f"workload, {n} simulated rank(s), per step; numpy single thread",
+                             **_host_info()},
             "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

@@ -212,6 +212,10 @@ int hvd_ll128_selftest(hvd_comm* c, int force_fail, int* status);
 int hvd_poll_error(hvd_comm* c);
 const char* hvd_strerror(int status);
 
+/* "hvd-src-<sha256 prefix>" of the sources this library was compiled from (the build
+ * step compares it with the tree to decide whether to recompile).  Static string. */
+const char* hvd_build_id(void);
+
 /* Device-side traffic counters of local rank `local` since init: bytes pushed
  * to the successor and chunk messages sent (one per ring iteration; P:L197-198
  * "communicates with two of its peers 2*(N-1) times").  Reads device memory
@@ -315,6 +319,37 @@ typedef struct {
   uint64_t words_per_channel;
 } hvd_timeline_info;
 int hvd_timeline(hvd_comm* c, int local, uint64_t* out, uint64_t cap_words, hvd_timeline_info* info);
+
+/* Job-wide Horovod Timeline ("view exactly what each node was doing at each
+ * time step throughout a training job"; "enable timelines by setting a single environment
+ * variable").  HVD_TIMELINE=<path> in the environment turns it on for every
+ * comm at hvd_init (single process / virtual) or hvd_connect (multi-process); these
+ * calls do the same programmatically.  Output: Chrome trace-event JSON (about:tracing /
+ * chrome://tracing), an array written incrementally, one event per line, without the
+ * closing bracket (Chrome accepts it; a crashed job keeps its trace).  Per rank (pid):
+ *   tid 0 "host calls":     one "X" span per public call (ALLREDUCE, ALLREDUCE_BUFFER,
+ *                           ALLREDUCE_HOST, NEGOTIATE_ALLREDUCE, BROADCAST, ALLGATHER),
+ *                           args {call, tensors, bytes, launches, status};
+ *   tid 1 "device kernels": one "X" span per kernel launch (FUSED_RING, LL_RING,
+ *                           LL128_RING, BULK_RING, PULL_RING, COPY_RING, SOLO, PACK, RING,
+ *                           UNPACK, SCALE) from its first CTA's start to its last CTA's
+ *                           end on that rank's GPU, args {seq, call, ctas, bytes};
+ *   "s"/"f" flow events link each call to its launches.
+ * Device times are %globaltimer converted to CLOCK_REALTIME (offset calibrated at start,
+ * uncertainty in the TIMELINE_START event), so the ranks of a node share one time axis.
+ * Every rank appends to the same file (O_APPEND, whole lines per write).  Records of
+ * finished launches are written at every call and by hvd_timeline_flush without a
+ * device synchronisation; hvd_timeline_stop / hvd_finalize synchronise and write the rest.
+ *
+ * hvd_timeline_start: path = trace file; truncate != 0 starts a new file (one rank of a
+ *   job; the others must start after it).  Errors: INVALID (already on, bad path), CUDA.
+ * hvd_timeline_stop:  synchronises the device, writes every record, closes.  Errors: CUDA.
+ * hvd_timeline_flush: writes the records of finished launches (non-blocking); *launches /
+ *   *dropped (either may be NULL) = launches traced / records lost (never finished, or
+ *   overwritten before being written: more than 4096 launches outstanding).           */
+int hvd_timeline_start(hvd_comm* c, const char* path, int truncate);
+int hvd_timeline_stop(hvd_comm* c);
+int hvd_timeline_flush(hvd_comm* c, uint64_t* launches, uint64_t* dropped);
 
 /* ---- host-only plan inspection (no device needed) -------------------------------------------- */
 

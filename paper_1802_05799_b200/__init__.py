@@ -13,8 +13,10 @@ The paper's user-facing calls:
 plus ``Comm.allgather`` (north_star).  Also: ``Comm.register`` (zero-copy
 gradients), ``Comm.allreduce(..., wire="bf16")`` (wire dtype, R14),
 ``negotiator`` / ``Comm.allreduce_negotiated`` (readiness cycle),
-``Comm.allreduce_host`` (pinned host gradients), ``Comm.timeline`` and
-``timeline.write_chrome_trace`` (Horovod Timeline).
+``Comm.allreduce_host`` (pinned host gradients), the job-wide Horovod Timeline
+(``HVD_TIMELINE=<path>`` or ``Comm.timeline_start``; read back with
+``timeline.load_trace``) and the per-slice ring detail of one launch (``Comm.timeline``,
+``timeline.write_chrome_trace``).
 """
 from __future__ import annotations
 
@@ -295,6 +297,22 @@ class Comm:
         sig = buf[_lib.MAX_CHANNELS * wpc:].reshape(_lib.MAX_CHANNELS, wpc // 2, 2)[:info.channels, :info.signals]
         return {"rank": info.rank, "size": info.size, "K": info.K, "T": info.T, "channels": info.channels,
                 "kind": {1: "pull", 2: "registered"}.get(info.kind, "push"), "fin_lag": self.get_config(_lib.HVD_CFG_FIN_LAG), "data": data.copy(), "signals": sig.copy()}
+
+    def timeline_start(self, path: str, truncate: bool = True):
+        """Job-wide Horovod Timeline into ``path`` (``hvd_timeline_start``; the environment
+        variable ``HVD_TIMELINE=<path>`` does the same at init).  In a multi-process job
+        exactly one rank truncates, and the others start after it."""
+        check(lib.hvd_timeline_start(self._h, os.fsencode(path), int(bool(truncate))), "hvd_timeline_start")
+
+    def timeline_stop(self):
+        """Synchronise, write every remaining record and close the job timeline."""
+        check(lib.hvd_timeline_stop(self._h), "hvd_timeline_stop")
+
+    def timeline_flush(self):
+        """Write the records of finished launches; returns (launches traced, records dropped)."""
+        la, dr = C.c_uint64(0), C.c_uint64(0)
+        check(lib.hvd_timeline_flush(self._h, C.byref(la), C.byref(dr)), "hvd_timeline_flush")
+        return la.value, dr.value
 
     def poll_error(self) -> int:
         return lib.hvd_poll_error(self._h)

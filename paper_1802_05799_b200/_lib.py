@@ -113,6 +113,10 @@ def _load():
         "hvd_allgather": (C.c_int, [P, C.POINTER(hvd_tensor), C.POINTER(hvd_tensor), P]),
         "hvd_poll_error": (C.c_int, [P]),
         "hvd_strerror": (C.c_char_p, [C.c_int]),
+        "hvd_build_id": (C.c_char_p, []),
+        "hvd_timeline_start": (C.c_int, [P, C.c_char_p, C.c_int]),
+        "hvd_timeline_stop": (C.c_int, [P]),
+        "hvd_timeline_flush": (C.c_int, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
         "hvd_traffic": (C.c_int, [P, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
         "hvd_set_config": (C.c_int, [P, C.c_int, C.c_int64]),
         "hvd_get_config": (C.c_int64, [P, C.c_int]),
@@ -153,7 +157,8 @@ EXPORTS = sorted([
     "hvd_kernel_stats", "hvd_timeline", "hvd_allreduce_ex", "hvd_register_blob", "hvd_register",
     "hvd_allreduce_registered", "hvd_deregister", "hvd_negotiator_create", "hvd_negotiator_ready",
     "hvd_negotiator_cycle", "hvd_negotiator_pending", "hvd_negotiator_destroy", "hvd_allreduce_negotiated",
-    "hvd_allreduce_host", "hvd_negotiator_trace", "hvd_ll128_selftest",
+    "hvd_allreduce_host", "hvd_negotiator_trace", "hvd_ll128_selftest", "hvd_build_id",
+    "hvd_timeline_start", "hvd_timeline_stop", "hvd_timeline_flush",
 ])
 
 

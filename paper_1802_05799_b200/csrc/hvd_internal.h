@@ -26,6 +26,21 @@ inline int elem_size(int dtype) {
   }
 }
 
+// ---------------------------------------------------------------- job timeline
+// Horovod Timeline ("what each node was doing at each time step throughout
+// a training job"): every kernel launch of a comm with the job timeline on records, per
+// local rank, its first CTA's start and its last CTA's end (%globaltimer, ns).  CTAs
+// fold into a device record of the launch; the last CTA of a local rank copies the
+// result into a host-mapped slot (kJtWords words, seq written last) and re-arms the
+// device record, so the host drains finished launches without synchronising.
+constexpr int kJtSlots = 4096;   // launches in flight before a slot is reused
+constexpr int kJtWords = 4;      // device: {begin (min), end (max), CTAs done, 0}; host: {seq, begin, end, ctas}
+struct JtRef {
+  unsigned long long* rec;       // device record of this launch: [kMaxLocal][kJtWords] (nullptr = off)
+  unsigned long long* host;      // host-mapped slot of this launch: [kMaxLocal][kJtWords]
+  unsigned long long seq;        // launch sequence number (1-based)
+};
+
 // ---------------------------------------------------------------- ring kernel
 // One ring rank as seen by the kernel: its own buffers and its successor's.
 struct RingRank {
@@ -86,6 +101,7 @@ struct RingParams {
   int parity;                   // pull protocol: pull buffer of this call
   int call;                     // pull protocol: 1-based call index
   unsigned long long exits_target;  // pull protocol: cumulative CTA exits after this call
+  JtRef jt;                     // job timeline record of this launch
 };
 
 // Timeline buffer of one local rank (Horovod Timeline): for every
@@ -121,6 +137,7 @@ struct PackParams {
   int scale_on;                 // 1: multiply by `scale` (AVERAGE)
   float scale;                  // fl32(1/N)
   int pad;
+  JtRef jt;                     // job timeline record of this launch
 };
 
 // One fusion buffer of a multi-buffer fused launch (geometry + member tables).
@@ -211,7 +228,9 @@ cudaError_t launch_pack(const PackParams& p, int dtype, int nlocal, int grid, in
 cudaError_t launch_unpack(const PackParams& p, int dtype, int nlocal, int grid, int threads,
                           cudaStream_t s);
 cudaError_t launch_scale(char* const* bufs, int nlocal, unsigned long long count, int dtype,
-                         float scale, int grid, int threads, cudaStream_t s);
+                         float scale, int grid, int threads, const JtRef& jt, cudaStream_t s);
+unsigned long long kernels_launched();  // launches issued by the launchers above (monotone)
+cudaError_t launch_jt_clock(unsigned long long* host_out, cudaStream_t s);  // %globaltimer -> host word
 cudaError_t launch_ring(const RingParams& p, int dtype, int nch, int nlocal, int threads,
                         cudaStream_t s);
 cudaError_t ring_max_ctas_per_sm(int dtype, int threads, int* out);

@@ -1,0 +1,249 @@
+// Job-wide Horovod Timeline: see hvd_jobtrace.h.
+//
+// Output is the Chrome trace-event JSON array format, written incrementally: "[" then
+// one event object per line, each followed by ",".  Chrome's about:tracing reads the
+// array without its closing bracket (so a job that dies still leaves a readable
+// trace); paper_1802_05799_b200/timeline.py load_trace() parses it strictly.  Every rank
+// of a job appends to the same file (O_APPEND, one write() per batch of whole lines);
+// timestamps are CLOCK_REALTIME microseconds, so the ranks of a node share one axis.
+#include "hvd_jobtrace.h"
+
+#include <algorithm>
+#include <cerrno>
+#include <cstdio>
+#include <cstring>
+#include <ctime>
+
+#include <fcntl.h>
+#include <unistd.h>
+
+#include "../../include/hvd.h"
+
+namespace hvd {
+
+int64_t realtime_ns() {
+  timespec ts;
+  clock_gettime(CLOCK_REALTIME, &ts);
+  return (int64_t)ts.tv_sec * 1000000000ll + ts.tv_nsec;
+}
+
+namespace {
+const char* kKindName[HVD_KERNEL_KINDS] = {
+    "PACK",        // pack_kernel: Tensor Fusion step 3, three-launch path
+    "RING",        // ring_allreduce_kernel: the 2(N-1) iterations
+    "UNPACK",      // unpack: step 5
+    "SCALE",       // scale_kernel: 1/N of a raw buffer
+    "FUSED_RING",  // fused_allreduce_kernel: pack + ring + unpack in one launch
+    "COPY_RING",   // copy_collective_kernel: broadcast / allgather
+    "PULL_RING",   // pull_allreduce_kernel
+    "LL_RING",     // ll_allreduce_kernel (small buffers)
+    "SOLO",        // solo_kernel / persistent bulk variant: N = 1 gather x 1/N -> scatter
+    "LL128_RING",  // ll128_allreduce_kernel (mid-size buffers)
+    "BULK_RING",   // bulk_allreduce_kernel (TMA bulk-copy push)
+};
+}  // namespace
+
+int JobTrace::create(const char* path, bool truncate, int device, int nlocal, const int* ranks, int size,
+                     JobTrace** out) {
+  if (!path || !path[0] || !out || nlocal < 1 || nlocal > kMaxLocal) return HVD_ERR_INVALID;
+  *out = nullptr;
+  const int fd = ::open(path, O_WRONLY | O_CREAT | O_APPEND | (truncate ? O_TRUNC : 0), 0644);
+  if (fd < 0) {
+    std::fprintf(stderr, "[hvd] timeline: cannot open %s: %s\n", path, std::strerror(errno));
+    return HVD_ERR_INVALID;
+  }
+  JobTrace* t = new JobTrace();
+  t->fd_ = fd;
+  t->device_ = device;
+  t->nlocal_ = nlocal;
+  t->size_ = size;
+  for (int l = 0; l < nlocal; ++l) t->ranks_[l] = ranks[l];
+  const size_t bytes = (size_t)kJtSlots * kMaxLocal * kJtWords * sizeof(unsigned long long);
+  bool ok = cudaSetDevice(device) == cudaSuccess && cudaMalloc(&t->dev_, bytes) == cudaSuccess &&
+            cudaHostAlloc(&t->host_, bytes, cudaHostAllocMapped) == cudaSuccess &&
+            cudaHostGetDevicePointer(&t->hostd_, t->host_, 0) == cudaSuccess &&
+            cudaHostAlloc(&t->clk_, 64, cudaHostAllocMapped) == cudaSuccess &&
+            cudaHostGetDevicePointer(&t->clkd_, t->clk_, 0) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&t->stream_, cudaStreamNonBlocking) == cudaSuccess;
+  if (ok) {
+    // device records armed: begin = +inf (atomicMin), end = 0 (atomicMax), CTAs done = 0
+    std::vector<unsigned long long> init((size_t)kJtSlots * kMaxLocal * kJtWords, 0);
+    for (size_t i = 0; i < init.size(); i += kJtWords) init[i] = ~0ull;
+    ok = cudaMemcpy(t->dev_, init.data(), bytes, cudaMemcpyHostToDevice) == cudaSuccess;
+    std::memset(t->host_, 0, bytes);
+  }
+  if (ok) ok = t->calibrate() == HVD_OK;
+  if (!ok) {
+    std::fprintf(stderr, "[hvd] timeline: device setup failed\n");
+    delete t;
+    return HVD_ERR_CUDA;
+  }
+  char line[512];
+  if (truncate) t->append("[\n", 2);
+  for (int l = 0; l < nlocal; ++l) {
+    const int r = t->ranks_[l];
+    int n = std::snprintf(line, sizeof line,
+                          "{\"name\": \"process_name\", \"ph\": \"M\", \"pid\": %d, \"args\": {\"name\": \"rank %d "
+                          "(GPU %d)\"}},\n",
+                          r, r, device);
+    t->append(line, n);
+    n = std::snprintf(line, sizeof line,
+                      "{\"name\": \"process_sort_index\", \"ph\": \"M\", \"pid\": %d, \"args\": {\"sort_index\": %d}},\n",
+                      r, r);
+    t->append(line, n);
+    n = std::snprintf(line, sizeof line,
+                      "{\"name\": \"thread_name\", \"ph\": \"M\", \"pid\": %d, \"tid\": 0, \"args\": {\"name\": "
+                      "\"host calls\"}},\n{\"name\": \"thread_name\", \"ph\": \"M\", \"pid\": %d, \"tid\": 1, "
+                      "\"args\": {\"name\": \"device kernels\"}},\n",
+                      r, r);
+    t->append(line, n);
+    n = std::snprintf(line, sizeof line,
+                      "{\"name\": \"TIMELINE_START\", \"cat\": \"META\", \"ph\": \"i\", \"s\": \"p\", \"pid\": %d, "
+                      "\"tid\": 0, \"ts\": %.3f, \"args\": {\"size\": %d, \"local_ranks\": %d, \"device\": %d, "
+                      "\"clock_uncertainty_us\": %.3f}},\n",
+                      r, realtime_ns() * 1e-3, size, nlocal, device, t->clk_err_ns_ * 1e-3);
+    t->append(line, n);
+  }
+  t->flush();
+  *out = t;
+  return HVD_OK;
+}
+
+JobTrace::~JobTrace() {
+  if (fd_ >= 0) {
+    flush();
+    ::close(fd_);
+  }
+  if (stream_) cudaStreamDestroy(stream_);
+  if (dev_) cudaFree(dev_);
+  if (host_) cudaFreeHost(host_);
+  if (clk_) cudaFreeHost(clk_);
+}
+
+// %globaltimer vs CLOCK_REALTIME: a one-thread kernel writes the device clock into a
+// host-mapped word; the host brackets it with its own clock.  The bracket with the
+// smallest width of 8 gives the offset, uncertain by half that width.
+int JobTrace::calibrate() {
+  int64_t best_w = INT64_MAX;
+  for (int i = 0; i < 8; ++i) {
+    volatile unsigned long long* w = clk_;
+    *w = 0;
+    const int64_t t0 = realtime_ns();
+    if (launch_jt_clock(clkd_, stream_) != cudaSuccess) return HVD_ERR_CUDA;
+    const int64_t deadline = t0 + 2000000000ll;
+    unsigned long long g = 0;
+    while ((g = *w) == 0)
+      if (realtime_ns() > deadline) return HVD_ERR_TIMEOUT;
+    const int64_t t1 = realtime_ns();
+    if (t1 - t0 < best_w) {
+      best_w = t1 - t0;
+      offset_ns_ = (int64_t)g - (t0 + (t1 - t0) / 2);
+    }
+  }
+  if (cudaStreamSynchronize(stream_) != cudaSuccess) return HVD_ERR_CUDA;
+  clk_err_ns_ = best_w / 2;
+  return HVD_OK;
+}
+
+double JobTrace::dev_us(uint64_t g) const { return ((int64_t)g - offset_ns_) * 1e-3; }
+
+void JobTrace::append(const char* line, int len) {
+  if (len > 0) out_.append(line, (size_t)len);
+  if (out_.size() > (1u << 20)) flush();
+}
+
+void JobTrace::flush() {
+  size_t off = 0;
+  while (off < out_.size()) {
+    const ssize_t w = ::write(fd_, out_.data() + off, out_.size() - off);
+    if (w <= 0) {
+      if (w < 0 && errno == EINTR) continue;
+      break;
+    }
+    off += (size_t)w;
+  }
+  out_.clear();
+}
+
+JtRef JobTrace::reserve() {
+  const uint64_t seq = seq_ + 1;
+  // the slot's previous launch must be written out before its host record is reused
+  if (!pending_.empty() && pending_.front().seq + kJtSlots <= seq) drain(false);
+  while (!pending_.empty() && pending_.front().seq + kJtSlots <= seq) {
+    pending_.pop_front();
+    ++dropped_;
+  }
+  const size_t slot = (size_t)(seq % kJtSlots) * kMaxLocal * kJtWords;
+  return JtRef{dev_ + slot, hostd_ + slot, seq};
+}
+
+void JobTrace::launched(int kind, uint64_t bytes) {
+  ++seq_;
+  ++call_launches_;
+  pending_.push_back(Meta{seq_, call_id_, bytes, kind, realtime_ns()});
+}
+
+void JobTrace::call_begin(const char* name, uint64_t tensors, uint64_t bytes) {
+  if (depth_++ > 0) return;
+  drain(false);
+  ++call_id_;
+  call_t0_ = realtime_ns();
+  call_launches_ = 0;
+  call_name_ = name;
+  call_tensors_ = tensors;
+  call_bytes_ = bytes;
+}
+
+void JobTrace::call_end(int status) {
+  if (depth_ == 0 || --depth_ > 0) return;
+  const int64_t t1 = realtime_ns();
+  char line[512];
+  for (int l = 0; l < nlocal_; ++l) {
+    const int n = std::snprintf(
+        line, sizeof line,
+        "{\"name\": \"%s\", \"cat\": \"CALL\", \"ph\": \"X\", \"pid\": %d, \"tid\": 0, \"ts\": %.3f, \"dur\": %.3f, "
+        "\"args\": {\"call\": %llu, \"tensors\": %llu, \"bytes\": %llu, \"launches\": %llu, \"status\": %d}},\n",
+        call_name_.c_str(), ranks_[l], call_t0_ * 1e-3, std::max<int64_t>(t1 - call_t0_, 1) * 1e-3,
+        (unsigned long long)call_id_, (unsigned long long)call_tensors_, (unsigned long long)call_bytes_,
+        (unsigned long long)call_launches_, status);
+    append(line, n);
+  }
+  drain(false);
+  flush();
+}
+
+void JobTrace::drain(bool all) {
+  char line[768];
+  while (!pending_.empty()) {
+    const Meta m = pending_.front();
+    volatile unsigned long long* h = host_ + (size_t)(m.seq % kJtSlots) * kMaxLocal * kJtWords;
+    bool done = true;
+    for (int l = 0; l < nlocal_ && done; ++l) done = h[(size_t)l * kJtWords] == m.seq;
+    if (!done) {
+      if (!all) break;
+      pending_.pop_front();
+      ++dropped_;
+      continue;
+    }
+    for (int l = 0; l < nlocal_; ++l) {
+      const volatile unsigned long long* r = h + (size_t)l * kJtWords;
+      const unsigned long long b = r[1], e = r[2], ctas = r[3];
+      const unsigned long long fid = m.seq * kMaxLocal + l;
+      const int n = std::snprintf(
+          line, sizeof line,
+          "{\"name\": \"launch\", \"cat\": \"FLOW\", \"ph\": \"s\", \"id\": %llu, \"pid\": %d, \"tid\": 0, "
+          "\"ts\": %.3f},\n"
+          "{\"name\": \"%s\", \"cat\": \"KERNEL\", \"ph\": \"X\", \"pid\": %d, \"tid\": 1, \"ts\": %.3f, "
+          "\"dur\": %.3f, \"args\": {\"seq\": %llu, \"call\": %llu, \"ctas\": %llu, \"bytes\": %llu}},\n"
+          "{\"name\": \"launch\", \"cat\": \"FLOW\", \"ph\": \"f\", \"bp\": \"e\", \"id\": %llu, \"pid\": %d, "
+          "\"tid\": 1, \"ts\": %.3f},\n",
+          fid, ranks_[l], m.t_launch * 1e-3, kKindName[m.kind], ranks_[l], dev_us(b),
+          std::max<double>((double)(e - b), 1.0) * 1e-3, (unsigned long long)m.seq, (unsigned long long)m.call,
+          ctas, (unsigned long long)m.bytes, fid, ranks_[l], dev_us(b));
+      append(line, n);
+    }
+    pending_.pop_front();
+  }
+}
+
+}  // namespace hvd

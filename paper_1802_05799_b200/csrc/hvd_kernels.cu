@@ -62,6 +62,52 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+// ------------------------------------------------------------------ job timeline
+// One per kernel, constructed first thing (every thread of the CTA is present, so the
+// construction barrier is safe).  Its destructor runs at each thread's return, whichever
+// warp-specialised path it took: the last thread of the CTA folds the CTA's end into
+// the launch record of its local rank (blockIdx.y), and the last CTA of that rank
+// publishes the record to the host-mapped slot and re-arms it (JtRef, hvd_internal.h).
+struct JtGuard {
+  const JtRef& jt;
+  unsigned* left;
+  __device__ __forceinline__ explicit JtGuard(const JtRef& j) : jt(j), left(nullptr) {
+    if (jt.rec == nullptr) return;
+    __shared__ unsigned s_jt_left;
+    left = &s_jt_left;
+    if (threadIdx.x == 0) {
+      s_jt_left = blockDim.x;
+      atomicMin(jt.rec + blockIdx.y * kJtWords, globaltimer());
+    }
+    __syncthreads();
+  }
+  __device__ __forceinline__ ~JtGuard() {
+    if (jt.rec == nullptr) return;
+    if (atomicSub(left, 1u) != 1u) return;
+    unsigned long long* r = jt.rec + blockIdx.y * kJtWords;
+    atomicMax(r + 1, globaltimer());
+    __threadfence();
+    if (atomicAdd(r + 2, 1ull) != gridDim.x - 1) return;
+    __threadfence();
+    const unsigned long long b = atomicAdd(r + 0, 0ull), e = atomicAdd(r + 1, 0ull);
+    volatile unsigned long long* h = jt.host + blockIdx.y * kJtWords;
+    h[1] = b;
+    h[2] = e;
+    h[3] = gridDim.x;
+    __threadfence_system();
+    h[0] = jt.seq;
+    r[0] = ~0ull;  // re-arm for the launch that reuses this slot (kJtSlots launches later)
+    r[1] = 0;
+    r[2] = 0;
+  }
+};
+
+__global__ void jt_clock_kernel(unsigned long long* out) {
+  volatile unsigned long long* o = out;
+  *o = globaltimer();
+  __threadfence_system();
+}
+
 // ------------------------------------------------------------------ element ops
 // Each op works on 32-bit words of a vector (the wire layout) and on single
 // elements (ragged tails).  R4: bf16 adds go through fp32 and round RNE.
@@ -302,6 +348,7 @@ __device__ __forceinline__ void signal_loop_multi(const int* done, int* claimed,
 
 template <class Op>
 __global__ void __launch_bounds__(416, 1) ring_allreduce_kernel(const __grid_constant__ RingParams P) {
+  JtGuard jtg(P.jt);
   const RingRank& me = P.rk[blockIdx.y];
   const int ch = blockIdx.x;
   const int N = P.N;
@@ -439,6 +486,7 @@ __device__ __forceinline__ void scale_elem(const char* src, char* dst, float s, 
 // their loads before any store, so kPackBatch x 16 B per thread are in flight.
 template <int ESZ, bool PACK>
 __global__ void __launch_bounds__(256) pack_kernel(const __grid_constant__ PackParams P, int dtype) {
+  JtGuard jtg(P.jt);
   constexpr int VEL = kPackVecBytes / ESZ;
   char* const buf = P.buf[blockIdx.y];
   char* const* src_tab = P.src + (size_t)blockIdx.y * P.nseg;
@@ -904,6 +952,7 @@ __device__ __forceinline__ int chan_of(const BufDesc& D, int ch, int nch) {
 // push lands in a receive region the successor's previous launch still reads.
 template <class Op, int TESZ>
 __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_constant__ FusedParams P) {
+  JtGuard jtg(P.ring.jt);
   extern __shared__ __align__(16) unsigned long long s_dyn[];
   constexpr int VEL = 16 / Op::kEsz;
   const RingParams& R = P.ring;
@@ -1085,6 +1134,7 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
 // successor's before its first remote store.
 template <class Op>
 __global__ void __launch_bounds__(416, 1) copy_collective_kernel(const __grid_constant__ FusedParams P) {
+  JtGuard jtg(P.ring.jt);
   extern __shared__ __align__(16) unsigned long long s_dyn[];
   const RingParams& R = P.ring;
   const RingRank& me = R.rk[blockIdx.y];
@@ -1225,6 +1275,7 @@ __device__ __forceinline__ int pull_chunk(int t, int r, int N) {
 
 template <class Op>
 __global__ void __launch_bounds__(416, 1) pull_allreduce_kernel(const __grid_constant__ FusedParams P) {
+  JtGuard jtg(P.ring.jt);
   extern __shared__ __align__(128) unsigned long long s_dyn[];
   __shared__ __align__(8) unsigned long long full_bar[kStages], empty_bar[kStages];
   __shared__ int s_abort;
@@ -1481,6 +1532,7 @@ __device__ __forceinline__ bool ll_load(const unsigned long long* p, unsigned fl
 
 template <class Op>
 __global__ void __launch_bounds__(256) ll_allreduce_kernel(const __grid_constant__ FusedParams P) {
+  JtGuard jtg(P.ring.jt);
   constexpr int ESZ = Op::kEsz;
   constexpr int VEL = 16 / ESZ;
   const RingParams& R = P.ring;
@@ -1568,6 +1620,7 @@ __global__ void __launch_bounds__(256) ll_allreduce_kernel(const __grid_constant
 // bit-identical.  Slot of step t: lines of 7 vectors of the chunk, in a fixed LL half.
 template <class Op>
 __global__ void __launch_bounds__(256) ll128_allreduce_kernel(const __grid_constant__ FusedParams P) {
+  JtGuard jtg(P.ring.jt);
   constexpr int ESZ = Op::kEsz;
   constexpr int VEL = 16 / ESZ;
   constexpr unsigned FULL = 0xffffffffu;
@@ -1879,6 +1932,7 @@ __device__ __forceinline__ void mbar_wait_wd(unsigned long long* bar, unsigned p
 
 template <class Op>
 __global__ void __launch_bounds__(kBulkThreads, 1) bulk_allreduce_kernel(const __grid_constant__ FusedParams P) {
+  JtGuard jtg(P.ring.jt);
   extern __shared__ __align__(1024) unsigned char s_bulk[];
   constexpr int ESZ = Op::kEsz;
   constexpr int VEL = 16 / ESZ;
@@ -2370,7 +2424,8 @@ struct BufList { char* b[kMaxLocal]; };
 
 template <int ESZ>
 __global__ void __launch_bounds__(512) scale_kernel(const BufList bufs, unsigned long long count, float s,
-                                                    int dtype) {
+                                                    int dtype, const JtRef jt) {
+  JtGuard jtg(jt);
   char* buf = bufs.b[blockIdx.y];
   constexpr int VEL = 16 / ESZ;
   const unsigned long long nvec = count / VEL;
@@ -2387,18 +2442,28 @@ __global__ void __launch_bounds__(512) scale_kernel(const BufList bufs, unsigned
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
+// Kernels actually launched (a launcher with no work returns without one): the host
+// counts launches and opens timeline records only for launches that happened.
+static unsigned long long g_launched = 0;
+unsigned long long kernels_launched() { return g_launched; }
 template <bool PACK>
 static cudaError_t launch_pack_impl(const PackParams& p, int dtype, int nlocal, int grid, int threads,
                                     cudaStream_t s) {
   if (p.ntiles == 0) return cudaSuccess;
   unsigned long long g = p.ntiles < (unsigned long long)grid ? p.ntiles : (unsigned long long)grid;
   dim3 gd((unsigned)g, nlocal);
+  ++g_launched;
   switch (elem_size(dtype)) {
     case 4: pack_kernel<4, PACK><<<gd, threads, 0, s>>>(p, dtype); break;
     case 2: pack_kernel<2, PACK><<<gd, threads, 0, s>>>(p, dtype); break;
     case 8: pack_kernel<8, PACK><<<gd, threads, 0, s>>>(p, dtype); break;
     default: return cudaErrorInvalidValue;
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_jt_clock(unsigned long long* host_out, cudaStream_t s) {
+  jt_clock_kernel<<<1, 1, 0, s>>>(host_out);
   return cudaGetLastError();
 }
 
@@ -2411,14 +2476,15 @@ cudaError_t launch_unpack(const PackParams& p, int dtype, int nlocal, int grid, 
 }
 
 cudaError_t launch_scale(char* const* bufs, int nlocal, unsigned long long count, int dtype, float scale,
-                         int grid, int threads, cudaStream_t s) {
+                         int grid, int threads, const JtRef& jt, cudaStream_t s) {
   if (count == 0) return cudaSuccess;
   BufList b = {};
   for (int i = 0; i < nlocal && i < kMaxLocal; ++i) b.b[i] = bufs[i];
   dim3 gd(grid, nlocal);
+  ++g_launched;
   switch (elem_size(dtype)) {
-    case 4: scale_kernel<4><<<gd, threads, 0, s>>>(b, count, scale, dtype); break;
-    case 2: scale_kernel<2><<<gd, threads, 0, s>>>(b, count, scale, dtype); break;
+    case 4: scale_kernel<4><<<gd, threads, 0, s>>>(b, count, scale, dtype, jt); break;
+    case 2: scale_kernel<2><<<gd, threads, 0, s>>>(b, count, scale, dtype, jt); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -2436,6 +2502,7 @@ static cudaError_t launch_ring_t(const RingParams& p, int nch, int nlocal, int t
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  ++g_launched;
   return cudaLaunchKernelEx(&cfg, ring_allreduce_kernel<Op>, p);
 }
 
@@ -2470,6 +2537,7 @@ constexpr int kSoloU = HVD_SOLO_U;  // 16 B wire vectors per thread (same-dtype 
 
 template <class Op, int TESZ>
 __global__ void __launch_bounds__(kSoloThreads) solo_kernel(const __grid_constant__ FusedParams P) {
+  JtGuard jtg(P.ring.jt);
   constexpr int ESZ = Op::kEsz;
   constexpr int VEL = 16 / ESZ;
   constexpr int U = TESZ > ESZ ? (kSoloU + 1) / 2 : kSoloU;  // fp32 tensor, bf16 wire: 32 B of tensor each
@@ -2607,6 +2675,7 @@ static cudaError_t launch_solo_t(const FusedParams& p, int nlocal, cudaStream_t 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  ++g_launched;
   return cudaLaunchKernelEx(&cfg, solo_kernel<Op, TESZ>, p);
 }
 
@@ -2646,6 +2715,7 @@ static cudaError_t launch_fused_t(const FusedParams& p, int nch, int nlocal, int
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  ++g_launched;
   return cudaLaunchKernelEx(&cfg, fused_allreduce_kernel<Op, TESZ>, p);
 }
 
@@ -2686,6 +2756,7 @@ static cudaError_t launch_copy_t(const FusedParams& p, int nch, int nlocal, int 
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  ++g_launched;
   return cudaLaunchKernelEx(&cfg, copy_collective_kernel<Op>, p);
 }
 
@@ -2719,6 +2790,7 @@ static cudaError_t launch_pull_t(const FusedParams& p, int nch, int nlocal, int 
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  ++g_launched;
   return cudaLaunchKernelEx(&cfg, pull_allreduce_kernel<Op>, p);
 }
 
@@ -2754,6 +2826,7 @@ static cudaError_t launch_ll_t(const FusedParams& p, int nch, int nlocal, cudaSt
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  ++g_launched;
   return cudaLaunchKernelEx(&cfg, ll_allreduce_kernel<Op>, p);
 }
 
@@ -2768,6 +2841,7 @@ static cudaError_t launch_ll128_t(const FusedParams& p, int nch, int nlocal, cud
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  ++g_launched;
   return cudaLaunchKernelEx(&cfg, ll128_allreduce_kernel<Op>, p);
 }
 
@@ -2855,6 +2929,7 @@ static cudaError_t launch_bulk_t(const FusedParams& p, int nch, int nlocal, cuda
   }
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  ++g_launched;
   return cudaLaunchKernelEx(&cfg, bulk_allreduce_kernel<Op>, p);
 }
 

@@ -21,6 +21,7 @@
 #include "hvd_internal.h"
 #include "hvd_plan.h"
 #include "hvd_negotiate.h"
+#include "hvd_jobtrace.h"
 
 using namespace hvd;
 
@@ -126,6 +127,7 @@ struct hvd_comm {
   int tl_max = 0;
   unsigned long long* tl = nullptr;
   int tl_nch = 0, tl_K = 0, tl_T = 0, tl_slices = 0, tl_kind = 0;
+  JobTrace* jt = nullptr;  // job-wide timeline (HVD_TIMELINE / hvd_timeline_start)
   std::list<CachedPlan> cache;
   // launch statistics (hvd_kernel_stats)
   uint64_t launches[HVD_KERNEL_KINDS] = {};
@@ -447,9 +449,24 @@ cudaEvent_t pool_event(hvd_comm* c) {
 
 // Wraps one kernel launch: counts it and, when profiling, brackets it with events.
 constexpr size_t kMaxTimed = 1 << 16;
+// Payload bytes a launch reduces or copies (job timeline): its fusion buffers in the
+// wire dtype, or the ring's one buffer.
+uint64_t fused_bytes(const FusedParams& F) {
+  const uint64_t esz = (uint64_t)elem_size(F.dtype);
+  if (F.nbuf <= 0) return F.ring.L * esz;
+  uint64_t b = 0;
+  for (int i = 0; i < F.nbuf && i < kMaxMultiBufs; ++i) b += F.bufs[i].L * esz;
+  return b;
+}
+
+// Issue one kernel launch: launch statistics, optional per-launch events
+// (HVD_CFG_PROFILE) and the job timeline record (jt: the launch's JtRef field, filled
+// in before `launch` reads the parameters).  A launcher with no work issues no kernel
+// and is neither counted nor traced.
 template <class F>
-int launch_counted(hvd_comm* c, int kind, cudaStream_t s, F&& launch) {
+int launch_counted(hvd_comm* c, int kind, cudaStream_t s, JtRef* jt, uint64_t bytes, F&& launch) {
   hvd_comm::Timed t = {kind, nullptr, nullptr};
+  *jt = c->jt ? c->jt->reserve() : JtRef{nullptr, nullptr, 0};
   // per-launch events until hvd_kernel_stats collects them (bounded: a caller that
   // never collects stops being profiled instead of growing without limit)
   const bool prof = c->profile && c->timed.size() < kMaxTimed;
@@ -458,8 +475,17 @@ int launch_counted(hvd_comm* c, int kind, cudaStream_t s, F&& launch) {
     t.b = pool_event(c);
     CK(cudaEventRecord(t.a, s));
   }
+  const unsigned long long before = kernels_launched();
   CK(launch());
+  if (kernels_launched() == before) {
+    if (prof) {
+      c->event_pool.push_back(t.a);
+      c->event_pool.push_back(t.b);
+    }
+    return HVD_OK;
+  }
   c->launches[kind] += 1;
+  if (c->jt) c->jt->launched(kind, bytes);
   if (prof) {
     CK(cudaEventRecord(t.b, s));
     c->timed.push_back(t);
@@ -549,7 +575,7 @@ int enqueue_ring(hvd_comm* c, uint64_t L, int dtype, cudaStream_t s) {
     for (uint64_t v : {(uint64_t)1, L, (uint64_t)dtype, (uint64_t)nch, (uint64_t)P.K, (uint64_t)c->size}) ch.add(v);
     P.hash = ch.h;
   }
-  st = launch_counted(c, HVD_KERNEL_RING, s, [&] { return launch_ring(P, dtype, nch, c->nlocal, c->threads, s); });
+  st = launch_counted(c, HVD_KERNEL_RING, s, &P.jt, L * elem_size(dtype), [&] { return launch_ring(P, dtype, nch, c->nlocal, c->threads, s); });
   if (st != HVD_OK) return st;
   advance_base(c, P, nch);
   return HVD_OK;
@@ -575,7 +601,7 @@ int enqueue_pull(hvd_comm* c, DevPlanBuffer& b, cudaStream_t s) {
   F.scale = b.pp.scale;
   F.dtype = b.dtype;
   const int threads = std::max(256, c->threads);
-  st = launch_counted(c, HVD_KERNEL_PULL, s, [&] { return launch_pull(F, b.dtype, nch, c->nlocal, threads, s); });
+  st = launch_counted(c, HVD_KERNEL_PULL, s, &F.ring.jt, fused_bytes(F), [&] { return launch_pull(F, b.dtype, nch, c->nlocal, threads, s); });
   if (st != HVD_OK) return st;
   if (c->tl) {
     c->tl_nch = nch;
@@ -720,9 +746,9 @@ int enqueue_fused_multi(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStrea
       int per_sm = 0;
       CK(bulk_max_ctas_per_sm(dtype, c->solo_stages, c->solo_stage_bytes, &per_sm, false));
       const int grid = std::max(1, std::max(1, per_sm) * c->sm_count / c->nlocal);
-      return launch_counted(c, HVD_KERNEL_SOLO, s, [&] { return launch_bulk(F, dtype, grid, c->nlocal, s); });
+      return launch_counted(c, HVD_KERNEL_SOLO, s, &F.ring.jt, fused_bytes(F), [&] { return launch_bulk(F, dtype, grid, c->nlocal, s); });
     }
-    return launch_counted(c, HVD_KERNEL_SOLO, s, [&] { return launch_solo(F, dtype, c->nlocal, s); });
+    return launch_counted(c, HVD_KERNEL_SOLO, s, &F.ring.jt, fused_bytes(F), [&] { return launch_solo(F, dtype, c->nlocal, s); });
   }
   const int tdt = F.tdtype;
   F.ring.epoch = ++c->hs_epoch;
@@ -737,9 +763,9 @@ int enqueue_fused_multi(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStrea
     F.ring.hash = h.h;
   }
   if (bulk)
-    st = launch_counted(c, HVD_KERNEL_BULK, s, [&] { return launch_bulk(F, dtype, nch, c->nlocal, s); });
+    st = launch_counted(c, HVD_KERNEL_BULK, s, &F.ring.jt, fused_bytes(F), [&] { return launch_bulk(F, dtype, nch, c->nlocal, s); });
   else
-    st = launch_counted(c, HVD_KERNEL_FUSED, s, [&] { return launch_fused(F, dtype, nch, c->nlocal, c->threads, s); });
+    st = launch_counted(c, HVD_KERNEL_FUSED, s, &F.ring.jt, fused_bytes(F), [&] { return launch_fused(F, dtype, nch, c->nlocal, c->threads, s); });
   (void)tdt;
   if (st != HVD_OK) return st;
   if (c->tl) {
@@ -806,7 +832,7 @@ int enqueue_ll(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStream_t s, ui
   F.tdtype = dtype;
   F.ring.epoch = ++c->ll_epoch;
   if (c->tl) c->tl_slices = 0;  // the LL kernel records no timeline
-  return launch_counted(c, HVD_KERNEL_LL, s, [&] { return launch_ll(F, dtype, ctas, c->nlocal, s); });
+  return launch_counted(c, HVD_KERNEL_LL, s, &F.ring.jt, fused_bytes(F), [&] { return launch_ll(F, dtype, ctas, c->nlocal, s); });
 }
 
 // LL for a lone buffer up to ll_max; inside a multi-buffer plan only for buffers of at
@@ -879,7 +905,7 @@ int enqueue_ll128(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStream_t s)
   // dependency chain of the launch in between)
   F.ring.epoch = ++c->ll_epoch;
   if (c->tl) c->tl_slices = 0;
-  return launch_counted(c, HVD_KERNEL_LL128, s, [&] { return launch_ll128(F, dtype, ctas, c->nlocal, s); });
+  return launch_counted(c, HVD_KERNEL_LL128, s, &F.ring.jt, fused_bytes(F), [&] { return launch_ll128(F, dtype, ctas, c->nlocal, s); });
 }
 
 bool ll_eligible(const hvd_comm* c, const DevPlanBuffer& b, bool multi) {
@@ -996,6 +1022,21 @@ int enqueue_fused_plan(hvd_comm* c, CachedPlan* plan, cudaStream_t s) {
 
 int pack_grid(hvd_comm* c) { return c->sm_count * c->pack_ctas_per_sm / c->nlocal + 1; }
 
+// Job timeline host span of one public call (a no-op when the timeline is off).
+template <class Fn>
+int traced(hvd_comm* c, const char* name, uint64_t tensors, uint64_t bytes, Fn&& fn) {
+  if (!c || c->closed || !c->jt) return fn();
+  c->jt->call_begin(name, tensors, bytes);
+  const int st = fn();
+  if (c->jt) c->jt->call_end(st);
+  return st;
+}
+uint64_t list_bytes(const hvd_tensor* t, int n) {
+  uint64_t b = 0;
+  for (int k = 0; t && k < n; ++k) b += t[k].count * (uint64_t)elem_size(t[k].dtype);
+  return b;
+}
+
 int do_allreduce(hvd_comm* c, const hvd_tensor* t, int n, int op, uint64_t threshold, cudaStream_t s,
                  int wire = 0, const Registration* reg = nullptr) {
   int st = check_live(c);
@@ -1037,14 +1078,15 @@ int do_allreduce(hvd_comm* c, const hvd_tensor* t, int n, int op, uint64_t thres
   }
   if (c->fused) return enqueue_fused_plan(c, plan, s);  // steps 3-6, zero-copy, few launches
   for (DevPlanBuffer& b : plan->bufs) {       // step 6: repeat per fusion buffer
-    st = launch_counted(c, HVD_KERNEL_PACK, s, [&] {                          // step 3
-      return launch_pack(b.pp, b.dtype, c->nlocal, pack_grid(c), kPackThreads, s);
+    PackParams pp = b.pp;
+    st = launch_counted(c, HVD_KERNEL_PACK, s, &pp.jt, b.L * elem_size(b.dtype), [&] {  // step 3
+      return launch_pack(pp, b.dtype, c->nlocal, pack_grid(c), kPackThreads, s);
     });
     if (st != HVD_OK) return st;
     st = enqueue_ring(c, b.L, b.dtype, s);                                    // step 4
     if (st != HVD_OK) return st;
-    st = launch_counted(c, HVD_KERNEL_UNPACK, s, [&] {                        // step 5
-      return launch_unpack(b.pp, b.dtype, c->nlocal, pack_grid(c), kPackThreads, s);
+    st = launch_counted(c, HVD_KERNEL_UNPACK, s, &pp.jt, b.L * elem_size(b.dtype), [&] {  // step 5
+      return launch_unpack(pp, b.dtype, c->nlocal, pack_grid(c), kPackThreads, s);
     });
     if (st != HVD_OK) return st;
   }
@@ -1140,6 +1182,36 @@ int ll128_selftest(hvd_comm* c, int no_nvlink, int force_fail, int* status) {
 // ================================================================== C ABI
 extern "C" {
 
+static int allreduce_host_impl(hvd_comm* c, const void* const* in, void* const* out, uint64_t count, int dtype, int op,
+                               uint64_t chunk_bytes, void* stream);
+static int allreduce_negotiated_impl(hvd_comm* c, hvd_negotiator* g, const hvd_tensor* tensors, uint32_t n, int op,
+                                     uint64_t fusion_threshold, void* stream, uint32_t* ids_out, uint32_t* n_out);
+static int allreduce_buffer_impl(hvd_comm* c, uint64_t count, int dtype, int op, void* stream);
+static int broadcast_impl(hvd_comm* c, const hvd_tensor* t, int n, int root, void* stream);
+static int allgather_impl(hvd_comm* c, const hvd_tensor* in, const hvd_tensor* out, void* stream);
+
+// HVD_TIMELINE=<path> ("a single environment variable"): the job timeline of
+// every comm of the process goes to <path>.  The first comm of the process that writes
+// it starts a new file (rank 0 of a multi-process job: at hvd_init, before any rank can
+// connect); every rank appends from then on.
+static bool g_timeline_truncated = false;
+static const char* timeline_env() {
+  const char* p = std::getenv("HVD_TIMELINE");
+  return p && p[0] ? p : nullptr;
+}
+static int timeline_start(hvd_comm* c, const char* path, bool truncate) {
+  int ranks[kMaxLocal];
+  for (int l = 0; l < c->nlocal; ++l) ranks[l] = c->rk[l].rank;
+  return JobTrace::create(path, truncate, c->device, c->nlocal, ranks, c->size, &c->jt);
+}
+static int timeline_env_start(hvd_comm* c) {
+  const char* p = timeline_env();
+  if (!p || c->jt) return HVD_OK;
+  const bool trunc = !g_timeline_truncated && c->rank == 0;
+  g_timeline_truncated = true;
+  return timeline_start(c, p, trunc);
+}
+
 int hvd_init(int rank, int size, int device, uint64_t fusion_bytes, hvd_comm** out) {
   if (!out || size < 1 || rank < 0 || rank >= size || device < 0) return HVD_ERR_INVALID;
   *out = nullptr;
@@ -1157,6 +1229,19 @@ int hvd_init(int rank, int size, int device, uint64_t fusion_bytes, hvd_comm** o
   if (size == 1) {
     set_neighbours(c->rk[0], c->region[0], c->region[0], c->bufsz);
     c->connected = true;
+    st = timeline_env_start(c);
+  } else if (rank == 0 && timeline_env() && !g_timeline_truncated) {
+    // new file before any rank connects (the others append from hvd_connect on)
+    FILE* f = std::fopen(timeline_env(), "w");
+    if (f) {
+      std::fputs("[\n", f);
+      std::fclose(f);
+    }
+    g_timeline_truncated = true;
+  }
+  if (st != HVD_OK) {
+    hvd_finalize(c);
+    return st;
   }
   *out = c;
   return HVD_OK;
@@ -1179,6 +1264,11 @@ int hvd_init_virtual(int size, int device, uint64_t fusion_bytes, hvd_comm** out
   for (int l = 0; l < size; ++l)
     set_neighbours(c->rk[l], c->region[(l + 1) % size], c->region[(l + size - 1) % size], c->bufsz);
   c->connected = true;
+  st = timeline_env_start(c);
+  if (st != HVD_OK) {
+    hvd_finalize(c);
+    return st;
+  }
   *out = c;
   return HVD_OK;
 }
@@ -1246,7 +1336,9 @@ int hvd_connect(hvd_comm* c, const void* blobs, uint64_t len_each) {
   const int nv = nvlink_link(me_pci, bs.pci) == 1 && nvlink_link(me_pci, bp.pci) == 1;
   const char* ff = std::getenv("HVD_LL128_SELFTEST_FORCE_FAIL");
   int status = 0;
-  return ll128_selftest(c, !nv, ff && ff[0] == '1', &status);
+  const int st = ll128_selftest(c, !nv, ff && ff[0] == '1', &status);
+  if (st != HVD_OK) return st;
+  return timeline_env_start(c);
 }
 
 int hvd_ll128_selftest(hvd_comm* c, int force_fail, int* status) {
@@ -1261,6 +1353,11 @@ int hvd_finalize(hvd_comm* c) {
   if (!c->closed) {
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
+    if (c->jt) {  // the device is synchronised: every launch's record is final
+      c->jt->drain(true);
+      delete c->jt;
+      c->jt = nullptr;
+    }
     for (auto& p : c->cache) free_plan(p);
     for (auto& t : c->timed) {
       cudaEventDestroy(t.a);
@@ -1297,14 +1394,15 @@ int hvd_size(const hvd_comm* c) { return c ? c->size : -1; }
 int hvd_local_ranks(const hvd_comm* c) { return c ? c->nlocal : -1; }
 
 int hvd_allreduce(hvd_comm* c, const hvd_tensor* t, int n, int op, uint64_t fusion_threshold, void* stream) {
-  return do_allreduce(c, t, n, op, fusion_threshold, static_cast<cudaStream_t>(stream));
+  return traced(c, "ALLREDUCE", (uint64_t)n, list_bytes(t, n),
+                [&] { return do_allreduce(c, t, n, op, fusion_threshold, static_cast<cudaStream_t>(stream)); });
 }
 
 // Host-buffer allreduce: chunk i is copied in (copy stream 1), reduced on the
 // caller's stream by the same path as hvd_allreduce, and copied out (copy
 // stream 2) while chunk i+1 is copied in — PCIe in, the ring, and PCIe out
 // overlap through kHostSlots device staging slots.
-int hvd_allreduce_host(hvd_comm* c, const void* const* in, void* const* out, uint64_t count, int dtype, int op,
+static int allreduce_host_impl(hvd_comm* c, const void* const* in, void* const* out, uint64_t count, int dtype, int op,
                        uint64_t chunk_bytes, void* stream) {
   int st = check_live(c);
   if (st != HVD_OK) return st;
@@ -1378,7 +1476,15 @@ int hvd_allreduce_host(hvd_comm* c, const void* const* in, void* const* out, uin
 
 int hvd_allreduce_ex(hvd_comm* c, const hvd_tensor* t, int n, int op, uint64_t fusion_threshold, int wire_dtype,
                      void* stream) {
-  return do_allreduce(c, t, n, op, fusion_threshold, static_cast<cudaStream_t>(stream), wire_dtype);
+  return traced(c, "ALLREDUCE", (uint64_t)n, list_bytes(t, n), [&] {
+    return do_allreduce(c, t, n, op, fusion_threshold, static_cast<cudaStream_t>(stream), wire_dtype);
+  });
+}
+
+int hvd_allreduce_host(hvd_comm* c, const void* const* in, void* const* out, uint64_t count, int dtype, int op,
+                       uint64_t chunk_bytes, void* stream) {
+  return traced(c, "ALLREDUCE_HOST", 1, count * (uint64_t)elem_size(dtype),
+                [&] { return allreduce_host_impl(c, in, out, count, dtype, op, chunk_bytes, stream); });
 }
 
 // ---- registered tensors -------------------------------------------------------------------
@@ -1502,11 +1608,18 @@ int hvd_register(hvd_comm* c, const hvd_tensor* t, int n, const void* blobs, uin
 int hvd_allreduce_registered(hvd_comm* c, int reg_id, int op, uint64_t fusion_threshold, void* stream) {
   if (!c || reg_id < 0 || reg_id >= (int)c->regs.size() || !c->regs[reg_id].live) return HVD_ERR_INVALID;
   const Registration& R = c->regs[reg_id];
-  return do_allreduce(c, R.own.data(), R.n, op, fusion_threshold, static_cast<cudaStream_t>(stream), 0,
-                      c->size > 1 ? &R : nullptr);
+  return traced(c, "ALLREDUCE", (uint64_t)R.n, list_bytes(R.own.data(), R.n), [&] {
+    return do_allreduce(c, R.own.data(), R.n, op, fusion_threshold, static_cast<cudaStream_t>(stream), 0,
+                        c->size > 1 ? &R : nullptr);
+  });
 }
 
 int hvd_allreduce_negotiated(hvd_comm* c, hvd_negotiator* g, const hvd_tensor* tensors, uint32_t n, int op,
+                             uint64_t fusion_threshold, void* stream, uint32_t* ids_out, uint32_t* n_out) {
+  return allreduce_negotiated_impl(c, g, tensors, n, op, fusion_threshold, stream, ids_out, n_out);
+}
+
+static int allreduce_negotiated_impl(hvd_comm* c, hvd_negotiator* g, const hvd_tensor* tensors, uint32_t n, int op,
                              uint64_t fusion_threshold, void* stream, uint32_t* ids_out, uint32_t* n_out) {
   int st = check_live(c);
   if (st != HVD_OK) return st;
@@ -1514,7 +1627,9 @@ int hvd_allreduce_negotiated(hvd_comm* c, hvd_negotiator* g, const hvd_tensor* t
   if (hvd_neg::size_of(g) != c->size || hvd_neg::nlocal_of(g) != c->nlocal) return HVD_ERR_INVALID;
   std::vector<uint32_t> ids(hvd_neg::max_of(g));
   uint32_t m = 0;
-  st = hvd_negotiator_cycle(g, ids.data(), &m);  // step 1: what is ready on every rank
+  st = traced(c, "NEGOTIATE_ALLREDUCE", (uint64_t)n, 0, [&] {  // step 1: what is ready on every rank
+    return hvd_negotiator_cycle(g, ids.data(), &m);
+  });
   if (st != HVD_OK) {
     *n_out = m;
     return st;
@@ -1536,7 +1651,9 @@ int hvd_allreduce_negotiated(hvd_comm* c, hvd_negotiator* g, const hvd_tensor* t
   *n_out = m;
   if (m == 0) return HVD_OK;
   // steps 2-6 on the agreed tensors, in rank 0's submission order
-  return do_allreduce(c, list.data(), (int)m, op, fusion_threshold, static_cast<cudaStream_t>(stream));
+  return traced(c, "ALLREDUCE", (uint64_t)m, list_bytes(list.data(), (int)m), [&] {
+    return do_allreduce(c, list.data(), (int)m, op, fusion_threshold, static_cast<cudaStream_t>(stream));
+  });
 }
 
 int hvd_deregister(hvd_comm* c, int reg_id) {
@@ -1546,10 +1663,25 @@ int hvd_deregister(hvd_comm* c, int reg_id) {
 }
 
 int hvd_allreduce_average(hvd_comm* c, const hvd_tensor* t, int n, uint64_t fusion_threshold, void* stream) {
-  return do_allreduce(c, t, n, HVD_AVERAGE, fusion_threshold, static_cast<cudaStream_t>(stream));
+  return traced(c, "ALLREDUCE", (uint64_t)n, list_bytes(t, n), [&] {
+    return do_allreduce(c, t, n, HVD_AVERAGE, fusion_threshold, static_cast<cudaStream_t>(stream));
+  });
 }
 
 int hvd_allreduce_buffer(hvd_comm* c, uint64_t count, int dtype, int op, void* stream) {
+  return traced(c, "ALLREDUCE_BUFFER", 1, count * (uint64_t)elem_size(dtype),
+                [&] { return allreduce_buffer_impl(c, count, dtype, op, stream); });
+}
+
+int hvd_broadcast(hvd_comm* c, const hvd_tensor* t, int n, int root, void* stream) {
+  return traced(c, "BROADCAST", (uint64_t)n, list_bytes(t, n), [&] { return broadcast_impl(c, t, n, root, stream); });
+}
+
+int hvd_allgather(hvd_comm* c, const hvd_tensor* in, const hvd_tensor* out, void* stream) {
+  return traced(c, "ALLGATHER", 1, list_bytes(in, 1), [&] { return allgather_impl(c, in, out, stream); });
+}
+
+static int allreduce_buffer_impl(hvd_comm* c, uint64_t count, int dtype, int op, void* stream) {
   int st = check_live(c);
   if (st != HVD_OK) return st;
   const int esz = elem_size(dtype);
@@ -1577,8 +1709,9 @@ int hvd_allreduce_buffer(hvd_comm* c, uint64_t count, int dtype, int op, void* s
   if (op == HVD_AVERAGE) {
     char* bufs[kMaxLocal];
     for (int l = 0; l < c->nlocal; ++l) bufs[l] = c->rk[l].buf;
-    st = launch_counted(c, HVD_KERNEL_SCALE, s, [&] {
-      return launch_scale(bufs, c->nlocal, count, dtype, 1.0f / (float)c->size, pack_grid(c), kPackThreads, s);
+    JtRef jt;
+    st = launch_counted(c, HVD_KERNEL_SCALE, s, &jt, count * esz, [&] {
+      return launch_scale(bufs, c->nlocal, count, dtype, 1.0f / (float)c->size, pack_grid(c), kPackThreads, jt, s);
     });
     if (st != HVD_OK) return st;
   }
@@ -1592,7 +1725,7 @@ void* hvd_fusion_buffer(hvd_comm* c, int local) {
 
 uint64_t hvd_fusion_capacity(const hvd_comm* c) { return c ? c->cap : 0; }
 
-int hvd_broadcast(hvd_comm* c, const hvd_tensor* t, int n, int root, void* stream) {
+static int broadcast_impl(hvd_comm* c, const hvd_tensor* t, int n, int root, void* stream) {
   int st = check_live(c);
   if (st != HVD_OK) return st;
   if (root < 0 || root >= c->size || n < 0 || (n > 0 && !t)) return HVD_ERR_INVALID;
@@ -1627,7 +1760,7 @@ int hvd_broadcast(hvd_comm* c, const hvd_tensor* t, int n, int root, void* strea
     F.vbeg_global = b.vbeg;
     F.nseg = b.pp.nseg;
     F.dtype = b.dtype;
-    st = launch_counted(c, HVD_KERNEL_COPY, s, [&] { return launch_copy(F, b.dtype, nch, c->nlocal, c->threads, s); });
+    st = launch_counted(c, HVD_KERNEL_COPY, s, &F.ring.jt, fused_bytes(F), [&] { return launch_copy(F, b.dtype, nch, c->nlocal, c->threads, s); });
     if (st != HVD_OK) return st;
     const unsigned long long inc = ring_signals(kRingBroadcast, c->size, F.ring.K);
     for (int ch = 0; ch < nch; ++ch) c->base[ch] += inc;
@@ -1635,7 +1768,7 @@ int hvd_broadcast(hvd_comm* c, const hvd_tensor* t, int n, int root, void* strea
   return HVD_OK;
 }
 
-int hvd_allgather(hvd_comm* c, const hvd_tensor* in, const hvd_tensor* out, void* stream) {
+static int allgather_impl(hvd_comm* c, const hvd_tensor* in, const hvd_tensor* out, void* stream) {
   int st = check_live(c);
   if (st != HVD_OK) return st;
   if (!in || !out) return HVD_ERR_INVALID;
@@ -1705,7 +1838,7 @@ int hvd_allgather(hvd_comm* c, const hvd_tensor* in, const hvd_tensor* out, void
     }
     F.ring.mode = kRingAllgather;
     F.ring.epoch = ++c->hs_epoch;
-    st = launch_counted(c, HVD_KERNEL_COPY, s, [&] { return launch_copy(F, dtype, nch, c->nlocal, c->threads, s); });
+    st = launch_counted(c, HVD_KERNEL_COPY, s, &F.ring.jt, fused_bytes(F), [&] { return launch_copy(F, dtype, nch, c->nlocal, c->threads, s); });
     if (st != HVD_OK) return st;
     const unsigned long long inc = ring_signals(kRingAllgather, N, F.ring.K);
     for (int ch = 0; ch < nch; ++ch) c->base[ch] += inc;
@@ -1718,6 +1851,11 @@ int hvd_poll_error(hvd_comm* c) {
   if (c->closed) return HVD_ERR_CLOSED;
   return *c->err_host;
 }
+
+#ifndef HVD_BUILD_ID
+#define HVD_BUILD_ID "hvd-src-unknown"
+#endif
+const char* hvd_build_id(void) { return HVD_BUILD_ID; }
 
 const char* hvd_strerror(int status) {
   switch (status) {
@@ -1918,6 +2056,36 @@ int hvd_timeline(hvd_comm* c, int local, uint64_t* out, uint64_t cap_words, hvd_
   CK(cudaSetDevice(c->device));
   CK(cudaDeviceSynchronize());
   CK(cudaMemcpy(out, c->tl + words * local, words * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  return HVD_OK;
+}
+
+int hvd_timeline_start(hvd_comm* c, const char* path, int truncate) {
+  int st = check_live(c);
+  if (st != HVD_OK) return st;
+  if (!path || !path[0] || c->jt) return HVD_ERR_INVALID;
+  return timeline_start(c, path, truncate != 0);
+}
+
+int hvd_timeline_stop(hvd_comm* c) {
+  if (!c) return HVD_ERR_INVALID;
+  if (c->closed) return HVD_ERR_CLOSED;
+  if (!c->jt) return HVD_OK;
+  CK(cudaSetDevice(c->device));
+  const int st = cuda_fail(cudaDeviceSynchronize(), "timeline stop");
+  c->jt->drain(true);
+  delete c->jt;
+  c->jt = nullptr;
+  return st;
+}
+
+int hvd_timeline_flush(hvd_comm* c, uint64_t* launches, uint64_t* dropped) {
+  if (!c) return HVD_ERR_INVALID;
+  if (c->closed) return HVD_ERR_CLOSED;
+  if (launches) *launches = c->jt ? c->jt->launches() : 0;
+  if (dropped) *dropped = c->jt ? c->jt->dropped() : 0;
+  if (!c->jt) return HVD_OK;
+  c->jt->drain(false);
+  c->jt->flush();
   return HVD_OK;
 }
 

@@ -1,5 +1,13 @@
 """Horovod Timeline (§6) for the B200 path.
 
+Two views.  (1) The job-wide trace (``HVD_TIMELINE=<path>`` or
+``Comm.timeline_start``), written by the library itself (csrc/hvd_jobtrace.cpp): per
+rank, a span for every public call on a "host calls" lane and a span for every kernel
+launch — every kernel kind — on a "device kernels" lane, on one CLOCK_REALTIME axis
+for all ranks of the node.  ``load_trace`` reads it, ``validate_trace`` checks its
+schema, ``job_summary`` counts it.  (2) The per-slice detail of the most recent
+fused launch, described next.
+
 The paper's Timeline is a Chrome ``about:tracing`` view of "exactly what each
 node was doing at each time step", switched on by one setting.
 Here the events come from the device: with ``HVD_CFG_TIMELINE`` on, every
@@ -141,3 +149,123 @@ def summarize(tl) -> dict:
     return {"span_us": span, "busy_us_per_phase": busy,
             "mean_wait_us": float(sum(waits) / len(waits)) if waits else 0.0,
             "max_wait_us": float(max(waits)) if waits else 0.0}
+
+
+# ---------------------------------------------------------------- job-wide trace
+KERNEL_KINDS = ("PACK", "RING", "UNPACK", "SCALE", "FUSED_RING", "COPY_RING", "PULL_RING", "LL_RING", "SOLO",
+                "LL128_RING", "BULK_RING")
+CALL_NAMES = ("ALLREDUCE", "ALLREDUCE_BUFFER", "ALLREDUCE_HOST", "NEGOTIATE_ALLREDUCE", "BROADCAST", "ALLGATHER")
+
+
+def parse_trace_text(text: str) -> list:
+    """Events of a trace in the incremental array format the library writes: "[" then one
+    event per line, each followed by "," (Chrome accepts the missing "]")."""
+    body = text.strip()
+    if not body.startswith("["):
+        raise ValueError("not a Chrome trace-event array")
+    body = body[1:].rstrip()
+    if body.endswith("]"):
+        body = body[:-1].rstrip()
+    if body.endswith(","):
+        body = body[:-1]
+    return json.loads("[" + body + "]")
+
+
+def load_trace(path: str) -> list:
+    with open(path) as f:
+        return parse_trace_text(f.read())
+
+
+def validate_trace(events) -> dict:
+    """Check the job trace's schema; returns job_summary(events).  Raises ValueError.
+
+    Rules: metadata names every pid and its two lanes; "X" spans carry numeric ts >= 0 and
+    dur > 0; CALL spans are on tid 0 with a known name and {call, tensors, bytes, launches,
+    status}; KERNEL spans are on tid 1 with a known kind and {seq, call, ctas >= 1, bytes};
+    a kernel may run after its call returned (stream order) but never starts before the
+    call began (up to the clock calibration); each (pid, seq) appears once; every flow "s"
+    has its "f"; each call's launch count equals its kernel spans on that pid.
+    """
+    procs, lanes = set(), set()
+    calls, kernels, flows_s, flows_f = {}, {}, set(), set()
+    for e in events:
+        if not isinstance(e, dict) or "ph" not in e or "name" not in e:
+            raise ValueError(f"malformed event {e!r}")
+        ph = e["ph"]
+        if ph == "M":
+            if e["name"] == "process_name":
+                procs.add(e["pid"])
+            elif e["name"] == "thread_name":
+                lanes.add((e["pid"], e["tid"]))
+            continue
+        for k in ("pid", "ts"):
+            if k not in e:
+                raise ValueError(f"event without {k}: {e!r}")
+        if not isinstance(e["ts"], (int, float)) or e["ts"] < 0:
+            raise ValueError(f"bad ts: {e!r}")
+        if ph == "X":
+            if not isinstance(e.get("dur"), (int, float)) or e["dur"] <= 0:
+                raise ValueError(f"bad dur: {e!r}")
+            a = e.get("args", {})
+            if e.get("cat") == "CALL":
+                if e["tid"] != 0 or e["name"] not in CALL_NAMES:
+                    raise ValueError(f"bad call span: {e!r}")
+                for k in ("call", "tensors", "bytes", "launches", "status"):
+                    if k not in a:
+                        raise ValueError(f"call span without {k}: {e!r}")
+                key = (e["pid"], a["call"])
+                if key in calls:
+                    raise ValueError(f"call {key} twice")
+                calls[key] = e
+            elif e.get("cat") == "KERNEL":
+                if e["tid"] != 1 or e["name"] not in KERNEL_KINDS:
+                    raise ValueError(f"bad kernel span: {e!r}")
+                for k in ("seq", "call", "ctas", "bytes"):
+                    if k not in a:
+                        raise ValueError(f"kernel span without {k}: {e!r}")
+                if a["ctas"] < 1:
+                    raise ValueError(f"kernel span with no CTAs: {e!r}")
+                key = (e["pid"], a["seq"])
+                if key in kernels:
+                    raise ValueError(f"launch {key} twice")
+                kernels[key] = e
+            else:
+                raise ValueError(f"unknown span category: {e!r}")
+        elif ph == "s":
+            flows_s.add((e["pid"], e["id"]))
+        elif ph == "f":
+            flows_f.add((e["pid"], e["id"]))
+        elif ph != "i":
+            raise ValueError(f"unknown phase: {e!r}")
+    for e in list(calls.values()) + list(kernels.values()):
+        if e["pid"] not in procs or (e["pid"], e["tid"]) not in lanes:
+            raise ValueError(f"event on an unnamed lane: {e!r}")
+    if flows_s != flows_f:
+        raise ValueError(f"unmatched flow events: {sorted(flows_s ^ flows_f)[:5]}")
+    per_call = {}
+    for (pid, _), e in kernels.items():
+        ck = (pid, e["args"]["call"])
+        per_call[ck] = per_call.get(ck, 0) + 1
+        c = calls.get(ck)
+        if c is not None and e["ts"] + 1e-3 < c["ts"] - 50.0:
+            # device clock mapped to host time: allow the calibration uncertainty (< 50 us)
+            raise ValueError(f"kernel starts before its call: {e!r}")
+    for ck, c in calls.items():
+        if c["args"]["launches"] != per_call.get(ck, 0):
+            raise ValueError(f"call {ck}: {c['args']['launches']} launches, {per_call.get(ck, 0)} kernel spans")
+    return job_summary(events)
+
+
+def job_summary(events) -> dict:
+    """Per rank: calls by name, kernel launches by kind, device busy time (us)."""
+    out = {}
+    for e in events:
+        if e.get("ph") != "X":
+            continue
+        r = out.setdefault(e["pid"], {"calls": {}, "kernels": {}, "device_busy_us": 0.0})
+        if e.get("cat") == "CALL":
+            r["calls"][e["name"]] = r["calls"].get(e["name"], 0) + 1
+        elif e.get("cat") == "KERNEL":
+            r["kernels"][e["name"]] = r["kernels"].get(e["name"], 0) + 1
+            r["device_busy_us"] += e["dur"]
+    return out

@@ -436,3 +436,77 @@ def test_ll128_selftest_at_connect(force_rank):
               {"test": "test_ll128_selftest_at_connect", "n_gpus": n, "force_rank": force_rank,
                "status_per_rank": [res[r][0] for r in range(n)], "ll128_max_per_rank": [res[r][1] for r in range(n)],
                "kernels_per_rank": [res[r][2] for r in range(n)], "result": "bit-exact vs the oracle"})
+
+
+def _trace_worker(rank, world, port, q, path):
+    os.environ.update(RANK=str(rank), WORLD_SIZE=str(world), LOCAL_RANK=str(rank),
+                      MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), HVD_TIMELINE=path)
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import paper_1802_05799_b200 as hvd
+    import torch.distributed as dist
+    try:
+        comm = hvd.init()
+        comm.set_config(hvd._lib.HVD_CFG_TIMEOUT_MS, 20000)
+        small = torch.ones(1000, device="cuda")
+        mid = torch.ones(1 << 20, device="cuda")
+        big = torch.ones(12 << 20, device="cuda")
+        bc = torch.full((5000,), float(rank), device="cuda")
+        ag_in = torch.full((3000,), float(rank), device="cuda")
+        ag_out = torch.empty(3000 * world, device="cuda")
+        for _ in range(2):
+            comm.allreduce_average([small])
+            comm.allreduce_average([mid])
+            comm.allreduce_average([big])
+            comm.broadcast([bc], root=0)
+            comm.allgather(ag_in, ag_out)
+        torch.cuda.synchronize()
+        ok = bool(torch.equal(big, torch.ones_like(big))) and bool(torch.equal(bc, torch.zeros_like(bc)))
+        dist.barrier()
+        comm.finalize()  # writes this rank's remaining records
+        dist.barrier()
+        q.put((rank, ok))
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e)))
+
+
+def test_job_timeline_one_file_all_ranks(tmp_path):
+    """HVD_TIMELINE=<path> on every rank of a real multi-GPU job: one trace file, every
+    rank's calls and kernels on one time axis."""
+    n = min(torch.cuda.device_count(), 4)
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    import torch.multiprocessing as mp
+    from paper_1802_05799_b200 import timeline
+    path = str(tmp_path / "job.json")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_trace_worker, args=(r, n, port, q, path)) for r in range(n)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(n))
+    for p in procs:
+        p.join(timeout=120)
+    assert all(v is True for v in res.values()), res
+    ev = timeline.load_trace(path)
+    summ = timeline.validate_trace(ev)
+    assert sorted(summ) == list(range(n))
+    for r in range(n):
+        assert summ[r]["calls"] == {"ALLREDUCE": 6, "BROADCAST": 2, "ALLGATHER": 2}, summ[r]
+        assert summ[r]["kernels"].get("LL_RING") == 2 and summ[r]["kernels"].get("FUSED_RING") == 2, summ[r]
+        assert summ[r]["kernels"].get("COPY_RING") == 4, summ[r]
+    # one axis: the same call's kernels on different ranks overlap in time (a ring launch
+    # cannot finish on one rank before it started on another)
+    k = [e for e in ev if e.get("cat") == "KERNEL" and e["name"] == "FUSED_RING"]
+    by = {}
+    for e in k:
+        by.setdefault(e["args"]["seq"], []).append(e)
+    for seq, es in by.items():
+        if len(es) == n:
+            assert max(e["ts"] for e in es) < min(e["ts"] + e["dur"] for e in es) + 50.0, es
+    _evidence(f"mp_evidence_jobtrace_n{n}.json", {"test": "test_job_timeline_one_file_all_ranks", "n_gpus": n,
+                                                 "summary": {str(r): summ[r] for r in summ}})
+    import shutil
+    d = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+    shutil.copy(path, os.path.join(d, f"jobtrace_mp_n{n}.json"))
