@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -39,7 +40,10 @@ struct Header {
   uint64_t magic;  // written last by the creator (release)
   uint32_t size;
   uint32_t max_tensors;
-  uint64_t pad[6];
+  uint32_t creator_pid;    // rank 0's process: a segment whose creator is gone is stale
+  uint32_t pad0;
+  uint64_t creator_start;  // its start time (/proc/<pid>/stat field 22): pid reuse
+  uint64_t pad[4];
 };
 static_assert(sizeof(Header) == 64, "header");
 
@@ -55,6 +59,32 @@ struct SlotHead {
 };
 
 bool valid_dtype(int d) { return d >= 1 && d <= 4; }
+
+// Start time of a process in clock ticks since boot (/proc/<pid>/stat field 22); 0 if
+// the process does not exist.
+uint64_t proc_start(int pid) {
+  char path[64];
+  std::snprintf(path, sizeof path, "/proc/%d/stat", pid);
+  FILE* f = std::fopen(path, "r");
+  if (!f) return 0;
+  char buf[1024];
+  const size_t n = std::fread(buf, 1, sizeof buf - 1, f);
+  std::fclose(f);
+  buf[n] = 0;
+  const char* p = std::strrchr(buf, ')');  // the command name may contain spaces
+  if (!p) return 0;
+  int field = 2;
+  for (; *p && field < 22; ++p)
+    if (*p == ' ') ++field;
+  return std::strtoull(p, nullptr, 10);
+}
+
+// A segment left by a crashed run has a valid magic but a creator that no longer runs:
+// a rank attaching before rank 0 replaced it must not use it.
+bool creator_alive(const Header* h) {
+  const uint64_t st = proc_start((int)h->creator_pid);
+  return st != 0 && st == h->creator_start;
+}
 
 uint64_t now_ns() {  // CLOCK_REALTIME: comparable across the processes of one node
   timespec ts;
@@ -169,6 +199,8 @@ int hvd_negotiator_create(const char* shm_name, int rank, int size, int nlocal, 
       h = reinterpret_cast<Header*>(g->base);
       h->size = (uint32_t)size;
       h->max_tensors = max_tensors;
+      h->creator_pid = (uint32_t)getpid();
+      h->creator_start = proc_start((int)getpid());
       __atomic_store_n(&h->magic, kMagic, __ATOMIC_RELEASE);
     } else {
       for (;;) {  // wait for rank 0 to create and initialise the segment
@@ -180,7 +212,7 @@ int hvd_negotiator_create(const char* shm_name, int rank, int size, int nlocal, 
             close(fd);
             if (p != MAP_FAILED) {
               h = reinterpret_cast<Header*>(p);
-              if (__atomic_load_n(&h->magic, __ATOMIC_ACQUIRE) == kMagic) {
+              if (__atomic_load_n(&h->magic, __ATOMIC_ACQUIRE) == kMagic && creator_alive(h)) {
                 g->base = static_cast<char*>(p);
                 break;
               }

@@ -161,13 +161,23 @@ def _shm_worker(name, rank, size, reports, q, skip_cycles):
         q.put((rank, repr(e)))
 
 
-def _run_shm(size, reports, skip_cycles=False):
+def _crashed_creator(name, size):
+    """Rank 0 of a run that dies without hvd_negotiator_destroy: leaves a valid-looking segment."""
+    import paper_1802_05799_b200 as hvd
+    g = hvd.Negotiator(name, 0, size, 1, 64, 20000)  # noqa: F841 (kept alive until the exit)
+    os._exit(0)
+
+
+def _run_shm(size, reports, skip_cycles=False, name=None, rank0_delay=0.0):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    name = f"/hvd_test_{os.getpid()}_{random.randrange(1 << 30)}"
+    name = name or f"/hvd_test_{os.getpid()}_{random.randrange(1 << 30)}"
     ps = [ctx.Process(target=_shm_worker, args=(name, r, size, reports, q, skip_cycles)) for r in range(size)]
-    for p in ps:
+    for p in ps[1:]:
         p.start()
+    if rank0_delay:
+        time.sleep(rank0_delay)  # the other ranks look for the segment first
+    ps[0].start()
     res = dict(q.get(timeout=120) for _ in range(size))
     for p in ps:
         p.join(timeout=30)
@@ -182,6 +192,23 @@ def test_c_negotiator_shared_memory_processes(size):
     expect = neg.simulate(reports)
     res = _run_shm(size, reports)
     for r in range(size):
+        assert res[r] == expect, (r, res[r])
+
+
+def test_c_negotiator_ignores_a_stale_segment():
+    """A crashed run left a segment with the same name, magic and sizes: ranks
+    that look for it before rank 0 replaces it must not attach to it (its creator is gone)."""
+    name = f"/hvd_test_stale_{os.getpid()}_{random.randrange(1 << 30)}"
+    ctx = mp.get_context("spawn")
+    p = ctx.Process(target=_crashed_creator, args=(name, 2))
+    p.start()
+    p.join(timeout=60)
+    assert os.path.exists("/dev/shm" + name)
+    rng = random.Random(77)
+    reports, _ = _random_schedule(rng, 2, 4, 50)
+    expect = neg.simulate(reports)
+    res = _run_shm(2, reports, name=name, rank0_delay=1.0)
+    for r in range(2):
         assert res[r] == expect, (r, res[r])
 
 
