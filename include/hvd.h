@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define HVD_ABI_VERSION 1
+#define HVD_ABI_VERSION 2
 
 typedef enum {
   HVD_OK = 0,
@@ -105,7 +105,11 @@ int hvd_get_ipc_blob(hvd_comm* c, void* out, uint64_t* len);
 /* Map the ring successor's buffers from the gathered blobs
  * (`blobs` = size * len_each bytes, rank order).  Must be called on every
  * rank; the caller must barrier all ranks after it before the first
- * collective.  Errors: INVALID (blob mismatch), CUDA (IPC open failed). */
+ * collective.  A peer in another process is mapped by CUDA IPC; a peer in the
+ * SAME process (one process driving several GPUs, each with its own comm) by
+ * peer access to its allocation — then the ranks' hvd_connect calls must run
+ * concurrently (one thread each: the call ends with a collective self-test).
+ * Errors: INVALID (blob mismatch), CUDA (IPC open / peer access failed). */
 int hvd_connect(hvd_comm* c, const void* blobs, uint64_t len_each);
 
 /* Release everything.  Idempotent on a NULL comm; waits for the device.  */
@@ -285,7 +289,12 @@ typedef enum {
                                 Tensors whose dtype differs from the wire dtype always take
                                 the tile kernel.                                            */
   HVD_CFG_SOLO_STAGES = 24,  /* N = 1 bulk kernel: shared-memory stages per CTA (2..8)      */
-  HVD_CFG_SOLO_STAGE_BYTES = 25 /* N = 1 bulk kernel: bytes per stage (4..64 KiB, x 1 KiB)   */
+  HVD_CFG_SOLO_STAGE_BYTES = 25, /* N = 1 bulk kernel: bytes per stage (4..64 KiB, x 1 KiB)  */
+  HVD_CFG_PACE_GBPS = 26,    /* fused push: pace each rank's remote stores to this many GB/s,
+                                split evenly over the channels (0 = unpaced).  Keeps the NVLink
+                                store queue, and with it every ring hop's latency, short     */
+  HVD_CFG_PACE_BURST_ROWS = 27 /* pacing credit a channel may accumulate while idle, in rows
+                                of remote stores (threads x 16 B); default 2                */
 } hvd_config_key;
 /* Set a tuning knob; every rank must set identical values.  Errors: INVALID. */
 int hvd_set_config(hvd_comm* c, int key, int64_t value);

@@ -298,11 +298,22 @@ class Comm:
         return {"rank": info.rank, "size": info.size, "K": info.K, "T": info.T, "channels": info.channels,
                 "kind": {1: "pull", 2: "registered"}.get(info.kind, "push"), "fin_lag": self.get_config(_lib.HVD_CFG_FIN_LAG), "data": data.copy(), "signals": sig.copy()}
 
-    def timeline_start(self, path: str, truncate: bool = True):
+    def timeline_start(self, path: str, truncate=None, group=None):
         """Job-wide Horovod Timeline into ``path`` (``hvd_timeline_start``; the environment
-        variable ``HVD_TIMELINE=<path>`` does the same at init).  In a multi-process job
-        exactly one rank truncates, and the others start after it."""
-        check(lib.hvd_timeline_start(self._h, os.fsencode(path), int(bool(truncate))), "hvd_timeline_start")
+        variable ``HVD_TIMELINE=<path>`` does the same at init).  Collective in a
+        multi-process job: rank 0 starts a new file (``truncate`` None) and the other
+        ranks append after it, ordered by a barrier over ``group``."""
+        multi = self.size > 1 and self.local_ranks == 1
+        if truncate is None:
+            truncate = self.rank == 0
+        if multi:
+            import torch.distributed as dist
+        if not multi or truncate:
+            check(lib.hvd_timeline_start(self._h, os.fsencode(path), int(bool(truncate))), "hvd_timeline_start")
+        if multi:
+            dist.barrier(group)
+            if not truncate:
+                check(lib.hvd_timeline_start(self._h, os.fsencode(path), 0), "hvd_timeline_start")
 
     def timeline_stop(self):
         """Synchronise, write every remaining record and close the job timeline."""

@@ -52,6 +52,10 @@ int JobTrace::create(const char* path, bool truncate, int device, int nlocal, co
     std::fprintf(stderr, "[hvd] timeline: cannot open %s: %s\n", path, std::strerror(errno));
     return HVD_ERR_INVALID;
   }
+  if (truncate && ::write(fd, "[\n", 2) != 2) {  // the array opens before any rank appends
+    ::close(fd);
+    return HVD_ERR_INVALID;
+  }
   JobTrace* t = new JobTrace();
   t->fd_ = fd;
   t->device_ = device;
@@ -79,7 +83,6 @@ int JobTrace::create(const char* path, bool truncate, int device, int nlocal, co
     return HVD_ERR_CUDA;
   }
   char line[512];
-  if (truncate) t->append("[\n", 2);
   for (int l = 0; l < nlocal; ++l) {
     const int r = t->ranks_[l];
     int n = std::snprintf(line, sizeof line,

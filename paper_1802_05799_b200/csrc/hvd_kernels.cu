@@ -22,6 +22,24 @@ namespace {
 constexpr int kHvdErrTimeout = -5;   // HVD_ERR_TIMEOUT
 constexpr int kHvdErrMismatch = -7;  // HVD_ERR_MISMATCH
 
+// The error word kernels see (`err` in RingParams) lives in DEVICE memory: spin loops
+// poll it to give up early, and polling host-mapped memory would put a PCIe read in
+// every watchdog check — under heavy host<->device copy traffic those reads take so
+// long that the polling warps fall behind (measured: LL128 launches of 10 us turned
+// into 1.5 ms next to hvd_allreduce_host's copies).  Its second half points to the
+// host-mapped word hvd_poll_error reads; raise_err latches the code in both.
+struct ErrWords {
+  int code;        // device copy (read by spin loops)
+  int pad;
+  int* host;       // host-mapped word (written on error only)
+};
+__device__ __forceinline__ void raise_err(int* err, int code) {
+  *(volatile int*)err = code;
+  int* h = reinterpret_cast<ErrWords*>(err)->host;
+  if (h) *(volatile int*)h = code;
+  __threadfence_system();
+}
+
 // ------------------------------------------------------------------ memory helpers
 struct V32 { uint32_t w[8]; };
 
@@ -183,7 +201,7 @@ struct OpI64 {
 enum SliceKind { kCopy = 0, kAdd = 1, kAddLocal = 2 };
 
 constexpr int kPackBatch = 8;  // == kPackVecsPerThread in the runtime (tile = 256 x 8 vectors)
-constexpr int kUnroll = 2;  // 2 x (2 x 32 B) loads in flight per thread; 4 spills (wide-register alignment)
+constexpr int kUnroll = 2;  // 2 x (2 x 32 B) loads in flight per thread (ring_allreduce_kernel: 144 registers, no spills)
 
 template <class Op, int KIND>
 __device__ __forceinline__ void do_slice(const char* __restrict__ a, const char* __restrict__ b,
@@ -241,7 +259,7 @@ __device__ __forceinline__ bool spin_until(const unsigned long long* flag, unsig
   while (ld_acquire_sys(flag) < target) {
     if ((++spins & 1023u) == 0) {
       if (globaltimer() - t0 > timeout_ns || *(volatile int*)err != 0) {
-        *(volatile int*)err = kHvdErrTimeout;
+        raise_err(err, kHvdErrTimeout);
         return false;
       }
     }
@@ -347,7 +365,7 @@ __device__ __forceinline__ void signal_loop_multi(const int* done, int* claimed,
 }
 
 template <class Op>
-__global__ void __launch_bounds__(416, 1) ring_allreduce_kernel(const __grid_constant__ RingParams P) {
+__global__ void __maxnreg__(152) ring_allreduce_kernel(const __grid_constant__ RingParams P) {
   JtGuard jtg(P.jt);
   const RingRank& me = P.rk[blockIdx.y];
   const int ch = blockIdx.x;
@@ -379,7 +397,7 @@ __global__ void __launch_bounds__(416, 1) ring_allreduce_kernel(const __grid_con
     if (!spin_until(me.rflags + ch, P.epoch, P.err, P.timeout_ns)) {
       s_abort = 1;
     } else if (*(volatile const unsigned long long*)(me.rhash + ch) != P.hash) {
-      *(volatile int*)P.err = kHvdErrMismatch;
+      raise_err(P.err, kHvdErrMismatch);
       s_abort = 1;
     }
   }
@@ -586,7 +604,19 @@ struct FusedCtx {
   int scale_on;
   float scale;
   int dtype;
+  unsigned pace_cyc, pace_burst;    // remote-store pacing (RingParams)
 };
+
+// Remote-store pacing (HVD_CFG_PACE_GBPS): a channel issues at most one row of remote
+// stores per pace_cyc SM cycles, with up to pace_burst cycles of credit after idling.
+// Keeping the offered NVLink load just under what the link drains keeps the store
+// queue — and with it the fence and arrival latency of every ring hop — short.
+__device__ __forceinline__ void pace_row(const FusedCtx& F, long long& vft) {
+  long long now = clock64();
+  const long long start = vft > now - (long long)F.pace_burst ? vft : now - (long long)F.pace_burst;
+  vft = start + F.pace_cyc;
+  while (now < start) now = clock64();
+}
 
 __device__ __forceinline__ int seg_of(const FusedCtx& F, unsigned long long v, int s) {
   if (F.vbeg[s] <= v && (s + 1 == F.nseg || F.vbeg[s + 1] > v)) return s;
@@ -800,7 +830,7 @@ template <class Op, int KIND, int TESZ = Op::kEsz>
 __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& me, unsigned long long lo,
                                             unsigned long long hi, unsigned tid, unsigned nthr, SegCache& sc,
                                             Raw32* slots0, uint4* slots1, long long pv = 0,
-                                            const Handshake* hs = nullptr) {
+                                            const Handshake* hs = nullptr, long long* vft = nullptr) {
   // pv: shift from a buffer vector index to its slot in the channel-private layout of
   // the scratch / fusion-buffer regions (0: buffer order)
   constexpr int ESZ = Op::kEsz;  // wire element size
@@ -845,7 +875,7 @@ __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& m
       if (!spin_until(hs->flag, hs->epoch, hs->err, hs->timeout_ns)) {
         *(volatile int*)hs->abort = 1;
       } else if (*(volatile const unsigned long long*)hs->hash_flag != hs->hash) {  // ordered by the acquire
-        *(volatile int*)hs->err = kHvdErrMismatch;
+        raise_err(hs->err, kHvdErrMismatch);
         *(volatile int*)hs->abort = 1;
       }
     }
@@ -875,6 +905,7 @@ __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& m
       const uint4 y = slots1[(j % kPipe) * nthr + tid];
       Op::template add_words<4>(reinterpret_cast<uint32_t*>(&x), reinterpret_cast<const uint32_t*>(&y));
     }
+    if ((TO_NSCRATCH || TO_NBUF || RSCATTER) && F.pace_cyc) pace_row(F, *vft);
     if (TO_NSCRATCH) *reinterpret_cast<uint4*>(F.nscr + (v + pv) * 16) = x;
     if (TO_NBUF) *reinterpret_cast<uint4*>(me.nbuf + (v + pv) * 16) = x;
     if (SCATTER) Cvt::put(reinterpret_cast<char*>(sc.d + e * TESZ), left, x);
@@ -1008,6 +1039,7 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
   // after its first loads are issued)
   const Handshake hs0 = {me.rflags + ch, me.rhash + ch, R.hash, R.epoch, R.err, R.timeout_ns, &s_abort};
   bool hs_pending = true;
+  long long vft = 0;  // pacing: virtual finish time of this thread's last paced row
   for (int b = 0; b < P.nbuf; ++b) {
     const BufDesc& D = P.bufs[b];
     const int cg = chan_of(D, ch, gridDim.x);  // this channel's index in the buffer's geometry
@@ -1019,7 +1051,7 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
     if (cache)
       for (int j = tid; j < D.nseg; j += nd) s_vbeg[j] = D.vbeg[j];
     bar_sync(kBarData, nd);
-    FusedCtx F;
+    FusedCtx F = {};
     F.segs = D.segs;
     F.src = D.src + (size_t)blockIdx.y * D.nseg;
     F.dst = D.dst + (size_t)blockIdx.y * D.nseg;
@@ -1029,6 +1061,8 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
     F.scale_on = P.scale_on;
     F.scale = P.scale;
     F.dtype = P.dtype;
+    F.pace_cyc = R.pace_cyc;
+    F.pace_burst = R.pace_burst;
     // Receive halves alternate buffer by buffer on a channel: the predecessor may start
     // buffer b+1 (its reduce-scatter pushes) while this rank still reads buffer b's last
     // partials — registered mode has no final scatter to hold it back — but it cannot
@@ -1069,16 +1103,16 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
           hs_pending = false;
         }
         if (P.registered) {
-          if (rs && s == 0) fused_slice<Op, kF_RS0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs);
-          else if (rs) fused_slice<Op, kF_RS, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs);
-          else if (s == 0) fused_slice<Op, kF_RAG0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs);
-          else fused_slice<Op, kF_RAG, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs);
+          if (rs && s == 0) fused_slice<Op, kF_RS0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs, &vft);
+          else if (rs) fused_slice<Op, kF_RS, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs, &vft);
+          else if (s == 0) fused_slice<Op, kF_RAG0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs, &vft);
+          else fused_slice<Op, kF_RAG, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs, &vft);
         } else {
           if (t == T) fused_slice<Op, kF_FIN, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv);
-          else if (rs && s == 0) fused_slice<Op, kF_RS0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs);
-          else if (rs) fused_slice<Op, kF_RS, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs);
-          else if (s == 0) fused_slice<Op, kF_AG0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs);
-          else fused_slice<Op, kF_AG, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs);
+          else if (rs && s == 0) fused_slice<Op, kF_RS0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs, &vft);
+          else if (rs) fused_slice<Op, kF_RS, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs, &vft);
+          else if (s == 0) fused_slice<Op, kF_AG0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs, &vft);
+          else fused_slice<Op, kF_AG, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs, &vft);
         }
         if (t < T) sent += (hi - lo) * Op::kEsz;
       }
@@ -1165,7 +1199,7 @@ __global__ void __launch_bounds__(416, 1) copy_collective_kernel(const __grid_co
     if (threadIdx.x == nd) signal_loop(&s_done, nsig, me.nflags + ch, base, R.sig_mode, &s_pub);
     return;
   }
-  FusedCtx F;
+  FusedCtx F = {};
   F.segs = P.segs;
   F.src = P.src + (size_t)blockIdx.y * P.nseg;
   F.dst = (P.dst ? P.dst : P.src) + (size_t)blockIdx.y * P.nseg;
@@ -1352,7 +1386,7 @@ __global__ void __launch_bounds__(416, 1) pull_allreduce_kernel(const __grid_con
   }
 
   // ---- compute warps
-  FusedCtx F;
+  FusedCtx F = {};
   F.segs = P.segs;
   F.src = P.src + (size_t)blockIdx.y * P.nseg;
   F.dst = (P.dst ? P.dst : P.src) + (size_t)blockIdx.y * P.nseg;
@@ -1518,7 +1552,7 @@ __device__ __forceinline__ bool ll_load(const unsigned long long* p, unsigned fl
       const unsigned long long now = globaltimer();
       if (t0 == 0) t0 = now;
       else if (now - t0 > timeout_ns || *(volatile int*)err != 0) {
-        *(volatile int*)err = kHvdErrTimeout;
+        raise_err(err, kHvdErrTimeout);
         return false;
       }
     }
@@ -1552,7 +1586,7 @@ __global__ void __launch_bounds__(256) ll_allreduce_kernel(const __grid_constant
   constexpr unsigned long long kHalfWords = kLLHalfBytes / 8;
   unsigned long long* const in_ll = me.ll + (unsigned long long)par * kHalfWords + D.ll_off;
   unsigned long long* const out_ll = me.nll + (unsigned long long)par * kHalfWords + D.ll_off;
-  FusedCtx F;
+  FusedCtx F = {};
   F.segs = D.segs;
   F.src = D.src + (size_t)blockIdx.y * D.nseg;
   F.dst = D.dst + (size_t)blockIdx.y * D.nseg;
@@ -1649,7 +1683,7 @@ __global__ void __launch_bounds__(256) ll128_allreduce_kernel(const __grid_const
   const unsigned long long l_hi = l_lo + lpc < lines ? l_lo + lpc : lines;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, sub = lane % 8;
   const unsigned long long nvec = (D.L + VEL - 1) / VEL;
-  FusedCtx F;
+  FusedCtx F = {};
   F.segs = D.segs;
   F.src = D.src + (size_t)blockIdx.y * D.nseg;
   F.dst = D.dst + (size_t)blockIdx.y * D.nseg;
@@ -1705,7 +1739,7 @@ __global__ void __launch_bounds__(256) ll128_allreduce_kernel(const __grid_const
             else if (now - t0 > R.timeout_ns || *(volatile int*)R.err != 0) fail = true;
           }
           if (__any_sync(FULL, fail)) {
-            if (lane == 0) *(volatile int*)R.err = kHvdErrTimeout;
+            if (lane == 0) raise_err(R.err, kHvdErrTimeout);
             ok = false;
             break;
           }
@@ -1922,7 +1956,7 @@ __device__ __forceinline__ void mbar_wait_wd(unsigned long long* bar, unsigned p
       if (t0 == 0) {
         t0 = now;
       } else if (now - t0 > timeout_ns + 1000000000ull) {  // after the spin watchdogs had their chance
-        *(volatile int*)err = kHvdErrTimeout;
+        raise_err(err, kHvdErrTimeout);
         __threadfence_system();
         asm volatile("trap;");
       }
@@ -2223,7 +2257,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1) bulk_allreduce_kernel(const _
                    *(volatile unsigned long long*)(me.rflags + ch));
 #endif
           } else if (*(volatile const unsigned long long*)(me.rhash + ch) != R.hash) {
-            *(volatile int*)R.err = kHvdErrMismatch;
+            raise_err(R.err, kHvdErrMismatch);
             s_abort = 1;
           }
         }
@@ -2559,7 +2593,7 @@ __global__ void __launch_bounds__(kSoloThreads) solo_kernel(const __grid_constan
   }
   if (b == P.nbuf) return;
   const BufDesc& D = P.bufs[b];
-  FusedCtx F;
+  FusedCtx F = {};
   F.segs = D.segs;
   F.src = D.src + (size_t)blockIdx.y * D.nseg;
   F.dst = D.dst + (size_t)blockIdx.y * D.nseg;

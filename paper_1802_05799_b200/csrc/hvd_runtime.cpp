@@ -43,6 +43,8 @@ struct Blob {
   uint64_t region_bytes;
   cudaIpcMemHandle_t handle;
   char pci[32];  // PCI bus id of the rank's GPU (NVLink check of the ring links)
+  uint64_t region_addr;  // region address in the owner process (a rank in the SAME process
+                         // maps it by peer access: CUDA IPC cannot open its own handles)
 };
 
 struct DevPlanBuffer {
@@ -82,10 +84,12 @@ struct hvd_comm {
   char* region[kMaxLocal] = {};
   char* peer_region = nullptr;   // successor's region (IPC mapped), real mode
   char* pred_region = nullptr;   // predecessor's region (IPC mapped), real mode
+  bool peer_ipc = false, pred_ipc = false;  // mapped by IPC (else: same process, peer access)
+  int succ_device = -1;                     // successor's device (same-process registration)
   RingRank rk[kMaxLocal] = {};
   unsigned long long base[kMaxChannels] = {};
   int* err_host = nullptr;
-  int* err_dev = nullptr;
+  int* err_dev = nullptr;   // device-memory error words the kernels poll (ErrWords)
   int sm_count = 148;
   // tuning (hvd_set_config)
   int channels = 128;
@@ -116,6 +120,9 @@ struct hvd_comm {
   int solo_kernel = 0;              // HVD_CFG_SOLO_KERNEL: 1 persistent bulk kernel, 0 tile-per-CTA kernel
   int solo_stages = 6;              // HVD_CFG_SOLO_STAGES
   int solo_stage_bytes = 32 << 10;  // HVD_CFG_SOLO_STAGE_BYTES
+  int pace_gbps = 0;                // HVD_CFG_PACE_GBPS: fused push remote-store pacing (0 = off)
+  int pace_burst_rows = 2;          // HVD_CFG_PACE_BURST_ROWS
+  int clock_khz = 1965000;          // SM clock (cudaDevAttrClockRate): pacing cycles
   unsigned long long pbase[kMaxChannels] = {};  // pull-protocol progress counter bases
   int pull_calls = 0;
   unsigned long long pull_exits = 0;  // cumulative CTA exits of the pull kernel (per rank)
@@ -193,9 +200,18 @@ int common_init(hvd_comm* c, uint64_t fusion_bytes) {
   c->bufsz = (c->cap <= (256ull << 20) ? kRegionFactor : 1) * c->cap + kRegionSlack;
   CK(cudaSetDevice(c->device));
   CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device));
+  CK(cudaDeviceGetAttribute(&c->clock_khz, cudaDevAttrClockRate, c->device));
+  // error words: the host-mapped one hvd_poll_error reads, and the device-memory one the
+  // kernels poll (hvd_kernels.cu ErrWords: {code, pad, host-mapped address})
   CK(cudaHostAlloc(reinterpret_cast<void**>(&c->err_host), sizeof(int), cudaHostAllocMapped));
   *c->err_host = 0;
-  CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->err_dev), c->err_host, 0));
+  int* err_mapped = nullptr;
+  CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&err_mapped), c->err_host, 0));
+  {
+    struct { int code, pad; int* host; } words = {0, 0, err_mapped};
+    CK(cudaMalloc(reinterpret_cast<void**>(&c->err_dev), sizeof(words)));
+    CK(cudaMemcpy(c->err_dev, &words, sizeof(words), cudaMemcpyHostToDevice));
+  }
   const uint64_t region_bytes = kNumBufs * c->bufsz + kTailBytes + kLLRegionBytes;
   for (int l = 0; l < c->nlocal; ++l) {
     CK(cudaMalloc(reinterpret_cast<void**>(&c->region[l]), region_bytes));
@@ -541,6 +557,14 @@ int make_ring_params(hvd_comm* c, uint64_t L, int dtype, bool fused, RingParams*
   P->tl = c->tl;
   P->window = c->window;
   P->fin_lag = c->fin_lag;
+  if (fused && c->pace_gbps > 0 && c->size > 1) {
+    // one row of remote stores = threads x 16 B; channel share of the paced rank rate
+    const double row = 16.0 * c->threads;
+    const double per_ch = (double)c->pace_gbps * 1e9 / nch;
+    const double cyc = row / per_ch * (double)c->clock_khz * 1e3;
+    P->pace_cyc = (unsigned)std::max(1.0, cyc);
+    P->pace_burst = (unsigned)std::min(1e9, cyc * c->pace_burst_rows);
+  }
   P->tl_max = c->tl ? c->tl_max : 0;
   for (int ch = 0; ch < kMaxChannels; ++ch) P->base[ch] = pull ? c->pbase[ch] : c->base[ch];
   *nch_out = nch;
@@ -1099,6 +1123,8 @@ int nvlink_link(const char* a, const char* b) {
   typedef int (*InitFn)();
   typedef int (*HandleFn)(const char*, void**);
   typedef int (*P2PFn)(void*, void*, int, int*);
+  const char* chk = std::getenv("HVD_NVLINK_CHECK");  // "0": skip NVML (unknown -> LL128 off)
+  if (chk && chk[0] == '0') return -1;
   static void* lib = dlopen("libnvidia-ml.so.1", RTLD_NOW | RTLD_LOCAL);
   if (!lib) return -1;
   static InitFn init = reinterpret_cast<InitFn>(dlsym(lib, "nvmlInit_v2"));
@@ -1291,6 +1317,7 @@ int hvd_get_ipc_blob(hvd_comm* c, void* out, uint64_t* len) {
   b.pid = (int32_t)getpid();
   b.capacity = c->cap;
   b.region_bytes = kNumBufs * c->bufsz + kTailBytes + kLLRegionBytes;
+  b.region_addr = reinterpret_cast<uint64_t>(c->region[0]);
   CK(cudaSetDevice(c->device));
   CK(cudaIpcGetMemHandle(&b.handle, c->region[0]));
   CK(cudaDeviceGetPCIBusId(b.pci, (int)sizeof(b.pci), c->device));
@@ -1317,12 +1344,32 @@ int hvd_connect(hvd_comm* c, const void* blobs, uint64_t len_each) {
   Blob bs, bp;
   std::memcpy(&bs, p + (size_t)succ * len_each, sizeof(bs));
   std::memcpy(&bp, p + (size_t)pred * len_each, sizeof(bp));
-  void* ptr = nullptr;
-  CK(cudaIpcOpenMemHandle(&ptr, bs.handle, cudaIpcMemLazyEnablePeerAccess));
-  c->peer_region = static_cast<char*>(ptr);
+  // a peer in another process: CUDA IPC; in this process (one process driving several
+  // GPUs, e.g. for profiling): its allocation directly, through peer access
+  const int me_pid = (int)getpid();
+  auto map_peer = [&](const Blob& b, char** out, bool* ipc) -> int {
+    if (b.pid == me_pid) {
+      if (b.device != c->device) {
+        const cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else CK(e);
+      }
+      *out = reinterpret_cast<char*>(b.region_addr);
+      *ipc = false;
+      return HVD_OK;
+    }
+    void* ptr = nullptr;
+    CK(cudaIpcOpenMemHandle(&ptr, b.handle, cudaIpcMemLazyEnablePeerAccess));
+    *out = static_cast<char*>(ptr);
+    *ipc = true;
+    return HVD_OK;
+  };
+  int mst = map_peer(bs, &c->peer_region, &c->peer_ipc);
+  if (mst != HVD_OK) return mst;
+  c->succ_device = bs.device;
   if (pred != succ) {
-    CK(cudaIpcOpenMemHandle(&ptr, bp.handle, cudaIpcMemLazyEnablePeerAccess));
-    c->pred_region = static_cast<char*>(ptr);
+    mst = map_peer(bp, &c->pred_region, &c->pred_ipc);
+    if (mst != HVD_OK) return mst;
   } else {
     c->pred_region = c->peer_region;
   }
@@ -1377,11 +1424,12 @@ int hvd_finalize(hvd_comm* c) {
       if (c->stage[l]) cudaFree(c->stage[l]);
     c->cache.clear();
     for (auto& kv : c->ipc_maps) cudaIpcCloseMemHandle(kv.second);
-    if (c->peer_region) cudaIpcCloseMemHandle(c->peer_region);
-    if (c->pred_region && c->pred_region != c->peer_region) cudaIpcCloseMemHandle(c->pred_region);
+    if (c->peer_region && c->peer_ipc) cudaIpcCloseMemHandle(c->peer_region);
+    if (c->pred_region && c->pred_region != c->peer_region && c->pred_ipc) cudaIpcCloseMemHandle(c->pred_region);
     for (int l = 0; l < kMaxLocal; ++l)
       if (c->region[l]) cudaFree(c->region[l]);
     if (c->err_host) cudaFreeHost(c->err_host);
+    if (c->err_dev) cudaFree(c->err_dev);
     if (c->tl) cudaFree(c->tl);
     c->closed = true;
   }
@@ -1509,7 +1557,8 @@ struct RegEntry {
   uint64_t offset;  // tensor address - allocation base
   uint64_t count;
   int32_t dtype;
-  int32_t pad;
+  int32_t pid;      // owner process: the same process maps `addr` directly (peer access)
+  uint64_t addr;    // tensor address in the owner process
 };
 constexpr uint32_t kRegMagic = 0x48565247u;  // "HVRG"
 }  // namespace
@@ -1542,6 +1591,8 @@ int hvd_register_blob(hvd_comm* c, const hvd_tensor* t, int n, void* blob, uint6
         return HVD_ERR_CUDA;
       CK(cudaIpcGetMemHandle(&e.handle, reinterpret_cast<void*>(base)));
       e.offset = reinterpret_cast<uint64_t>(t[k].data) - (uint64_t)base;
+      e.pid = (int32_t)getpid();
+      e.addr = reinterpret_cast<uint64_t>(t[k].data);
     }
     std::memcpy(p + 8 + (size_t)k * sizeof(RegEntry), &e, sizeof(e));
   }
@@ -1583,6 +1634,10 @@ int hvd_register(hvd_comm* c, const hvd_tensor* t, int n, const void* blobs, uin
       if (e.count != t[k].count || e.dtype != t[k].dtype) return HVD_ERR_INVALID;
       if (!e.count) {
         R.succ[k] = nullptr;
+        continue;
+      }
+      if (e.pid == (int32_t)getpid()) {  // the successor runs in this process (peer access)
+        R.succ[k] = reinterpret_cast<char*>(e.addr);
         continue;
       }
       const std::string hk(reinterpret_cast<const char*>(&e.handle), sizeof(e.handle));
@@ -1943,6 +1998,14 @@ int hvd_set_config(hvd_comm* c, int key, int64_t value) {
         return HVD_ERR_INVALID;
       c->solo_stages = (int)value;
       return HVD_OK;
+    case HVD_CFG_PACE_GBPS:
+      if (value < 0 || value > 100000) return HVD_ERR_INVALID;
+      c->pace_gbps = (int)value;
+      return HVD_OK;
+    case HVD_CFG_PACE_BURST_ROWS:
+      if (value < 0 || value > 1024) return HVD_ERR_INVALID;
+      c->pace_burst_rows = (int)value;
+      return HVD_OK;
     case HVD_CFG_SOLO_STAGE_BYTES:
       if (value < (4 << 10) || value > (64 << 10) || value % 1024 ||
           bulk_smem_bytes(c->solo_stages, (int)value, false) > kBulkMaxSmem)
@@ -2026,6 +2089,8 @@ int64_t hvd_get_config(const hvd_comm* c, int key) {
     case HVD_CFG_LL128_STATUS: return c->ll128_status;
     case HVD_CFG_SOLO_KERNEL: return c->solo_kernel;
     case HVD_CFG_SOLO_STAGES: return c->solo_stages;
+    case HVD_CFG_PACE_GBPS: return c->pace_gbps;
+    case HVD_CFG_PACE_BURST_ROWS: return c->pace_burst_rows;
     case HVD_CFG_SOLO_STAGE_BYTES: return c->solo_stage_bytes;
     case HVD_CFG_BULK_STAGES: return c->bulk_stages;
     case HVD_CFG_BULK_STAGE_BYTES: return c->bulk_stage_bytes;

@@ -36,7 +36,7 @@ def test_job_trace_mixed_calls_every_kind(hvd, tmp_path):
     calls = []  # (name, expected kernel kinds)
     try:
         comm.set_config(L.HVD_CFG_TIMEOUT_MS, 20000)
-        comm.timeline_start(path, truncate=True)
+        comm.timeline_start(path)
         # 1. small buffer -> LL
         xs = workloads.all_ranks([1000, 3001], "f32", n)
         ref, _, _ = oracle.allreduce(xs, ["f32"] * 2, "average")
