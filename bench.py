@@ -290,7 +290,9 @@ def run_ours(args):
         roof["frac"] = roof["achieved"] / roof["peak"]
     roof["achieved_profiled"] = roof["achieved"] * avg_s / avg_s_prof
     roof["frac_profiled"] = roof["achieved_profiled"] / roof["peak"]
-    roof["traffic"] = _ncu_traffic(roof["kernel"])
+    roof["traffic"] = _ncu_traffic(roof["kernel"], n)
+    if n > 1:
+        roof["nvlink_counters"] = _ncu_profile(roof["kernel"], n, "nvlink")
     roof["share_of_step"] = dev_ms / ms_prof_local if ms_prof_local else None
     roof["timing"] = (("achieved: the dominant kernel is the only kernel of the step, so its average launch "
                        "duration = the timed region's CUDA events (max over ranks) / its launches. " if only_dom else
@@ -377,15 +379,24 @@ def run_ours(args):
     comm.finalize()
 
 
-def _ncu_traffic(kernel):
-    """DRAM bytes per launch of `kernel` from the committed ncu --set full summary, if any."""
+def _ncu_profile(kernel, n, key="dram"):
+    """Per-launch counters of `kernel` at N ranks from the committed ncu summary
+    (profiles/ncu_traffic.json): key "dram" -> dram__bytes_read + write (the roofline's
+    `traffic`), key "nvlink" -> {nvltx user / protocol bytes, nvlrx user bytes}."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get(kernel)
     except (OSError, ValueError):
         return None
+    v = d.get(kernel) if key == "dram" else d.get("nvlink", {}).get(kernel)
+    if isinstance(v, dict):
+        v = v.get(str(n))
+    return v
+
+
+def _ncu_traffic(kernel, n=1):
+    return _ncu_profile(kernel, n, "dram")
 
 
 # ---------------------------------------------------------------- CPU oracle (baseline / reference arm)

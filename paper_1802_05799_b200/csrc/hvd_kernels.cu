@@ -2476,6 +2476,8 @@ __global__ void __launch_bounds__(512) scale_kernel(const BufList bufs, unsigned
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
+constexpr int kMaxDevices = 64;
+
 // Kernels actually launched (a launcher with no work returns without one): the host
 // counts launches and opens timeline records only for launches that happened.
 static unsigned long long g_launched = 0;
@@ -2732,12 +2734,15 @@ cudaError_t launch_solo(const FusedParams& p, int dtype, int nlocal, cudaStream_
 template <class Op, int TESZ>
 static cudaError_t launch_fused_t(const FusedParams& p, int nch, int nlocal, int threads, cudaStream_t s) {
   const size_t smem = (size_t)p.cache_segs * 8 + fused_smem_bytes(kFusedSmemSegs + 1, threads);
-  static bool attr_set = false;
-  if (!attr_set) {
+  static bool attr_set[kMaxDevices] = {};  // function attributes are per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  if (!attr_set[dev]) {
     cudaError_t e = cudaFuncSetAttribute(fused_allreduce_kernel<Op, TESZ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)fused_smem_bytes(kFusedSmemSegs, kMaxRingThreads));
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set[dev] = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nch, nlocal);
@@ -2773,12 +2778,15 @@ cudaError_t launch_fused(const FusedParams& p, int dtype, int nch, int nlocal, i
 template <class Op>
 static cudaError_t launch_copy_t(const FusedParams& p, int nch, int nlocal, int threads, cudaStream_t s) {
   const size_t smem = fused_smem_bytes(p.nseg, threads);
-  static bool attr_set = false;
-  if (!attr_set) {
+  static bool attr_set[kMaxDevices] = {};  // function attributes are per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  if (!attr_set[dev]) {
     cudaError_t e = cudaFuncSetAttribute(copy_collective_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)fused_smem_bytes(kFusedSmemSegs, kMaxRingThreads));
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set[dev] = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nch, nlocal);
@@ -2807,12 +2815,15 @@ cudaError_t launch_copy(const FusedParams& p, int dtype, int nch, int nlocal, in
 template <class Op>
 static cudaError_t launch_pull_t(const FusedParams& p, int nch, int nlocal, int threads, cudaStream_t s) {
   const size_t smem = pull_smem_bytes(p.nseg);
-  static bool attr_set = false;
-  if (!attr_set) {
+  static bool attr_set[kMaxDevices] = {};  // function attributes are per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  if (!attr_set[dev]) {
     cudaError_t e = cudaFuncSetAttribute(pull_allreduce_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)pull_smem_bytes(kFusedSmemSegs));
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set[dev] = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nch, nlocal);
@@ -2914,13 +2925,23 @@ cudaError_t ll_max_ctas_per_sm(int* out) {
   return e;
 }
 
+template <class K>
+static cudaError_t occupancy_big_smem(int* out, K kernel, int block, size_t smem, size_t max_smem) {
+  // the opt-in shared-memory limit is a per-device function attribute: set it on the
+  // current device before asking (the answer is 0 blocks without it)
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_smem);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, kernel, block, smem);
+}
+
 cudaError_t fused_max_ctas_per_sm(int dtype, int threads, int* out) {
   const size_t smem = fused_smem_bytes(kFusedSmemSegs, threads);
+  const size_t mx = fused_smem_bytes(kFusedSmemSegs, kMaxRingThreads);
   switch (dtype) {
-    case 1: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fused_allreduce_kernel<OpF32, 4>, threads + 32, smem);
-    case 2: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fused_allreduce_kernel<OpBF16, 2>, threads + 32, smem);
-    case 3: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fused_allreduce_kernel<OpI32, 4>, threads + 32, smem);
-    case 4: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fused_allreduce_kernel<OpI64, 8>, threads + 32, smem);
+    case 1: return occupancy_big_smem(out, fused_allreduce_kernel<OpF32, 4>, threads + 32, smem, mx);
+    case 2: return occupancy_big_smem(out, fused_allreduce_kernel<OpBF16, 2>, threads + 32, smem, mx);
+    case 3: return occupancy_big_smem(out, fused_allreduce_kernel<OpI32, 4>, threads + 32, smem, mx);
+    case 4: return occupancy_big_smem(out, fused_allreduce_kernel<OpI64, 8>, threads + 32, smem, mx);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -30,7 +30,7 @@ lib = _lib.lib
 def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 2
     iters = int(sys.argv[2]) if len(sys.argv) > 2 else 8
-    L = 16 << 20
+    L = int(os.environ.get("NVL_MIB", "64")) << 18  # fp32 elements
     comms = []
     for r in range(n):
         torch.cuda.set_device(r)
@@ -57,8 +57,10 @@ def main():
     for t in ths:
         t.join()
     assert all(rc == 0 for rc in rcs), rcs
+    proto = int(os.environ.get("NVL_PROTOCOL", "1"))
     for c in comms:
         c.set_config(_lib.HVD_CFG_TIMEOUT_MS, 120000)
+        c.set_config(_lib.HVD_CFG_PROTOCOL, proto)
     g = []
     for r in range(n):
         gen = torch.Generator(device=f"cuda:{r}").manual_seed(180205799 + r)
@@ -101,6 +103,14 @@ def main():
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
     for _ in range(2):
         step()
+    rng = os.environ.get("NVL_RANGE") == "1"  # ncu range replay: the timed loop is the range
+    rdevs = [int(x) for x in os.environ.get("NVL_RANGE_DEVS", "0").split(",")]
+    if rng:
+        for r in range(n):
+            torch.cuda.synchronize(r)
+        for r in rdevs:
+            with torch.cuda.device(r):
+                torch.cuda.cudart().cudaProfilerStart()
     for r in range(n):
         ev[r][0].record(streams[r])
     for _ in range(iters):
@@ -109,11 +119,15 @@ def main():
         ev[r][1].record(streams[r])
     for r in range(n):
         torch.cuda.synchronize(r)
+    if rng:
+        for r in rdevs:
+            with torch.cuda.device(r):
+                torch.cuda.cudart().cudaProfilerStop()
     t_ms = max(ev[r][0].elapsed_time(ev[r][1]) for r in range(n)) / iters
     s1 = [c.traffic() for c in comms]
     bounds = hvd.chunk_bounds(L, n, hvd.HVD_FLOAT32)
     size = [int(bounds[c + 1] - bounds[c]) for c in range(n)]
-    out = {"n": n, "iters": iters, "payload_bytes": L * 4, "us_per_launch": t_ms * 1e3,
+    out = {"n": n, "iters": iters, "payload_bytes": L * 4, "protocol": proto, "us_per_launch": t_ms * 1e3,
            "busbw_GBps": L * 4 / (t_ms / 1e3) / 1e9 * 2 * (n - 1) / n,
            "max_abs_err_vs_fp64_mean": err, "ranks_bitwise_equal": True,
            "kernels": {k: v[0] for k, v in comms[0].kernel_stats().items() if v[0]},
