@@ -678,6 +678,28 @@ __device__ __forceinline__ void seg_lookup(const FusedCtx& F, unsigned long long
   if (F.rdst) c.rd = reinterpret_cast<uintptr_t>(F.rdst[s]) - dst_off * ESZ;
 }
 
+// seg_lookup for a vector whose member is among the nc members s0.. whose start vectors
+// are staged in shared memory (vb[i] = vbeg[s0 + i]; v < vb[nc - 1] or s0 + nc == nseg).
+template <int ESZ>
+__device__ __forceinline__ void seg_lookup_staged(const FusedCtx& F, unsigned long long v, SegCache& c,
+                                                  const unsigned long long* vb, int s0, int nc) {
+  if (v >= c.vlo && v < c.vhi) return;
+  int lo = c.s >= s0 && c.s < s0 + nc && vb[c.s - s0] <= v ? c.s - s0 : 0, hi = nc - 1;
+  while (lo < hi) {  // largest i with vb[i] <= v
+    const int mid = (lo + hi + 1) >> 1;
+    if (vb[mid] <= v) lo = mid; else hi = mid - 1;
+  }
+  const int s = s0 + lo;
+  c.s = s;
+  c.vlo = vb[lo];
+  c.vhi = lo + 1 < nc ? vb[lo + 1] : (s + 1 < F.nseg ? F.vbeg[s + 1] : ~0ull);
+  const unsigned long long dst_off = F.segs[s].dst_off;
+  c.end_el = dst_off + F.segs[s].count;
+  c.g = reinterpret_cast<uintptr_t>(F.src[s]) - dst_off * ESZ;
+  c.d = reinterpret_cast<uintptr_t>(F.dst[s]) - dst_off * ESZ;
+  if (F.rdst) c.rd = reinterpret_cast<uintptr_t>(F.rdst[s]) - dst_off * ESZ;
+}
+
 template <int ESZ>
 __device__ __forceinline__ bool fast16(const char* tp, unsigned long long left) {
   return left >= (unsigned long long)(16 / ESZ) && ((reinterpret_cast<uintptr_t>(tp) & 15) == 0);
@@ -2570,6 +2592,7 @@ cudaError_t launch_ring(const RingParams& p, int dtype, int nch, int nlocal, int
 #endif
 constexpr int kSoloThreads = HVD_SOLO_THREADS;
 constexpr int kSoloU = HVD_SOLO_U;  // 16 B wire vectors per thread (same-dtype wire)
+constexpr int kSoloSegCache = 256;  // member starts a boundary tile stages in shared memory
 
 template <class Op, int TESZ>
 __global__ void __launch_bounds__(kSoloThreads) solo_kernel(const __grid_constant__ FusedParams P) {
@@ -2662,7 +2685,17 @@ __global__ void __launch_bounds__(kSoloThreads) solo_kernel(const __grid_constan
     return;
   }
   // member boundary, ragged end or misaligned tensor: per-vector member lookup, the
-  // loads of each group of H vectors issued together (memory-level parallelism)
+  // loads of each group of H vectors issued together (memory-level parallelism).
+  // The member starts from the tile's first member on are staged in shared memory
+  // first: a tile of many small members (Inception V3) would otherwise pay a binary
+  // search of dependent global loads for every vector whose member changed.
+  __shared__ unsigned long long s_vb[kSoloSegCache];
+  const int s0 = sc.s;
+  const int nc = F.nseg - s0 < kSoloSegCache ? F.nseg - s0 : kSoloSegCache;
+  for (int i = tid; i < nc; i += kSoloThreads) s_vb[i] = F.vbeg[s0 + i];
+  __syncthreads();
+  // vectors below `vcached` have their member among the staged ones
+  const unsigned long long vcached = s0 + nc < F.nseg ? s_vb[nc - 1] : ~0ull;
   constexpr int H = U / 4 > 0 ? U / 4 : 1;
   for (int u0 = 0; u0 < U; u0 += H) {
     Raw32 raw[H];
@@ -2675,7 +2708,8 @@ __global__ void __launch_bounds__(kSoloThreads) solo_kernel(const __grid_constan
       left[h] = 0;
       fast[h] = false;
       if (v < t_end) {
-        seg_lookup<TESZ>(F, v, sc);
+        if (v < vcached) seg_lookup_staged<TESZ>(F, v, sc, s_vb, s0, nc);
+        else seg_lookup<TESZ>(F, v, sc);
         const unsigned long long e = v * VEL;
         left[h] = sc.end_el > e ? sc.end_el - e : 0;  // 0: padding after a member
         gp[h] = sc.g + e * TESZ;

@@ -557,6 +557,31 @@ def test_solo_stream_n1(hvd):
         comm.finalize()
 
 
+def test_solo_many_small_members_n1(hvd):
+    """N = 1 boundary tiles whose members are staged in shared memory (up to 256 per tile)
+    and tiles that span more members than that (the rest found in global memory): 900 tiny
+    tensors (1-40 elements, so one 16 KiB tile holds hundreds of members) between large
+    ones; same bits as the oracle."""
+    import random
+    rng = random.Random(1802)
+    counts = [rng.randint(1, 40) for _ in range(600)] + [70_001] + [rng.randint(1, 9) for _ in range(300)] + [5]
+    comm = hvd.init_virtual(1, 0, 64 << 20)
+    try:
+        for dt in ("f32", "bf16"):
+            xs = workloads.all_ranks(counts, dt, 1, seed=78)
+            ref, _, plan = oracle.allreduce(xs, [dt] * len(counts), "average")
+            ts = [[to_torch(x, dt) for x in xs[0]]]
+            comm.kernel_stats()
+            comm.allreduce(ts, op="average")
+            torch.cuda.synchronize()
+            assert comm.poll_error() == 0
+            assert comm.kernel_stats()["solo"][0] == 1
+            for k in range(len(counts)):
+                assert_same(from_torch(ts[0][k], dt), ref[0][k], dt, f"{dt} k={k}")
+    finally:
+        comm.finalize()
+
+
 @pytest.mark.parametrize("n", [2, 3, 4])
 def test_negotiated_allreduce_cycles(hvd, n):
     """Readiness negotiation + Tensor Fusion (R15): each cycle reduces exactly the

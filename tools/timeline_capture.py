@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--channels", type=int, default=0)
     ap.add_argument("--slice-kib", type=int, default=0)
     ap.add_argument("--registered", action="store_true", help="registered tensor (the bench's path)")
+    ap.add_argument("--config", action="append", default=[], metavar="KEY=VALUE", help="hvd_set_config")
+    ap.add_argument("--summary-out", default="")
     a = ap.parse_args()
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
     dist.init_process_group("gloo")
@@ -32,6 +34,9 @@ def main():
         comm.set_config(L.HVD_CFG_CHANNELS, a.channels)
     if a.slice_kib:
         comm.set_config(L.HVD_CFG_SLICE_BYTES, a.slice_kib << 10)
+    for kv in a.config:
+        k, v = kv.split("=")
+        comm.set_config(getattr(L, "HVD_CFG_" + k), int(v))
     comm.set_config(L.HVD_CFG_TIMELINE, 1024)
     x = torch.randn((a.mib << 20) // 4, device="cuda")
     h = comm.register([x]) if a.registered else [x]
