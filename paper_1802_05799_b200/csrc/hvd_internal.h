@@ -101,8 +101,8 @@ struct RingParams {
   int parity;                   // pull protocol: pull buffer of this call
   int call;                     // pull protocol: 1-based call index
   unsigned long long exits_target;  // pull protocol: cumulative CTA exits after this call
-  unsigned pace_cyc;            // fused: SM cycles per row of remote stores per channel (0 = unpaced)
-  unsigned pace_burst;          // fused: credit a paced channel may build up while idle, cycles
+  unsigned pace_cyc;            // fused: ns per row of remote stores per channel (0 = unpaced)
+  unsigned pace_burst;          // fused: credit a paced channel may build up while idle, ns
   JtRef jt;                     // job timeline record of this launch
 };
 

@@ -608,14 +608,16 @@ struct FusedCtx {
 };
 
 // Remote-store pacing (HVD_CFG_PACE_GBPS): a channel issues at most one row of remote
-// stores per pace_cyc SM cycles, with up to pace_burst cycles of credit after idling.
+// stores per pace_cyc ns, with up to pace_burst ns of credit after idling.
 // Keeping the offered NVLink load just under what the link drains keeps the store
 // queue — and with it the fence and arrival latency of every ring hop — short.
+// Time is %globaltimer (ns), not SM cycles: the SM clock drops under load and differs
+// between GPUs, which would pace the ranks of a ring at different real rates.
 __device__ __forceinline__ void pace_row(const FusedCtx& F, long long& vft) {
-  long long now = clock64();
+  long long now = (long long)globaltimer();
   const long long start = vft > now - (long long)F.pace_burst ? vft : now - (long long)F.pace_burst;
   vft = start + F.pace_cyc;
-  while (now < start) now = clock64();
+  while (now < start) now = (long long)globaltimer();
 }
 
 __device__ __forceinline__ int seg_of(const FusedCtx& F, unsigned long long v, int s) {

@@ -561,7 +561,7 @@ int make_ring_params(hvd_comm* c, uint64_t L, int dtype, bool fused, RingParams*
     // one row of remote stores = threads x 16 B; channel share of the paced rank rate
     const double row = 16.0 * c->threads;
     const double per_ch = (double)c->pace_gbps * 1e9 / nch;
-    const double cyc = row / per_ch * (double)c->clock_khz * 1e3;
+    const double cyc = row / per_ch * 1e9;  // ns per row (%globaltimer)
     P->pace_cyc = (unsigned)std::max(1.0, cyc);
     P->pace_burst = (unsigned)std::min(1e9, cyc * c->pace_burst_rows);
   }
