@@ -38,6 +38,32 @@ def test_library_exports_every_header_symbol(L):
     assert set(declared) <= exported
 
 
+def test_library_build_id_matches_the_sources(L):
+    """build() recompiles when any source changes: the library embeds the sha256 of its
+    sources (hvd_build_id) and the loaded one is the tree's."""
+    from paper_1802_05799_b200 import _build
+    assert L.lib.hvd_build_id().decode() == "hvd-src-" + _build.source_hash()
+    assert not _build._stale()
+
+
+def test_build_hash_tracks_every_source(tmp_path, monkeypatch):
+    """A change to any compiled file changes the build id (so a stale .so is rebuilt)."""
+    import shutil
+    from paper_1802_05799_b200 import _build
+    h0 = _build.source_hash()
+    src = tmp_path / "csrc"
+    shutil.copytree(_build.CSRC, src)
+    monkeypatch.setattr(_build, "CSRC", src)
+    assert _build.source_hash() == h0
+    for name in _build.SOURCES + _build.HEADERS:
+        f = src / name
+        old = f.read_bytes()
+        f.write_bytes(old + b"\n// touched\n")
+        assert _build.source_hash() != h0, name
+        f.write_bytes(old)
+    assert _build.source_hash() == h0
+
+
 def test_library_is_sm100a(L):
     out = subprocess.run(["cuobjdump", "--list-elf", str(L.LIB_PATH)], capture_output=True, text=True).stdout
     assert "sm_100a" in out

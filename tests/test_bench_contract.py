@@ -27,6 +27,25 @@ def test_reference_arm_line():
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    # host metadata next to the oracle timing
+    assert cb["host_cpus"] >= 1 and cb["sched_getaffinity"] >= 1 and cb["threads_used"] == 1
+    assert "cpu_model" in cb
+
+
+def test_roofline_traffic_and_nvlink_counters_per_n():
+    """bench.py's roofline reads the committed ncu summary per rank count: DRAM traffic of the
+    solo kernel (N = 1) and of the fused kernel at N = 2 / 4, and the NVLink counters whose
+    user bytes equal the algorithmic (2L - |c_{r+1}| - |c_{r+2}|) * esz within 0.1 %."""
+    sys.path.insert(0, ROOT)
+    import importlib
+    bench = importlib.import_module("bench")
+    assert bench._ncu_traffic("solo_kernel", 1) > 0
+    for n in (2, 4):
+        assert bench._ncu_traffic("fused_allreduce_kernel", n) > 0
+        nv = bench._ncu_profile("fused_allreduce_kernel", n, "nvlink")
+        assert abs(nv["nvltx_user_bytes"] / nv["algorithmic_bytes"] - 1) < 1e-3
+        assert nv["nvlrx_user_bytes"] == nv["nvltx_user_bytes"]
+        assert 0 < nv["protocol_over_user"] < 0.3
 
 
 def test_committed_gpu_lines_follow_the_contract():
