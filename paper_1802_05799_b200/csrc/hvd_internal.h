@@ -149,6 +149,8 @@ struct BufDesc {
   char* const* dst;                  // [nlocal * nseg] scatter addresses
   char* const* rdst;                 // [nlocal * nseg] registered: successor's addresses
   const unsigned long long* vbeg;    // [nseg] member start vectors
+  const int* tile_seg;               // [L / tile_vecs + 2] member of vector p * tile_vecs (+ last member):
+  unsigned long long tile_vecs;      //   bounds the member search of any vector to [tile_seg[p], tile_seg[p+1]]
   unsigned long long L, q, ch_el, slice_el;
   int nseg, K;
   int owner;                         // fused: -1 = every channel takes a share; else the first

@@ -605,6 +605,8 @@ struct FusedCtx {
   float scale;
   int dtype;
   unsigned pace_cyc, pace_burst;    // remote-store pacing (RingParams)
+  const int* tile_seg;              // BufDesc::tile_seg when vbeg is in global memory (else nullptr)
+  unsigned long long tile_vecs;
 };
 
 // Remote-store pacing (HVD_CFG_PACE_GBPS): a channel issues at most one row of remote
@@ -623,6 +625,11 @@ __device__ __forceinline__ void pace_row(const FusedCtx& F, long long& vft) {
 __device__ __forceinline__ int seg_of(const FusedCtx& F, unsigned long long v, int s) {
   if (F.vbeg[s] <= v && (s + 1 == F.nseg || F.vbeg[s + 1] > v)) return s;
   int lo = 0, hi = F.nseg - 1;
+  if (F.tile_seg) {  // the plan's tile -> member map narrows the search to a few members
+    const unsigned long long p = v / F.tile_vecs;
+    lo = __ldg(F.tile_seg + p);
+    hi = __ldg(F.tile_seg + p + 1);
+  }
   while (lo < hi) {  // largest s with vbeg[s] <= v
     const int mid = (lo + hi + 1) >> 1;
     if (F.vbeg[mid] <= v) lo = mid; else hi = mid - 1;
@@ -1081,6 +1088,8 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
     F.dst = D.dst + (size_t)blockIdx.y * D.nseg;
     F.rdst = P.registered ? D.rdst + (size_t)blockIdx.y * D.nseg : nullptr;
     F.vbeg = cache ? s_vbeg : D.vbeg;
+    F.tile_seg = cache ? nullptr : D.tile_seg;
+    F.tile_vecs = D.tile_vecs;
     F.nseg = D.nseg;
     F.scale_on = P.scale_on;
     F.scale = P.scale;
@@ -1616,6 +1625,8 @@ __global__ void __launch_bounds__(256) ll_allreduce_kernel(const __grid_constant
   F.dst = D.dst + (size_t)blockIdx.y * D.nseg;
   F.rdst = nullptr;
   F.vbeg = D.vbeg;
+  F.tile_seg = D.tile_seg;
+  F.tile_vecs = D.tile_vecs;
   F.nseg = D.nseg;
   F.scale_on = P.scale_on;
   F.scale = P.scale;
@@ -1713,6 +1724,8 @@ __global__ void __launch_bounds__(256) ll128_allreduce_kernel(const __grid_const
   F.dst = D.dst + (size_t)blockIdx.y * D.nseg;
   F.rdst = nullptr;
   F.vbeg = D.vbeg;
+  F.tile_seg = D.tile_seg;
+  F.tile_vecs = D.tile_vecs;
   F.nseg = D.nseg;
   F.scale_on = P.scale_on;
   F.scale = P.scale;
@@ -2626,6 +2639,8 @@ __global__ void __launch_bounds__(kSoloThreads) solo_kernel(const __grid_constan
   F.dst = D.dst + (size_t)blockIdx.y * D.nseg;
   F.rdst = nullptr;
   F.vbeg = D.vbeg;
+  F.tile_seg = D.tile_seg;
+  F.tile_vecs = D.tile_vecs;
   F.nseg = D.nseg;
   F.scale_on = P.scale_on;
   F.scale = P.scale;
@@ -2656,11 +2671,15 @@ __global__ void __launch_bounds__(kSoloThreads) solo_kernel(const __grid_constan
         tma_load(s_tile, g0, bytes, &s_bar);
       }
       __syncthreads();
-      mbar_wait(&s_bar, 0);
-      for (unsigned long long v = tid; v < t_end - base; v += kSoloThreads)
-        s_tile[v] = Pack16<ESZ>::conv(s_tile[v], F.scale, F.scale_on, F.dtype);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async-proxy reads
-      __syncthreads();
+      if (F.scale_on) {  // (N = 1 sums and averages by 1 move the tile unchanged)
+        mbar_wait(&s_bar, 0);
+        for (unsigned long long v = tid; v < t_end - base; v += kSoloThreads)
+          s_tile[v] = Pack16<ESZ>::conv(s_tile[v], F.scale, F.scale_on, F.dtype);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async-proxy reads
+        __syncthreads();
+      } else if (tid == 0) {
+        mbar_wait(&s_bar, 0);  // the bulk store reads what the bulk load wrote (both async proxy)
+      }
       if (tid == 0) {
         asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
                      ::"l"(d0), "r"(smem_u32(s_tile)), "r"(bytes) : "memory");

@@ -740,6 +740,8 @@ int enqueue_fused_multi(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStrea
     D.dst = b.dst ? b.dst : b.pp.src;
     D.rdst = b.rdst;
     D.vbeg = b.vbeg;
+    D.tile_seg = b.pp.tile_seg;
+    D.tile_vecs = b.pp.tile_vecs;
     D.nseg = b.pp.nseg;
     D.L = b.L;
     D.q = chunk_len(b.L, N, dtype);
@@ -839,6 +841,8 @@ int enqueue_ll(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStream_t s, ui
     D.src = b.pp.src;
     D.dst = b.dst ? b.dst : b.pp.src;
     D.vbeg = b.vbeg;
+    D.tile_seg = b.pp.tile_seg;
+    D.tile_vecs = b.pp.tile_vecs;
     D.nseg = b.pp.nseg;
     D.L = b.L;
     D.ch_el = (D.q + (uint64_t)D.nch * g - 1) / ((uint64_t)D.nch * g) * g;
@@ -907,6 +911,8 @@ int enqueue_ll128(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStream_t s)
     D.src = b.pp.src;
     D.dst = b.dst ? b.dst : b.pp.src;
     D.vbeg = b.vbeg;
+    D.tile_seg = b.pp.tile_seg;
+    D.tile_vecs = b.pp.tile_vecs;
     D.nseg = b.pp.nseg;
     D.L = b.L;
     D.ch_el = D.q;
@@ -1098,7 +1104,9 @@ int do_allreduce(hvd_comm* c, const hvd_tensor* t, int n, int op, uint64_t thres
   const float scale = 1.0f / (float)c->size;  // s = fl32(1/N) (R1)
   for (DevPlanBuffer& b : plan->bufs) {
     b.pp.scale = scale;
-    b.pp.scale_on = op == HVD_AVERAGE ? 1 : 0;
+    // N = 1: s = fl32(1/1) = 1 and fl32(x * 1) = x for every x (NaN stays NaN), so the
+    // prescale is the identity and is not computed (R1)
+    b.pp.scale_on = op == HVD_AVERAGE && c->size > 1 ? 1 : 0;
   }
   if (c->fused) return enqueue_fused_plan(c, plan, s);  // steps 3-6, zero-copy, few launches
   for (DevPlanBuffer& b : plan->bufs) {       // step 6: repeat per fusion buffer
@@ -1761,7 +1769,7 @@ static int allreduce_buffer_impl(hvd_comm* c, uint64_t count, int dtype, int op,
     c->bufreg.live = true;
     return do_allreduce(c, c->bufreg.own.data(), 1, op, c->cap, s, 0, c->size > 1 ? &c->bufreg : nullptr);
   }
-  if (op == HVD_AVERAGE) {
+  if (op == HVD_AVERAGE && c->size > 1) {  // N = 1: x * 1 = x (R1)
     char* bufs[kMaxLocal];
     for (int l = 0; l < c->nlocal; ++l) bufs[l] = c->rk[l].buf;
     JtRef jt;
