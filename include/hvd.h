@@ -293,8 +293,11 @@ typedef enum {
   HVD_CFG_PACE_GBPS = 26,    /* fused push: pace each rank's remote stores to this many GB/s,
                                 split evenly over the channels (0 = unpaced).  Keeps the NVLink
                                 store queue, and with it every ring hop's latency, short     */
-  HVD_CFG_PACE_BURST_ROWS = 27 /* pacing credit a channel may accumulate while idle, in rows
+  HVD_CFG_PACE_BURST_ROWS = 27, /* pacing credit a channel may accumulate while idle, in rows
                                 of remote stores (threads x 16 B); default 2                */
+  HVD_CFG_FUSED_PDL = 28     /* fused push: programmatic dependent launch, so back-to-back calls
+                                overlap the next launch with this one's tail (0 off; 1 with the
+                                cooperative launch; 2 instead of it, one local rank only)   */
 } hvd_config_key;
 /* Set a tuning knob; every rank must set identical values.  Errors: INVALID. */
 int hvd_set_config(hvd_comm* c, int key, int64_t value);

@@ -1014,6 +1014,13 @@ __device__ __forceinline__ int chan_of(const BufDesc& D, int ch, int nch) {
 // push lands in a receive region the successor's previous launch still reads.
 template <class Op, int TESZ>
 __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_constant__ FusedParams P) {
+  if (P.ring.pdl) {
+    // programmatic dependent launch: the next launch on the stream may be scheduled onto
+    // SMs as they free up; this grid touches memory only once the previous one has
+    // completed (its receive regions are free: the handshake below still means that)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   JtGuard jtg(P.ring.jt);
   extern __shared__ __align__(16) unsigned long long s_dyn[];
   constexpr int VEL = 16 / Op::kEsz;
@@ -2804,11 +2811,23 @@ static cudaError_t launch_fused_t(const FusedParams& p, int nch, int nlocal, int
   cfg.blockDim = dim3(threads + 32 * p.ring.sig_warps);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  // the CTAs of virtual ranks wait on each other: co-residency is required; a launch of
+  // one local rank has no dependency between its own CTAs (each channel talks to the same
+  // channel of the neighbouring GPUs), so it may drop the cooperative launch for PDL
+  if (p.ring.pdl != 2 || nlocal > 1) {
+    attr[na].id = cudaLaunchAttributeCooperative;
+    attr[na].val.cooperative = 1;
+    ++na;
+  }
+  if (p.ring.pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = na;
   ++g_launched;
   return cudaLaunchKernelEx(&cfg, fused_allreduce_kernel<Op, TESZ>, p);
 }

@@ -121,6 +121,7 @@ struct hvd_comm {
   int solo_stages = 6;              // HVD_CFG_SOLO_STAGES
   int solo_stage_bytes = 32 << 10;  // HVD_CFG_SOLO_STAGE_BYTES
   int pace_gbps = 0;                // HVD_CFG_PACE_GBPS: fused push remote-store pacing (0 = off)
+  int fused_pdl = 0;                // HVD_CFG_FUSED_PDL
   int pace_burst_rows = 2;          // HVD_CFG_PACE_BURST_ROWS
   int clock_khz = 1965000;          // SM clock (cudaDevAttrClockRate): pacing cycles
   unsigned long long pbase[kMaxChannels] = {};  // pull-protocol progress counter bases
@@ -557,6 +558,7 @@ int make_ring_params(hvd_comm* c, uint64_t L, int dtype, bool fused, RingParams*
   P->tl = c->tl;
   P->window = c->window;
   P->fin_lag = c->fin_lag;
+  P->pdl = fused ? c->fused_pdl : 0;
   if (fused && c->pace_gbps > 0 && c->size > 1) {
     // one row of remote stores = threads x 16 B; channel share of the paced rank rate
     const double row = 16.0 * c->threads;
@@ -2006,6 +2008,10 @@ int hvd_set_config(hvd_comm* c, int key, int64_t value) {
         return HVD_ERR_INVALID;
       c->solo_stages = (int)value;
       return HVD_OK;
+    case HVD_CFG_FUSED_PDL:
+      if (value < 0 || value > 2) return HVD_ERR_INVALID;
+      c->fused_pdl = (int)value;
+      return HVD_OK;
     case HVD_CFG_PACE_GBPS:
       if (value < 0 || value > 100000) return HVD_ERR_INVALID;
       c->pace_gbps = (int)value;
@@ -2098,6 +2104,7 @@ int64_t hvd_get_config(const hvd_comm* c, int key) {
     case HVD_CFG_SOLO_KERNEL: return c->solo_kernel;
     case HVD_CFG_SOLO_STAGES: return c->solo_stages;
     case HVD_CFG_PACE_GBPS: return c->pace_gbps;
+    case HVD_CFG_FUSED_PDL: return c->fused_pdl;
     case HVD_CFG_PACE_BURST_ROWS: return c->pace_burst_rows;
     case HVD_CFG_SOLO_STAGE_BYTES: return c->solo_stage_bytes;
     case HVD_CFG_BULK_STAGES: return c->bulk_stages;
