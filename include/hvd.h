@@ -346,6 +346,8 @@ int hvd_timeline(hvd_comm* c, int local, uint64_t* out, uint64_t cap_words, hvd_
  *                           LL128_RING, BULK_RING, PULL_RING, COPY_RING, SOLO, PACK, RING,
  *                           UNPACK, SCALE) from its first CTA's start to its last CTA's
  *                           end on that rank's GPU, args {seq, call, ctas, bytes};
+ *   tid 2 "negotiation":    one "X" span per tensor agreed by hvd_allreduce_negotiated, from
+ *                           its ready report to the cycle that agreed it, args {tensor, call};
  *   "s"/"f" flow events link each call to its launches.
  * Device times are %globaltimer converted to CLOCK_REALTIME (offset calibrated at start,
  * uncertainty in the TIMELINE_START event), so the ranks of a node share one time axis.

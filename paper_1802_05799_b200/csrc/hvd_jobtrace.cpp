@@ -97,8 +97,9 @@ int JobTrace::create(const char* path, bool truncate, int device, int nlocal, co
     n = std::snprintf(line, sizeof line,
                       "{\"name\": \"thread_name\", \"ph\": \"M\", \"pid\": %d, \"tid\": 0, \"args\": {\"name\": "
                       "\"host calls\"}},\n{\"name\": \"thread_name\", \"ph\": \"M\", \"pid\": %d, \"tid\": 1, "
-                      "\"args\": {\"name\": \"device kernels\"}},\n",
-                      r, r);
+                      "\"args\": {\"name\": \"device kernels\"}},\n{\"name\": \"thread_name\", \"ph\": \"M\", "
+                      "\"pid\": %d, \"tid\": 2, \"args\": {\"name\": \"negotiation\"}},\n",
+                      r, r, r);
     t->append(line, n);
     n = std::snprintf(line, sizeof line,
                       "{\"name\": \"TIMELINE_START\", \"cat\": \"META\", \"ph\": \"i\", \"s\": \"p\", \"pid\": %d, "
@@ -213,6 +214,18 @@ void JobTrace::call_end(int status) {
   }
   drain(false);
   flush();
+}
+
+void JobTrace::negotiate(int local, uint64_t id, int64_t t_ready, int64_t t_agreed) {
+  if (local < 0 || local >= nlocal_) return;
+  char line[320];
+  const int n = std::snprintf(
+      line, sizeof line,
+      "{\"name\": \"NEGOTIATE\", \"cat\": \"NEGOTIATE\", \"ph\": \"X\", \"pid\": %d, \"tid\": 2, "
+      "\"ts\": %.3f, \"dur\": %.3f, \"args\": {\"tensor\": %llu, \"call\": %llu}},\n",
+      ranks_[local], t_ready * 1e-3, std::max<int64_t>(t_agreed - t_ready, 1) * 1e-3, (unsigned long long)id,
+      (unsigned long long)call_id_);
+  append(line, n);
 }
 
 void JobTrace::drain(bool all) {

@@ -31,6 +31,10 @@ class JobTrace {
   // Host span of one public API call (nested calls fold into the outermost).
   void call_begin(const char* name, uint64_t tensors, uint64_t bytes);
   void call_end(int status);
+  // Negotiation phase of one tensor on local rank `local`: reported ready at
+  // t_ready, agreed by every rank at t_agreed (CLOCK_REALTIME ns); a span on the
+  // "negotiation" lane.
+  void negotiate(int local, uint64_t id, int64_t t_ready, int64_t t_agreed);
 
   // Write the records of finished launches; all = the device is synchronised, so a
   // launch still unfinished never will be (dropped and counted).

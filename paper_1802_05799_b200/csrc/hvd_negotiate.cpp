@@ -135,6 +135,18 @@ bool agreed_meta(const hvd_negotiator* g, uint32_t i, uint32_t* id, uint64_t* co
 int size_of(const hvd_negotiator* g) { return g ? g->size : 0; }
 int nlocal_of(const hvd_negotiator* g) { return g ? g->nlocal : 0; }
 uint32_t max_of(const hvd_negotiator* g) { return g ? g->max : 0; }
+uint32_t trace_recent(const hvd_negotiator* g, int local, uint32_t m, uint64_t* out) {
+  if (!g || local < 0 || local >= g->nlocal) return 0;
+  const std::vector<TraceRec>& t = g->trace[local];
+  const uint32_t n = (uint32_t)std::min<size_t>(t.size(), m);
+  for (uint32_t i = 0; i < n; ++i) {
+    const TraceRec& r = t[t.size() - n + i];
+    out[3 * i] = r.id;
+    out[3 * i + 1] = r.t_ready;
+    out[3 * i + 2] = r.t_agreed;
+  }
+  return n;
+}
 }  // namespace hvd_neg
 
 extern "C" {

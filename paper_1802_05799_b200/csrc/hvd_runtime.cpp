@@ -1699,6 +1699,14 @@ static int allreduce_negotiated_impl(hvd_comm* c, hvd_negotiator* g, const hvd_t
     *n_out = m;
     return st;
   }
+  if (c->jt && m > 0) {  // Horovod Timeline: each agreed tensor's negotiation phase
+    std::vector<uint64_t> rec((size_t)3 * m);
+    for (int l = 0; l < c->nlocal; ++l) {
+      const uint32_t k = hvd_neg::trace_recent(g, l, m, rec.data());
+      for (uint32_t i = 0; i < k; ++i)
+        c->jt->negotiate(l, rec[3 * i], (int64_t)rec[3 * i + 1], (int64_t)rec[3 * i + 2]);
+    }
+  }
   std::vector<hvd_tensor> list((size_t)c->nlocal * m);
   for (uint32_t i = 0; i < m; ++i) {
     uint32_t id = 0;

@@ -183,11 +183,12 @@ def validate_trace(events) -> dict:
     dur > 0; CALL spans are on tid 0 with a known name and {call, tensors, bytes, launches,
     status}; KERNEL spans are on tid 1 with a known kind and {seq, call, ctas >= 1, bytes};
     a kernel may run after its call returned (stream order) but never starts before the
-    call began (up to the clock calibration); each (pid, seq) appears once; every flow "s"
-    has its "f"; each call's launch count equals its kernel spans on that pid.
+    call began (up to the clock calibration); NEGOTIATE spans (one per agreed tensor: ready
+    report -> agreement) are on tid 2 with {tensor}; each (pid, seq) appears once; every
+    flow "s" has its "f"; each call's launch count equals its kernel spans on that pid.
     """
     procs, lanes = set(), set()
-    calls, kernels, flows_s, flows_f = {}, {}, set(), set()
+    calls, kernels, flows_s, flows_f, negs = {}, {}, set(), set(), []
     for e in events:
         if not isinstance(e, dict) or "ph" not in e or "name" not in e:
             raise ValueError(f"malformed event {e!r}")
@@ -229,6 +230,10 @@ def validate_trace(events) -> dict:
                 if key in kernels:
                     raise ValueError(f"launch {key} twice")
                 kernels[key] = e
+            elif e.get("cat") == "NEGOTIATE":
+                if e["tid"] != 2 or "tensor" not in a:
+                    raise ValueError(f"bad negotiation span: {e!r}")
+                negs.append(e)
             else:
                 raise ValueError(f"unknown span category: {e!r}")
         elif ph == "s":
@@ -237,7 +242,7 @@ def validate_trace(events) -> dict:
             flows_f.add((e["pid"], e["id"]))
         elif ph != "i":
             raise ValueError(f"unknown phase: {e!r}")
-    for e in list(calls.values()) + list(kernels.values()):
+    for e in list(calls.values()) + list(kernels.values()) + negs:
         if e["pid"] not in procs or (e["pid"], e["tid"]) not in lanes:
             raise ValueError(f"event on an unnamed lane: {e!r}")
     if flows_s != flows_f:
@@ -262,8 +267,10 @@ def job_summary(events) -> dict:
     for e in events:
         if e.get("ph") != "X":
             continue
-        r = out.setdefault(e["pid"], {"calls": {}, "kernels": {}, "device_busy_us": 0.0})
-        if e.get("cat") == "CALL":
+        r = out.setdefault(e["pid"], {"calls": {}, "kernels": {}, "device_busy_us": 0.0, "negotiated": 0})
+        if e.get("cat") == "NEGOTIATE":
+            r["negotiated"] += 1
+        elif e.get("cat") == "CALL":
             r["calls"][e["name"]] = r["calls"].get(e["name"], 0) + 1
         elif e.get("cat") == "KERNEL":
             r["kernels"][e["name"]] = r["kernels"].get(e["name"], 0) + 1

@@ -86,6 +86,17 @@ def test_job_trace_mixed_calls_every_kind(hvd, tmp_path):
         comm.allreduce_buffer(1 << 20, hvd.HVD_FLOAT32, "average")
         calls.append(("ALLREDUCE_BUFFER", {"SCALE", "RING"}))
         comm.set_config(L.HVD_CFG_FUSED, 1)
+        # 12-13. readiness negotiation: the cycle (host only), then the agreed tensors
+        neg = hvd.negotiator(comm, max_tensors=8)
+        tn = [[torch.ones(4000 + 1000 * k, device="cuda") for k in range(3)] for _ in range(n)]
+        for r in range(n):
+            for k in range(3):
+                neg.ready_tensor(k, tn[r][k], local=r)
+        ids = comm.allreduce_negotiated(neg, tn)
+        assert ids == [0, 1, 2]
+        calls.append(("NEGOTIATE_ALLREDUCE", None))
+        calls.append(("ALLREDUCE", {"LL_RING"}))
+        neg.close()
         torch.cuda.synchronize()
         assert comm.poll_error() == 0
         launched, dropped = comm.timeline_flush()
@@ -111,9 +122,13 @@ def test_job_trace_mixed_calls_every_kind(hvd, tmp_path):
             kern.setdefault(e["args"]["call"], set()).add(e["name"])
     for span, (name, kinds) in zip(spans, calls):
         got = kern.get(span["args"]["call"], set())
+        if name == "NEGOTIATE_ALLREDUCE":  # host only: no launch
+            assert not got
+            continue
         assert got, name
         if kinds is not None:
             assert got == kinds, (name, got, kinds)
+    assert all(v["negotiated"] == 3 for v in summ.values())
     allk = set().union(*kern.values())
     assert {"LL_RING", "LL128_RING", "FUSED_RING", "COPY_RING", "PULL_RING", "BULK_RING", "PACK", "RING",
             "UNPACK", "SCALE"} <= allk

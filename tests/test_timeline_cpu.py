@@ -52,6 +52,9 @@ def _job_text(nranks=2, drop_last_comma=False):
             {"name": "process_name", "ph": "M", "pid": r, "args": {"name": f"rank {r} (GPU 0)"}},
             {"name": "thread_name", "ph": "M", "pid": r, "tid": 0, "args": {"name": "host calls"}},
             {"name": "thread_name", "ph": "M", "pid": r, "tid": 1, "args": {"name": "device kernels"}},
+            {"name": "thread_name", "ph": "M", "pid": r, "tid": 2, "args": {"name": "negotiation"}},
+            {"name": "NEGOTIATE", "cat": "NEGOTIATE", "ph": "X", "pid": r, "tid": 2, "ts": 990.0, "dur": 8.0,
+             "args": {"tensor": 7, "call": 1}},
             {"name": "TIMELINE_START", "cat": "META", "ph": "i", "s": "p", "pid": r, "tid": 0, "ts": 100.0,
              "args": {"size": nranks, "local_ranks": nranks, "device": 0, "clock_uncertainty_us": 3.0}},
             {"name": "ALLREDUCE", "cat": "CALL", "ph": "X", "pid": r, "tid": 0, "ts": 1000.0, "dur": 20.0,
@@ -77,7 +80,7 @@ def test_job_trace_parse_and_validate():
     s = timeline.validate_trace(ev)
     assert s[0]["calls"] == {"ALLREDUCE": 1, "BROADCAST": 1}
     assert s[1]["kernels"] == {"LL_RING": 1, "FUSED_RING": 1, "COPY_RING": 1}
-    assert abs(s[0]["device_busy_us"] - 22.5) < 1e-9
+    assert abs(s[0]["device_busy_us"] - 22.5) < 1e-9 and s[1]["negotiated"] == 1
     # the unterminated array, without the trailing comma, and closed: all the same events
     assert timeline.parse_trace_text(_job_text(drop_last_comma=True)) == ev
     assert timeline.parse_trace_text(_job_text(drop_last_comma=True) + "]") == ev
@@ -100,6 +103,8 @@ def _mutated(fn):
     ("unmatched flow", lambda ev: ev.remove(next(e for e in ev if e.get("ph") == "f"))),
     ("unnamed lane", lambda ev: ev.remove(next(e for e in ev if e.get("name") == "thread_name"))),
     ("kernel before call", lambda ev: next(e for e in ev if e.get("cat") == "KERNEL").update(ts=500.0)),
+    ("negotiation lane", lambda ev: next(e for e in ev if e.get("cat") == "NEGOTIATE").update(tid=0)),
+    ("negotiation args", lambda ev: next(e for e in ev if e.get("cat") == "NEGOTIATE")["args"].pop("tensor")),
 ])
 def test_job_trace_validator_rejects(what, fn):
     with pytest.raises(ValueError):
