@@ -247,7 +247,7 @@ typedef enum {
   HVD_CFG_LL128_MAX_BYTES = 15, /* a call that is one fusion buffer larger than LL_MAX_BYTES
                                 and of at most this many bytes uses the LL128 protocol: flags
                                 inside 128-byte lines (relies on NVLink delivering a warp's
-                                128 B line store whole; 8/7 wire bytes).  In a call of more
+                                128 B line store whole; 16/15 wire bytes).  In a call of more
                                 than 16 buffers at N > 2 (fusion off), buffers above the
                                 multi-buffer LL limit and up to min(this, 16 MiB) go to
                                 grouped LL128 launches.  Default 16 MiB at N = 2, 32 MiB at

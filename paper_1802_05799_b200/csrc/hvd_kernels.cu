@@ -1686,19 +1686,31 @@ __global__ void __launch_bounds__(256) ll_allreduce_kernel(const __grid_constant
 }
 
 // LL128 protocol: like LL, the data carries its own arrival flag, but per 128-byte
-// line instead of per 8-byte word.  Lanes 0..6 of an 8-lane group store 7 x 16 B of
-// data and lane 7 stores the flag {~epoch, ~epoch}, all in ONE warp store
-// instruction; the receiver loads the line the same way and accepts it when the flag
-// matches.  This relies on NVLink (and L2) delivering one warp store of a 128-byte
-// line whole — what NCCL's LL128 also relies on; PTX does not promise it.  Measured:
-// 134M lines, 0 torn (tools/ll128_probe.cu, profiles/r01_ll128_probe.json).  Wire
-// bytes are 8/7 of the data (LL: 2x).  Same chunks, same reduction order as the ring:
-// bit-identical.  Slot of step t: lines of 7 vectors of the chunk, in a fixed LL half.
+// line instead of per 8-byte word.  An 8-lane group stores a line with ONE warp store
+// instruction (16 B per lane); lane 7's second 8 B are the flag {~epoch}; the receiver
+// loads the line the same way and accepts it when the flag matches.  This relies on
+// NVLink (and L2) delivering one warp store of a 128-byte line whole — what NCCL's
+// LL128 also relies on; PTX does not promise it, so hvd_connect enables LL128 only after
+// a self-test of exactly this store pattern passes on every rank.  Wire bytes are 16/15
+// of the data (lane 7's first 8 B carry data: a pair of lines holds 15 vectors); LL: 2x.
+// Same chunks, same reduction order as the ring: bit-identical.
+// A half vector (8 B: VEL/2 elements) of an LL128 line's last lane: `left` valid
+// elements, placed in x.x / x.y.
+template <int ESZ>
+__device__ __forceinline__ void put_half(char* p, unsigned long long left, const uint4& x) {
+  constexpr int HV = 8 / ESZ;
+  if (left >= (unsigned long long)HV && (reinterpret_cast<uintptr_t>(p) & 7) == 0)
+    *reinterpret_cast<uint2*>(p) = make_uint2(x.x, x.y);
+  else
+    scatter_slow<ESZ>(p, left < (unsigned long long)HV ? left : HV, x);
+}
+
 template <class Op>
 __global__ void __launch_bounds__(256) ll128_allreduce_kernel(const __grid_constant__ FusedParams P) {
   JtGuard jtg(P.ring.jt);
   constexpr int ESZ = Op::kEsz;
   constexpr int VEL = 16 / ESZ;
+  constexpr int HV = VEL / 2;  // elements in half a vector
   constexpr unsigned FULL = 0xffffffffu;
   const RingParams& R = P.ring;
   const RingRank& me = R.rk[blockIdx.y];
@@ -1713,17 +1725,21 @@ __global__ void __launch_bounds__(256) ll128_allreduce_kernel(const __grid_const
   const unsigned long long flag = ~R.epoch;  // never an LL word nor zeroed memory
   const int par = (int)(R.epoch & 1);
   const unsigned long long qv = D.q / VEL;         // vectors per chunk
-  const unsigned long long lines = (qv + 6) / 7;   // 128 B lines per chunk slot
-  const unsigned long long slot_words = lines * 16;
+  // Lines of 128 B go in pairs: a pair carries 15 vectors (240 B) and two 8 B flags.  In
+  // each line lanes 0..6 of an 8-lane group hold 16 B of data; lane 7 holds 8 B of data
+  // (half of the pair's vector 7: the low half in the first line, the high half in the
+  // second) and the flag.  Wire bytes: 16/15 of the data.
+  const unsigned long long pairs = (qv + 14) / 15;
+  const unsigned long long slot_words = pairs * 32;  // 2 lines x 16 words per pair
   // the LL128 area follows the two LL halves (the protocols never share memory)
   constexpr unsigned long long kBaseWords = 2 * kLLHalfBytes / 8;
   constexpr unsigned long long kHalfWords = kLL128HalfBytes / 8;
   unsigned long long* const in_ll = me.ll + kBaseWords + (unsigned long long)par * kHalfWords + D.ll_off;
   unsigned long long* const out_ll = me.nll + kBaseWords + (unsigned long long)par * kHalfWords + D.ll_off;
-  const unsigned long long lpc = (lines + nch - 1) / nch;  // lines of this channel
-  const unsigned long long l_lo = (unsigned long long)ch * lpc < lines ? (unsigned long long)ch * lpc : lines;
-  const unsigned long long l_hi = l_lo + lpc < lines ? l_lo + lpc : lines;
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, sub = lane % 8;
+  const unsigned long long ppc = (pairs + nch - 1) / nch;  // pairs of this channel
+  const unsigned long long p_lo = (unsigned long long)ch * ppc < pairs ? (unsigned long long)ch * ppc : pairs;
+  const unsigned long long p_hi = p_lo + ppc < pairs ? p_lo + ppc : pairs;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, sub = lane % 8, h = (lane >> 3) & 1;
   const unsigned long long nvec = (D.L + VEL - 1) / VEL;
   FusedCtx F = {};
   F.segs = D.segs;
@@ -1741,17 +1757,20 @@ __global__ void __launch_bounds__(256) ll128_allreduce_kernel(const __grid_const
   SegCache sc;
   bool ok = true;
   unsigned long long sent = 0;
+  const bool half = sub == 7;  // this lane carries half of the pair's vector 7
   for (int t = 0; t <= T && ok; ++t) {  // t == T: the chunk received in the last step
     const bool rs = t < N - 1;
     const int s = rs ? t : t - (N - 1);
     const int c = t == T ? mod(r + 2, N) : (rs ? mod(r - s, N) : mod(r + 1 - s, N));
     const unsigned long long c0v = (unsigned long long)c * qv;  // first vector of chunk c
-    for (unsigned long long lg = l_lo + (unsigned long long)warp * 4; lg < l_hi && ok; lg += 32) {
-      const unsigned long long line = lg + lane / 8;
-      const bool active = line < l_hi;
-      const unsigned long long cvec = line * 7 + sub;  // vector inside the chunk
+    // a warp moves 2 pairs (4 lines) per step: lanes 0..15 the first pair, 16..31 the second
+    for (unsigned long long pg = p_lo + (unsigned long long)warp * 2; pg < p_hi && ok; pg += (blockDim.x / 32) * 2) {
+      const unsigned long long pair = pg + lane / 16;
+      const bool active = pair < p_hi;
+      const unsigned long long line = 2 * pair + h;
+      const unsigned long long cvec = pair * 15 + (half ? 7 : sub + 8 * h);  // vector inside the chunk
       const unsigned long long v = c0v + cvec;
-      const bool valid = active && sub < 7 && cvec < qv && v < nvec;
+      const bool valid = active && cvec < qv && v < nvec;
       unsigned long long left = 0;
       uint4 g = make_uint4(0, 0, 0, 0);
       if (valid) {
@@ -1765,15 +1784,16 @@ __global__ void __launch_bounds__(256) ll128_allreduce_kernel(const __grid_const
                                   : Cvt::slow(gp, left, F.scale, F.scale_on, F.dtype);
         }
       }
+      if (half && h) g = make_uint4(g.z, g.w, 0, 0);  // the high half of vector 7, in x/y
       uint4 x = g;
       if (t > 0) {
         const unsigned long long* src = in_ll + (unsigned long long)(t - 1) * slot_words + line * 16 + sub * 2;
         bool got = !active;
-        unsigned long long a = 0, b = 0, t0 = 0;
+        unsigned long long a = 0, bw = 0, t0 = 0;
         unsigned spins = 0;
         for (;;) {
-          if (!got) asm volatile("ld.relaxed.sys.global.v2.u64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "l"(src) : "memory");
-          const unsigned long long f = __shfl_sync(FULL, b, (lane & ~7) | 7);
+          if (!got) asm volatile("ld.relaxed.sys.global.v2.u64 {%0,%1}, [%2];" : "=l"(a), "=l"(bw) : "l"(src) : "memory");
+          const unsigned long long f = __shfl_sync(FULL, bw, (lane & ~7) | 7);
           if (!got && f == flag) got = true;  // the line arrived whole (one 128 B warp store)
           if (__all_sync(FULL, got)) break;
           bool fail = false;
@@ -1789,22 +1809,30 @@ __global__ void __launch_bounds__(256) ll128_allreduce_kernel(const __grid_const
           }
         }
         if (!ok) break;
-        x = make_uint4((uint32_t)a, (uint32_t)(a >> 32), (uint32_t)b, (uint32_t)(b >> 32));
-        if (t <= N - 1) Op::template add_words<4>(reinterpret_cast<uint32_t*>(&x), reinterpret_cast<const uint32_t*>(&g));
+        x = half ? make_uint4((uint32_t)a, (uint32_t)(a >> 32), 0, 0)
+                 : make_uint4((uint32_t)a, (uint32_t)(a >> 32), (uint32_t)bw, (uint32_t)(bw >> 32));
+        if (t <= N - 1) {
+          if (half) Op::template add_words<2>(reinterpret_cast<uint32_t*>(&x), reinterpret_cast<const uint32_t*>(&g));
+          else Op::template add_words<4>(reinterpret_cast<uint32_t*>(&x), reinterpret_cast<const uint32_t*>(&g));
+        }
       }
       if (t < T && active) {
         unsigned long long* dst = out_ll + (unsigned long long)t * slot_words + line * 16 + sub * 2;
-        const unsigned long long w0 = sub < 7 ? ((unsigned long long)x.y << 32 | x.x) : flag;
-        const unsigned long long w1 = sub < 7 ? ((unsigned long long)x.w << 32 | x.z) : flag;
+        const unsigned long long w0 = (unsigned long long)x.y << 32 | x.x;
+        const unsigned long long w1 = half ? flag : ((unsigned long long)x.w << 32 | x.z);
         asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1,%2};" ::"l"(dst), "l"(w0), "l"(w1) : "memory");
       }
-      if (t >= N - 1 && valid && left) Cvt::put(reinterpret_cast<char*>(sc.d + v * VEL * ESZ), left, x);
+      if (t >= N - 1 && valid && left) {
+        char* dp = reinterpret_cast<char*>(sc.d + v * VEL * ESZ);
+        if (!half) Cvt::put(dp, left, x);
+        else if (left > (unsigned long long)(h * HV)) put_half<ESZ>(dp + h * 8, left - h * HV, x);
+      }
     }
-    if (t < T) {  // data elements of this channel's lines of chunk c
+    if (t < T) {  // data elements of this channel's pairs of chunk c
       const unsigned long long cl = (unsigned long long)c * D.q;
       unsigned long long ce = cl + D.q < D.L ? cl + D.q : D.L;
-      const unsigned long long el = cl + l_lo * 7 * VEL;
-      unsigned long long eh = cl + l_hi * 7 * VEL;
+      const unsigned long long el = cl + p_lo * 15 * VEL;
+      unsigned long long eh = cl + p_hi * 15 * VEL;
       eh = eh < ce ? eh : ce;
       if (eh > el && threadIdx.x == 0) sent += (eh - el) * ESZ;
     }

@@ -871,10 +871,11 @@ int enqueue_ll(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStream_t s, ui
 // 256 KiB is best; at N = 4 1 MiB cuts bf16 from 679 to 413 us and fp32 from 686 to 649 us)
 constexpr int64_t kLLMultiBytes = 256 << 10;     // N = 2
 constexpr int64_t kLLMultiBytesN4 = 1 << 20;     // N > 2
-// LL128 (ll128_allreduce_kernel) for one buffer: lines of 7 vectors + a flag vector.
+// LL128 (ll128_allreduce_kernel) for one buffer: pairs of 128-byte lines carrying 15
+// vectors and two 8-byte flags.
 uint64_t ll128_lines(const hvd_comm* c, const DevPlanBuffer& b) {
   const uint64_t qv = chunk_len(b.L, c->size, b.dtype) * elem_size(b.dtype) / 16;
-  return (qv + 6) / 7;
+  return 2 * ((qv + 14) / 15);
 }
 
 bool ll128_eligible(const hvd_comm* c, const DevPlanBuffer& b) {

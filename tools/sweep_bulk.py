@@ -15,7 +15,7 @@ import sys
 import torch
 import torch.distributed as dist
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.environ.get("HVD_PKG_ROOT") or os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1802_05799_b200 as hvd  # noqa: E402
 
 
@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--points", nargs="+", default=["PROTOCOL=1", "PROTOCOL=2"])
     ap.add_argument("--out", default="gpurun_out/sweep_bulk.json")
     ap.add_argument("--nccl", action="store_true")
+    ap.add_argument("--max-sets", type=int, default=0, help="cap on rotated input sets (0: none)")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
@@ -43,6 +44,8 @@ def main():
     for mib in a.mib:
         cnt = int(mib * (1 << 20)) // 4
         nsets = max(2, -(-(2 * 126 << 20) // (cnt * 4)))
+        if a.max_sets:
+            nsets = min(nsets, a.max_sets)
         g = torch.Generator(device="cuda").manual_seed(77 + rank)
         sets = [[torch.randn(cnt, generator=g, device="cuda")] for _ in range(nsets)]
         regs = [comm.register(s) for s in sets]
