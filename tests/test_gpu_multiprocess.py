@@ -342,6 +342,7 @@ def _mismatch_worker(rank, world, port, q):
     try:
         comm = hvd.init()
         comm.set_config(hvd._lib.HVD_CFG_TIMEOUT_MS, 3000)
+        comm.set_config(hvd._lib.HVD_CFG_LL128_MAX_BYTES, 0)  # both sizes on the fused push
         dist.barrier()
         # the collective contract broken: rank 0 reduces 6M elements, rank 1 10M (both on the
         # fused push kernel, whose launch handshake compares call hashes; the LL protocols have
