@@ -290,9 +290,11 @@ def run_ours(args):
         roof["frac"] = roof["achieved"] / roof["peak"]
     roof["achieved_profiled"] = roof["achieved"] * avg_s / avg_s_prof
     roof["frac_profiled"] = roof["achieved_profiled"] / roof["peak"]
-    roof["traffic"] = _ncu_traffic(roof["kernel"], n)
+    # the committed ncu captures are of the default workload (one 64 MiB fp32 gradient)
+    cap = args.workload == "fp32_64MiB"
+    roof["traffic"] = _ncu_traffic(roof["kernel"], n) if cap else None
     if n > 1:
-        roof["nvlink_counters"] = _ncu_profile(roof["kernel"], n, "nvlink")
+        roof["nvlink_counters"] = _ncu_profile(roof["kernel"], n, "nvlink") if cap else None
     roof["share_of_step"] = dev_ms / ms_prof_local if ms_prof_local else None
     roof["timing"] = (("achieved: the dominant kernel is the only kernel of the step, so its average launch "
                        "duration = the timed region's CUDA events (max over ranks) / its launches. " if only_dom else

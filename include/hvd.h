@@ -250,7 +250,7 @@ typedef enum {
                                 128 B line store whole; 16/15 wire bytes).  In a call of more
                                 than 16 buffers at N > 2 (fusion off), buffers above the
                                 multi-buffer LL limit and up to min(this, 16 MiB) go to
-                                grouped LL128 launches.  Default 24 MiB at N = 2, 40 MiB at
+                                grouped LL128 launches.  Default 24 MiB at N = 2, 48 MiB at
                                 N > 2 when every ring link is NVLink and the connect-time
                                 line-atomicity self-test passed, else 0; max 64 MiB;
                                 0 = never.                                                  */

@@ -238,11 +238,12 @@ int common_init(hvd_comm* c, uint64_t fusion_bytes) {
   CK(ll_max_ctas_per_sm(&ll_per_sm));
   c->ll_ctas = std::max(1, std::min(ll_per_sm, 4) * c->sm_count / c->nlocal);
   // Protocol limits for a lone buffer (profiles/r02_ll128_crossover_n{2,4}.json, the 16/15
-  // line layout): LL up to 256 KiB, LL128 up to 24 MiB (N = 2) / 40 MiB (N > 2), the fused
+  // line layout): LL up to 256 KiB, LL128 up to 24 MiB (N = 2) / 48 MiB (N > 2), the fused
   // push beyond (N = 2: LL128 55 vs 58 us at 24 MiB, 71 vs 65 at 32; N = 4: 94 vs 110 us at
-  // 32 MiB, a tie at 48, 181 vs 166 at 64)
+  // 32 MiB, a tie at 48, 181 vs 166 at 64; Inception V3 bf16's one 45 MiB buffer thus runs
+  // LL128 at N > 2)
   c->ll_max = (int64_t)kLLMaxBytes;
-  c->ll128_max = c->size <= 2 ? (int64_t)(24ull << 20) : (int64_t)(40ull << 20);
+  c->ll128_max = c->size <= 2 ? (int64_t)(24ull << 20) : (int64_t)(48ull << 20);
   CK(cudaDeviceSynchronize());
   return HVD_OK;
 }

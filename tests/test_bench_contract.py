@@ -50,8 +50,8 @@ def test_roofline_traffic_and_nvlink_counters_per_n():
 
 def test_committed_gpu_lines_follow_the_contract():
     """The GPU lines committed under profiles/ carry every key the driver reads."""
-    for n in (1, 2, 4):
-        p = os.path.join(ROOT, "profiles", f"r01_bench_n{n}.json")
+    for n, rnd in ((1, "r01"), (2, "r01"), (4, "r01"), (1, "r02"), (2, "r02"), (4, "r02")):
+        p = os.path.join(ROOT, "profiles", f"{rnd}_bench_n{n}.json")
         if not os.path.exists(p):
             continue
         d = json.load(open(p))

@@ -451,7 +451,7 @@ def _trace_worker(rank, world, port, q, path):
         comm.set_config(hvd._lib.HVD_CFG_TIMEOUT_MS, 20000)
         small = torch.ones(1000, device="cuda")
         mid = torch.ones(1 << 20, device="cuda")
-        big = torch.ones(12 << 20, device="cuda")
+        big = torch.ones(14 << 20, device="cuda")  # 56 MiB: above the LL128 limits
         bc = torch.full((5000,), float(rank), device="cuda")
         ag_in = torch.full((3000,), float(rank), device="cuda")
         ag_out = torch.empty(3000 * world, device="cuda")

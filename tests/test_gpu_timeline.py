@@ -50,7 +50,7 @@ def test_job_trace_mixed_calls_every_kind(hvd, tmp_path):
         comm.allreduce(tm, "average")
         calls.append(("ALLREDUCE", {"LL128_RING"}))
         # 3. large buffer -> fused push ring
-        xl = workloads.all_ranks([12_000_000], "f32", n)
+        xl = workloads.all_ranks([14_000_000], "f32", n)
         refl, _, _ = oracle.allreduce(xl, ["f32"], "average")
         tl = _ranks(xl, "f32")
         comm.allreduce(tl, "average")
