@@ -735,7 +735,6 @@ struct Raw32 { uint4 a, b; };
 template <int W, int T> struct WireCvt;
 
 template <int E> struct WireCvt<E, E> {
-  static constexpr int VEL = 16 / E;
   __device__ static __forceinline__ bool fast(const char* p, unsigned long long left) { return fast16<E>(p, left); }
   __device__ static __forceinline__ void issue(Raw32* slot, const char* p) { cp_async16(&slot->a, p); }
   __device__ static __forceinline__ void load(Raw32& r, const char* p) { r.a = __ldcs(reinterpret_cast<const uint4*>(p)); }
@@ -752,7 +751,6 @@ template <int E> struct WireCvt<E, E> {
 };
 
 template <> struct WireCvt<2, 4> {  // fp32 tensor, bf16 wire
-  static constexpr int VEL = 8;
   __device__ static __forceinline__ bool fast(const char* p, unsigned long long left) {
     return left >= 8 && ((reinterpret_cast<uintptr_t>(p) & 15) == 0);
   }
@@ -802,7 +800,6 @@ template <> struct WireCvt<2, 4> {  // fp32 tensor, bf16 wire
 };
 
 template <> struct WireCvt<4, 2> {  // bf16 tensor, fp32 wire
-  static constexpr int VEL = 4;
   __device__ static __forceinline__ bool fast(const char* p, unsigned long long left) {
     return left >= 4 && ((reinterpret_cast<uintptr_t>(p) & 7) == 0);
   }
@@ -1350,7 +1347,7 @@ __device__ __forceinline__ int pull_chunk(int t, int r, int N) {
 template <class Op>
 __global__ void __launch_bounds__(416, 1) pull_allreduce_kernel(const __grid_constant__ FusedParams P) {
   JtGuard jtg(P.ring.jt);
-  extern __shared__ __align__(128) unsigned long long s_dyn[];
+  extern __shared__ __align__(128) unsigned long long s_dyn_pull[];  // (own name: 128 B alignment)
   __shared__ __align__(8) unsigned long long full_bar[kStages], empty_bar[kStages];
   __shared__ int s_abort;
   constexpr int ESZ = Op::kEsz;
@@ -1369,8 +1366,8 @@ __global__ void __launch_bounds__(416, 1) pull_allreduce_kernel(const __grid_con
   char* const myB = me.pull[par];
   const char* const predB = me.ppull[par];
   const bool cache = P.nseg <= kFusedSmemSegs;
-  unsigned long long* s_vbeg = s_dyn;
-  char* stages = reinterpret_cast<char*>(s_dyn + (cache ? (P.nseg + 15) / 16 * 16 : 0));
+  unsigned long long* s_vbeg = s_dyn_pull;
+  char* stages = reinterpret_cast<char*>(s_dyn_pull + (cache ? (P.nseg + 15) / 16 * 16 : 0));
   if (cache)
     for (int j = threadIdx.x; j < P.nseg; j += blockDim.x) s_vbeg[j] = P.segs[j].vbeg;
   if (threadIdx.x == 0) {
