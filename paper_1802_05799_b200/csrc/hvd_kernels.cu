@@ -2632,7 +2632,8 @@ cudaError_t launch_ring(const RingParams& p, int dtype, int nch, int nlocal, int
 #define HVD_SOLO_THREADS 128
 #endif
 #ifndef HVD_SOLO_U
-#define HVD_SOLO_U 8
+#define HVD_SOLO_U 4  // 8 KiB tiles (profiles/r02_solo_tile_sweep/: vs 16 KiB, 64 MiB 0.938 -> 0.945 of HBM,
+                      // Inception V3 fp32 0.835 -> 0.848, bf16 0.666 -> 0.712; 4 KiB tiles lose on the model sets)
 #endif
 #ifndef HVD_SOLO_TMA
 #define HVD_SOLO_TMA 1
