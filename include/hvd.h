@@ -295,9 +295,12 @@ typedef enum {
                                 store queue, and with it every ring hop's latency, short     */
   HVD_CFG_PACE_BURST_ROWS = 27, /* pacing credit a channel may accumulate while idle, in rows
                                 of remote stores (threads x 16 B); default 2                */
-  HVD_CFG_FUSED_PDL = 28     /* fused push: programmatic dependent launch, so back-to-back calls
+  HVD_CFG_FUSED_PDL = 28,    /* fused push: programmatic dependent launch, so back-to-back calls
                                 overlap the next launch with this one's tail (0 off; 1 with the
                                 cooperative launch; 2 instead of it, one local rank only)   */
+  HVD_CFG_WATCHER = 29       /* fused push: 1 = a lane of the signal warp watches the
+                                predecessor's counter and mirrors it in shared memory; the
+                                slice loop then waits on shared memory                      */
 } hvd_config_key;
 /* Set a tuning knob; every rank must set identical values.  Errors: INVALID. */
 int hvd_set_config(hvd_comm* c, int key, int64_t value);

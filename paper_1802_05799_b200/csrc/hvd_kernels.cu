@@ -312,6 +312,14 @@ constexpr int kBarData = 1;
 __device__ __forceinline__ void st_release_cta_shared(int* p, int v) {
   asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
 }
+__device__ __forceinline__ void st_release_cta_shared64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.cta.shared.u64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_cta_shared64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.cta.shared.u64 %0, [%1];" : "=l"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
+  return v;
+}
 __device__ __forceinline__ int ld_acquire_cta_shared(const int* p) {
   int v;
   asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
@@ -942,6 +950,25 @@ __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& m
   cp_async_wait<0>();
 }
 
+// The fused kernel's wait for the predecessor's counter: through the watcher's shared
+// copy when the watcher runs, else a system-scope spin on the counter itself.
+__device__ __forceinline__ bool dep_wait(const RingParams& R, const unsigned long long* s_flag,
+                                         const unsigned long long* flag, unsigned long long target) {
+  if (!R.watcher) return spin_until(flag, target, R.err, R.timeout_ns);
+  if (ld_acquire_cta_shared64(s_flag) >= target) return true;
+  const unsigned long long t0 = globaltimer();
+  unsigned spins = 0;
+  while (ld_acquire_cta_shared64(s_flag) < target) {
+    if ((++spins & 1023u) == 0) {
+      if (globaltimer() - t0 > R.timeout_ns || *(volatile int*)R.err != 0) {
+        raise_err(R.err, kHvdErrTimeout);
+        return false;
+      }
+    }
+  }
+  return true;
+}
+
 // j-th operation of a fused launch -> (iteration t, slice k).  Iterations
 // 0..T-2 come in order; then the last all-gather iteration T-1 and the final
 // local scatter T are interleaved with a lag of `lag` slices:
@@ -1028,8 +1055,9 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
   const int r = me.rank;
   const unsigned long long base0 = R.base[ch];
   const int T = N > 1 ? 2 * (N - 1) : 0;
-  const int nd = blockDim.x - 32 * R.sig_warps;
+  const int nd = blockDim.x - 32 * (R.sig_warps + R.watcher);  // data threads
   __shared__ int s_abort, s_done, s_pub, s_claim;
+  __shared__ unsigned long long s_flag;  // watcher: newest value of the predecessor's counter
   unsigned long long* s_vbeg = s_dyn;
   Raw32* slots0 = reinterpret_cast<Raw32*>(s_dyn + P.cache_segs);
   uint4* slots1 = reinterpret_cast<uint4*>(slots0 + kPipe * nd);
@@ -1038,6 +1066,7 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
     s_done = 0;
     s_pub = 0;
     s_claim = 0;
+    s_flag = 0;
   }
   __syncthreads();
   if (N == 1) return;  // N = 1 runs solo_kernel
@@ -1051,6 +1080,33 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
     int total = 0;
     for (int b = 0; b < P.nbuf; ++b)
       if (chan_of(P.bufs[b], ch, gridDim.x) >= 0) total += T * P.bufs[b].K;
+    if (R.watcher && threadIdx.x >= blockDim.x - 32) {  // the last warp: the watcher
+      if (threadIdx.x != blockDim.x - 32) return;
+      // dependency watcher (HVD_CFG_WATCHER): keeps the newest value of the predecessor's
+      // counter in shared memory, so the data-warp leader waits on a CTA-scope acquire of
+      // shared memory instead of a system-scope load after each slice.  Causality: the
+      // predecessor's release (sys) -> this acquire (sys) -> release (cta) -> the leader's
+      // acquire (cta) -> bar.sync -> the data warps' loads.
+      const unsigned long long need = base0 + (unsigned long long)total;
+      unsigned long long seen = 0, t0 = 0;
+      unsigned spins = 0;
+      while (seen < need) {
+        const unsigned long long v = ld_acquire_sys(me.flags + ch);
+        if (v != seen) {
+          seen = v;
+          st_release_cta_shared64(&s_flag, v);
+          t0 = 0;
+          continue;
+        }
+        if ((++spins & 1023u) == 0) {
+          if (*(volatile int*)&s_abort) break;
+          const unsigned long long now = globaltimer();
+          if (t0 == 0) t0 = now;
+          else if (now - t0 > R.timeout_ns + 1000000000ull) break;  // the leader's watchdog reports it
+        }
+      }
+      return;
+    }
     if (R.sig_warps > 1) {
       if ((threadIdx.x - nd) % 32 == 0 && total > 0)
         signal_loop_multi(&s_done, &s_claim, total, me.nflags + ch, base0, &s_pub);
@@ -1175,7 +1231,7 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
       if (tid == 0) {
         if (t < T) st_release_cta_shared(&s_done, i);
         const unsigned long long target = tn > 0 ? bbase + (unsigned long long)(tn - 1) * K + kn + 1 : 0;
-        if (target && !s_abort && !spin_until(me.flags + ch, target, R.err, R.timeout_ns)) s_abort = 1;
+        if (target && !s_abort && !dep_wait(R, &s_flag, me.flags + ch, target)) s_abort = 1;
       }
       if (tn > 0) bar_sync(kBarData, nd);
     }
@@ -1184,7 +1240,7 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
   if (tid == 0) {
     // registered: the predecessor's last all-gather slices land in this rank's tensors;
     // completion on the stream means they have arrived
-    if (P.registered && N > 1 && !s_abort) spin_until(me.flags + ch, bbase, R.err, R.timeout_ns);
+    if (P.registered && N > 1 && !s_abort) dep_wait(R, &s_flag, me.flags + ch, bbase);
     atomicAdd(me.stats + 0, sent);
     if (ch == 0) atomicAdd(me.stats + 1, (unsigned long long)T * P.nbuf);  // messages per buffer
   }
@@ -2834,7 +2890,7 @@ static cudaError_t launch_fused_t(const FusedParams& p, int nch, int nlocal, int
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nch, nlocal);
-  cfg.blockDim = dim3(threads + 32 * p.ring.sig_warps);
+  cfg.blockDim = dim3(threads + 32 * (p.ring.sig_warps + p.ring.watcher));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];

@@ -122,6 +122,7 @@ struct hvd_comm {
   int solo_stage_bytes = 32 << 10;  // HVD_CFG_SOLO_STAGE_BYTES
   int pace_gbps = 0;                // HVD_CFG_PACE_GBPS: fused push remote-store pacing (0 = off)
   int fused_pdl = 0;                // HVD_CFG_FUSED_PDL
+  int watcher = 0;                  // HVD_CFG_WATCHER
   int pace_burst_rows = 2;          // HVD_CFG_PACE_BURST_ROWS
   int clock_khz = 1965000;          // SM clock (cudaDevAttrClockRate): pacing cycles
   unsigned long long pbase[kMaxChannels] = {};  // pull-protocol progress counter bases
@@ -562,6 +563,8 @@ int make_ring_params(hvd_comm* c, uint64_t L, int dtype, bool fused, RingParams*
   P->window = c->window;
   P->fin_lag = c->fin_lag;
   P->pdl = fused ? c->fused_pdl : 0;
+  // the watcher is one more warp: only while the block stays within the kernel's 416 threads
+  P->watcher = fused && c->watcher && c->threads + 32 * (P->sig_warps + 1) <= kMaxRingThreads + 32 ? 1 : 0;
   if (fused && c->pace_gbps > 0 && c->size > 1) {
     // one row of remote stores = threads x 16 B; channel share of the paced rank rate
     const double row = 16.0 * c->threads;
@@ -2020,6 +2023,10 @@ int hvd_set_config(hvd_comm* c, int key, int64_t value) {
         return HVD_ERR_INVALID;
       c->solo_stages = (int)value;
       return HVD_OK;
+    case HVD_CFG_WATCHER:
+      if (value < 0 || value > 1) return HVD_ERR_INVALID;
+      c->watcher = (int)value;
+      return HVD_OK;
     case HVD_CFG_FUSED_PDL:
       if (value < 0 || value > 2) return HVD_ERR_INVALID;
       c->fused_pdl = (int)value;
@@ -2117,6 +2124,7 @@ int64_t hvd_get_config(const hvd_comm* c, int key) {
     case HVD_CFG_SOLO_STAGES: return c->solo_stages;
     case HVD_CFG_PACE_GBPS: return c->pace_gbps;
     case HVD_CFG_FUSED_PDL: return c->fused_pdl;
+    case HVD_CFG_WATCHER: return c->watcher;
     case HVD_CFG_PACE_BURST_ROWS: return c->pace_burst_rows;
     case HVD_CFG_SOLO_STAGE_BYTES: return c->solo_stage_bytes;
     case HVD_CFG_BULK_STAGES: return c->bulk_stages;
