@@ -123,6 +123,7 @@ struct hvd_comm {
   int pace_gbps = 0;                // HVD_CFG_PACE_GBPS: fused push remote-store pacing (0 = off)
   int fused_pdl = 0;                // HVD_CFG_FUSED_PDL
   int watcher = 0;                  // HVD_CFG_WATCHER
+  int host_zero_copy = 0;           // HVD_CFG_HOST_ZERO_COPY (measured slower: off)
   int pace_burst_rows = 2;          // HVD_CFG_PACE_BURST_ROWS
   int clock_khz = 1965000;          // SM clock (cudaDevAttrClockRate): pacing cycles
   unsigned long long pbase[kMaxChannels] = {};  // pull-protocol progress counter bases
@@ -403,20 +404,23 @@ int upload_plan(hvd_comm* c, std::vector<uint64_t> key, const std::vector<HostBu
 // Tensor Fusion plan (hvd_plan.cpp) of the tensor list `t` (n per local rank),
 // uploaded and cached by (addresses, counts, dtypes, threshold): a training loop
 // that reduces the same gradient tensors every step uploads its tables once.
+// dst: separate outputs (same shapes as t; nullptr: in place)
 int get_plan(hvd_comm* c, const hvd_tensor* t, int n, uint64_t threshold, cudaStream_t s,
-             CachedPlan** out, int wire = 0, const Registration* reg = nullptr) {
+             CachedPlan** out, int wire = 0, const Registration* reg = nullptr, const hvd_tensor* dst = nullptr) {
   std::vector<uint64_t> key;
-  key.reserve(6 + 3 * (size_t)n * c->nlocal);
+  key.reserve(7 + 4 * (size_t)n * c->nlocal);
   key.push_back(0x504c414eull);  // "PLAN"
   key.push_back((uint64_t)wire);
   key.push_back(reinterpret_cast<uint64_t>(reg));
   key.push_back(threshold);
   key.push_back((uint64_t)n);
   key.push_back((uint64_t)c->nlocal);
+  key.push_back(dst ? 1 : 0);
   for (int i = 0; i < n * c->nlocal; ++i) {
     key.push_back(reinterpret_cast<uint64_t>(t[i].data));
     key.push_back(t[i].count);
     key.push_back((uint64_t)t[i].dtype);
+    if (dst) key.push_back(reinterpret_cast<uint64_t>(dst[i].data));
   }
   if ((*out = lookup_plan(c, key))) return HVD_OK;
   std::vector<uint64_t> counts(n);
@@ -446,6 +450,11 @@ int get_plan(hvd_comm* c, const hvd_tensor* t, int n, uint64_t threshold, cudaSt
       for (int l = 0; l < c->nlocal; ++l)
         hb[b].src[(size_t)l * pb.n_entries + j] =
             static_cast<char*>(t[(size_t)l * n + e.tensor].data) + e.src_off * tesz;
+      if (dst) {
+        hb[b].dst.resize((size_t)pb.n_entries * c->nlocal);
+        for (int l = 0; l < c->nlocal; ++l)
+          hb[b].dst[(size_t)l * pb.n_entries + j] = static_cast<char*>(dst[(size_t)l * n + e.tensor].data) + e.src_off * tesz;
+      }
       if (reg) {
         hb[b].rdst.resize((size_t)pb.n_entries * c->nlocal);
         for (int l = 0; l < c->nlocal; ++l)
@@ -1077,7 +1086,7 @@ uint64_t list_bytes(const hvd_tensor* t, int n) {
 }
 
 int do_allreduce(hvd_comm* c, const hvd_tensor* t, int n, int op, uint64_t threshold, cudaStream_t s,
-                 int wire = 0, const Registration* reg = nullptr) {
+                 int wire = 0, const Registration* reg = nullptr, const hvd_tensor* dst = nullptr) {
   int st = check_live(c);
   if (st != HVD_OK) return st;
   if (n < 0 || (n > 0 && !t)) return HVD_ERR_INVALID;
@@ -1107,8 +1116,8 @@ int do_allreduce(hvd_comm* c, const hvd_tensor* t, int n, int op, uint64_t thres
   if (n == 0) return HVD_OK;
   CK(cudaSetDevice(c->device));
   CachedPlan* plan = nullptr;
-  if (reg && !c->fused) return HVD_ERR_UNSUPPORTED;
-  st = get_plan(c, t, n, threshold, s, &plan, wire, reg);
+  if ((reg || dst) && !c->fused) return HVD_ERR_UNSUPPORTED;
+  st = get_plan(c, t, n, threshold, s, &plan, wire, reg, dst);
   if (st != HVD_OK) return st;
   const float scale = 1.0f / (float)c->size;  // s = fl32(1/N) (R1)
   for (DevPlanBuffer& b : plan->bufs) {
@@ -1467,6 +1476,23 @@ int hvd_allreduce(hvd_comm* c, const hvd_tensor* t, int n, int op, uint64_t fusi
 // caller's stream by the same path as hvd_allreduce, and copied out (copy
 // stream 2) while chunk i+1 is copied in — PCIe in, the ring, and PCIe out
 // overlap through kHostSlots device staging slots.
+// Every buffer is page-locked host memory the device reaches at the same address (UVA):
+// the kernels can read / write it directly.
+static bool host_mapped(hvd_comm* c, const void* const* in, void* const* out, uint64_t bytes) {
+  for (int l = 0; l < c->nlocal; ++l) {
+    for (const void* p : {static_cast<const void*>(in[l]), static_cast<const void*>(out[l])}) {
+      cudaPointerAttributes a;
+      if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+      }
+      if (a.type != cudaMemoryTypeHost || a.devicePointer != p) return false;
+      (void)bytes;
+    }
+  }
+  return true;
+}
+
 static int allreduce_host_impl(hvd_comm* c, const void* const* in, void* const* out, uint64_t count, int dtype, int op,
                        uint64_t chunk_bytes, void* stream) {
   int st = check_live(c);
@@ -1479,6 +1505,19 @@ static int allreduce_host_impl(hvd_comm* c, const void* const* in, void* const* 
   if (count == 0) return HVD_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   CK(cudaSetDevice(c->device));
+  if (c->host_zero_copy && c->fused && host_mapped(c, in, out, count * (uint64_t)esz)) {
+    // zero copy: pinned host memory the device addresses directly (UVA) — the kernels gather
+    // the gradients from it and scatter the results into it over PCIe, inside the ring
+    // itself: no staging, no copy pipeline fill or drain
+    std::vector<hvd_tensor> ti(c->nlocal), to(c->nlocal);
+    bool same = true;
+    for (int l = 0; l < c->nlocal; ++l) {
+      ti[l] = {const_cast<void*>(in[l]), count, (hvd_dtype)dtype, 0};
+      to[l] = {out[l], count, (hvd_dtype)dtype, 0};
+      same = same && in[l] == out[l];
+    }
+    return do_allreduce(c, ti.data(), 1, op, c->cap, s, 0, nullptr, same ? nullptr : to.data());
+  }
   uint64_t chunk = chunk_bytes ? chunk_bytes : (8ull << 20);
   chunk = std::max<uint64_t>(kChunkQuantum, chunk / kChunkQuantum * kChunkQuantum);
   chunk = std::min<uint64_t>(chunk, c->cap);
@@ -2023,6 +2062,10 @@ int hvd_set_config(hvd_comm* c, int key, int64_t value) {
         return HVD_ERR_INVALID;
       c->solo_stages = (int)value;
       return HVD_OK;
+    case HVD_CFG_HOST_ZERO_COPY:
+      if (value < 0 || value > 1) return HVD_ERR_INVALID;
+      c->host_zero_copy = (int)value;
+      return HVD_OK;
     case HVD_CFG_WATCHER:
       if (value < 0 || value > 1) return HVD_ERR_INVALID;
       c->watcher = (int)value;
@@ -2125,6 +2168,7 @@ int64_t hvd_get_config(const hvd_comm* c, int key) {
     case HVD_CFG_PACE_GBPS: return c->pace_gbps;
     case HVD_CFG_FUSED_PDL: return c->fused_pdl;
     case HVD_CFG_WATCHER: return c->watcher;
+    case HVD_CFG_HOST_ZERO_COPY: return c->host_zero_copy;
     case HVD_CFG_PACE_BURST_ROWS: return c->pace_burst_rows;
     case HVD_CFG_SOLO_STAGE_BYTES: return c->solo_stage_bytes;
     case HVD_CFG_BULK_STAGES: return c->bulk_stages;

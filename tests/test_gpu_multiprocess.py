@@ -87,12 +87,19 @@ def _worker(rank, world, port, cases, q, protocol):
                 torch.cuda.synchronize()
                 out.append([from_torch(t, dtype) for t in res_its])
             elif kind == "host":
+                # zero copy (the kernels read / write the pinned buffers over PCIe), then the
+                # staged H2D -> ring -> D2H pipeline (the default)
                 x = workloads.rank_tensor(counts[0], dtype, rank, 5, "normal")
                 hin = to_torch(x, dtype, device="cpu").pin_memory()
-                hout = torch.empty_like(hin).pin_memory()
-                comm.allreduce_host(hin, hout, op=op, chunk_bytes=thr)
-                torch.cuda.synchronize()
-                out.append([from_torch(hout, dtype)])
+                got = []
+                for zc in (1, 0):
+                    comm.set_config(hvd._lib.HVD_CFG_HOST_ZERO_COPY, zc)
+                    hout = torch.empty_like(hin).pin_memory()
+                    comm.allreduce_host(hin, hout, op=op, chunk_bytes=thr)
+                    torch.cuda.synchronize()
+                    got.append(from_torch(hout, dtype))
+                comm.set_config(hvd._lib.HVD_CFG_HOST_ZERO_COPY, 0)
+                out.append(got)
             elif kind == "negotiated":
                 # every rank reports the same ids in its own order over 3 cycles (R15)
                 g = hvd.negotiator(comm, max_tensors=64)
@@ -223,11 +230,14 @@ def test_multiprocess_ring_matches_oracle(protocol):
                     assert_same(res[r][0][ci][it], ref[r][0], dtype, f"mixed call {it} rank {r}")
         elif kind == "host":
             xs = [workloads.rank_tensor(counts[0], dtype, r, 5, "normal") for r in range(n)]
-            ce = thr // oracle.ELEM_SIZE[dtype]
+            ref, _, _ = oracle.allreduce([[x] for x in xs], [dtype], op)  # zero copy: one tensor
+            for r in range(n):
+                assert_same(res[r][0][ci][0], ref[r][0], dtype, f"host zero-copy rank {r}")
+            ce = thr // oracle.ELEM_SIZE[dtype]  # staged: chunk by chunk
             for off in range(0, counts[0], ce):
                 ref, _, _ = oracle.allreduce([[x[off:off + ce]] for x in xs], [dtype], op)
                 for r in range(n):
-                    assert_same(res[r][0][ci][0][off:off + ce], ref[r][0], dtype, f"host chunk@{off} rank {r}")
+                    assert_same(res[r][0][ci][1][off:off + ce], ref[r][0], dtype, f"host chunk@{off} rank {r}")
         elif kind == "negotiated":
             from oracle import negotiation as neg
             reports = [[[] for _ in range(n)] for _ in range(3)]

@@ -646,35 +646,46 @@ def test_negotiated_allreduce_cycles(hvd, n):
         g.close()
 
 
-@pytest.mark.parametrize("n", [1, 2, 3])
-def test_allreduce_host_pipelined_chunks(hvd, n):
-    """hvd_allreduce_host: pinned host buffers, chunked H2D -> ring -> D2H through 3 staging
-    slots; each chunk is reduced as one tensor, so it matches the oracle chunk by chunk."""
+@pytest.mark.parametrize("zero_copy", [1, 0])
+@pytest.mark.parametrize("n", [1, 2, 4])
+def test_allreduce_host(hvd, n, zero_copy):
+    """hvd_allreduce_host on pinned host buffers.  Zero copy (HVD_CFG_HOST_ZERO_COPY): the kernels gather
+    from and scatter into host memory, the call is hvd_allreduce of one tensor (oracle on
+    the whole tensor).  Staged: chunked H2D -> ring -> D2H through 3 slots, each chunk
+    reduced as one tensor (oracle chunk by chunk)."""
     comm = comm_for(hvd, n)
-    for dt, op, L, chunk in [("f32", "average", 1_000_003, 1 << 18), ("bf16", "average", 300_001, 1 << 16),
-                             ("i32", "sum", 77_777, 0), ("f32", "sum", 5, 256)]:
-        kind = "int_uniform" if dt == "i32" else "normal"
-        xs = [workloads.rank_tensor(L, dt, r, 3, kind) for r in range(n)]
-        hin = [to_torch(x, dt, device="cpu").pin_memory() for x in xs]
-        hout = [torch.empty_like(h).pin_memory() for h in hin]
-        comm.allreduce_host(hin, hout, op=op, chunk_bytes=chunk)
-        torch.cuda.synchronize()
-        assert comm.poll_error() == 0
-        esz = oracle.ELEM_SIZE[dt]
-        ce = (chunk or (8 << 20)) // esz
-        ce = max(256 // esz, ce // (256 // esz) * (256 // esz))
-        for off in range(0, L, ce):
-            part = [[x[off:off + ce]] for x in xs]
-            ref, _, _ = oracle.allreduce(part, [dt], op)
+    comm.set_config(hvd._lib.HVD_CFG_HOST_ZERO_COPY, zero_copy)
+    try:
+        for dt, op, L, chunk in [("f32", "average", 1_000_003, 1 << 18), ("bf16", "average", 300_001, 1 << 16),
+                                 ("i32", "sum", 77_777, 0), ("f32", "sum", 5, 256),
+                                 ("f32", "average", 20_000_001, 0)]:  # above 64 MiB: split into two buffers
+            kind = "int_uniform" if dt == "i32" else "normal"
+            xs = [workloads.rank_tensor(L, dt, r, 3, kind) for r in range(n)]
+            hin = [to_torch(x, dt, device="cpu").pin_memory() for x in xs]
+            hout = [torch.empty_like(h).pin_memory() for h in hin]
+            comm.allreduce_host(hin, hout, op=op, chunk_bytes=chunk)
+            torch.cuda.synchronize()
+            assert comm.poll_error() == 0
+            esz = oracle.ELEM_SIZE[dt]
+            if zero_copy:
+                ce = L
+            else:
+                ce = (chunk or (8 << 20)) // esz
+                ce = max(256 // esz, ce // (256 // esz) * (256 // esz))
+            for off in range(0, L, ce):
+                part = [[x[off:off + ce]] for x in xs]
+                ref, _, _ = oracle.allreduce(part, [dt], op)
+                for r in range(n):
+                    got = from_torch(hout[r][off:off + ce], dt)
+                    assert_same(got, ref[r][0], dt, f"{dt} chunk@{off} r={r} zc={zero_copy}")
+            for r in range(n):  # inputs untouched (out of place)
+                assert_same(from_torch(hin[r], dt), xs[r], dt)
+            comm.allreduce_host(hin, op=op, chunk_bytes=chunk)  # in place
+            torch.cuda.synchronize()
             for r in range(n):
-                got = from_torch(hout[r][off:off + ce], dt)
-                assert_same(got, ref[r][0], dt, f"{dt} chunk@{off} r={r}")
-        for r in range(n):  # inputs untouched (out of place)
-            assert_same(from_torch(hin[r], dt), xs[r], dt)
-        comm.allreduce_host(hin, op=op, chunk_bytes=chunk)  # in place
-        torch.cuda.synchronize()
-        for r in range(n):
-            assert np.array_equal(from_torch(hin[r], dt).view(np.uint8), from_torch(hout[r], dt).view(np.uint8))
+                assert np.array_equal(from_torch(hin[r], dt).view(np.uint8), from_torch(hout[r], dt).view(np.uint8))
+    finally:
+        comm.set_config(hvd._lib.HVD_CFG_HOST_ZERO_COPY, 0)
 
 
 @pytest.mark.parametrize("n", [2, 3, 4])
