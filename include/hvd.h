@@ -301,11 +301,16 @@ typedef enum {
   HVD_CFG_WATCHER = 29,      /* fused push: 1 = a lane of the signal warp watches the
                                 predecessor's counter and mirrors it in shared memory; the
                                 slice loop then waits on shared memory                      */
-  HVD_CFG_HOST_ZERO_COPY = 30 /* hvd_allreduce_host: 1 = when every buffer is pinned host
+  HVD_CFG_HOST_ZERO_COPY = 30, /* hvd_allreduce_host: 1 = when every buffer is pinned host
                                 memory the device addresses directly, the ring kernels gather
                                 from / scatter to it over PCIe (no staging copies); 0
                                 (default) = the staged H2D / ring / D2H pipeline, measured
                                 faster (64 MiB: N = 1 1.7 vs 1.9 ms, N = 4 3.9 vs 8.9 ms)   */
+  HVD_CFG_PREISSUE = 31      /* fused push: 1 = a slice that gathers the local gradient and adds
+                                the received partial issues its first gradient loads before
+                                waiting for the predecessor's signal; 0 = after; -1 (default)
+                                = on for N > 2 (64 MiB at N = 4: 165.4 -> 162.2 us; N = 2
+                                neutral)                                                   */
 } hvd_config_key;
 /* Set a tuning knob; every rank must set identical values.  Errors: INVALID. */
 int hvd_set_config(hvd_comm* c, int key, int64_t value);

@@ -852,6 +852,33 @@ template <> struct WireCvt<4, 2> {  // bf16 tensor, fp32 wire
 // Handshake to complete inside a slice (the launch's first remote push): the
 // slice's first loads are issued, then the leader waits for the successor's
 // ready flag while they fly.
+// The fused kernel's wait for the predecessor's counter: through the watcher's shared
+// copy when the watcher runs, else a system-scope spin on the counter itself.
+__device__ __forceinline__ bool dep_wait(const RingParams& R, const unsigned long long* s_flag,
+                                         const unsigned long long* flag, unsigned long long target) {
+  if (!R.watcher) return spin_until(flag, target, R.err, R.timeout_ns);
+  if (ld_acquire_cta_shared64(s_flag) >= target) return true;
+  const unsigned long long t0 = globaltimer();
+  unsigned spins = 0;
+  while (ld_acquire_cta_shared64(s_flag) < target) {
+    if ((++spins & 1023u) == 0) {
+      if (globaltimer() - t0 > R.timeout_ns || *(volatile int*)R.err != 0) {
+        raise_err(R.err, kHvdErrTimeout);
+        return false;
+      }
+    }
+  }
+  return true;
+}
+
+struct DepWait {  // the ring dependency of a slice, waited for inside fused_slice
+  const RingParams* R;
+  const unsigned long long* s_flag;  // watcher's shared copy
+  const unsigned long long* flag;    // the predecessor's counter
+  unsigned long long target;
+  int* abort;                        // shared abort flag of the CTA
+};
+
 struct Handshake {
   const unsigned long long* flag;  // nullptr: none
   const unsigned long long* hash_flag;  // the successor's call hash, written before its flag
@@ -866,7 +893,8 @@ template <class Op, int KIND, int TESZ = Op::kEsz>
 __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& me, unsigned long long lo,
                                             unsigned long long hi, unsigned tid, unsigned nthr, SegCache& sc,
                                             Raw32* slots0, uint4* slots1, long long pv = 0,
-                                            const Handshake* hs = nullptr, long long* vft = nullptr) {
+                                            const Handshake* hs = nullptr, long long* vft = nullptr,
+                                            const DepWait* dep = nullptr) {
   // pv: shift from a buffer vector index to its slot in the channel-private layout of
   // the scratch / fusion-buffer regions (0: buffer order)
   constexpr int ESZ = Op::kEsz;  // wire element size
@@ -883,7 +911,7 @@ __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& m
   constexpr bool TO_NBUF = KIND == kF_AG0 || KIND == kF_AG || KIND == kF_G2B || KIND == kF_G2BS;
   const unsigned long long v_lo = lo / VEL;
   const unsigned long long v_hi = (hi + VEL - 1) / VEL;
-  if (!hs && v_hi <= v_lo + tid) return;  // (with a handshake every thread reaches its barrier)
+  if (!hs && !dep && v_hi <= v_lo + tid) return;  // (with a wait inside every thread reaches its barrier)
   const int rows = v_hi <= v_lo + tid ? 0 : (int)((v_hi - v_lo - tid + nthr - 1) / nthr);  // rows this thread owns
   SegCache ci = sc;  // issue-side cache (runs kPipe-1 rows ahead of the consume side)
   auto issue = [&](int j) {
@@ -903,9 +931,38 @@ __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& m
     }
     cp_async_commit();  // one group per row, possibly empty: keeps wait_group counting uniform
   };
-#pragma unroll
-  for (int j = 0; j < kPipe - 1; ++j) issue(j);
   int nrows = rows;
+  if (GATHER && ADD && dep) {
+    // the ring dependency is waited for here, after this op's first gradient loads are in
+    // flight: only the received partials (scratch) must wait for the predecessor
+    auto issue_a = [&](int j) {
+      if (j < rows) {
+        const unsigned long long v = v_lo + (unsigned long long)j * nthr + tid;
+        seg_lookup<TESZ>(F, v, ci);
+        const unsigned long long e = v * VEL;
+        const unsigned long long left = ci.end_el > e ? ci.end_el - e : 0;
+        const char* tp = reinterpret_cast<const char*>(ci.g + e * TESZ);
+        if (Cvt::fast(tp, left)) Cvt::issue(slots0 + (j % kPipe) * nthr + tid, tp);
+      }
+    };
+#pragma unroll
+    for (int j = 0; j < kPipe - 1; ++j) issue_a(j);  // uncommitted: they join row 0's group
+    if (tid == 0 && !*(volatile int*)dep->abort && !dep_wait(*dep->R, dep->s_flag, dep->flag, dep->target))
+      *(volatile int*)dep->abort = 1;
+    bar_sync(kBarData, nthr);
+    if (*(volatile int*)dep->abort) nrows = 0;
+#pragma unroll
+    for (int j = 0; j < kPipe - 1; ++j) {
+      if (j < rows) {
+        const unsigned long long v = v_lo + (unsigned long long)j * nthr + tid;
+        cp_async16(slots1 + (j % kPipe) * nthr + tid, F.scr + (v + pv) * 16);
+      }
+      cp_async_commit();
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kPipe - 1; ++j) issue(j);
+  }
   if (hs) {
     if (tid == 0) {
       if (!spin_until(hs->flag, hs->epoch, hs->err, hs->timeout_ns)) {
@@ -948,25 +1005,6 @@ __device__ __forceinline__ void fused_slice(const FusedCtx& F, const RingRank& m
     if (RSCATTER) Cvt::put(reinterpret_cast<char*>(sc.rd + e * TESZ), left, x);
   }
   cp_async_wait<0>();
-}
-
-// The fused kernel's wait for the predecessor's counter: through the watcher's shared
-// copy when the watcher runs, else a system-scope spin on the counter itself.
-__device__ __forceinline__ bool dep_wait(const RingParams& R, const unsigned long long* s_flag,
-                                         const unsigned long long* flag, unsigned long long target) {
-  if (!R.watcher) return spin_until(flag, target, R.err, R.timeout_ns);
-  if (ld_acquire_cta_shared64(s_flag) >= target) return true;
-  const unsigned long long t0 = globaltimer();
-  unsigned spins = 0;
-  while (ld_acquire_cta_shared64(s_flag) < target) {
-    if ((++spins & 1023u) == 0) {
-      if (globaltimer() - t0 > R.timeout_ns || *(volatile int*)R.err != 0) {
-        raise_err(R.err, kHvdErrTimeout);
-        return false;
-      }
-    }
-  }
-  return true;
 }
 
 // j-th operation of a fused launch -> (iteration t, slice k).  Iterations
@@ -1131,6 +1169,7 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
   const Handshake hs0 = {me.rflags + ch, me.rhash + ch, R.hash, R.epoch, R.err, R.timeout_ns, &s_abort};
   bool hs_pending = true;
   long long vft = 0;  // pacing: virtual finish time of this thread's last paced row
+  unsigned long long dep_next = 0;  // PREISSUE: the next op's dependency, waited for in its slice
   for (int b = 0; b < P.nbuf; ++b) {
     const BufDesc& D = P.bufs[b];
     const int cg = chan_of(D, ch, gridDim.x);  // this channel's index in the buffer's geometry
@@ -1189,6 +1228,13 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
         bar_sync(kBarData, nd);
       }
       const unsigned long long tb = tl_d ? globaltimer() : 0;
+      const DepWait dw = {&R, &s_flag, me.flags + ch, dep_next, &s_abort};
+      const DepWait* dep = dep_next ? &dw : nullptr;
+      if (dep && !(hi > lo && !s_abort)) {  // no data here: the wait still orders this op
+        if (tid == 0 && !s_abort && !dep_wait(R, &s_flag, me.flags + ch, dep_next)) s_abort = 1;
+        bar_sync(kBarData, nd);
+      }
+      dep_next = 0;
       if (hi > lo && !s_abort) {
         const Handshake* hs = nullptr;
         if (hs_pending && t < T) {  // every op but the final local scatter pushes
@@ -1197,14 +1243,14 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
         }
         if (P.registered) {
           if (rs && s == 0) fused_slice<Op, kF_RS0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs, &vft);
-          else if (rs) fused_slice<Op, kF_RS, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs, &vft);
-          else if (s == 0) fused_slice<Op, kF_RAG0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs, &vft);
+          else if (rs) fused_slice<Op, kF_RS, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs, &vft, dep);
+          else if (s == 0) fused_slice<Op, kF_RAG0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs, &vft, dep);
           else fused_slice<Op, kF_RAG, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs, &vft);
         } else {
           if (t == T) fused_slice<Op, kF_FIN, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv);
           else if (rs && s == 0) fused_slice<Op, kF_RS0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs, &vft);
-          else if (rs) fused_slice<Op, kF_RS, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs, &vft);
-          else if (s == 0) fused_slice<Op, kF_AG0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs, &vft);
+          else if (rs) fused_slice<Op, kF_RS, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs, &vft, dep);
+          else if (s == 0) fused_slice<Op, kF_AG0, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs, &vft, dep);
           else fused_slice<Op, kF_AG, TESZ>(F, me, lo, hi, tid, nd, sc, slots0, slots1, pv, hs, &vft);
         }
         if (t < T) sent += (hi - lo) * Op::kEsz;
@@ -1228,12 +1274,16 @@ __global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_co
           fused_op(j + 1, K, T, R.fin_lag, tn, kn);
         }
       }
+      const unsigned long long target = tn > 0 ? bbase + (unsigned long long)(tn - 1) * K + kn + 1 : 0;
+      // HVD_CFG_PREISSUE: an op that gathers the local gradient and adds the received partial
+      // waits for its dependency inside the slice, after its first gradient loads are issued
+      const bool inslice = R.preissue && target && tn <= N - 1;
       if (tid == 0) {
         if (t < T) st_release_cta_shared(&s_done, i);
-        const unsigned long long target = tn > 0 ? bbase + (unsigned long long)(tn - 1) * K + kn + 1 : 0;
-        if (target && !s_abort && !dep_wait(R, &s_flag, me.flags + ch, target)) s_abort = 1;
+        if (target && !inslice && !s_abort && !dep_wait(R, &s_flag, me.flags + ch, target)) s_abort = 1;
       }
-      if (tn > 0) bar_sync(kBarData, nd);
+      if (tn > 0 && !inslice) bar_sync(kBarData, nd);
+      dep_next = inslice ? target : 0;
     }
     bbase += (unsigned long long)T * K;
   }

@@ -203,7 +203,7 @@ def test_tuning_knobs_keep_bits(hvd):
         comm.set_config(L.HVD_CFG_SLICE_BYTES, 0)
         comm.set_config(L.HVD_CFG_THREADS, 256)
         for key, val in ((L.HVD_CFG_PACE_GBPS, 300), (L.HVD_CFG_PACE_BURST_ROWS, 0), (L.HVD_CFG_FUSED_PDL, 1),
-                         (L.HVD_CFG_WATCHER, 1)):
+                         (L.HVD_CFG_WATCHER, 1), (L.HVD_CFG_PREISSUE, 1), (L.HVD_CFG_WATCHER, 0)):
             comm.set_config(key, val)
             for _ in range(2):  # back to back (PDL overlaps the launches)
                 ts = [[to_torch(x, "f32") for x in xs[r]] for r in range(n)]
