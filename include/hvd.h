@@ -306,11 +306,14 @@ typedef enum {
                                 from / scatter to it over PCIe (no staging copies); 0
                                 (default) = the staged H2D / ring / D2H pipeline, measured
                                 faster (64 MiB: N = 1 1.7 vs 1.9 ms, N = 4 3.9 vs 8.9 ms)   */
-  HVD_CFG_PREISSUE = 31      /* fused push: 1 = a slice that gathers the local gradient and adds
+  HVD_CFG_PREISSUE = 31,     /* fused push: 1 = a slice that gathers the local gradient and adds
                                 the received partial issues its first gradient loads before
                                 waiting for the predecessor's signal; 0 = after; -1 (default)
                                 = on for N > 2 (64 MiB at N = 4: 165.4 -> 162.2 us; N = 2
                                 neutral)                                                   */
+  HVD_CFG_LL_PDL = 32        /* LL / LL128 launches: programmatic dependent launch (back-to-back
+                                small calls overlap the next launch with this one's tail);
+                                default 1 (N = 4, <= 1 MiB: 1-7 % lower latency)           */
 } hvd_config_key;
 /* Set a tuning knob; every rank must set identical values.  Errors: INVALID. */
 int hvd_set_config(hvd_comm* c, int key, int64_t value);

@@ -103,6 +103,7 @@ struct RingParams {
   unsigned long long exits_target;  // pull protocol: cumulative CTA exits after this call
   int watcher;                  // fused: dependency watcher lane (HVD_CFG_WATCHER)
   int preissue;                 // fused: gather loads before the dependency wait (HVD_CFG_PREISSUE)
+  int ll_pdl;                   // LL / LL128: programmatic dependent launch (HVD_CFG_LL_PDL)
   int pdl;                      // fused: programmatic dependent launch (HVD_CFG_FUSED_PDL: 0 off,
                                 //   1 with the cooperative launch, 2 instead of it; one local rank only)
   unsigned pace_cyc;            // fused: ns per row of remote stores per channel (0 = unpaced)

@@ -1709,6 +1709,10 @@ __device__ __forceinline__ bool ll_load(const unsigned long long* p, unsigned fl
 
 template <class Op>
 __global__ void __launch_bounds__(256) ll_allreduce_kernel(const __grid_constant__ FusedParams P) {
+  if (P.ring.ll_pdl) {  // HVD_CFG_LL_PDL: the next launch may be scheduled; memory after the previous grid
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   JtGuard jtg(P.ring.jt);
   constexpr int ESZ = Op::kEsz;
   constexpr int VEL = 16 / ESZ;
@@ -1810,6 +1814,10 @@ __device__ __forceinline__ void put_half(char* p, unsigned long long left, const
 
 template <class Op>
 __global__ void __launch_bounds__(256) ll128_allreduce_kernel(const __grid_constant__ FusedParams P) {
+  if (P.ring.ll_pdl) {  // HVD_CFG_LL_PDL: the next launch may be scheduled; memory after the previous grid
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   JtGuard jtg(P.ring.jt);
   constexpr int ESZ = Op::kEsz;
   constexpr int VEL = 16 / ESZ;
@@ -3072,11 +3080,13 @@ static cudaError_t launch_ll_t(const FusedParams& p, int nch, int nlocal, cudaSt
   cfg.gridDim = dim3(nch, nlocal);
   cfg.blockDim = dim3(256);
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;  // CTAs of all ranks wait on each other's words
   attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = p.ring.ll_pdl ? 2 : 1;
   ++g_launched;
   return cudaLaunchKernelEx(&cfg, ll_allreduce_kernel<Op>, p);
 }
@@ -3087,11 +3097,13 @@ static cudaError_t launch_ll128_t(const FusedParams& p, int nch, int nlocal, cud
   cfg.gridDim = dim3(nch, nlocal);
   cfg.blockDim = dim3(256);
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;  // CTAs of all ranks wait on each other's lines
   attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = p.ring.ll_pdl ? 2 : 1;
   ++g_launched;
   return cudaLaunchKernelEx(&cfg, ll128_allreduce_kernel<Op>, p);
 }

@@ -125,6 +125,7 @@ struct hvd_comm {
   int watcher = 0;                  // HVD_CFG_WATCHER
   int host_zero_copy = 0;           // HVD_CFG_HOST_ZERO_COPY (measured slower: off)
   int preissue = -1;                // HVD_CFG_PREISSUE (-1: on for N > 2, measured +2 % at N = 4)
+  int ll_pdl = 1;                   // HVD_CFG_LL_PDL (N = 4 <= 1 MiB: 1-7 % lower latency; N = 2 neutral)
   int pace_burst_rows = 2;          // HVD_CFG_PACE_BURST_ROWS
   int clock_khz = 1965000;          // SM clock (cudaDevAttrClockRate): pacing cycles
   unsigned long long pbase[kMaxChannels] = {};  // pull-protocol progress counter bases
@@ -574,6 +575,7 @@ int make_ring_params(hvd_comm* c, uint64_t L, int dtype, bool fused, RingParams*
   P->fin_lag = c->fin_lag;
   P->pdl = fused ? c->fused_pdl : 0;
   P->preissue = fused ? (c->preissue < 0 ? (c->size > 2 ? 1 : 0) : c->preissue) : 0;
+  P->ll_pdl = c->ll_pdl;
   // the watcher is one more warp: only while the block stays within the kernel's 416 threads
   P->watcher = fused && c->watcher && c->threads + 32 * (P->sig_warps + 1) <= kMaxRingThreads + 32 ? 1 : 0;
   if (fused && c->pace_gbps > 0 && c->size > 1) {
@@ -2064,6 +2066,10 @@ int hvd_set_config(hvd_comm* c, int key, int64_t value) {
         return HVD_ERR_INVALID;
       c->solo_stages = (int)value;
       return HVD_OK;
+    case HVD_CFG_LL_PDL:
+      if (value < 0 || value > 1) return HVD_ERR_INVALID;
+      c->ll_pdl = (int)value;
+      return HVD_OK;
     case HVD_CFG_PREISSUE:
       if (value < -1 || value > 1) return HVD_ERR_INVALID;
       c->preissue = (int)value;
@@ -2176,6 +2182,7 @@ int64_t hvd_get_config(const hvd_comm* c, int key) {
     case HVD_CFG_WATCHER: return c->watcher;
     case HVD_CFG_HOST_ZERO_COPY: return c->host_zero_copy;
     case HVD_CFG_PREISSUE: return c->preissue;
+    case HVD_CFG_LL_PDL: return c->ll_pdl;
     case HVD_CFG_PACE_BURST_ROWS: return c->pace_burst_rows;
     case HVD_CFG_SOLO_STAGE_BYTES: return c->solo_stage_bytes;
     case HVD_CFG_BULK_STAGES: return c->bulk_stages;

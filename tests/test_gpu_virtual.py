@@ -203,7 +203,8 @@ def test_tuning_knobs_keep_bits(hvd):
         comm.set_config(L.HVD_CFG_SLICE_BYTES, 0)
         comm.set_config(L.HVD_CFG_THREADS, 256)
         for key, val in ((L.HVD_CFG_PACE_GBPS, 300), (L.HVD_CFG_PACE_BURST_ROWS, 0), (L.HVD_CFG_FUSED_PDL, 1),
-                         (L.HVD_CFG_WATCHER, 1), (L.HVD_CFG_PREISSUE, 1), (L.HVD_CFG_WATCHER, 0)):
+                         (L.HVD_CFG_WATCHER, 1), (L.HVD_CFG_PREISSUE, 1), (L.HVD_CFG_WATCHER, 0),
+                         (L.HVD_CFG_LL_PDL, 1)):
             comm.set_config(key, val)
             for _ in range(2):  # back to back (PDL overlaps the launches)
                 ts = [[to_torch(x, "f32") for x in xs[r]] for r in range(n)]
@@ -215,6 +216,35 @@ def test_tuning_knobs_keep_bits(hvd):
                     assert_same(from_torch(ts[r][k], "f32"), ref[r][k], "f32", f"knob {key}={val}")
     finally:
         comm.finalize()
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_ll_pdl_back_to_back(hvd, n):
+    """HVD_CFG_LL_PDL: LL and LL128 launches back to back without host syncs, each launch
+    scheduled while the previous one drains; same bits as the oracle."""
+    comm = comm_for(hvd, n)
+    L = hvd._lib
+    comm.set_config(L.HVD_CFG_LL_PDL, 1)  # (the default)
+    try:
+        cases = [[1000, 3001], [300_001], [7], [1_000_003], [65_536, 5]]
+        runs = []
+        for it in range(2):
+            for k, counts in enumerate(cases):
+                xs = workloads.all_ranks(counts, "f32", n, seed=500 + 10 * it + k)
+                ts = [[to_torch(x, "f32") for x in xs[r]] for r in range(n)]
+                comm.allreduce(ts, op="average")
+                runs.append((xs, ts, counts))
+        torch.cuda.synchronize()
+        assert comm.poll_error() == 0
+        st = comm.kernel_stats()
+        assert st["ll"][0] >= 1 and st["ll128"][0] >= 1
+        for xs, ts, counts in runs:
+            ref, _, _ = oracle.allreduce(xs, ["f32"] * len(counts), "average")
+            for r in range(n):
+                for k in range(len(counts)):
+                    assert_same(from_torch(ts[r][k], "f32"), ref[r][k], "f32", f"{counts} r={r} k={k}")
+    finally:
+        comm.set_config(L.HVD_CFG_LL_PDL, 1)
 
 
 def test_errors_on_device(hvd):

@@ -57,7 +57,7 @@ def main():
                          ("BULK_STAGE_BYTES", 16384), ("BULK_DEPTH", 1), ("BULK_CHANNELS", 148),
                          ("BULK_SLICE_BYTES", 65536), ("SIGNAL_WARPS", 1), ("WINDOW", 2), ("SLICE_BYTES", 0),
                          ("CHANNELS", 128), ("LL128_MAX_BYTES", 24 << 20 if world == 2 else 48 << 20),
-                         ("PACE_GBPS", 0), ("PACE_BURST_ROWS", 2), ("FUSED_PDL", 0), ("WATCHER", 0), ("PREISSUE", -1)):  # defaults, then the point's settings
+                         ("PACE_GBPS", 0), ("PACE_BURST_ROWS", 2), ("FUSED_PDL", 0), ("WATCHER", 0), ("PREISSUE", -1), ("LL_PDL", 1)):  # defaults, then the point's settings
                 comm.set_config(getattr(L, "HVD_CFG_" + k), v)
             for k, v in cfg:
                 comm.set_config(getattr(L, "HVD_CFG_" + k), int(v))
