@@ -51,7 +51,7 @@ def main():
     rows["device_allreduce_64MiB_ms"] = timed(lambda: comm.allreduce_average([dev]))
     for ll128 in (1, 0):
         comm.set_config(L.HVD_CFG_LL128_MAX_BYTES, (16 << 20 if world == 2 else 32 << 20) if ll128 else 0)
-        for chunk in (4 << 20, 8 << 20, 16 << 20, 32 << 20, 64 << 20):
+        for chunk in (1 << 20, 2 << 20, 4 << 20, 8 << 20, 16 << 20, 32 << 20, 64 << 20):
             rows[f"e2e_ms_chunk{chunk >> 20}MiB_ll128{ll128}"] = timed(
                 lambda: comm.allreduce_host(hin, hout, op="average", chunk_bytes=chunk))
     t0 = time.perf_counter()
