@@ -1,4 +1,4 @@
-"""Summarise the ncu range captures of tools/r02_call13.sh (gpurun_out/nvlink/range_n*_p*_*.csv
+"""Summarise the ncu range captures of tools/r02/c13_nvlink_counters.sh (gpurun_out/nvlink/range_n*_p*_*.csv
 + the matching oneproc_*.json) into profiles/r02_nvlink_counters.json, per launch:
 NVLink TX/RX user and protocol bytes on device 0 (rank 0), DRAM bytes, and the ratio of
 user bytes to the algorithmic (2L - |c_{r+1}| - |c_{r+2}|) * esz of SURVEY §8(d)."""
