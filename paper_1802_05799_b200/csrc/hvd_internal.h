@@ -168,7 +168,10 @@ constexpr int kMaxMultiBufs = 96;    // fusion buffers per fused launch (kernel 
 
 // Fused zero-copy allreduce of one fusion buffer (pack + ring + unpack in one launch).
 constexpr int kFusedSmemSegs = 4096;  // member-offset table cached in shared memory up to this size
-constexpr int kPipe = 8;              // cp.async prefetch depth (rows of 16 B per data thread)
+#ifndef HVD_PIPE
+#define HVD_PIPE 8
+#endif
+constexpr int kPipe = HVD_PIPE;       // cp.async prefetch depth (rows of 16 B per data thread)
 constexpr int kMaxRingThreads = 384;  // data threads per ring / fused CTA
 inline size_t pull_smem_bytes(int nseg) {
   const size_t vb = nseg <= kFusedSmemSegs ? (size_t)(nseg + 15) / 16 * 16 * 8 : 0;
