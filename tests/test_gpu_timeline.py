@@ -161,3 +161,29 @@ def test_job_trace_env_var_solo(tmp_path):
     assert summ[0]["kernels"] == {"SOLO": 3}
     start = [e for e in ev if e["name"] == "TIMELINE_START"]
     assert len(start) == 1 and start[0]["args"]["clock_uncertainty_us"] < 1000
+
+
+def test_job_trace_accounts_for_every_launch(hvd, tmp_path):
+    """Thousands of back-to-back launches without a host sync: every launch is either in the
+    trace or counted as dropped (the host slots hold 4096 launches in flight)."""
+    from paper_1802_05799_b200 import timeline
+    n = 2
+    path = str(tmp_path / "many.json")
+    comm = hvd.init_virtual(n, 0, 64 << 20)
+    try:
+        comm.timeline_start(path)
+        xs = [[torch.ones(1000, device="cuda")] for _ in range(n)]
+        calls = 5000
+        for _ in range(calls):
+            comm.allreduce(xs, "sum")
+        launched, dropped = comm.timeline_flush()
+        comm.timeline_stop()
+        assert comm.poll_error() == 0
+    finally:
+        comm.finalize()
+    assert launched == calls
+    ev = timeline.load_trace(path)
+    summ = timeline.validate_trace(ev) if dropped == 0 else timeline.job_summary(ev)
+    for r in range(n):
+        assert summ[r]["calls"] == {"ALLREDUCE": calls}
+        assert sum(summ[r]["kernels"].values()) + dropped == calls
