@@ -294,7 +294,14 @@ def run_ours(args):
     cap = args.workload == "fp32_64MiB"
     roof["traffic"] = _ncu_traffic(roof["kernel"], n) if cap else None
     if n > 1:
-        roof["nvlink_counters"] = _ncu_profile(roof["kernel"], n, "nvlink") if cap else None
+        nvc = _ncu_profile(roof["kernel"], n, "nvlink") if cap else None
+        roof["nvlink_counters"] = nvc
+        if nvc and roof["bound"] == "nvlink":
+            # wire bytes on the link per launch = user (= algorithmic) bytes x (1 + the link's
+            # measured protocol share): against the 900 GB/s raw per-direction NVLink rate
+            wire = roof["achieved"] * nvc["user_over_algorithmic"] * (1 + nvc["protocol_over_user"])
+            roof["wire_GBps"] = wire
+            roof["frac_of_raw_link_900"] = wire / NVLINK_NOMINAL_GBPS
     roof["share_of_step"] = dev_ms / ms_prof_local if ms_prof_local else None
     roof["timing"] = (("achieved: the dominant kernel is the only kernel of the step, so its average launch "
                        "duration = the timed region's CUDA events (max over ranks) / its launches. " if only_dom else
