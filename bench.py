@@ -164,7 +164,7 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("gloo")
-    comm = hvd.init(fusion_bytes=64 * MIB, device=local)
+    comm = hvd.init(fusion_bytes=64 * MIB, device=local, pull_buffers="PROTOCOL=0" in args.config)
     for kv in args.config:
         k, v = kv.split("=")
         comm.set_config(getattr(hvd._lib, "HVD_CFG_" + k), int(v))

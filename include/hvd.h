@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define HVD_ABI_VERSION 2
+#define HVD_ABI_VERSION 3
 
 typedef enum {
   HVD_OK = 0,
@@ -84,11 +84,13 @@ typedef struct hvd_comm hvd_comm; /* opaque */
 /* Create the comm of ring rank `rank` of `size` on CUDA device `device` and
  * allocate its fusion buffer of `fusion_bytes` (0 = default 64 MiB, P:L368-369;
  * rounded up to 4 KiB).  One device region holds it together with two
- * reduce-scatter scratch halves, two pull-protocol buffers, the signal / ready
- * / hash words and the LL region.  Each region buffer is sized 3x the capacity
- * (capacity <= 256 MiB) so that the buffers of a multi-buffer call fit side by
- * side, plus a 320 MiB LL / LL128 region: about 1.3 GB at the default.  For size > 1 the comm must then
- * exchange blobs and hvd_connect().
+ * reduce-scatter scratch halves, the signal / ready / hash words and the LL
+ * region.  Each region buffer is sized 3x the capacity (capacity <= 256 MiB) so
+ * that the buffers of a multi-buffer call fit side by side, plus a 416 MiB LL /
+ * LL128 region: 998 MiB at the default.  The pull protocol's two buffers (2 x
+ * 194 MiB) are allocated only when it is enabled (HVD_CFG_PULL_BUFFERS; the
+ * environment variable HVD_PULL_BUFFERS=1 sets it at init).  For size > 1 the
+ * comm must then exchange blobs and hvd_connect().
  * Errors: INVALID (size < 1, rank out of range, null out), CUDA. */
 int hvd_init(int rank, int size, int device, uint64_t fusion_bytes, hvd_comm** out);
 
@@ -265,7 +267,9 @@ typedef enum {
                                 through shared memory (cp.async.bulk loads and stores into
                                 the successor's HBM), only for calls whose tensors share the
                                 wire dtype; 1 push — SM stores into the successor's HBM;
-                                0 pull — each rank TMA-loads its predecessor's partials.
+                                0 pull — each rank TMA-loads its predecessor's partials
+                                (needs HVD_CFG_PULL_BUFFERS: virtual mode allocates them
+                                here, a real rank returns INVALID without them).
                                 Same ring order, same bits.                                 */
   HVD_CFG_BULK_STAGES = 16,  /* bulk push: shared-memory stages per CTA (2..8)                */
   HVD_CFG_BULK_STAGE_BYTES = 17, /* bulk push: bytes per stage (4 KiB..64 KiB, multiple of 1 KiB) */
@@ -311,9 +315,16 @@ typedef enum {
                                 waiting for the predecessor's signal; 0 = after; -1 (default)
                                 = on for N > 2 (64 MiB at N = 4: 165.4 -> 162.2 us; N = 2
                                 neutral)                                                   */
-  HVD_CFG_LL_PDL = 32        /* LL / LL128 launches: programmatic dependent launch (back-to-back
+  HVD_CFG_LL_PDL = 32,       /* LL / LL128 launches: programmatic dependent launch (back-to-back
                                 small calls overlap the next launch with this one's tail);
                                 default 1 (N = 4, <= 1 MiB: 1-7 % lower latency)           */
+  HVD_CFG_PULL_BUFFERS = 33  /* 1 = allocate the pull protocol's two buffers (2 x the region
+                                buffer size, a separate device allocation) so that
+                                HVD_CFG_PROTOCOL = 0 can be chosen.  Real ranks: set before
+                                hvd_get_ipc_blob, identically on every rank (hvd_connect
+                                returns INVALID otherwise); virtual mode: any time.  Default 0
+                                (the environment variable HVD_PULL_BUFFERS=1 at init: 1).
+                                Cannot be turned off once allocated (INVALID).              */
 } hvd_config_key;
 /* Set a tuning knob; every rank must set identical values.  Errors: INVALID. */
 int hvd_set_config(hvd_comm* c, int key, int64_t value);

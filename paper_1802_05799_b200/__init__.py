@@ -461,13 +461,16 @@ def exchange_blobs(blob: bytes, group=None):
     return out
 
 
-def init(fusion_bytes: int = DEFAULT_FUSION_BYTES, device: int | None = None, group=None) -> Comm:
+def init(fusion_bytes: int = DEFAULT_FUSION_BYTES, device: int | None = None, group=None,
+         pull_buffers: bool = False) -> Comm:
     """``hvd.init()`` for one process per GPU.
 
     Reads RANK / WORLD_SIZE / LOCAL_RANK from the environment (torchrun), pins
     the GPU to the local rank, allocates the buffers and maps the
     ring successor through CUDA IPC; blobs travel over ``group`` (a gloo group
-    is created if torch.distributed is not initialised).
+    is created if torch.distributed is not initialised).  ``pull_buffers`` also
+    allocates the pull protocol's buffers (HVD_CFG_PULL_BUFFERS, needed for
+    HVD_CFG_PROTOCOL = 0); every rank must pass the same value.
     """
     import torch
     import torch.distributed as dist
@@ -479,6 +482,8 @@ def init(fusion_bytes: int = DEFAULT_FUSION_BYTES, device: int | None = None, gr
     h = C.c_void_p()
     check(lib.hvd_init(rank, world, device, int(fusion_bytes), C.byref(h)), "hvd_init")
     comm = Comm(h, device)
+    if pull_buffers:
+        comm.set_config(_lib.HVD_CFG_PULL_BUFFERS, 1)
     if world > 1:
         if not dist.is_initialized():
             dist.init_process_group("gloo")

@@ -45,6 +45,9 @@ struct Blob {
   char pci[32];  // PCI bus id of the rank's GPU (NVLink check of the ring links)
   uint64_t region_addr;  // region address in the owner process (a rank in the SAME process
                          // maps it by peer access: CUDA IPC cannot open its own handles)
+  int32_t has_pull, pad;       // pull protocol buffers allocated (HVD_CFG_PULL_BUFFERS)
+  cudaIpcMemHandle_t pull_handle;
+  uint64_t pull_addr;
 };
 
 struct DevPlanBuffer {
@@ -82,6 +85,12 @@ struct hvd_comm {
   uint64_t cap = 0;    // fusion capacity (plans, limits)
   uint64_t bufsz = 0;  // bytes of each region buffer (cap + slack)
   char* region[kMaxLocal] = {};
+  char* pull_mem[kMaxLocal] = {};  // pull protocol: [pull 0][pull 1], bufsz each (lazy)
+  const char* pred_pull = nullptr; // predecessor's pull buffers, real mode
+  bool pred_pull_ipc = false;
+  bool want_pull = false;          // real mode: allocate pull buffers at hvd_get_ipc_blob
+  bool pull_ok = false;            // every rank's pull buffers are mapped: protocol 0 usable
+  bool blob_out = false;           // real mode: the IPC blob was exported
   char* peer_region = nullptr;   // successor's region (IPC mapped), real mode
   char* pred_region = nullptr;   // predecessor's region (IPC mapped), real mode
   bool peer_ipc = false, pred_ipc = false;  // mapped by IPC (else: same process, peer access)
@@ -168,17 +177,18 @@ int cuda_fail(cudaError_t e, const char* what) {
     if (_st != HVD_OK) return _st;                  \
   } while (0)
 
-// Region: [fusion buffer][RS scratch][pull buffer 0][pull buffer 1][tail]; each
-// buffer is `bufsz` = capacity + slack bytes (the slack absorbs the quantum rounding
-// of the channel-private layout).  `cap` arguments below are bufsz.
+// Region: [fusion buffer][RS scratch 0][RS scratch 1][tail][LL]; each buffer is
+// `bufsz` = kRegionFactor x capacity + slack bytes (the slack absorbs the quantum
+// rounding of the channel-private layout).  `cap` arguments below are bufsz.  scratch1
+// is the second reduce-scatter receive half (a channel alternates halves buffer by
+// buffer).  The pull protocol's two buffers are a separate allocation made only when
+// that protocol is enabled (HVD_CFG_PULL_BUFFERS).
 constexpr uint64_t kRegionSlack = 2ull << 20;
 constexpr uint64_t kRegionFactor = 3;
-// [buf][scratch][pull0][pull1][scratch1][tail][LL]: scratch1 is the second
-// reduce-scatter receive half (a channel alternates halves buffer by buffer).
-constexpr uint64_t kNumBufs = 5;
+constexpr uint64_t kNumBufs = 3;
 char* buf_of(char* region) { return region; }
 char* scratch_of(char* region, uint64_t cap) { return region + cap; }
-char* scratch1_of(char* region, uint64_t cap) { return region + 4 * cap; }
+char* scratch1_of(char* region, uint64_t cap) { return region + 2 * cap; }
 unsigned long long* flags_of(char* region, uint64_t cap) {
   return reinterpret_cast<unsigned long long*>(region + kNumBufs * cap);
 }
@@ -193,7 +203,6 @@ unsigned long long* rhash_of(char* region, uint64_t cap) { return tail_of(region
 unsigned long long* pflags_of(char* region, uint64_t cap) { return tail_of(region, cap) + 1024; }
 unsigned long long* done_of(char* region, uint64_t cap) { return tail_of(region, cap) + 1536; }
 unsigned long long* exits_of(char* region, uint64_t cap) { return tail_of(region, cap) + 1537; }
-char* pull_of(char* region, uint64_t cap, int p) { return region + (2 + p) * cap; }
 unsigned long long* ll_of(char* region, uint64_t cap) {
   return reinterpret_cast<unsigned long long*>(region + kNumBufs * cap + kTailBytes);
 }
@@ -230,8 +239,6 @@ int common_init(hvd_comm* c, uint64_t fusion_bytes) {
     r.stats = stats_of(c->region[l], bz);
     r.rflags = rflags_of(c->region[l], bz);
     r.rhash = rhash_of(c->region[l], bz);
-    r.pull[0] = pull_of(c->region[l], bz, 0);
-    r.pull[1] = pull_of(c->region[l], bz, 1);
     r.pflags_own = pflags_of(c->region[l], bz);
     r.done_own = done_of(c->region[l], bz);
     r.exits = exits_of(c->region[l], bz);
@@ -259,11 +266,33 @@ void set_neighbours(RingRank& r, char* succ_region, char* pred_region, uint64_t 
   r.nflags = flags_of(succ_region, cap);
   r.pready = rflags_of(pred_region, cap);
   r.phash = rhash_of(pred_region, cap);
-  r.ppull[0] = pull_of(pred_region, cap, 0);
-  r.ppull[1] = pull_of(pred_region, cap, 1);
   r.pflags_pred = pflags_of(pred_region, cap);
   r.done_succ = done_of(succ_region, cap);
   r.nll = ll_of(succ_region, cap);
+}
+
+// The pull protocol's two buffers (HVD_CFG_PULL_BUFFERS): a separate allocation, made
+// only when that protocol is enabled, so the default footprint is the push path's.
+int alloc_pull(hvd_comm* c) {
+  if (c->pull_mem[0]) return HVD_OK;
+  CK(cudaSetDevice(c->device));
+  CK(cudaDeviceSynchronize());
+  for (int l = 0; l < c->nlocal; ++l) {
+    CK(cudaMalloc(reinterpret_cast<void**>(&c->pull_mem[l]), 2 * c->bufsz));
+    c->rk[l].pull[0] = c->pull_mem[l];
+    c->rk[l].pull[1] = c->pull_mem[l] + c->bufsz;
+  }
+  if (c->virt) {
+    for (int l = 0; l < c->nlocal; ++l)
+      for (int p = 0; p < 2; ++p) c->rk[l].ppull[p] = c->rk[(l + c->nlocal - 1) % c->nlocal].pull[p];
+    c->pull_ok = true;
+  }
+  return HVD_OK;
+}
+
+bool env_on(const char* name) {
+  const char* e = std::getenv(name);
+  return e && e[0] == '1';
 }
 
 int check_live(hvd_comm* c) {
@@ -1055,7 +1084,7 @@ int enqueue_fused_plan(hvd_comm* c, CachedPlan* plan, cudaStream_t s) {
   };
   for (DevPlanBuffer& b : plan->bufs) {
     if (b.L == 0 || ll_eligible(c, b, multi) || ll128_multi(b)) continue;
-    if (c->protocol == 0 && c->size > 1 && b.tdtype == b.dtype && !b.rdst) {
+    if (c->protocol == 0 && c->pull_ok && c->size > 1 && b.tdtype == b.dtype && !b.rdst) {
       int st = flush();
       if (st != HVD_OK) return st;
       st = enqueue_pull(c, b, s);
@@ -1277,6 +1306,7 @@ int hvd_init(int rank, int size, int device, uint64_t fusion_bytes, hvd_comm** o
   c->device = device;
   c->nlocal = 1;
   c->virt = false;
+  c->want_pull = env_on("HVD_PULL_BUFFERS");
   int st = common_init(c, fusion_bytes);
   if (st != HVD_OK) {
     hvd_finalize(c);
@@ -1320,7 +1350,8 @@ int hvd_init_virtual(int size, int device, uint64_t fusion_bytes, hvd_comm** out
   for (int l = 0; l < size; ++l)
     set_neighbours(c->rk[l], c->region[(l + 1) % size], c->region[(l + size - 1) % size], c->bufsz);
   c->connected = true;
-  st = timeline_env_start(c);
+  st = env_on("HVD_PULL_BUFFERS") ? alloc_pull(c) : HVD_OK;
+  if (st == HVD_OK) st = timeline_env_start(c);
   if (st != HVD_OK) {
     hvd_finalize(c);
     return st;
@@ -1350,6 +1381,14 @@ int hvd_get_ipc_blob(hvd_comm* c, void* out, uint64_t* len) {
   b.region_addr = reinterpret_cast<uint64_t>(c->region[0]);
   CK(cudaSetDevice(c->device));
   CK(cudaIpcGetMemHandle(&b.handle, c->region[0]));
+  if (c->want_pull) {
+    const int st = alloc_pull(c);
+    if (st != HVD_OK) return st;
+    b.has_pull = 1;
+    b.pull_addr = reinterpret_cast<uint64_t>(c->pull_mem[0]);
+    CK(cudaIpcGetMemHandle(&b.pull_handle, c->pull_mem[0]));
+  }
+  c->blob_out = true;
   CK(cudaDeviceGetPCIBusId(b.pci, (int)sizeof(b.pci), c->device));
   std::memcpy(out, &b, sizeof(b));
   *len = sizeof(Blob);
@@ -1361,13 +1400,17 @@ int hvd_connect(hvd_comm* c, const void* blobs, uint64_t len_each) {
   if (c->closed) return HVD_ERR_CLOSED;
   if (c->virt || c->size == 1) return HVD_OK;
   const char* p = static_cast<const char*>(blobs);
+  int npull = 0;
   for (int r = 0; r < c->size; ++r) {
     Blob b;
     std::memcpy(&b, p + (size_t)r * len_each, sizeof(b));
     if (b.magic != kBlobMagic || b.version != HVD_ABI_VERSION || b.rank != r || b.size != c->size ||
         b.capacity != c->cap)
       return HVD_ERR_INVALID;
+    npull += b.has_pull != 0;
   }
+  // HVD_CFG_PULL_BUFFERS must be identical on every rank
+  if (npull != 0 && npull != c->size) return HVD_ERR_INVALID;
   CK(cudaSetDevice(c->device));
   const int succ = (c->rank + 1) % c->size;
   const int pred = (c->rank + c->size - 1) % c->size;
@@ -1404,6 +1447,19 @@ int hvd_connect(hvd_comm* c, const void* blobs, uint64_t len_each) {
     c->pred_region = c->peer_region;
   }
   set_neighbours(c->rk[0], c->peer_region, c->pred_region, c->bufsz);
+  if (npull == c->size) {
+    if (bp.pid == me_pid) {
+      c->pred_pull = reinterpret_cast<const char*>(bp.pull_addr);
+    } else {
+      void* ptr = nullptr;
+      CK(cudaIpcOpenMemHandle(&ptr, bp.pull_handle, cudaIpcMemLazyEnablePeerAccess));
+      c->pred_pull = static_cast<const char*>(ptr);
+      c->pred_pull_ipc = true;
+    }
+    c->rk[0].ppull[0] = c->pred_pull;
+    c->rk[0].ppull[1] = c->pred_pull + c->bufsz;
+    c->pull_ok = true;
+  }
   c->connected = true;
   // LL128 only over verified NVLink ring links whose 128-byte lines arrive whole
   // (ADVICE r1): NVML's NVLink P2P status of both links, then the line-atomicity
@@ -1456,8 +1512,11 @@ int hvd_finalize(hvd_comm* c) {
     for (auto& kv : c->ipc_maps) cudaIpcCloseMemHandle(kv.second);
     if (c->peer_region && c->peer_ipc) cudaIpcCloseMemHandle(c->peer_region);
     if (c->pred_region && c->pred_region != c->peer_region && c->pred_ipc) cudaIpcCloseMemHandle(c->pred_region);
-    for (int l = 0; l < kMaxLocal; ++l)
+    if (c->pred_pull && c->pred_pull_ipc) cudaIpcCloseMemHandle(const_cast<char*>(c->pred_pull));
+    for (int l = 0; l < kMaxLocal; ++l) {
       if (c->region[l]) cudaFree(c->region[l]);
+      if (c->pull_mem[l]) cudaFree(c->pull_mem[l]);
+    }
     if (c->err_host) cudaFreeHost(c->err_host);
     if (c->err_dev) cudaFree(c->err_dev);
     if (c->tl) cudaFree(c->tl);
@@ -2055,7 +2114,21 @@ int hvd_set_config(hvd_comm* c, int key, int64_t value) {
       return HVD_OK;
     case HVD_CFG_PROTOCOL:
       if (value < 0 || value > 2) return HVD_ERR_INVALID;
+      if (value == 0 && c->size > 1 && !c->pull_ok) {
+        // the pull protocol reads the predecessor's pull buffers: virtual mode allocates
+        // them now; a real rank needs HVD_CFG_PULL_BUFFERS on every rank before connecting
+        if (!c->virt) return HVD_ERR_INVALID;
+        const int st = alloc_pull(c);
+        if (st != HVD_OK) return st;
+      }
       c->protocol = (int)value;
+      return HVD_OK;
+    case HVD_CFG_PULL_BUFFERS:
+      if (value != 0 && value != 1) return HVD_ERR_INVALID;
+      if (value == 0) return (c->pull_mem[0] || (c->want_pull && c->blob_out)) ? HVD_ERR_INVALID : (c->want_pull = false, HVD_OK);
+      if (c->virt) return alloc_pull(c);
+      if (c->blob_out) return c->want_pull ? HVD_OK : HVD_ERR_INVALID;
+      c->want_pull = true;
       return HVD_OK;
     case HVD_CFG_SOLO_KERNEL:
       if (value != 0 && value != 1) return HVD_ERR_INVALID;
@@ -2169,6 +2242,7 @@ int64_t hvd_get_config(const hvd_comm* c, int key) {
     case HVD_CFG_TIMELINE: return c->tl_max;
     case HVD_CFG_WINDOW: return c->window;
     case HVD_CFG_PROTOCOL: return c->protocol;
+    case HVD_CFG_PULL_BUFFERS: return (c->pull_ok || c->want_pull) ? 1 : 0;
     case HVD_CFG_MULTI_BUFFERS: return c->multi_bufs;
     case HVD_CFG_LL_MAX_BYTES: return c->ll_max;
     case HVD_CFG_LL128_MAX_BYTES: return c->ll128_max;

@@ -33,7 +33,7 @@ def _worker(rank, world, port, cases, q, protocol):
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import paper_1802_05799_b200 as hvd
     try:
-        comm = hvd.init()
+        comm = hvd.init(pull_buffers=protocol == 0)
         comm.set_config(hvd._lib.HVD_CFG_TIMEOUT_MS, 20000)
         comm.set_config(hvd._lib.HVD_CFG_PROTOCOL, protocol)
         out = []

@@ -445,6 +445,75 @@ def test_both_protocols_bitexact(hvd, n, protocol):
         comm.finalize()
 
 
+def test_pull_buffers_allocated_only_for_the_pull_protocol(hvd):
+    """The pull protocol's two buffers per rank are a separate allocation, made only when
+    that protocol is chosen (the default footprint is the push path's)."""
+    L = hvd._lib
+    n, cap = 4, 8 << 20
+    free0 = torch.cuda.mem_get_info()[0]
+    comm = hvd.init_virtual(n, 0, cap)
+    try:
+        free1 = torch.cuda.mem_get_info()[0]
+        bufsz = 3 * cap + (2 << 20)
+        # regions: 3 buffers + tail + 416 MiB LL areas per rank, no pull buffers
+        assert free0 - free1 < n * (3 * bufsz + (420 << 20)) + (64 << 20)
+        assert comm.get_config(L.HVD_CFG_PULL_BUFFERS) == 0
+        comm.set_config(L.HVD_CFG_PROTOCOL, 0)      # virtual mode: allocates them here
+        assert comm.get_config(L.HVD_CFG_PULL_BUFFERS) == 1
+        free2 = torch.cuda.mem_get_info()[0]
+        assert free1 - free2 >= n * 2 * bufsz
+        with pytest.raises(hvd.HvdError):
+            comm.set_config(L.HVD_CFG_PULL_BUFFERS, 0)
+        comm.set_config(L.HVD_CFG_LL_MAX_BYTES, 0)
+        counts = [5, 300_001, 1 << 20]
+        xs = workloads.all_ranks(counts, "f32", n, seed=9100)
+        ref, _, _ = oracle.allreduce(xs, ["f32"] * 3, "average", threshold=cap, capacity=cap)
+        ts = [[to_torch(x, "f32") for x in xs[r]] for r in range(n)]
+        comm.allreduce(ts, op="average", fusion_threshold=cap)
+        torch.cuda.synchronize()
+        assert comm.poll_error() == 0 and comm.kernel_stats()["pull"][0] >= 1
+        for r in range(n):
+            for k in range(3):
+                assert_same(from_torch(ts[r][k], "f32"), ref[r][k], "f32", f"r={r} k={k}")
+    finally:
+        comm.finalize()
+
+
+def test_pull_buffers_real_ranks_must_agree(hvd):
+    """Real ranks: HVD_CFG_PULL_BUFFERS before the blob export, identical on every rank —
+    hvd_connect refuses a mismatch before mapping anything; without the buffers the pull
+    protocol cannot be chosen.  Two ranks of one process on one GPU (no kernel runs)."""
+    import ctypes as C
+    L = hvd._lib
+    lib = L.lib
+    hs = []
+    try:
+        for r in range(2):
+            h = C.c_void_p()
+            assert lib.hvd_init(r, 2, 0, 4 << 20, C.byref(h)) == L.HVD_OK
+            hs.append(h)
+        assert lib.hvd_set_config(hs[0], L.HVD_CFG_PULL_BUFFERS, 1) == L.HVD_OK
+        assert lib.hvd_set_config(hs[1], L.HVD_CFG_PROTOCOL, 0) == L.HVD_ERR_INVALID
+        ln = C.c_uint64(0)
+        assert lib.hvd_get_ipc_blob(hs[0], None, C.byref(ln)) == L.HVD_OK
+        blobs = []
+        for h in hs:
+            b = C.create_string_buffer(ln.value)
+            assert lib.hvd_get_ipc_blob(h, b, C.byref(ln)) == L.HVD_OK
+            blobs.append(bytes(b.raw))
+        # after the export the setting is fixed
+        assert lib.hvd_set_config(hs[1], L.HVD_CFG_PULL_BUFFERS, 1) == L.HVD_ERR_INVALID
+        assert lib.hvd_set_config(hs[0], L.HVD_CFG_PULL_BUFFERS, 1) == L.HVD_OK
+        assert lib.hvd_get_config(hs[0], L.HVD_CFG_PULL_BUFFERS) == 1
+        assert lib.hvd_get_config(hs[1], L.HVD_CFG_PULL_BUFFERS) == 0
+        joined = b"".join(blobs)
+        for h in hs:
+            assert lib.hvd_connect(h, joined, ln.value) == L.HVD_ERR_INVALID
+    finally:
+        for h in hs:
+            lib.hvd_finalize(h)
+
+
 @pytest.mark.parametrize("n", [1, 2, 3, 4, 8])
 @pytest.mark.parametrize("tdt,wire", [("f32", "bf16"), ("bf16", "f32")])
 def test_wire_dtype_variants_bitexact(hvd, n, tdt, wire):

@@ -50,7 +50,7 @@ def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     iters = int(os.environ.get("NVL_ITERS", "6"))
     protocol = int(os.environ.get("NVL_PROTOCOL", "1"))
-    comm = hvd.init(64 << 20)
+    comm = hvd.init(64 << 20, pull_buffers=protocol == 0)
     comm.set_config(hvd._lib.HVD_CFG_TIMEOUT_MS, 120000)
     comm.set_config(hvd._lib.HVD_CFG_PROTOCOL, protocol)
     L = 16 << 20

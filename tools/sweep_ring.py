@@ -47,7 +47,7 @@ def main():
     torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
     dist.init_process_group("gloo")
     cap = max(a.mib) << 20
-    comm = hvd.init(fusion_bytes=cap)
+    comm = hvd.init(fusion_bytes=cap, pull_buffers=a.protocol == 0)
     L = hvd._lib
     code = {"f32": L.HVD_FLOAT32, "bf16": L.HVD_BFLOAT16}[a.dtype]
     esz = 4 if a.dtype == "f32" else 2
