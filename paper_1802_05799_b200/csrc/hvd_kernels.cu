@@ -2835,6 +2835,72 @@ __global__ void __launch_bounds__(kSoloThreads) solo_kernel(const __grid_constan
       }
       return;
     }
+    // A tile across member boundaries (many small members: Inception V3) whose members
+    // are all 16 B aligned: one bulk copy per member piece, issued by the lanes of warp 0
+    // (one member each) into the tile's shared memory on one mbarrier; a member's ragged
+    // last vector goes element by element.  Misaligned members take the per-vector path.
+    __shared__ int s_mis, s_last;
+    const int sa = sc.s;
+    if (tid < 32) {
+      const int sb = seg_of(F, t_end - 1, sa);
+      bool mis = false;
+      for (int m = sa + (int)tid; m <= sb; m += 32)
+        mis |= F.segs[m].count > 0 && ((reinterpret_cast<uintptr_t>(F.src[m]) | reinterpret_cast<uintptr_t>(F.dst[m])) & 15);
+      mis = __any_sync(~0u, mis);
+      if (tid == 0) {
+        s_mis = mis;
+        s_last = sb;
+      }
+    }
+    __syncthreads();
+    if (!s_mis) {
+      const int sb = s_last;
+      if (tid < 32) {
+        if (tid == 0) {
+          mbar_init(&s_bar, 1);
+          asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+        unsigned bytes = 0;
+        for (int m = sa + (int)tid; m <= sb; m += 32) {
+          const unsigned long long cnt = F.segs[m].count, v0 = F.segs[m].vbeg, vf = v0 + cnt / VEL;
+          const unsigned long long lo = v0 > base ? v0 : base, hi = vf < t_end ? vf : t_end;
+          if (hi > lo) {
+            tma_load(s_tile + (lo - base), F.src[m] + (lo - v0) * 16, (unsigned)((hi - lo) * 16), &s_bar);
+            bytes += (unsigned)((hi - lo) * 16);
+          }
+          if (cnt % VEL && vf >= base && vf < t_end) {  // ragged last vector
+            const unsigned long long left = cnt % VEL;
+            Cvt::put(F.dst[m] + (vf - v0) * 16, left,
+                     Cvt::slow(F.src[m] + (vf - v0) * 16, left, F.scale, F.scale_on, F.dtype));
+          }
+        }
+        bytes = __reduce_add_sync(~0u, bytes);
+        if (tid == 0) mbar_expect_tx(&s_bar, bytes);  // the one arrival: completes with the loads
+      }
+      if (F.scale_on) {
+        __syncthreads();
+        mbar_wait(&s_bar, 0);
+        for (unsigned long long v = tid; v < t_end - base; v += kSoloThreads)
+          s_tile[v] = Pack16<ESZ>::conv(s_tile[v], F.scale, F.scale_on, F.dtype);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+      }
+      if (tid < 32) {
+        if (!F.scale_on) mbar_wait(&s_bar, 0);
+        for (int m = sa + (int)tid; m <= sb; m += 32) {
+          const unsigned long long cnt = F.segs[m].count, v0 = F.segs[m].vbeg, vf = v0 + cnt / VEL;
+          const unsigned long long lo = v0 > base ? v0 : base, hi = vf < t_end ? vf : t_end;
+          if (hi > lo)
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                         ::"l"(F.dst[m] + (lo - v0) * 16), "r"(smem_u32(s_tile + (lo - base))),
+                         "r"((unsigned)((hi - lo) * 16)) : "memory");
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      }
+      return;
+    }
   }
 #endif
   if (fast) {
