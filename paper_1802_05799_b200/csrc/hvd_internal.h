@@ -147,6 +147,24 @@ struct PackParams {
   JtRef jt;                     // job timeline record of this launch
 };
 
+// N = 1 (solo_kernel): tiles of at most kSoloTileVecs 16 B vectors that never cross a
+// member, built with the plan (same-dtype buffers, one local rank).  A tile either moves
+// `bytes` (whole vectors) from src to dst by bulk copies plus `ragged` elements of the
+// member's partial last vector after them, or (flags & 1: a misaligned member) covers the
+// buffer vectors [src, dst) through the per-vector member lookup.
+#ifndef HVD_SOLO_THREADS
+#define HVD_SOLO_THREADS 128
+#endif
+#ifndef HVD_SOLO_U
+#define HVD_SOLO_U 4  // 8 KiB tiles (profiles/r02_solo_tile_sweep/: vs 16 KiB, 64 MiB 0.938 -> 0.945 of HBM,
+                      // Inception V3 fp32 0.835 -> 0.848, bf16 0.666 -> 0.712; 4 KiB tiles lose on the model sets)
+#endif
+constexpr unsigned long long kSoloTileVecs = (unsigned long long)HVD_SOLO_THREADS * HVD_SOLO_U;
+struct SoloTile {
+  unsigned long long src, dst;
+  unsigned bytes, ragged, flags, member;
+};
+
 // One fusion buffer of a multi-buffer fused launch (geometry + member tables).
 struct BufDesc {
   const PackSeg* segs;               // [nseg]
@@ -163,6 +181,8 @@ struct BufDesc {
   int nch;                           // fused: channels of this buffer; LL: its CTAs
   unsigned ll_off;                   // LL: word offset of this buffer's slots in a parity half
   int pad;
+  const SoloTile* stile;             // N = 1: member tiles (nullptr: tiles over the buffer's vectors)
+  unsigned long long nstile;
 };
 constexpr int kMaxMultiBufs = 96;    // fusion buffers per fused launch (kernel parameter space)
 

@@ -2742,19 +2742,18 @@ cudaError_t launch_ring(const RingParams& p, int dtype, int nch, int nlocal, int
 // tail; a persistent grid-stride walk left the SMs idle 28 % of the kernel in
 // ncu).  A tile inside one member with aligned addresses (the common case)
 // issues its U independent 16 B loads off one pointer, then its U stores.
-#ifndef HVD_SOLO_THREADS
-#define HVD_SOLO_THREADS 128
-#endif
-#ifndef HVD_SOLO_U
-#define HVD_SOLO_U 4  // 8 KiB tiles (profiles/r02_solo_tile_sweep/: vs 16 KiB, 64 MiB 0.938 -> 0.945 of HBM,
-                      // Inception V3 fp32 0.835 -> 0.848, bf16 0.666 -> 0.712; 4 KiB tiles lose on the model sets)
-#endif
 #ifndef HVD_SOLO_TMA
 #define HVD_SOLO_TMA 1
 #endif
 constexpr int kSoloThreads = HVD_SOLO_THREADS;
 constexpr int kSoloU = HVD_SOLO_U;  // 16 B wire vectors per thread (same-dtype wire)
 constexpr int kSoloSegCache = 256;  // member starts a boundary tile stages in shared memory
+
+// A member's partial last vector (fewer than 16 / ESZ elements), same dtype.
+template <int ESZ>
+__device__ __noinline__ void solo_ragged(char* d, const char* g, unsigned left, float scale, int on, int dtype) {
+  scatter_slow<ESZ>(d, left, Pack16<ESZ>::conv(gather_slow<ESZ>(g, left), scale, on, dtype));
+}
 
 template <class Op, int TESZ>
 __global__ void __launch_bounds__(kSoloThreads) solo_kernel(const __grid_constant__ FusedParams P) {
@@ -2765,6 +2764,9 @@ __global__ void __launch_bounds__(kSoloThreads) solo_kernel(const __grid_constan
   constexpr unsigned long long TILE = (unsigned long long)kSoloThreads * U;
   using Cvt = WireCvt<ESZ, TESZ>;
   const unsigned tid = threadIdx.x;
+  // same dtype: the tile's bulk-copy staging (one per CTA, shared by every tile path)
+  __shared__ __align__(128) uint4 s_tile[TESZ == ESZ ? TILE : 1];
+  __shared__ __align__(8) unsigned long long s_bar;
   // programmatic dependent launch: the next kernel on the stream may be launched as soon
   // as every CTA of this grid has started; this grid's own memory work waits for the
   // previous grid's completion (griddepcontrol.wait), so back-to-back calls overlap only
@@ -2774,12 +2776,56 @@ __global__ void __launch_bounds__(kSoloThreads) solo_kernel(const __grid_constan
   unsigned long long t = blockIdx.x;  // -> (buffer b, tile t of b)
   int b = 0;
   for (; b < P.nbuf; ++b) {
-    const unsigned long long nt = ((P.bufs[b].L + VEL - 1) / VEL + TILE - 1) / TILE;
+    const unsigned long long nt =
+        P.bufs[b].stile ? P.bufs[b].nstile : ((P.bufs[b].L + VEL - 1) / VEL + TILE - 1) / TILE;
     if (t < nt) break;
     t -= nt;
   }
   if (b == P.nbuf) return;
   const BufDesc& D = P.bufs[b];
+#if HVD_SOLO_TMA
+  if constexpr (TESZ == ESZ) {
+    if (D.stile) {
+      // member tile (built with the plan): one descriptor load, then bulk copies
+      const uint4* dp4 = reinterpret_cast<const uint4*>(D.stile + t);
+      const uint4 d0v = __ldg(dp4), d1v = __ldg(dp4 + 1);
+      const char* gsrc = reinterpret_cast<const char*>((unsigned long long)d0v.x | ((unsigned long long)d0v.y << 32));
+      char* gdst = reinterpret_cast<char*>((unsigned long long)d0v.z | ((unsigned long long)d0v.w << 32));
+      const unsigned bytes = d1v.x, ragged = d1v.y;
+      if (!(d1v.z & 1u)) {
+        if (bytes) {
+          if (tid == 0) {
+            mbar_init(&s_bar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            mbar_expect_tx(&s_bar, bytes);
+            tma_load(s_tile, gsrc, bytes, &s_bar);
+          }
+          if (ragged && tid == 32)  // the member's partial last vector, element by element
+            solo_ragged<ESZ>(gdst + bytes, gsrc + bytes, ragged, P.scale, P.scale_on, P.dtype);
+          __syncthreads();
+          if (P.scale_on) {
+            mbar_wait(&s_bar, 0);
+            for (unsigned v = tid; v < bytes / 16; v += kSoloThreads)
+              s_tile[v] = Pack16<ESZ>::conv(s_tile[v], P.scale, P.scale_on, P.dtype);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+          } else if (tid == 0) {
+            mbar_wait(&s_bar, 0);
+          }
+          if (tid == 0) {
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                         ::"l"(gdst), "r"(smem_u32(s_tile)), "r"(bytes) : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          }
+        } else if (ragged && tid == 0) {
+          solo_ragged<ESZ>(gdst, gsrc, ragged, P.scale, P.scale_on, P.dtype);
+        }
+        return;
+      }
+    }
+  }
+#endif
   FusedCtx F = {};
   F.segs = D.segs;
   F.src = D.src + (size_t)blockIdx.y * D.nseg;
@@ -2794,8 +2840,12 @@ __global__ void __launch_bounds__(kSoloThreads) solo_kernel(const __grid_constan
   F.dtype = P.dtype;
   SegCache sc;
   const unsigned long long nvec = (D.L + VEL - 1) / VEL;
-  const unsigned long long base = t * TILE;
-  const unsigned long long t_end = base + TILE < nvec ? base + TILE : nvec;
+  unsigned long long base = t * TILE;
+  unsigned long long t_end = base + TILE < nvec ? base + TILE : nvec;
+  if (D.stile) {  // a misaligned member's tile: buffer vectors [src, dst) of the descriptor
+    base = D.stile[t].src;
+    t_end = D.stile[t].dst;
+  }
   seg_lookup<TESZ>(F, base, sc);
   const unsigned long long e0 = base * VEL;
   const char* g0 = reinterpret_cast<const char*>(sc.g + e0 * TESZ);
@@ -2807,8 +2857,6 @@ __global__ void __launch_bounds__(kSoloThreads) solo_kernel(const __grid_constan
     // same dtype: the tile moves HBM -> shared -> HBM by bulk copies (TMA engine), the
     // threads only scale it in shared memory; in-flight bytes cost shared memory, not
     // registers (~14 CTAs x 16 KiB per SM)
-    __shared__ __align__(128) uint4 s_tile[TILE];
-    __shared__ __align__(8) unsigned long long s_bar;
     if (fast) {
       const unsigned bytes = (unsigned)((t_end - base) * 16);
       if (tid == 0) {
@@ -2967,7 +3015,8 @@ static cudaError_t launch_solo_t(const FusedParams& p, int nlocal, cudaStream_t 
   constexpr int VEL = 16 / Op::kEsz;
   constexpr unsigned long long TILE = (unsigned long long)kSoloThreads * (TESZ > Op::kEsz ? (kSoloU + 1) / 2 : kSoloU);
   unsigned long long tiles = 0;
-  for (int b = 0; b < p.nbuf; ++b) tiles += ((p.bufs[b].L + VEL - 1) / VEL + TILE - 1) / TILE;
+  for (int b = 0; b < p.nbuf; ++b)
+    tiles += p.bufs[b].stile ? p.bufs[b].nstile : ((p.bufs[b].L + VEL - 1) / VEL + TILE - 1) / TILE;
   if (tiles == 0) return cudaSuccess;
   if (tiles > 0x7fffffffull) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg = {};

@@ -58,6 +58,8 @@ struct DevPlanBuffer {
   const unsigned long long* vbeg;       // [nseg] member start vectors (fused kernel, large plans)
   char* const* dst = nullptr;           // [nlocal * nseg] scatter addresses (nullptr: = pp.src)
   char* const* rdst = nullptr;          // [nlocal * nseg] registered: successor's addresses
+  const SoloTile* stile = nullptr;      // N = 1: member tiles (solo_kernel)
+  uint64_t nstile = 0;
 };
 
 // A registered tensor list (hvd_register): this rank's tensors plus the successor's
@@ -327,6 +329,11 @@ struct HostBuf {
   std::vector<char*> dst;         // [nlocal * nseg] scatter addresses; empty = same as src
 };
 
+// solo_kernel tiles of one member of `count` elements (vel per 16 B vector)
+uint64_t solo_member_tiles(uint64_t count, uint64_t vel) {
+  return ((count + vel - 1) / vel + kSoloTileVecs - 1) / kSoloTileVecs;
+}
+
 CachedPlan* lookup_plan(hvd_comm* c, const std::vector<uint64_t>& key) {
   for (auto it = c->cache.begin(); it != c->cache.end(); ++it) {
     if (it->key == key) {
@@ -341,8 +348,8 @@ CachedPlan* lookup_plan(hvd_comm* c, const std::vector<uint64_t>& key) {
 // stream) and cache them under `key` (LRU of kPlanCacheSize plans).
 int upload_plan(hvd_comm* c, std::vector<uint64_t> key, const std::vector<HostBuf>& hb, cudaStream_t s,
                 CachedPlan** out) {
-  // layout per buffer: [segs][src][dst][tile_seg][vbeg]
-  struct Off { size_t segs, src, dst, rdst, tiles, vbeg; uint64_t nvec, ntiles; };
+  // layout per buffer: [segs][src][dst][tile_seg][vbeg][solo tiles]
+  struct Off { size_t segs, src, dst, rdst, tiles, vbeg, stile; uint64_t nvec, ntiles, nstile; };
   std::vector<Off> offs(hb.size());
   const uint64_t tile_vecs = (uint64_t)kPackThreads * kPackVecsPerThread;
   size_t total = 0;
@@ -364,6 +371,12 @@ int upload_plan(hvd_comm* c, std::vector<uint64_t> key, const std::vector<HostBu
     total = align256(total + sizeof(int) * (offs[b].ntiles + 1));
     offs[b].vbeg = total;
     total = align256(total + sizeof(unsigned long long) * nseg);
+    // N = 1, one local rank, same dtype: member tiles for solo_kernel
+    offs[b].nstile = 0;
+    if (c->size == 1 && c->nlocal == 1 && (hb[b].tdtype == 0 || hb[b].tdtype == hb[b].dtype))
+      for (const PackSeg& sg : hb[b].segs) offs[b].nstile += solo_member_tiles(sg.count, vel);
+    offs[b].stile = total;
+    total = align256(total + sizeof(SoloTile) * offs[b].nstile);
   }
   CachedPlan p;
   p.key = std::move(key);
@@ -398,6 +411,41 @@ int upload_plan(hvd_comm* c, std::vector<uint64_t> key, const std::vector<HostBu
       tiles[tile] = sidx;
     }
     tiles[offs[b].ntiles] = nseg - 1;
+    if (offs[b].nstile) {
+      // member tiles: whole 16 B vectors by bulk copy (+ the ragged last elements), or, for a
+      // member whose tensor is not 16 B aligned, a range of buffer vectors for the lookup path
+      SoloTile* st = reinterpret_cast<SoloTile*>(h + offs[b].stile);
+      const int esz = elem_size(B.dtype);
+      const uint64_t vel = kPackVecBytes / esz;
+      uint64_t k = 0;
+      for (int j = 0; j < nseg; ++j) {
+        const PackSeg& sg = B.segs[j];
+        if (sg.count == 0) continue;
+        const char* g = B.src[j];
+        const char* dd = B.dst.empty() ? B.src[j] : B.dst[j];
+        const bool mis = ((reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(dd)) & 15) != 0;
+        const uint64_t nv = (sg.count + vel - 1) / vel, full = sg.count / vel;
+        for (uint64_t v = 0; v < nv; v += kSoloTileVecs) {
+          const uint64_t e = std::min<uint64_t>(nv, v + kSoloTileVecs);
+          SoloTile& T = st[k++];
+          T.member = (unsigned)j;
+          if (mis) {
+            T.src = sg.vbeg + v;
+            T.dst = sg.vbeg + e;
+            T.bytes = 0;
+            T.ragged = 0;
+            T.flags = 1;
+          } else {
+            const uint64_t fe = std::min<uint64_t>(full, e);
+            T.src = reinterpret_cast<uintptr_t>(g) + v * kPackVecBytes;
+            T.dst = reinterpret_cast<uintptr_t>(dd) + v * kPackVecBytes;
+            T.bytes = (unsigned)((fe > v ? fe - v : 0) * kPackVecBytes);
+            T.ragged = e > full ? (unsigned)(sg.count - full * vel) : 0;
+            T.flags = 0;
+          }
+        }
+      }
+    }
     DevPlanBuffer db;
     db.dtype = B.dtype;
     db.tdtype = B.tdtype ? B.tdtype : B.dtype;
@@ -414,6 +462,8 @@ int upload_plan(hvd_comm* c, std::vector<uint64_t> key, const std::vector<HostBu
     db.pp.tile_vecs = tile_vecs;
     db.pp.ntiles = offs[b].ntiles;
     db.pp.nseg = nseg;
+    db.stile = offs[b].nstile ? reinterpret_cast<const SoloTile*>(d + offs[b].stile) : nullptr;
+    db.nstile = offs[b].nstile;
     p.bufs.push_back(db);
   }
   if (total) {
@@ -793,6 +843,8 @@ int enqueue_fused_multi(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStrea
     D.tile_seg = b.pp.tile_seg;
     D.tile_vecs = b.pp.tile_vecs;
     D.nseg = b.pp.nseg;
+    D.stile = N == 1 ? b.stile : nullptr;
+    D.nstile = N == 1 ? b.nstile : 0;
     D.L = b.L;
     D.q = chunk_len(b.L, N, dtype);
     const int k = kk[i];

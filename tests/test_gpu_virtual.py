@@ -696,6 +696,38 @@ def test_solo_many_small_members_n1(hvd):
         comm.finalize()
 
 
+@pytest.mark.parametrize("dt", ["f32", "bf16", "i32", "i64"])
+def test_solo_member_tiles_mixed_alignment_n1(hvd, dt):
+    """N = 1 member tiles (built with the plan): members of several tiles with a ragged last
+    vector, members smaller than one vector, and misaligned views (their tiles take the
+    per-vector path) in one call; every tensor bit-exact to the oracle, one solo launch."""
+    counts = [1, 3, 4097 * 8 + 5, 7, 65_536, 2, 9_001, 123_457, 0, 31]
+    mis = {2, 5, 7}  # views off the 16 B grid
+    op = "sum" if dt in ("i32", "i64") else "average"
+    comm = hvd.init_virtual(1, 0, 8 << 20)
+    try:
+        xs = workloads.all_ranks(counts, dt, 1, "int_uniform" if dt in ("i32", "i64") else "normal", seed=4242)
+        ref, _, _ = oracle.allreduce(xs, [dt] * len(counts), op, threshold=8 << 20, capacity=8 << 20)
+        keep, ts = [], []
+        for k, x in enumerate(xs[0]):
+            t = to_torch(x, dt)
+            if k in mis and len(x) > 0:
+                big = torch.empty(len(x) + 1, dtype=t.dtype, device="cuda")
+                big[1:].copy_(t)
+                keep.append(big)
+                t = big[1:]
+            ts.append(t)
+        comm.kernel_stats()
+        comm.allreduce([ts], op=op, fusion_threshold=8 << 20)
+        torch.cuda.synchronize()
+        assert comm.poll_error() == 0
+        assert comm.kernel_stats()["solo"][0] == 1
+        for k in range(len(counts)):
+            assert_same(from_torch(ts[k], dt), ref[0][k], dt, f"k={k}")
+    finally:
+        comm.finalize()
+
+
 @pytest.mark.parametrize("n", [2, 3, 4])
 def test_negotiated_allreduce_cycles(hvd, n):
     """Readiness negotiation + Tensor Fusion (R15): each cycle reduces exactly the
