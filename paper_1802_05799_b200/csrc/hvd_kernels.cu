@@ -2755,8 +2755,16 @@ __device__ __noinline__ void solo_ragged(char* d, const char* g, unsigned left, 
   scatter_slow<ESZ>(d, left, Pack16<ESZ>::conv(gather_slow<ESZ>(g, left), scale, on, dtype));
 }
 
+#ifndef HVD_SOLO_MINB
+#define HVD_SOLO_MINB 0  // > 0: CTAs per SM the register allocation must allow
+#endif
+#if HVD_SOLO_MINB
+#define HVD_SOLO_BOUNDS __launch_bounds__(kSoloThreads, HVD_SOLO_MINB)
+#else
+#define HVD_SOLO_BOUNDS __launch_bounds__(kSoloThreads)
+#endif
 template <class Op, int TESZ>
-__global__ void __launch_bounds__(kSoloThreads) solo_kernel(const __grid_constant__ FusedParams P) {
+__global__ void HVD_SOLO_BOUNDS solo_kernel(const __grid_constant__ FusedParams P) {
   JtGuard jtg(P.ring.jt);
   constexpr int ESZ = Op::kEsz;
   constexpr int VEL = 16 / ESZ;
