@@ -318,13 +318,16 @@ typedef enum {
   HVD_CFG_LL_PDL = 32,       /* LL / LL128 launches: programmatic dependent launch (back-to-back
                                 small calls overlap the next launch with this one's tail);
                                 default 1 (N = 4, <= 1 MiB: 1-7 % lower latency)           */
-  HVD_CFG_PULL_BUFFERS = 33  /* 1 = allocate the pull protocol's two buffers (2 x the region
+  HVD_CFG_PULL_BUFFERS = 33, /* 1 = allocate the pull protocol's two buffers (2 x the region
                                 buffer size, a separate device allocation) so that
                                 HVD_CFG_PROTOCOL = 0 can be chosen.  Real ranks: set before
                                 hvd_get_ipc_blob, identically on every rank (hvd_connect
                                 returns INVALID otherwise); virtual mode: any time.  Default 0
                                 (the environment variable HVD_PULL_BUFFERS=1 at init: 1).
                                 Cannot be turned off once allocated (INVALID).              */
+  HVD_CFG_SOLO_TAIL = 34     /* N = 1: the last this many member tiles of a buffer are cut in
+                                half so that the final wave drains sooner (-1 = one wave,
+                                9 x the SM count; 0 = off, the default).  Drops cached plans. */
 } hvd_config_key;
 /* Set a tuning knob; every rank must set identical values.  Errors: INVALID. */
 int hvd_set_config(hvd_comm* c, int key, int64_t value);

@@ -55,6 +55,7 @@ HVD_CFG_HOST_ZERO_COPY = 30
 HVD_CFG_PREISSUE = 31
 HVD_CFG_LL_PDL = 32
 HVD_CFG_PULL_BUFFERS = 33
+HVD_CFG_SOLO_TAIL = 34
 MAX_CHANNELS = 256
 HVD_KERNEL_PACK, HVD_KERNEL_RING, HVD_KERNEL_UNPACK, HVD_KERNEL_SCALE, HVD_KERNEL_FUSED = 0, 1, 2, 3, 4
 HVD_KERNEL_COPY = 5

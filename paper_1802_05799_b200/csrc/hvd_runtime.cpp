@@ -131,6 +131,7 @@ struct hvd_comm {
   int solo_kernel = 0;              // HVD_CFG_SOLO_KERNEL: 1 persistent bulk kernel, 0 tile-per-CTA kernel
   int solo_stages = 6;              // HVD_CFG_SOLO_STAGES
   int solo_stage_bytes = 32 << 10;  // HVD_CFG_SOLO_STAGE_BYTES
+  int64_t solo_tail = 0;            // HVD_CFG_SOLO_TAIL: member tiles at a buffer's end cut in half
   int pace_gbps = 0;                // HVD_CFG_PACE_GBPS: fused push remote-store pacing (0 = off)
   int fused_pdl = 0;                // HVD_CFG_FUSED_PDL
   int watcher = 0;                  // HVD_CFG_WATCHER
@@ -165,6 +166,13 @@ struct hvd_comm {
   cudaEvent_t ev_in[kHostSlots] = {}, ev_red[kHostSlots] = {}, ev_out[kHostSlots] = {};
   cudaEvent_t ev_start = nullptr, ev_done = nullptr;
 };
+
+namespace {
+uint64_t solo_tail_tiles(const hvd_comm* c) {
+  return c->solo_tail >= 0 ? (uint64_t)c->solo_tail : (uint64_t)c->sm_count * 9;
+}
+}  // namespace
+
 
 namespace {
 
@@ -314,6 +322,13 @@ void free_plan(CachedPlan& p) {
 
 size_t align256(size_t v) { return (v + 255) / 256 * 256; }
 
+// Free every cached plan (after the device is done with them).
+void drop_plans(std::list<CachedPlan>& cache) {
+  if (!cache.empty()) cudaDeviceSynchronize();
+  for (CachedPlan& p : cache) free_plan(p);
+  cache.clear();
+}
+
 // Build (or fetch) the device-resident pack/unpack tables of the plan of the
 // tensor list `t` (n per local rank).  The key is every tensor's address,
 // count and dtype plus the threshold, so repeated calls on the same gradient
@@ -328,6 +343,10 @@ struct HostBuf {
   std::vector<char*> src;         // [nlocal * nseg] gather addresses
   std::vector<char*> dst;         // [nlocal * nseg] scatter addresses; empty = same as src
 };
+
+// member tiles cut in half at the end of a buffer (HVD_CFG_SOLO_TAIL; -1 = one wave of
+// the solo kernel: 9 resident CTAs per SM)
+uint64_t solo_tail_tiles(const hvd_comm* c);
 
 // solo_kernel tiles of one member of `count` elements (vel per 16 B vector)
 uint64_t solo_member_tiles(uint64_t count, uint64_t vel) {
@@ -373,8 +392,10 @@ int upload_plan(hvd_comm* c, std::vector<uint64_t> key, const std::vector<HostBu
     total = align256(total + sizeof(unsigned long long) * nseg);
     // N = 1, one local rank, same dtype: member tiles for solo_kernel
     offs[b].nstile = 0;
-    if (c->size == 1 && c->nlocal == 1 && (hb[b].tdtype == 0 || hb[b].tdtype == hb[b].dtype))
+    if (c->size == 1 && c->nlocal == 1 && (hb[b].tdtype == 0 || hb[b].tdtype == hb[b].dtype)) {
       for (const PackSeg& sg : hb[b].segs) offs[b].nstile += solo_member_tiles(sg.count, vel);
+      offs[b].nstile += std::min<uint64_t>(offs[b].nstile, solo_tail_tiles(c));  // halves of the tail
+    }
     offs[b].stile = total;
     total = align256(total + sizeof(SoloTile) * offs[b].nstile);
   }
@@ -443,6 +464,28 @@ int upload_plan(hvd_comm* c, std::vector<uint64_t> key, const std::vector<HostBu
             T.ragged = e > full ? (unsigned)(sg.count - full * vel) : 0;
             T.flags = 0;
           }
+        }
+      }
+      // HVD_CFG_SOLO_TAIL: the last tiles are cut in half (the block scheduler runs tiles
+      // in order, so the final wave drains sooner)
+      const uint64_t nt = k, ns = std::min<uint64_t>(nt, offs[b].nstile - nt);
+      for (uint64_t i = nt; i-- > nt - ns;) {
+        const SoloTile T = st[i];
+        SoloTile& a = st[i + (i - (nt - ns))];
+        SoloTile& z = st[i + (i - (nt - ns)) + 1];
+        const unsigned half = T.flags ? 0 : T.bytes / 32 * 16;
+        a = T;
+        z = T;
+        if (T.flags) {  // vector range of a misaligned member
+          const uint64_t mid = T.src + (T.dst - T.src) / 2;
+          a.dst = mid;
+          z.src = mid;
+        } else {
+          a.bytes = half;
+          a.ragged = 0;
+          z.src = T.src + half;
+          z.dst = T.dst + half;
+          z.bytes = T.bytes - half;
         }
       }
     }
@@ -1560,7 +1603,7 @@ int hvd_finalize(hvd_comm* c) {
     if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
     for (int l = 0; l < kMaxLocal; ++l)
       if (c->stage[l]) cudaFree(c->stage[l]);
-    c->cache.clear();
+    drop_plans(c->cache);
     for (auto& kv : c->ipc_maps) cudaIpcCloseMemHandle(kv.second);
     if (c->peer_region && c->peer_ipc) cudaIpcCloseMemHandle(c->peer_region);
     if (c->pred_region && c->pred_region != c->peer_region && c->pred_ipc) cudaIpcCloseMemHandle(c->pred_region);
@@ -2219,6 +2262,12 @@ int hvd_set_config(hvd_comm* c, int key, int64_t value) {
       if (value < 0 || value > 1024) return HVD_ERR_INVALID;
       c->pace_burst_rows = (int)value;
       return HVD_OK;
+    case HVD_CFG_SOLO_TAIL:
+      if (value < -1) return HVD_ERR_INVALID;
+      c->solo_tail = value;
+      CK(cudaSetDevice(c->device));
+      drop_plans(c->cache);  // member tables are built with the plan
+      return HVD_OK;
     case HVD_CFG_SOLO_STAGE_BYTES:
       if (value < (4 << 10) || value > (64 << 10) || value % 1024 ||
           bulk_smem_bytes(c->solo_stages, (int)value, false) > kBulkMaxSmem)
@@ -2311,6 +2360,7 @@ int64_t hvd_get_config(const hvd_comm* c, int key) {
     case HVD_CFG_LL_PDL: return c->ll_pdl;
     case HVD_CFG_PACE_BURST_ROWS: return c->pace_burst_rows;
     case HVD_CFG_SOLO_STAGE_BYTES: return c->solo_stage_bytes;
+    case HVD_CFG_SOLO_TAIL: return c->solo_tail;
     case HVD_CFG_BULK_STAGES: return c->bulk_stages;
     case HVD_CFG_BULK_STAGE_BYTES: return c->bulk_stage_bytes;
     case HVD_CFG_BULK_DEPTH: return c->bulk_depth;

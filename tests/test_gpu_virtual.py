@@ -696,8 +696,9 @@ def test_solo_many_small_members_n1(hvd):
         comm.finalize()
 
 
+@pytest.mark.parametrize("tail", [0, 7, -1, 1 << 20])
 @pytest.mark.parametrize("dt", ["f32", "bf16", "i32", "i64"])
-def test_solo_member_tiles_mixed_alignment_n1(hvd, dt):
+def test_solo_member_tiles_mixed_alignment_n1(hvd, dt, tail):
     """N = 1 member tiles (built with the plan): members of several tiles with a ragged last
     vector, members smaller than one vector, and misaligned views (their tiles take the
     per-vector path) in one call; every tensor bit-exact to the oracle, one solo launch."""
@@ -706,6 +707,7 @@ def test_solo_member_tiles_mixed_alignment_n1(hvd, dt):
     op = "sum" if dt in ("i32", "i64") else "average"
     comm = hvd.init_virtual(1, 0, 8 << 20)
     try:
+        comm.set_config(hvd._lib.HVD_CFG_SOLO_TAIL, tail)  # tail tiles cut in half (HVD_CFG_SOLO_TAIL)
         xs = workloads.all_ranks(counts, dt, 1, "int_uniform" if dt in ("i32", "i64") else "normal", seed=4242)
         ref, _, _ = oracle.allreduce(xs, [dt] * len(counts), op, threshold=8 << 20, capacity=8 << 20)
         keep, ts = [], []
