@@ -160,6 +160,10 @@ struct PackParams {
                       // Inception V3 fp32 0.835 -> 0.848, bf16 0.666 -> 0.712; 4 KiB tiles lose on the model sets)
 #endif
 constexpr unsigned long long kSoloTileVecs = (unsigned long long)HVD_SOLO_THREADS * HVD_SOLO_U;
+#ifndef HVD_SOLO_TPC
+#define HVD_SOLO_TPC 1  // member tiles per CTA when every tile of a launch is a plain bulk copy
+#endif
+constexpr int kSoloTPC = HVD_SOLO_TPC;
 struct SoloTile {
   unsigned long long src, dst;
   unsigned bytes, ragged, flags, member;
@@ -222,7 +226,7 @@ struct FusedParams {
   int bulk_stages;                   // shared-memory stages per CTA
   int bulk_stage_bytes;              // bytes per stage (multiple of 16)
   int bulk_depth;                    // bulk store groups left incomplete before retiring a stage
-  int pad2;
+  int solo_tpc;                      // N = 1 member tiles per CTA (solo_kernel; 1 = one)
   BufDesc bufs[kMaxMultiBufs];
 };
 

@@ -2773,14 +2773,71 @@ __global__ void HVD_SOLO_BOUNDS solo_kernel(const __grid_constant__ FusedParams 
   using Cvt = WireCvt<ESZ, TESZ>;
   const unsigned tid = threadIdx.x;
   // same dtype: the tile's bulk-copy staging (one per CTA, shared by every tile path)
-  __shared__ __align__(128) uint4 s_tile[TESZ == ESZ ? TILE : 1];
+  __shared__ __align__(128) uint4 s_tile[TESZ == ESZ ? TILE * kSoloTPC : 1];
   __shared__ __align__(8) unsigned long long s_bar;
   // programmatic dependent launch: the next kernel on the stream may be launched as soon
   // as every CTA of this grid has started; this grid's own memory work waits for the
   // previous grid's completion (griddepcontrol.wait), so back-to-back calls overlap only
-  // the launch, never the data
+  // the launch, never the data.  Member-tile descriptors are plan tables no kernel writes:
+  // they are read before the wait.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+#if HVD_SOLO_TMA
+  if constexpr (TESZ == ESZ && kSoloTPC > 1) {
+    if (P.solo_tpc > 1) {
+      // several member tiles per CTA (every tile of the launch a plain bulk copy): all
+      // descriptors in one round trip, all bulk loads in flight, each store as its load lands
+      __shared__ __align__(8) unsigned long long s_bars[kSoloTPC];
+      uint4 dA[kSoloTPC], dB[kSoloTPC];
+      bool ok[kSoloTPC];
+#pragma unroll
+      for (int j = 0; j < kSoloTPC; ++j) {
+        unsigned long long tj = (unsigned long long)blockIdx.x * kSoloTPC + j;
+        int bj = 0;
+        for (; bj < P.nbuf; ++bj) {
+          if (tj < P.bufs[bj].nstile) break;
+          tj -= P.bufs[bj].nstile;
+        }
+        ok[j] = bj < P.nbuf;
+        if (ok[j]) {
+          const uint4* q = reinterpret_cast<const uint4*>(P.bufs[bj].stile + tj);
+          dA[j] = __ldg(q);
+          dB[j] = __ldg(q + 1);
+        }
+      }
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      if (tid == 0) {
+#pragma unroll
+        for (int j = 0; j < kSoloTPC; ++j)
+          if (ok[j] && dB[j].x) {
+            mbar_init(&s_bars[j], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            mbar_expect_tx(&s_bars[j], dB[j].x);
+            tma_load(s_tile + j * TILE, reinterpret_cast<const char*>((unsigned long long)dA[j].x | ((unsigned long long)dA[j].y << 32)),
+                     dB[j].x, &s_bars[j]);
+          }
+#pragma unroll
+        for (int j = 0; j < kSoloTPC; ++j)
+          if (ok[j] && dB[j].x) {
+            mbar_wait(&s_bars[j], 0);
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                         ::"l"((unsigned long long)dA[j].z | ((unsigned long long)dA[j].w << 32)),
+                         "r"(smem_u32(s_tile + j * TILE)), "r"(dB[j].x) : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      } else if (tid == 32) {
+#pragma unroll
+        for (int j = 0; j < kSoloTPC; ++j)
+          if (ok[j] && dB[j].y) {
+            const char* g = reinterpret_cast<const char*>((unsigned long long)dA[j].x | ((unsigned long long)dA[j].y << 32));
+            char* d = reinterpret_cast<char*>((unsigned long long)dA[j].z | ((unsigned long long)dA[j].w << 32));
+            solo_ragged<ESZ>(d + dB[j].x, g + dB[j].x, dB[j].y, P.scale, P.scale_on, P.dtype);
+          }
+      }
+      return;
+    }
+  }
+#endif
   unsigned long long t = blockIdx.x;  // -> (buffer b, tile t of b)
   int b = 0;
   for (; b < P.nbuf; ++b) {
@@ -2797,6 +2854,7 @@ __global__ void HVD_SOLO_BOUNDS solo_kernel(const __grid_constant__ FusedParams 
       // member tile (built with the plan): one descriptor load, then bulk copies
       const uint4* dp4 = reinterpret_cast<const uint4*>(D.stile + t);
       const uint4 d0v = __ldg(dp4), d1v = __ldg(dp4 + 1);
+      asm volatile("griddepcontrol.wait;" ::: "memory");
       const char* gsrc = reinterpret_cast<const char*>((unsigned long long)d0v.x | ((unsigned long long)d0v.y << 32));
       char* gdst = reinterpret_cast<char*>((unsigned long long)d0v.z | ((unsigned long long)d0v.w << 32));
       const unsigned bytes = d1v.x, ragged = d1v.y;
@@ -2834,6 +2892,7 @@ __global__ void HVD_SOLO_BOUNDS solo_kernel(const __grid_constant__ FusedParams 
     }
   }
 #endif
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (a no-op after the wait above)
   FusedCtx F = {};
   F.segs = D.segs;
   F.src = D.src + (size_t)blockIdx.y * D.nseg;
@@ -3025,6 +3084,7 @@ static cudaError_t launch_solo_t(const FusedParams& p, int nlocal, cudaStream_t 
   unsigned long long tiles = 0;
   for (int b = 0; b < p.nbuf; ++b)
     tiles += p.bufs[b].stile ? p.bufs[b].nstile : ((p.bufs[b].L + VEL - 1) / VEL + TILE - 1) / TILE;
+  if (p.solo_tpc > 1) tiles = (tiles + p.solo_tpc - 1) / p.solo_tpc;
   if (tiles == 0) return cudaSuccess;
   if (tiles > 0x7fffffffull) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg = {};

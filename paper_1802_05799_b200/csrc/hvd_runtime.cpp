@@ -60,6 +60,7 @@ struct DevPlanBuffer {
   char* const* rdst = nullptr;          // [nlocal * nseg] registered: successor's addresses
   const SoloTile* stile = nullptr;      // N = 1: member tiles (solo_kernel)
   uint64_t nstile = 0;
+  bool stile_slow = false;              // some member tile takes the per-vector path
 };
 
 // A registered tensor list (hvd_register): this rank's tensors plus the successor's
@@ -507,6 +508,8 @@ int upload_plan(hvd_comm* c, std::vector<uint64_t> key, const std::vector<HostBu
     db.pp.nseg = nseg;
     db.stile = offs[b].nstile ? reinterpret_cast<const SoloTile*>(d + offs[b].stile) : nullptr;
     db.nstile = offs[b].nstile;
+    for (uint64_t i = 0; i < offs[b].nstile; ++i)
+      db.stile_slow |= reinterpret_cast<const SoloTile*>(h + offs[b].stile)[i].flags != 0;
     p.bufs.push_back(db);
   }
   if (total) {
@@ -918,6 +921,12 @@ int enqueue_fused_multi(hvd_comm* c, DevPlanBuffer* const* bs, int nb, cudaStrea
       CK(bulk_max_ctas_per_sm(dtype, c->solo_stages, c->solo_stage_bytes, &per_sm, false));
       const int grid = std::max(1, std::max(1, per_sm) * c->sm_count / c->nlocal);
       return launch_counted(c, HVD_KERNEL_SOLO, s, &F.ring.jt, fused_bytes(F), [&] { return launch_bulk(F, dtype, grid, c->nlocal, s); });
+    }
+    F.solo_tpc = 1;
+    if (kSoloTPC > 1 && !F.scale_on && F.tdtype == dtype) {  // several plain member tiles per CTA
+      bool plain = true;
+      for (int i = 0; i < nb; ++i) plain = plain && bs[i]->stile && !bs[i]->stile_slow;
+      if (plain) F.solo_tpc = kSoloTPC;
     }
     return launch_counted(c, HVD_KERNEL_SOLO, s, &F.ring.jt, fused_bytes(F), [&] { return launch_solo(F, dtype, c->nlocal, s); });
   }
