@@ -450,6 +450,8 @@ def test_pull_buffers_allocated_only_for_the_pull_protocol(hvd):
     that protocol is chosen (the default footprint is the push path's)."""
     L = hvd._lib
     n, cap = 4, 8 << 20
+    hvd.init_virtual(1, 0, 1 << 20).finalize()  # library and module loading happen before free0
+    torch.cuda.synchronize()
     free0 = torch.cuda.mem_get_info()[0]
     comm = hvd.init_virtual(n, 0, cap)
     try:
