@@ -1075,7 +1075,12 @@ __device__ __forceinline__ int chan_of(const BufDesc& D, int ch, int nch) {
 // A launch begins with a handshake (ready flag per channel and epoch) so that no
 // push lands in a receive region the successor's previous launch still reads.
 template <class Op, int TESZ>
-__global__ void __launch_bounds__(416, 1) fused_allreduce_kernel(const __grid_constant__ FusedParams P) {
+#ifdef HVD_FUSED_MAXNREG  // tuning builds: a register cap instead of the launch bounds
+#define HVD_FUSED_BOUNDS __maxnreg__(HVD_FUSED_MAXNREG)
+#else
+#define HVD_FUSED_BOUNDS __launch_bounds__(416, 1)
+#endif
+__global__ void HVD_FUSED_BOUNDS fused_allreduce_kernel(const __grid_constant__ FusedParams P) {
   if (P.ring.pdl) {
     // programmatic dependent launch: the next launch on the stream may be scheduled onto
     // SMs as they free up; this grid touches memory only once the previous one has
