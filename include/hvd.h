@@ -230,7 +230,9 @@ int hvd_traffic(hvd_comm* c, int local, uint64_t* sent_bytes, uint64_t* sends);
 
 typedef enum {
   HVD_CFG_CHANNELS = 1,      /* CTAs per rank in the ring kernel (1..256)               */
-  HVD_CFG_SLICE_BYTES = 2,   /* pipelining slice per channel (multiple of 256 B; 0 = auto)  */
+  HVD_CFG_SLICE_BYTES = 2,   /* pipelining slice target per channel (0 = auto: half of a
+                                channel's share of a chunk, 32..128 KiB); a share is cut into
+                                ceil(share / target) equal slices, rounded up to 256 B     */
   HVD_CFG_THREADS = 3,       /* data threads per ring CTA (64..384, multiple of 32, default 256; +1 signal warp) */
   HVD_CFG_TIMEOUT_MS = 4,    /* device spin-wait watchdog                               */
   HVD_CFG_PACK_CTAS_PER_SM = 5,
