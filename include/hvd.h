@@ -133,8 +133,10 @@ int hvd_local_ranks(const hvd_comm* c); /* ranks driven by this comm (1 or N)   
  * bits every way): by default one persistent launch per call gathers in the
  * first ring step and scatters in the all-gather steps (zero-copy, all buffers
  * of the call pipelined); buffers up to HVD_CFG_LL_MAX_BYTES (or 256 KiB / 1 MiB at N = 2 / N > 2 in a
- * multi-buffer call) take the LL latency protocol, a lone buffer up to
- * HVD_CFG_LL128_MAX_BYTES the LL128 protocol; at N = 1 a plain HBM stream.
+ * multi-buffer call) take the LL latency protocol — except that in a call of at most 16
+ * buffers with a buffer for the persistent launch, small buffers of the same dtype join
+ * that launch — and a lone buffer up to HVD_CFG_LL128_MAX_BYTES the LL128 protocol; at
+ * N = 1 a plain HBM stream.
  * op: HVD_SUM (all dtypes) or HVD_AVERAGE (float dtypes only).
  * Errors: INVALID (null/size), UNSUPPORTED (AVERAGE on integers, bad dtype),
  * NOT_CONNECTED, TIMEOUT / MISMATCH (latched), CUDA. */
